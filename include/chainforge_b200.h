@@ -1,0 +1,254 @@
+/*
+ * chainforge_b200.h -- C ABI of libchainforge_b200.so, the B200-native deep-copy hot path.
+ *
+ * The reference (arxiv 1906.01128's `chainforge`, pure Python) has no FFI; its seam is the
+ * Python call triple inside execute_case's metered window (harness.py:369-373).  Each entry
+ * point below replaces one reference function (cited as file:line under
+ * /root/reference/pkg/src/chainforge); INTEGRATION.md shows the ctypes binding a chainforge
+ * maintainer would add.  Conventions:
+ *   - plain C types only; every function returns int (CF_OK = 0, negative CF_E_* on failure);
+ *   - cf_last_error() returns a thread-local message for the last failure on this thread;
+ *   - device work is enqueued on an explicit stream (NULL = the context's compute stream);
+ *   - one cf_ctx per GPU, used by one host thread (SPEC.md concurrency model).
+ * Error codes map onto the reference exceptions (memory.py:44-57, harness.py:46-51):
+ *   CF_E_OOM -> OutOfSimMemory, CF_E_WILD -> WildAccess,
+ *   CF_E_OUTSIDE_ARENA -> AttachOutsideArena, CF_E_STATE -> SimMemoryError.
+ */
+#ifndef CHAINFORGE_B200_H
+#define CHAINFORGE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_ABI_VERSION 1
+
+enum {
+  CF_OK = 0,
+  CF_E_INVALID = -1,        /* bad argument (ValueError) */
+  CF_E_OOM = -2,            /* OutOfSimMemory (memory.py:48) */
+  CF_E_WILD = -3,           /* WildAccess (memory.py:52) */
+  CF_E_OUTSIDE_ARENA = -4,  /* AttachOutsideArena (memory.py:56) */
+  CF_E_CUDA = -5,           /* CUDA runtime failure (message carries cudaGetErrorString) */
+  CF_E_NODEVICE = -6,       /* no CUDA device: the product path refuses to run without one */
+  CF_E_STATE = -7           /* SimMemoryError: call out of order (memory.py:333-334) */
+};
+
+/* tree kinds / layouts (scenarios.py:30-68) */
+enum { CF_LINEAR = 0, CF_DENSE = 1 };
+enum { CF_ALLINIT_ALLUSED = 0, CF_ALLINIT_LLUSED = 1, CF_LLINIT_LLUSED = 2 };
+/* host memory kinds */
+enum { CF_MEM_PAGEABLE = 0, CF_MEM_PINNED = 1, CF_MEM_MANAGED = 2 };
+/* target policies: CF_TARGET_REF = targeted_arrays (scenarios.py:270-284); the other two are
+ * the BASELINE configs' "consume every leaf" / "every array" policies */
+enum { CF_TARGET_REF = 0, CF_TARGET_ALL_LEAVES = 1, CF_TARGET_ALL_ARRAYS = 2 };
+/* leaf-kernel modes: resolved effective address (pointerchain) vs chase-per-access (Listing 2) */
+enum { CF_MODE_RESOLVED = 0, CF_MODE_CHASE = 1 };
+
+typedef struct cf_ctx cf_ctx;       /* one GPU: streams, events, scratch */
+typedef struct cf_tree cf_tree;     /* planned graph layout + relocation/chain tables */
+typedef struct cf_window cf_window; /* a planned, pipelined metered window */
+
+/* LinearSpec / DenseSpec (scenarios.py:33-68) plus the B200 build parameters.
+ * elem: 8 = float64 (reference), 4 = float32 (BASELINE configs).
+ * align: 1 = packed arena (Arena.allocate, memory.py:217-227), 8 = host bump allocator
+ *        (MemorySpace.allocate, memory.py:124-137), 16 = aligned production arena.
+ * leaf_only: dense trees with arrays on the depth-D leaves only (BASELINE C2/C5). */
+typedef struct {
+  int32_t kind;
+  int32_t layout;
+  int64_t k_or_q;
+  int64_t n;
+  int64_t depth;
+  int32_t elem;
+  int32_t leaf_only;
+  int32_t align;
+  int32_t reserved;
+} cf_spec;
+
+typedef struct {
+  uint64_t total_bytes;   /* arena bytes (== closed form when align == 1) */
+  uint64_t nallocs, nnodes, narrays, nsites;
+  uint64_t root_off;      /* offset of the root node */
+  uint64_t payload_bytes; /* sum of array bytes */
+  uint64_t padding_bytes; /* total_bytes - sum of allocation sizes */
+} cf_tree_info;
+
+/* tables exposed by cf_tree_table (pointers stay valid until cf_tree_free) */
+enum {
+  CF_TAB_ALLOC_OFF = 0,   /* u64[nallocs]   allocation order (request_list)          */
+  CF_TAB_ALLOC_SIZE = 1,  /* u64[nallocs]                                             */
+  CF_TAB_NODE_OFF = 2,    /* u64[nnodes]    pre-order (TreeHandle.node_addrs)         */
+  CF_TAB_NODE_LEVEL = 3,  /* i32[nnodes]                                              */
+  CF_TAB_NODE_SIZE = 4,   /* u32[nnodes]                                              */
+  CF_TAB_ARR_LEVEL = 5,   /* i32[narrays]   TreeHandle.arrays (ArrayRef)              */
+  CF_TAB_ARR_OWNER = 6,   /* u64[narrays]                                             */
+  CF_TAB_ARR_OFF = 7,     /* u64[narrays]                                             */
+  CF_TAB_ARR_COUNT = 8,   /* u64[narrays]                                             */
+  CF_TAB_SITE_OFF = 9,    /* u64[nsites]    DFS order (Arena.pointer_sites)           */
+  CF_TAB_SITE_TARGET = 10,/* u64[nsites]    target offset of each pointer field      */
+  CF_TAB_SITE_SORTED = 11,/* u64[nsites]    ascending offsets (the relocation table)  */
+  CF_TAB_ARR_ORDINAL = 12 /* u64[narrays]   owner's ordinal among nodes of its level  */
+};
+
+/* Chain shape walked by the resolve / chase kernels (kernel_scale walk, harness.py:285-304).
+ * A target is (level L, ordinal): L hops through Lnext from the root; for dense trees the
+ * hop at level l takes child digit_l of the ordinal written in base q. */
+typedef struct {
+  int32_t kind;
+  int32_t depth;        /* dense D (leaf level uses 12-byte nodes); linear: k-1 */
+  uint32_t q;           /* dense fan-out; 1 for linear */
+  uint32_t reserved;
+  uint64_t root_off;    /* root node offset inside the image */
+  uint64_t image_bytes; /* every hop must stay inside [image, image + image_bytes) */
+} cf_chain_shape;
+
+/* ---------------- runtime ---------------- */
+int cf_abi_version(void);
+const char* cf_last_error(void);
+int cf_device_count(int* count);
+/* nstreams: H2D copy streams (>= 1); a compute and a D2H stream are added. */
+int cf_ctx_create(int device, int nstreams, cf_ctx** out);
+int cf_ctx_destroy(cf_ctx* ctx);
+int cf_ctx_sync(cf_ctx* ctx);
+void* cf_ctx_stream(cf_ctx* ctx);               /* compute stream (cudaStream_t) */
+uint64_t cf_ctx_launches(cf_ctx* ctx);          /* kernels launched so far */
+int cf_ctx_sm_count(cf_ctx* ctx);
+
+/* Host memory for arenas / host spaces (MemorySpace storage, memory.py:101-137).
+ * PINNED = cudaHostAlloc(portable), MANAGED = cudaMallocManaged (UVM mode, memory.py:239-261),
+ * PAGEABLE = page-aligned malloc (host-only builds, CPU tests). Memory is zero-filled. */
+int cf_host_alloc(uint64_t bytes, int kind, void** out);
+int cf_host_free(void* p, int kind);            /* PINNED / MANAGED */
+int cf_host_free_sized(void* p, uint64_t bytes, int kind); /* any kind */
+int cf_dev_alloc(cf_ctx* ctx, uint64_t bytes, void** out);
+int cf_dev_free(cf_ctx* ctx, void* p);
+/* Synchronous copy between any two spaces (Machine.transfer_range, memory.py:294-303). */
+int cf_memcpy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int cf_memcpy_async(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, void* stream);
+int cf_memset(cf_ctx* ctx, void* dst, int value, uint64_t bytes);
+
+/* ---------------- host marshaller (scenarios.py:122-267) ---------------- */
+/* Plan the layout: allocation order, node/array tables, pointer sites (tree_total_bytes,
+ * iter_*_allocations, scenarios.py:122-149). No payload is touched. */
+int cf_tree_plan(const cf_spec* spec, cf_tree** out);
+int cf_tree_info_get(const cf_tree* tree, cf_tree_info* out);
+int cf_tree_table(const cf_tree* tree, int which, const void** ptr, uint64_t* count);
+/* Write the graph into host memory at `host` (>= total_bytes): node fields, pointer fields
+ * (= ptr_base + target offset) and payload_values(seed) (scenarios.py:152-252), multi-threaded.
+ * ptr_base is normally (uint64_t)host. */
+int cf_tree_build(const cf_tree* tree, void* host, uint64_t ptr_base, uint64_t seed, int nthreads);
+/* targeted_arrays (scenarios.py:270-284) and the all-leaves / all-arrays policies: writes
+ * array indices into out (capacity cap) and their number into *n. */
+int cf_tree_targets(const cf_tree* tree, int policy, int64_t* out, uint64_t cap, uint64_t* n);
+int cf_tree_chain_shape(const cf_tree* tree, cf_chain_shape* out);
+int cf_tree_free(cf_tree* tree);
+
+/* ---------------- device kernels (sm_100a) ---------------- */
+/* Relocation (attach/detach) kernel: for each site s, v = *(u64*)(image+s);
+ * require from_base <= v < from_base + image_bytes, write to_base + (v - from_base).
+ * Attach: from = host arena base, to = device image (memory.py:316-323);
+ * detach: from = image, to = host base (memory.py:337-344). Misaligned (4 mod 8) fields are
+ * handled with 2 x u32 accesses. On a bad field, d_bad receives min(bad site index)
+ * (initialise to UINT64_MAX). */
+int cf_relocate(cf_ctx* ctx, void* image, uint64_t image_bytes, const uint64_t* d_sites,
+                uint64_t nsites, uint64_t from_base, uint64_t to_base, uint64_t* d_bad,
+                void* stream);
+/* Pointerchain resolve kernel: one thread per chain, walks it once in the relocated image and
+ * writes its effective address + node count (targeted_arrays, scenarios.py:270-284, done on
+ * the device; harness.py:228-238 pointerchain buffers). */
+int cf_resolve(cf_ctx* ctx, const void* image, const cf_chain_shape* shape,
+               const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets,
+               uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad, void* stream);
+/* Leaf kernel (kernel_scale / _scale_block, harness.py:244-309): x *= scale over
+ * [begin, end) of every target, elem = 4 (f32) or 8 (f64).
+ * mode CF_MODE_RESOLVED reads d_ea (from cf_resolve); CF_MODE_CHASE re-walks the chain from
+ * the image root on every 16-byte access with non-hoistable loads (d_ea unused).
+ * parts: (target, elem_begin, elem_end) triples, u64[3*nparts]; NULL = whole arrays of
+ * d_count. d_bad is raised if a part exceeds the count read from the node. */
+int cf_scale(cf_ctx* ctx, int elem, int mode, const void* image, const cf_chain_shape* shape,
+             const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
+             const uint32_t* d_count, uint64_t ntargets, const uint64_t* d_parts, uint64_t nparts,
+             const uint64_t* d_part_tile_base, uint64_t ntiles, double scale, uint64_t* d_bad,
+             void* stream);
+
+/* ---------------- reference-named composite operations ---------------- */
+/* Machine.marshal_transfer_and_attach (memory.py:307-325): chunked multi-stream H2D of the
+ * pinned arena into `image`, relocation-table upload, per-chunk relocation as chunks land.
+ * Synchronous; returns CF_E_OUTSIDE_ARENA with *bad_site = index into the sorted site table. */
+int cf_marshal_transfer_and_attach(cf_ctx* ctx, const void* host_arena, uint64_t total,
+                                   void* image, const uint64_t* h_sites_sorted, uint64_t nsites,
+                                   uint64_t chunk_bytes, uint64_t* bad_site);
+/* Machine.demarshal (memory.py:327-345): detach kernel on the image, then chunked D2H into
+ * host_arena. Synchronous. */
+int cf_demarshal(cf_ctx* ctx, void* host_arena, uint64_t total, void* image,
+                 const uint64_t* h_sites_sorted, uint64_t nsites, uint64_t chunk_bytes,
+                 uint64_t* bad_site);
+/* kernel_scale over a device image (harness.py:244-304): resolve every target chain on the
+ * device, then run the leaf kernel in `mode`. h_level/h_ordinal/h_count are host arrays of
+ * the targets' chain keys and planned element counts. Synchronous; d_ea_out (optional,
+ * device) receives the effective addresses. */
+int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain_shape* shape,
+                    const int32_t* h_level, const uint64_t* h_ordinal, const uint64_t* h_count,
+                    uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad);
+/* Pointerchain scheme leaf kernel over host-resolved buffers (harness.py:255-259): every
+ * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */
+int cf_scale_resolved(cf_ctx* ctx, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,
+                      double scale);
+/* naive_deep_copy fixups (memory.py:349-365): per-object copies are issued by the caller with
+ * cf_memcpy_batch; this kernel rewrites every site through a sorted interval map
+ * (AddressMap.translate, memory.py:409-419) on the device. */
+int cf_memcpy_batch(cf_ctx* ctx, void* const* dsts, const void* const* srcs,
+                    const uint64_t* sizes, uint64_t count, void* stream);
+int cf_naive_fixup(cf_ctx* ctx, const uint64_t* d_site_field_host, const uint64_t* d_site_target_host,
+                   uint64_t nsites, const uint64_t* d_map_host_base, const uint64_t* d_map_size,
+                   const uint64_t* d_map_dev_base, uint64_t nmap, uint64_t* d_bad, void* stream);
+
+/* ---------------- pipelined metered window (harness.py:369-373) ---------------- */
+/* Flags for the window */
+enum {
+  CF_WIN_H2D = 1u << 0,      /* upload the arena from host_src (else the image is resident) */
+  CF_WIN_TABLES = 1u << 1,   /* upload the relocation / chain tables every run */
+  CF_WIN_ATTACH = 1u << 2,   /* relocation kernel (attach) */
+  CF_WIN_RESOLVE = 1u << 3,  /* pointerchain resolve kernel */
+  CF_WIN_SCALE = 1u << 4,    /* leaf kernel */
+  CF_WIN_DETACH = 1u << 5,   /* inverse relocation before copy-back */
+  CF_WIN_D2H = 1u << 6,      /* copy the image back to host_dst */
+  CF_WIN_GRAPH = 1u << 7     /* capture the enqueue sequence into a CUDA graph once, replay */
+};
+
+typedef struct {
+  const cf_tree* tree;        /* layout, relocation table and chain tables */
+  const int64_t* h_targets;   /* array indices to consume (cf_tree_targets) */
+  uint64_t ntargets;
+  const void* host_src;       /* pinned arena (input) */
+  void* host_dst;             /* pinned copy-back destination (may equal host_src) */
+  uint64_t host_base;         /* pointer base used inside the arena (cf_tree_build ptr_base) */
+  void* image;                /* device image, >= total bytes */
+  int32_t mode;               /* CF_MODE_RESOLVED / CF_MODE_CHASE */
+  uint32_t flags;             /* CF_WIN_* */
+  double scale;
+  uint64_t chunk_bytes;       /* pipeline granularity (0 = whole arena in one chunk) */
+} cf_window_desc;
+
+typedef struct {
+  float ms_total;             /* device time from first enqueue to last completion */
+  float ms_kernel;            /* sum of leaf-kernel launches (events around each) */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t launches;          /* kernels launched by this run */
+  uint64_t bad;               /* UINT64_MAX if no error */
+  uint64_t nchunks, nsteps;
+} cf_window_stats;
+
+int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
+/* Enqueue one window; if sync != 0 wait and fill stats (ms from CUDA events). */
+int cf_window_run(cf_window* w, int sync, cf_window_stats* stats);
+int cf_window_set_scale(cf_window* w, double scale);
+int cf_window_free(cf_window* w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHAINFORGE_B200_H */

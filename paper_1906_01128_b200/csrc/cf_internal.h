@@ -1,0 +1,98 @@
+// Internal declarations shared by the libchainforge_b200 translation units.
+#pragma once
+#include "chainforge_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <vector>
+
+namespace cf {
+
+// Node layout of the reference (scenarios.py:20-28): 24-byte node {u32 nA@0, u32 nLnext@4,
+// u64 A@8, u64 Lnext@16}; dense depth-D leaves are packed 12-byte {u32 nA@0, u64 A@4}.
+constexpr uint32_t NODE_SIZE = 24, LEAF_NODE_SIZE = 12;
+constexpr uint32_t OFF_NA = 0, OFF_NLNEXT = 4, OFF_A = 8, OFF_LNEXT = 16, LEAF_OFF_A = 4;
+constexpr uint64_t NO_BAD = ~0ull;
+// Leaf-kernel tile: 256 threads x 4 vectors x 16 B.  Host planners split work on this grain.
+constexpr uint32_t SCALE_THREADS = 256;
+constexpr uint32_t SCALE_UNROLL = 4;
+constexpr uint64_t TILE_BYTES = uint64_t(SCALE_THREADS) * SCALE_UNROLL * 16;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+void clear_error();
+
+#define CF_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return ::cf::fail(CF_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define CF_TRY(expr)            \
+  do {                          \
+    int r_ = (expr);            \
+    if (r_ != CF_OK) return r_; \
+  } while (0)
+
+// Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
+int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
+                    uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s);
+int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh,
+                   const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea,
+                   uint32_t* count, uint64_t* bad, cudaStream_t s);
+int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
+                 const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
+                 const uint32_t* count, const uint64_t* parts, uint64_t nparts,
+                 const uint64_t* tile_base, uint64_t tile_begin, uint64_t tile_end, double scale,
+                 uint64_t* bad, cudaStream_t s);
+int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
+                       uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
+                       const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);
+int launch_fill_u64(cf_ctx* ctx, uint64_t* p, uint64_t value, uint64_t n, cudaStream_t s);
+
+inline uint64_t tiles_for(uint64_t elems, int elem) {
+  const uint64_t per = TILE_BYTES / uint64_t(elem);
+  return (elems + per - 1) / per;
+}
+
+}  // namespace cf
+
+struct cf_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t compute = nullptr;
+  cudaStream_t d2h = nullptr;
+  std::vector<cudaStream_t> h2d;
+  uint64_t* d_bad = nullptr;   // device scratch error word
+  uint64_t* h_bad = nullptr;   // pinned mirror
+  std::atomic<uint64_t> launches{0};
+};
+
+struct cf_tree {
+  cf_spec spec{};
+  uint64_t total = 0, root_off = 0, payload_bytes = 0, served = 0;
+  std::vector<uint64_t> alloc_off, alloc_size;
+  std::vector<int64_t> alloc_array;   // array index of an allocation, -1 for node blocks
+  std::vector<uint64_t> node_off;
+  std::vector<int32_t> node_level;
+  std::vector<uint32_t> node_size;
+  std::vector<uint32_t> node_na;      // value of the nA field
+  std::vector<int64_t> node_nlnext;   // value of nLnext, -1 when the node has no such field
+  std::vector<int32_t> arr_level;
+  std::vector<uint64_t> arr_owner, arr_off, arr_count, arr_ordinal;
+  std::vector<uint64_t> site_off, site_target, site_sorted;
+  std::vector<std::vector<uint64_t>> level_nodes;  // per level: node offsets by ordinal
+};
+
+// RAII: make ctx's device current on this thread.
+struct CfDevice {
+  int prev = -1;
+  explicit CfDevice(const cf_ctx* c) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (c && prev != c->device) cudaSetDevice(c->device);
+  }
+  ~CfDevice() {}
+};

@@ -1,0 +1,369 @@
+// sm_100a kernels of the deep-copy hot path.
+//
+//   k_relocate    attach / detach fix-ups over the relocation table
+//                 (Machine.marshal_transfer_and_attach site loop, memory.py:316-323;
+//                  Machine.demarshal site loop, memory.py:337-344)
+//   k_resolve     pointerchain: walk each target chain once, emit its effective address
+//                 (targeted_arrays, scenarios.py:270-284, on the device)
+//   k_scale       leaf kernel x *= s (_scale_block, harness.py:307-309) in two modes:
+//                   RESOLVED  reads the effective-address table (pointerchain)
+//                   CHASE     re-walks the chain per 16-byte access with non-hoistable loads
+//                             (Listing 2 per-iteration chain)
+//   k_naive_fixup per-object deep-copy fix-ups through a sorted interval map
+//                 (naive_deep_copy + AddressMap.translate, memory.py:349-365, 409-419)
+//
+// All of these are HBM/latency-bound integer or streaming work: no tensor cores.  The leaf
+// kernel is the HBM-roofline kernel: 16-byte vector loads/stores with streaming cache hints,
+// 4 independent vectors in flight per thread, a persistent grid sized to 148 SMs x resident
+// CTAs, and a flattened (target, tile) work list so 64 huge leaves and 1M small leaves both
+// balance.  Pointer fields in the packed reference layout sit at 4 (mod 8); every 64-bit field
+// access goes through ld_u64_any/st_u64_any (2 x u32 when misaligned).
+#include "cf_internal.h"
+
+#include <algorithm>
+
+namespace cf {
+namespace {
+
+__device__ __forceinline__ uint64_t ld_u64_any(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 7) == 0) return *reinterpret_cast<const uint64_t*>(p);
+  if ((a & 3) == 0) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
+    return uint64_t(w[0]) | (uint64_t(w[1]) << 32);
+  }
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+__device__ __forceinline__ void st_u64_any(uint8_t* p, uint64_t v) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 7) == 0) {
+    *reinterpret_cast<uint64_t*>(p) = v;
+  } else if ((a & 3) == 0) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(p);
+    w[0] = uint32_t(v);
+    w[1] = uint32_t(v >> 32);
+  } else {
+    for (int i = 0; i < 8; ++i) p[i] = uint8_t(v >> (8 * i));
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_u32_any(const uint8_t* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) return *reinterpret_cast<const uint32_t*>(p);
+  return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+
+// Non-hoistable chain loads for CHASE mode: asm volatile keeps one load per access in SASS
+// (LDG.E.64.CONSTANT), the per-iteration dereference cost the paper measures.
+__device__ __forceinline__ uint64_t ld_chain_u64(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 7) == 0) {
+    uint64_t v;
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+  }
+  uint32_t lo, hi;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(lo) : "l"(p));
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(hi) : "l"(p + 4));
+  return uint64_t(lo) | (uint64_t(hi) << 32);
+}
+
+__device__ __forceinline__ void raise_bad(uint64_t* bad, uint64_t idx) {
+  if (bad) atomicMin(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)idx);
+}
+
+// ---------------------------------------------------------------- relocation (attach/detach)
+__global__ void __launch_bounds__(256) k_relocate(uint8_t* __restrict__ image, uint64_t total,
+                                                  const uint64_t* __restrict__ sites, uint64_t n,
+                                                  uint64_t from, uint64_t to, uint64_t* bad) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t s = sites[i];  // coalesced table read
+    if (s + 8 > total) { raise_bad(bad, i); continue; }
+    uint8_t* p = image + s;
+    const uint64_t v = ld_u64_any(p);
+    const uint64_t d = v - from;  // wraps when v < from
+    if (d >= total) { raise_bad(bad, i); continue; }
+    st_u64_any(p, to + d);
+  }
+}
+
+// ---------------------------------------------------------------- chain walk
+struct Walk {
+  const uint8_t* node;  // terminal node (nullptr on failure)
+  bool leaf;
+};
+
+template <bool CHASE>
+__device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_shape& sh, int level,
+                                           uint64_t ordinal) {
+  const uint8_t* p = image + sh.root_off;
+  const bool dense = sh.kind == CF_DENSE;
+  uint64_t qpow = 1;
+  if (dense)
+    for (int l = 1; l < level; ++l) qpow *= sh.q;
+  for (int l = 1; l <= level; ++l) {
+    const uint64_t blk = CHASE ? ld_chain_u64(p + OFF_LNEXT) : ld_u64_any(p + OFF_LNEXT);
+    uint64_t child = 0, digit = 0;
+    if (dense) {
+      child = (l < sh.depth) ? NODE_SIZE : LEAF_NODE_SIZE;
+      digit = (ordinal / qpow) % sh.q;
+      qpow = qpow > 1 ? qpow / sh.q : 1;
+    }
+    const uint64_t next = blk + digit * child;
+    if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+    p = reinterpret_cast<const uint8_t*>(next);
+  }
+  return {p, dense && level == sh.depth};
+}
+
+__global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ image, cf_chain_shape sh,
+                                                 const int32_t* __restrict__ level,
+                                                 const uint64_t* __restrict__ ordinal, uint64_t n,
+                                                 uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
+                                                 uint64_t* bad) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Walk w = walk_chain<false>(image, sh, level[i], ordinal[i]);
+  if (!w.node) {
+    ea[i] = 0;
+    count[i] = 0;
+    raise_bad(bad, i);
+    return;
+  }
+  ea[i] = ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A));
+  count[i] = ld_u32_any(w.node + OFF_NA);
+}
+
+// ---------------------------------------------------------------- leaf kernel
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  using V = float4;
+  static constexpr int N = 4;
+  __device__ static V ld(const V* p) { return __ldcs(p); }
+  __device__ static void st(V* p, V v) { __stcs(p, v); }
+  __device__ static V mul(V v, float s) { return make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s)); }
+};
+template <> struct Vec<double> {
+  using V = double2;
+  static constexpr int N = 2;
+  __device__ static V ld(const V* p) { return __ldcs(p); }
+  __device__ static void st(V* p, V v) { __stcs(p, v); }
+  __device__ static V mul(V v, double s) { return make_double2(__dmul_rn(v.x, s), __dmul_rn(v.y, s)); }
+};
+
+template <typename T>
+__device__ __forceinline__ T scalar_ld(const uint8_t* p) {
+  if constexpr (sizeof(T) == 8) {
+    uint64_t u = ld_u64_any(p);
+    return __longlong_as_double((long long)u);
+  } else {
+    return __uint_as_float(ld_u32_any(p));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void scalar_st(uint8_t* p, T v) {
+  if constexpr (sizeof(T) == 8) {
+    st_u64_any(p, (uint64_t)__double_as_longlong(v));
+  } else {
+    if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) *reinterpret_cast<float*>(p) = v;
+    else { uint32_t u = __float_as_uint(v); for (int i = 0; i < 4; ++i) p[i] = uint8_t(u >> (8 * i)); }
+  }
+}
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+
+struct ScaleArgs {
+  const uint8_t* image;
+  cf_chain_shape sh;
+  const int32_t* level;
+  const uint64_t* ordinal;
+  const uint64_t* ea;
+  const uint32_t* count;
+  const uint64_t* parts;      // (target, begin, end) x nparts
+  uint64_t nparts;
+  const uint64_t* tile_base;  // per-part first tile (absolute tile numbers)
+  uint64_t tile_begin;        // tiles [tile_begin, tile_end) belong to these parts
+  uint64_t tile_end;
+  uint64_t* bad;
+};
+
+template <typename T, bool CHASE>
+__global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
+  using VT = Vec<T>;
+  using V = typename VT::V;
+  constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
+  constexpr uint64_t VN = VT::N;
+  for (uint64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+    // locate the part owning this tile (uniform across the CTA; loads are broadcast)
+    uint64_t lo = 0, hi = a.nparts;
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (a.tile_base[mid] <= tile) lo = mid; else hi = mid;
+    }
+    const uint64_t t = a.parts[3 * lo];
+    const uint64_t pb = a.parts[3 * lo + 1], pe = a.parts[3 * lo + 2];
+    const uint64_t e0 = pb + (tile - a.tile_base[lo]) * TILE;
+    const uint64_t e1 = min(pe, e0 + TILE);
+    const uint8_t* arr;
+    uint64_t cnt;
+    if (CHASE) {
+      Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+      if (!w.node) { if (threadIdx.x == 0) raise_bad(a.bad, t); continue; }
+      arr = reinterpret_cast<const uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
+      cnt = ld_u32_any(w.node + OFF_NA);
+    } else {
+      arr = reinterpret_cast<const uint8_t*>(a.ea[t]);
+      cnt = a.count[t];
+    }
+    if (arr == nullptr || e1 > cnt) { if (threadIdx.x == 0) raise_bad(a.bad, t); continue; }
+    uint8_t* base = const_cast<uint8_t*>(arr);
+    const uintptr_t first = reinterpret_cast<uintptr_t>(base + e0 * sizeof(T));
+    // vector body [v0, v1) in elements; scalar head/tail
+    uint64_t v0 = e1, v1 = e1;
+    if ((first % sizeof(T)) == 0) {
+      const uint64_t head = ((16 - (first & 15)) & 15) / sizeof(T);
+      v0 = min(e1, e0 + head);
+      v1 = v0 + (e1 - v0) / VN * VN;
+    }
+    for (uint64_t i = e0 + threadIdx.x; i < v0; i += SCALE_THREADS)
+      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
+    for (uint64_t i = v1 + threadIdx.x; i < e1; i += SCALE_THREADS)
+      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
+    const uint64_t nv = (v1 - v0) / VN;
+    if (nv == 0) continue;
+    if (CHASE) {
+      // every 16-byte access re-derives its address through the chain (Listing 2 semantics)
+      for (uint64_t j = threadIdx.x; j < nv; j += SCALE_THREADS) {
+        Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+        const uint8_t* A = reinterpret_cast<const uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
+        V* p = reinterpret_cast<V*>(const_cast<uint8_t*>(A) + v0 * sizeof(T)) + j;
+        VT::st(p, VT::mul(VT::ld(p), s));
+      }
+    } else {
+      V* p = reinterpret_cast<V*>(base + v0 * sizeof(T));
+      uint64_t j = threadIdx.x;
+      // full tiles: SCALE_UNROLL independent 16-byte loads in flight per thread
+      for (; j + (SCALE_UNROLL - 1) * SCALE_THREADS < nv; j += SCALE_UNROLL * SCALE_THREADS) {
+        V r[SCALE_UNROLL];
+#pragma unroll
+        for (int u = 0; u < int(SCALE_UNROLL); ++u) r[u] = VT::ld(p + j + u * SCALE_THREADS);
+#pragma unroll
+        for (int u = 0; u < int(SCALE_UNROLL); ++u) VT::st(p + j + u * SCALE_THREADS, VT::mul(r[u], s));
+      }
+      for (; j < nv; j += SCALE_THREADS) VT::st(p + j, VT::mul(VT::ld(p + j), s));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- naive fix-up
+__device__ __forceinline__ bool translate(uint64_t addr, const uint64_t* hb, const uint64_t* sz,
+                                          const uint64_t* db, uint64_t n, uint64_t* out) {
+  // AddressMap.translate (memory.py:409-419): bisect_right over sorted host bases
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (hb[mid] <= addr) lo = mid + 1; else hi = mid;
+  }
+  if (lo == 0) return false;
+  const uint64_t i = lo - 1;
+  if (addr - hb[i] >= sz[i]) return false;
+  *out = db[i] + (addr - hb[i]);
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_naive_fixup(const uint64_t* __restrict__ field_host,
+                                                     const uint64_t* __restrict__ target_host, uint64_t n,
+                                                     const uint64_t* __restrict__ hb, const uint64_t* __restrict__ sz,
+                                                     const uint64_t* __restrict__ db, uint64_t nmap, uint64_t* bad) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t f, tg;
+    if (!translate(field_host[i], hb, sz, db, nmap, &f) || !translate(target_host[i], hb, sz, db, nmap, &tg)) {
+      raise_bad(bad, i);
+      continue;
+    }
+    st_u64_any(reinterpret_cast<uint8_t*>(f), tg);
+  }
+}
+
+__global__ void k_fill_u64(uint64_t* p, uint64_t v, uint64_t n) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+unsigned grid_for(cf_ctx* ctx, uint64_t work, unsigned threads, unsigned per_sm) {
+  const uint64_t want = (work + threads - 1) / threads;
+  const uint64_t cap = uint64_t(ctx->sm_count > 0 ? ctx->sm_count : 148) * per_sm;
+  return unsigned(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+}  // namespace
+
+#define CF_LAUNCHED(ctx)                                                                 \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(CF_E_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                   \
+    (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                             \
+  } while (0)
+
+int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t n,
+                    uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, n, from, to, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const int32_t* level,
+                   const uint64_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count, uint64_t* bad,
+                   cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, level, ordinal, n, ea, count, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
+                 const int32_t* level, const uint64_t* ordinal, const uint64_t* ea, const uint32_t* count,
+                 const uint64_t* parts, uint64_t nparts, const uint64_t* tile_base, uint64_t tile_begin,
+                 uint64_t tile_end, double scale, uint64_t* bad, cudaStream_t s) {
+  if (tile_end <= tile_begin || nparts == 0) return CF_OK;
+  const uint64_t ntiles = tile_end - tile_begin;
+  ScaleArgs a{image, sh, level, ordinal, ea, count, parts, nparts, tile_base, tile_begin, tile_end, bad};
+  // persistent grid: 148 SMs x 8 resident CTAs of 256 threads (2048 threads / SM)
+  const unsigned cap = unsigned((ctx->sm_count > 0 ? ctx->sm_count : 148) * 8);
+  const unsigned grid = unsigned(std::min<uint64_t>(ntiles, cap));
+  if (elem == 4) {
+    if (mode == CF_MODE_CHASE) k_scale<float, true><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
+    else k_scale<float, false><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
+  } else {
+    if (mode == CF_MODE_CHASE) k_scale<double, true><<<grid, SCALE_THREADS, 0, s>>>(a, scale);
+    else k_scale<double, false><<<grid, SCALE_THREADS, 0, s>>>(a, scale);
+  }
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host, uint64_t n,
+                       const uint64_t* hb, const uint64_t* sz, const uint64_t* db, uint64_t nmap,
+                       uint64_t* bad, cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_naive_fixup<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(field_host, target_host, n, hb, sz, db, nmap, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_fill_u64(cf_ctx* ctx, uint64_t* p, uint64_t v, uint64_t n, cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_fill_u64<<<unsigned((n + 255) / 256), 256, 0, s>>>(p, v, n);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+}  // namespace cf

@@ -1,0 +1,300 @@
+// C-ABI entry points for the device kernels and the reference-named composite operations:
+//   cf_marshal_transfer_and_attach  <- Machine.marshal_transfer_and_attach  memory.py:307-325
+//   cf_demarshal                    <- Machine.demarshal                    memory.py:327-345
+//   cf_kernel_scale                 <- kernel_scale (marshalling/naive walk) harness.py:244-304
+//   cf_naive_fixup                  <- naive_deep_copy fix-up loop         memory.py:362-364
+#include "cf_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+using namespace cf;
+
+namespace {
+
+cudaStream_t pick(cf_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->compute; }
+
+// RAII device buffer
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  int alloc(uint64_t bytes) {
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "cudaMalloc(%llu): %s",
+                  (unsigned long long)bytes, cudaGetErrorString(e));
+    }
+    return CF_OK;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct EventSet {
+  std::vector<cudaEvent_t> ev;
+  ~EventSet() { for (auto e : ev) cudaEventDestroy(e); }
+  int make(size_t n) {
+    ev.resize(n, nullptr);
+    for (auto& e : ev) CF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return CF_OK;
+  }
+};
+
+// Chunk boundaries over [0, total) at multiples of chunk, moved down so that no 8-byte pointer
+// field straddles two chunks (packed layouts put fields at 4 mod 8).
+std::vector<uint64_t> chunk_bounds(uint64_t total, uint64_t chunk, const uint64_t* sites, uint64_t nsites) {
+  std::vector<uint64_t> b{0};
+  if (chunk == 0 || chunk >= total) {
+    b.push_back(total);
+    return b;
+  }
+  for (uint64_t x = chunk; x < total; x += chunk) {
+    uint64_t y = x;
+    if (nsites) {
+      const uint64_t* it = std::lower_bound(sites, sites + nsites, x >= 7 ? x - 7 : 0);
+      if (it != sites + nsites && *it < x && *it + 8 > x) y = *it;
+    }
+    if (y > b.back()) b.push_back(y);
+  }
+  b.push_back(total);
+  return b;
+}
+
+int read_bad(cf_ctx* c, const uint64_t* d_bad, cudaStream_t s, uint64_t* out) {
+  CF_CUDA(cudaMemcpyAsync(c->h_bad, d_bad, 8, cudaMemcpyDeviceToHost, s));
+  CF_CUDA(cudaStreamSynchronize(s));
+  *out = c->h_bad[0];
+  return CF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cf_relocate(cf_ctx* c, void* image, uint64_t image_bytes, const uint64_t* d_sites, uint64_t nsites,
+                uint64_t from_base, uint64_t to_base, uint64_t* d_bad, void* stream) {
+  if (!c || (!image && nsites)) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  return launch_relocate(c, static_cast<uint8_t*>(image), image_bytes, d_sites, nsites, from_base, to_base,
+                         d_bad, pick(c, stream));
+}
+
+int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const int32_t* d_level,
+               const uint64_t* d_ordinal, uint64_t ntargets, uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad,
+               void* stream) {
+  if (!c || !shape) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  return launch_resolve(c, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, ntargets, d_ea,
+                        d_count, d_bad, pick(c, stream));
+}
+
+int cf_scale(cf_ctx* c, int elem, int mode, const void* image, const cf_chain_shape* shape,
+             const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea, const uint32_t* d_count,
+             uint64_t ntargets, const uint64_t* d_parts, uint64_t nparts, const uint64_t* d_part_tile_base,
+             uint64_t ntiles, double scale, uint64_t* d_bad, void* stream) {
+  (void)ntargets;
+  if (!c || !shape) return fail(CF_E_INVALID, "null argument");
+  if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
+  if (!d_parts || !d_part_tile_base) return fail(CF_E_INVALID, "parts and tile bases are required");
+  CfDevice g(c);
+  return launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, d_ea,
+                      d_count, d_parts, nparts, d_part_tile_base, 0, ntiles, scale, d_bad, pick(c, stream));
+}
+
+int cf_marshal_transfer_and_attach(cf_ctx* c, const void* host_arena, uint64_t total, void* image,
+                                   const uint64_t* h_sites, uint64_t nsites, uint64_t chunk_bytes,
+                                   uint64_t* bad_site) {
+  if (!c || !host_arena || !image || (nsites && !h_sites)) return fail(CF_E_INVALID, "null argument");
+  if (total == 0) return fail(CF_E_INVALID, "empty arena");
+  CfDevice g(c);
+  if (bad_site) *bad_site = NO_BAD;
+  DevBuf d_sites;
+  CF_TRY(d_sites.alloc(nsites * 8));
+  const uint64_t base = reinterpret_cast<uint64_t>(host_arena);
+  const uint64_t dimg = reinterpret_cast<uint64_t>(image);
+  // relocation table + error word first, on the compute stream
+  if (nsites) CF_CUDA(cudaMemcpyAsync(d_sites.p, h_sites, nsites * 8, cudaMemcpyHostToDevice, c->compute));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, c->compute));
+  std::vector<uint64_t> b = chunk_bounds(total, chunk_bytes, h_sites, nsites);
+  const size_t nch = b.size() - 1;
+  EventSet ev;
+  CF_TRY(ev.make(nch + 1));
+  CF_CUDA(cudaEventRecord(ev.ev[nch], c->compute));
+  for (size_t i = 0; i < nch; ++i) {
+    cudaStream_t s = c->h2d[i % c->h2d.size()];
+    if (i < c->h2d.size()) CF_CUDA(cudaStreamWaitEvent(s, ev.ev[nch], 0));
+    CF_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(image) + b[i], static_cast<const uint8_t*>(host_arena) + b[i],
+                            b[i + 1] - b[i], cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaEventRecord(ev.ev[i], s));
+    // sites whose field lies in this chunk are relocated as soon as it lands
+    const uint64_t s0 = uint64_t(std::lower_bound(h_sites, h_sites + nsites, b[i]) - h_sites);
+    const uint64_t s1 = uint64_t(std::lower_bound(h_sites, h_sites + nsites, b[i + 1]) - h_sites);
+    CF_CUDA(cudaStreamWaitEvent(c->compute, ev.ev[i], 0));
+    CF_TRY(launch_relocate(c, static_cast<uint8_t*>(image), total, d_sites.as<uint64_t>() + s0, s1 - s0, base,
+                           dimg, c->d_bad, c->compute));
+  }
+  uint64_t bad = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, c->compute, &bad));
+  if (bad != NO_BAD) {
+    // the device flags chunk-relative indices; the host arena is untouched, so report the
+    // first offending field in table order (memory.py:319-321 raises on the first one)
+    const uint8_t* h = static_cast<const uint8_t*>(host_arena);
+    for (uint64_t i = 0; i < nsites; ++i) {
+      uint64_t v;
+      memcpy(&v, h + h_sites[i], 8);
+      if (v - base >= total) {
+        if (bad_site) *bad_site = i;
+        return fail(CF_E_OUTSIDE_ARENA, "pointer field at arena offset %llu targets 0x%llx outside the arena",
+                    (unsigned long long)h_sites[i], (unsigned long long)v);
+      }
+    }
+    return fail(CF_E_OUTSIDE_ARENA, "relocation kernel reported a field outside the arena");
+  }
+  return CF_OK;
+}
+
+int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const uint64_t* h_sites,
+                 uint64_t nsites, uint64_t chunk_bytes, uint64_t* bad_site) {
+  if (!c || !host_arena || !image || (nsites && !h_sites)) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  if (bad_site) *bad_site = NO_BAD;
+  DevBuf d_sites;
+  CF_TRY(d_sites.alloc(nsites * 8));
+  const uint64_t base = reinterpret_cast<uint64_t>(host_arena);
+  const uint64_t dimg = reinterpret_cast<uint64_t>(image);
+  if (nsites) CF_CUDA(cudaMemcpyAsync(d_sites.p, h_sites, nsites * 8, cudaMemcpyHostToDevice, c->compute));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, c->compute));
+  // detach on the device (memory.py:337-344), then copy the image home
+  CF_TRY(launch_relocate(c, static_cast<uint8_t*>(image), total, d_sites.as<uint64_t>(), nsites, dimg, base,
+                         c->d_bad, c->compute));
+  EventSet ev;
+  CF_TRY(ev.make(1));
+  CF_CUDA(cudaEventRecord(ev.ev[0], c->compute));
+  CF_CUDA(cudaStreamWaitEvent(c->d2h, ev.ev[0], 0));
+  std::vector<uint64_t> b = chunk_bounds(total, chunk_bytes, h_sites, nsites);
+  for (size_t i = 0; i + 1 < b.size(); ++i)
+    CF_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(host_arena) + b[i], static_cast<const uint8_t*>(image) + b[i],
+                            b[i + 1] - b[i], cudaMemcpyDeviceToHost, c->d2h));
+  CF_CUDA(cudaStreamSynchronize(c->d2h));
+  uint64_t bad = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, c->compute, &bad));
+  if (bad != NO_BAD) {
+    if (bad_site) *bad_site = bad;
+    return fail(CF_E_OUTSIDE_ARENA, "pointer field at arena offset %llu holds a value outside the device image",
+                (unsigned long long)h_sites[bad]);
+  }
+  return CF_OK;
+}
+
+int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_shape* shape,
+                    const int32_t* h_level, const uint64_t* h_ordinal, const uint64_t* h_count, uint64_t ntargets,
+                    double scale, uint64_t* h_ea_out, uint64_t* bad) {
+  if (!c || !shape || (ntargets && (!h_level || !h_ordinal || !h_count))) return fail(CF_E_INVALID, "null argument");
+  if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
+  CfDevice g(c);
+  if (bad) *bad = NO_BAD;
+  if (ntargets == 0) return CF_OK;
+  // parts: whole arrays; tile prefix from the planned counts
+  std::vector<uint64_t> parts, tb;
+  uint64_t nt = 0;
+  for (uint64_t t = 0; t < ntargets; ++t) {
+    if (h_count[t] == 0) continue;
+    parts.insert(parts.end(), {t, 0, h_count[t]});
+    tb.push_back(nt);
+    nt += tiles_for(h_count[t], elem);
+  }
+  const uint64_t np = tb.size();
+  // one device block: level | ordinal | ea | count | parts | tile_base
+  const uint64_t off_ord = ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_ea = off_ord + ntargets * 8;
+  const uint64_t off_cnt = off_ea + ntargets * 8;
+  const uint64_t off_parts = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_tb = off_parts + np * 24;
+  DevBuf blk;
+  CF_TRY(blk.alloc(off_tb + np * 8 + 8));
+  uint8_t* d = blk.as<uint8_t>();
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemcpyAsync(d, h_level, ntargets * 4, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + off_ord, h_ordinal, ntargets * 8, cudaMemcpyHostToDevice, s));
+  if (np) {
+    CF_CUDA(cudaMemcpyAsync(d + off_parts, parts.data(), np * 24, cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaMemcpyAsync(d + off_tb, tb.data(), np * 8, cudaMemcpyHostToDevice, s));
+  }
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  const int32_t* lv = reinterpret_cast<const int32_t*>(d);
+  const uint64_t* od = reinterpret_cast<const uint64_t*>(d + off_ord);
+  uint64_t* ea = reinterpret_cast<uint64_t*>(d + off_ea);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(d + off_cnt);
+  CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, lv, od, ntargets, ea, cnt, c->d_bad, s));
+  uint64_t rb = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) {
+    if (bad) *bad = rb;
+    return fail(CF_E_WILD, "chain walk for target %llu left the device image", (unsigned long long)rb);
+  }
+  if (np) {
+    CF_TRY(launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, lv, od, ea, cnt,
+                        reinterpret_cast<const uint64_t*>(d + off_parts), np,
+                        reinterpret_cast<const uint64_t*>(d + off_tb), 0, nt, scale, c->d_bad, s));
+  }
+  if (h_ea_out) CF_CUDA(cudaMemcpyAsync(h_ea_out, ea, ntargets * 8, cudaMemcpyDeviceToHost, s));
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) {
+    if (bad) *bad = rb;
+    return fail(CF_E_WILD, "leaf kernel: target %llu count/address mismatch", (unsigned long long)rb);
+  }
+  return CF_OK;
+}
+
+int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,
+                      double scale) {
+  if (!c || (n && (!h_ea || !h_count))) return fail(CF_E_INVALID, "null argument");
+  if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
+  CfDevice g(c);
+  std::vector<uint64_t> parts, tb;
+  std::vector<uint32_t> cnt(n);
+  uint64_t nt = 0;
+  for (uint64_t t = 0; t < n; ++t) {
+    if (h_count[t] >> 32) return fail(CF_E_INVALID, "count does not fit the u32 nA field");
+    cnt[t] = uint32_t(h_count[t]);
+    if (h_count[t] == 0 || h_ea[t] == 0) continue;
+    parts.insert(parts.end(), {t, 0, h_count[t]});
+    tb.push_back(nt);
+    nt += tiles_for(h_count[t], elem);
+  }
+  const uint64_t np = tb.size();
+  if (np == 0) return CF_OK;
+  const uint64_t off_cnt = n * 8, off_parts = off_cnt + ((n * 4 + 7) / 8) * 8, off_tb = off_parts + np * 24;
+  DevBuf blk;
+  CF_TRY(blk.alloc(off_tb + np * 8));
+  uint8_t* d = blk.as<uint8_t>();
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemcpyAsync(d, h_ea, n * 8, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + off_cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + off_parts, parts.data(), np * 24, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + off_tb, tb.data(), np * 8, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  cf_chain_shape sh;
+  memset(&sh, 0, sizeof sh);
+  CF_TRY(launch_scale(c, elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, reinterpret_cast<const uint64_t*>(d),
+                      reinterpret_cast<const uint32_t*>(d + off_cnt), reinterpret_cast<const uint64_t*>(d + off_parts), np,
+                      reinterpret_cast<const uint64_t*>(d + off_tb), 0, nt, scale, c->d_bad, s));
+  uint64_t rb = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) return fail(CF_E_WILD, "leaf kernel: buffer %llu rejected", (unsigned long long)rb);
+  return CF_OK;
+}
+
+int cf_naive_fixup(cf_ctx* c, const uint64_t* d_field_host, const uint64_t* d_target_host, uint64_t nsites,
+                   const uint64_t* d_map_host_base, const uint64_t* d_map_size, const uint64_t* d_map_dev_base,
+                   uint64_t nmap, uint64_t* d_bad, void* stream) {
+  if (!c) return fail(CF_E_INVALID, "null ctx");
+  CfDevice g(c);
+  return launch_naive_fixup(c, d_field_host, d_target_host, nsites, d_map_host_base, d_map_size, d_map_dev_base,
+                            nmap, d_bad, pick(c, stream));
+}
+
+}  // extern "C"

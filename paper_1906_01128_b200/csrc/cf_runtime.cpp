@@ -1,0 +1,225 @@
+// Runtime plumbing behind the C ABI: errors, per-GPU context, host/device memory, copies.
+// Replaces the simulated Machine/MemorySpace storage of the reference (memory.py:101-303) with
+// real pinned host memory, HBM and CUDA streams.
+#include "cf_internal.h"
+
+#include <sys/mman.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace cf {
+namespace {
+thread_local char g_err[1024] = "";
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+void clear_error() { g_err[0] = 0; }
+const char* last_error() { return g_err; }
+
+}  // namespace cf
+
+using namespace cf;
+
+extern "C" {
+
+int cf_abi_version(void) { return CF_ABI_VERSION; }
+const char* cf_last_error(void) { return cf::last_error(); }
+
+int cf_device_count(int* count) {
+  if (!count) return fail(CF_E_INVALID, "null count");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return CF_OK;
+  }
+  *count = n;
+  return CF_OK;
+}
+
+int cf_ctx_create(int device, int nstreams, cf_ctx** out) {
+  if (!out || nstreams < 1 || nstreams > 16) return fail(CF_E_INVALID, "bad ctx arguments");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(CF_E_NODEVICE, "no CUDA device visible: the chainforge_b200 path requires a GPU");
+  }
+  if (device < 0 || device >= n) return fail(CF_E_INVALID, "device %d out of range (%d)", device, n);
+  CF_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CF_CUDA(cudaGetDeviceProperties(&prop, device));
+  cf_ctx* c = new cf_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  CF_CUDA(cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking));
+  CF_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  c->h2d.resize(nstreams);
+  for (auto& s : c->h2d) CF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CF_CUDA(cudaMalloc(&c->d_bad, 64));
+  CF_CUDA(cudaHostAlloc(&c->h_bad, 64, cudaHostAllocPortable));
+  *out = c;
+  return CF_OK;
+}
+
+int cf_ctx_destroy(cf_ctx* c) {
+  if (!c) return CF_OK;
+  CfDevice g(c);
+  cudaDeviceSynchronize();
+  cudaStreamDestroy(c->compute);
+  cudaStreamDestroy(c->d2h);
+  for (auto s : c->h2d) cudaStreamDestroy(s);
+  cudaFree(c->d_bad);
+  cudaFreeHost(c->h_bad);
+  delete c;
+  return CF_OK;
+}
+
+int cf_ctx_sync(cf_ctx* c) {
+  if (!c) return fail(CF_E_INVALID, "null ctx");
+  CfDevice g(c);
+  CF_CUDA(cudaDeviceSynchronize());
+  return CF_OK;
+}
+
+void* cf_ctx_stream(cf_ctx* c) { return c ? (void*)c->compute : nullptr; }
+uint64_t cf_ctx_launches(cf_ctx* c) { return c ? c->launches.load() : 0; }
+int cf_ctx_sm_count(cf_ctx* c) { return c ? c->sm_count : 0; }
+
+int cf_host_alloc(uint64_t bytes, int kind, void** out) {
+  if (!out) return fail(CF_E_INVALID, "null out");
+  if (bytes == 0) return fail(CF_E_INVALID, "allocation size must be positive");
+  void* p = nullptr;
+  if (kind == CF_MEM_PAGEABLE) {
+    // page-aligned, zero-filled (anonymous mmap)
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return fail(CF_E_OOM, "host mmap of %llu bytes failed", (unsigned long long)bytes);
+  } else if (kind == CF_MEM_PINNED) {
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA,
+                  "cudaHostAlloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    }
+    // zero-fill in parallel: the reference's storage is zero-initialised (memory.py:135)
+    const uint64_t CH = 8ull << 20;
+    int64_t nch = (int64_t)((bytes + CH - 1) / CH);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nch; ++i) {
+      uint64_t o = uint64_t(i) * CH;
+      memset((char*)p + o, 0, bytes - o < CH ? bytes - o : CH);
+    }
+  } else if (kind == CF_MEM_MANAGED) {
+    cudaError_t e = cudaMallocManaged(&p, bytes, cudaMemAttachGlobal);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA,
+                  "cudaMallocManaged(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    }
+    memset(p, 0, bytes);
+  } else {
+    return fail(CF_E_INVALID, "unknown memory kind %d", kind);
+  }
+  *out = p;
+  return CF_OK;
+}
+
+int cf_host_free(void* p, int kind) {
+  if (!p) return CF_OK;
+  if (kind == CF_MEM_PAGEABLE) return fail(CF_E_INVALID, "pageable blocks are freed by size: use cf_host_free_sized");
+  if (kind == CF_MEM_PINNED) CF_CUDA(cudaFreeHost(p));
+  else if (kind == CF_MEM_MANAGED) CF_CUDA(cudaFree(p));
+  else return fail(CF_E_INVALID, "unknown memory kind %d", kind);
+  return CF_OK;
+}
+
+int cf_host_free_sized(void* p, uint64_t bytes, int kind) {
+  if (!p) return CF_OK;
+  if (kind == CF_MEM_PAGEABLE) {
+    munmap(p, bytes);
+    return CF_OK;
+  }
+  return cf_host_free(p, kind);
+}
+
+int cf_dev_alloc(cf_ctx* c, uint64_t bytes, void** out) {
+  if (!c || !out) return fail(CF_E_INVALID, "null argument");
+  if (bytes == 0) return fail(CF_E_INVALID, "allocation size must be positive");
+  CfDevice g(c);
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "cudaMalloc(%llu): %s",
+                (unsigned long long)bytes, cudaGetErrorString(e));
+  }
+  return CF_OK;
+}
+
+int cf_dev_free(cf_ctx* c, void* p) {
+  if (!p) return CF_OK;
+  CfDevice g(c);
+  CF_CUDA(cudaFree(p));
+  return CF_OK;
+}
+
+int cf_memcpy(cf_ctx* c, void* dst, const void* src, uint64_t bytes) {
+  if (bytes == 0) return CF_OK;
+  CfDevice g(c);
+  CF_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  return CF_OK;
+}
+
+int cf_memcpy_async(cf_ctx* c, void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (!c) return fail(CF_E_INVALID, "null ctx");
+  if (bytes == 0) return CF_OK;
+  CfDevice g(c);
+  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream ? (cudaStream_t)stream : c->compute));
+  return CF_OK;
+}
+
+int cf_memset(cf_ctx* c, void* dst, int value, uint64_t bytes) {
+  CfDevice g(c);
+  CF_CUDA(cudaMemset(dst, value, bytes));
+  return CF_OK;
+}
+
+int cf_memcpy_batch(cf_ctx* c, void* const* dsts, const void* const* srcs, const uint64_t* sizes,
+                    uint64_t count, void* stream) {
+  if (!c) return fail(CF_E_INVALID, "null ctx");
+  if (count == 0) return CF_OK;
+  CfDevice g(c);
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->compute;
+  // cudaMemcpyBatchAsync (CUDA >= 12.8) submits the per-object copies of naive_deep_copy
+  // (memory.py:358-361) as one driver call; it rejects the legacy stream, so s is non-blocking.
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof attr);
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0;
+  const uint64_t BATCH = 1u << 16;
+  for (uint64_t b = 0; b < count; b += BATCH) {
+    uint64_t m = count - b < BATCH ? count - b : BATCH;
+    size_t fail_idx = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(const_cast<void**>(dsts + b), const_cast<void**>(srcs + b),
+                                         const_cast<size_t*>(reinterpret_cast<const size_t*>(sizes + b)),
+                                         m, &attr, &attr_idx, 1, &fail_idx, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      // fall back to individual async copies (same semantics, more driver calls)
+      for (uint64_t i = b; i < b + m; ++i)
+        CF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));
+    }
+  }
+  return CF_OK;
+}
+
+}  // extern "C"

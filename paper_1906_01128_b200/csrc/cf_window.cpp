@@ -1,0 +1,383 @@
+// Pipelined metered window: the reference's transfer_to_device -> kernel_scale -> copy_back
+// (harness.py:369-373, marshalling scheme + device pointerchain) as one planned, multi-stream
+// schedule on a B200.
+//
+// The arena is cut into chunks (boundaries never split a pointer field).  Step c of the
+// schedule, on the compute stream, after chunk c has landed:
+//   1. relocate (attach) the sites inside chunk c                       memory.py:316-323
+//   2. resolve the targets whose chain fields are all in chunks <= c     scenarios.py:270-284
+//   3. scale the array pieces that are ready at step c                   harness.py:307-309
+//   4. detach every chunk whose last reader ran at step <= c, then
+//      copy it home on the D2H stream                                    memory.py:327-345
+// H2D copies alternate over the context's copy streams, D2H runs concurrently on its own
+// stream, so copy-in, compute and copy-out overlap over the full-duplex host link.  All
+// dependency bookkeeping (ready / release steps) is computed once here on the host; a run is
+// only enqueues.  The tables the device needs are packed into one pinned block and uploaded
+// at the start of every run (CF_WIN_TABLES), since in a real deep copy they travel with the
+// arena.
+#include "cf_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+using namespace cf;
+
+struct cf_window {
+  cf_ctx* ctx = nullptr;
+  cf_window_desc d{};
+  cf_chain_shape sh{};
+  int elem = 8;
+  std::vector<uint64_t> bounds;        // chunk boundaries, nchunks + 1
+  std::vector<uint64_t> reloc_lo;      // sorted-site ranges per chunk, nchunks + 1
+  std::vector<uint64_t> res_lo;        // resolve-target ranges per step, nchunks + 1
+  std::vector<uint64_t> part_lo;       // part ranges per step, nchunks + 1
+  std::vector<uint64_t> det_lo;        // detach-site ranges per step, nchunks + 1
+  std::vector<std::vector<uint32_t>> released;  // chunks whose copy-back may start after step c
+  std::vector<uint64_t> tile_base;     // per part (+ sentinel): absolute first tile
+  // one pinned table block and its device mirror
+  uint8_t* h_tab = nullptr;
+  uint8_t* d_tab = nullptr;
+  uint64_t tab_bytes = 0;
+  uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_parts = 0, off_tb = 0;
+  uint64_t* d_ea = nullptr;
+  uint32_t* d_count = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_rel;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr;
+  std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
+  uint64_t nsites = 0;
+};
+
+namespace {
+
+uint64_t chunk_of(const std::vector<uint64_t>& b, uint64_t off) {
+  return uint64_t(std::upper_bound(b.begin(), b.end(), off) - b.begin()) - 1;
+}
+
+void destroy(cf_window* w) {
+  if (!w) return;
+  CfDevice g(w->ctx);
+  if (w->h_tab) cudaFreeHost(w->h_tab);
+  if (w->d_tab) cudaFree(w->d_tab);
+  if (w->d_ea) cudaFree(w->d_ea);
+  if (w->d_count) cudaFree(w->d_count);
+  for (auto e : w->ev_h2d) cudaEventDestroy(e);
+  for (auto e : w->ev_rel) cudaEventDestroy(e);
+  for (auto e : w->ev_k0) cudaEventDestroy(e);
+  for (auto e : w->ev_k1) cudaEventDestroy(e);
+  if (w->ev_start) cudaEventDestroy(w->ev_start);
+  if (w->ev_end) cudaEventDestroy(w->ev_end);
+  if (w->ev_join) cudaEventDestroy(w->ev_join);
+  delete w;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
+  if (!ctx || !desc || !out || !desc->tree) return fail(CF_E_INVALID, "null argument");
+  const cf_tree* t = desc->tree;
+  const uint32_t fl = desc->flags;
+  if ((fl & CF_WIN_H2D) && !desc->host_src) return fail(CF_E_INVALID, "H2D needs host_src");
+  if ((fl & CF_WIN_D2H) && !desc->host_dst) return fail(CF_E_INVALID, "D2H needs host_dst");
+  if (!desc->image) return fail(CF_E_INVALID, "null image");
+  if (desc->ntargets && !desc->h_targets) return fail(CF_E_INVALID, "null targets");
+  CfDevice g(ctx);
+  cf_window* w = new cf_window();
+  w->ctx = ctx;
+  w->d = *desc;
+  w->elem = t->spec.elem;
+  cf_tree_chain_shape(t, &w->sh);
+  const uint64_t total = t->total;
+  const uint64_t nsites = t->site_sorted.size();
+  w->nsites = nsites;
+  const uint64_t* sites = t->site_sorted.data();
+
+  // ---- chunks (no pointer field straddles a boundary)
+  std::vector<uint64_t>& b = w->bounds;
+  b.push_back(0);
+  const uint64_t ch = desc->chunk_bytes;
+  if (ch && ch < total) {
+    for (uint64_t x = ch; x < total; x += ch) {
+      uint64_t y = x;
+      const uint64_t* it = std::lower_bound(sites, sites + nsites, x >= 7 ? x - 7 : 0);
+      if (it != sites + nsites && *it < x && *it + 8 > x) y = *it;
+      if (y > b.back()) b.push_back(y);
+    }
+  }
+  b.push_back(total);
+  const uint64_t nch = b.size() - 1;
+  w->reloc_lo.resize(nch + 1);
+  for (uint64_t c = 0; c <= nch; ++c)
+    w->reloc_lo[c] = uint64_t(std::lower_bound(sites, sites + nsites, b[c]) - sites);
+
+  // ---- per target: chain fields -> ready step
+  const uint64_t nt = desc->ntargets;
+  const bool dense = t->spec.kind == CF_DENSE;
+  const uint64_t q = dense ? uint64_t(t->spec.k_or_q) : 1;
+  std::vector<uint64_t> ready(nt, 0), max_step(nt, 0);
+  std::vector<std::vector<uint64_t>> field_chunks(nt);
+  std::vector<uint64_t> release(nch);
+  std::iota(release.begin(), release.end(), 0);
+  for (uint64_t i = 0; i < nt; ++i) {
+    const int64_t a = desc->h_targets[i];
+    if (a < 0 || uint64_t(a) >= t->arr_off.size()) { destroy(w); return fail(CF_E_INVALID, "target %lld out of range", (long long)a); }
+    const int L = t->arr_level[a];
+    const uint64_t ord = t->arr_ordinal[a];
+    uint64_t r = 0;
+    for (int l = 0; l <= L; ++l) {
+      // ancestor at level l: ordinal prefix ord / q^(L-l) (pre-order within a level)
+      uint64_t pw = 1;
+      for (int m = l; m < L; ++m) pw *= q;
+      const uint64_t node = t->level_nodes[l][dense ? ord / pw : 0];
+      const bool leaf = dense && l == t->spec.depth;
+      uint64_t lo, hi;  // byte range read at this level
+      if (l < L) { lo = node + OFF_LNEXT; hi = lo + 8; }
+      else { lo = node + OFF_NA; hi = node + (leaf ? LEAF_NODE_SIZE : OFF_LNEXT); }
+      const uint64_t c0 = chunk_of(b, lo), c1 = chunk_of(b, hi - 1);
+      for (uint64_t c = c0; c <= c1; ++c) field_chunks[i].push_back(c);
+      r = std::max(r, c1);
+    }
+    ready[i] = r;
+  }
+  // ---- parts: each target's array cut at chunk boundaries; element i belongs to the chunk
+  //      holding its last byte
+  struct Part { uint64_t t, b, e, step; };
+  std::vector<Part> parts;
+  const uint64_t e = uint64_t(w->elem);
+  for (uint64_t i = 0; i < nt; ++i) {
+    const int64_t a = desc->h_targets[i];
+    const uint64_t off = t->arr_off[a], n = t->arr_count[a];
+    if (n == 0) continue;
+    const uint64_t end = off + e * n;
+    // first element whose last byte lies at or after byte x
+    auto first_i = [&](uint64_t x) -> uint64_t {
+      if (x <= off + e - 1) return 0;
+      return std::min(n, (x - (off + e - 1) + e - 1) / e);
+    };
+    const uint64_t c_first = chunk_of(b, off + e - 1), c_last = chunk_of(b, end - 1);
+    for (uint64_t c = c_first; c <= c_last; ++c) {
+      const uint64_t i0 = first_i(b[c]);
+      const uint64_t i1 = (c == c_last) ? n : first_i(b[c + 1]);
+      if (i1 <= i0) continue;
+      const uint64_t step = std::max(c, ready[i]);
+      parts.push_back({i, i0, i1, step});
+      max_step[i] = std::max(max_step[i], step);
+      // every chunk this piece touches is copied back no earlier than its step
+      const uint64_t cb = chunk_of(b, off + e * i0), ce = chunk_of(b, off + e * i1 - 1);
+      for (uint64_t x = cb; x <= ce; ++x) release[x] = std::max(release[x], step);
+    }
+  }
+  const bool chase = desc->mode == CF_MODE_CHASE;
+  for (uint64_t i = 0; i < nt; ++i)
+    for (uint64_t c : field_chunks[i])
+      release[c] = std::max(release[c], chase ? std::max(ready[i], max_step[i]) : ready[i]);
+
+  // ---- order targets by ready step, parts by step, detach sites by release step
+  std::vector<uint64_t> torder(nt);
+  std::iota(torder.begin(), torder.end(), 0);
+  std::stable_sort(torder.begin(), torder.end(), [&](uint64_t x, uint64_t y) { return ready[x] < ready[y]; });
+  std::vector<uint64_t> tpos(nt);
+  for (uint64_t k = 0; k < nt; ++k) tpos[torder[k]] = k;
+  w->res_lo.assign(nch + 1, 0);
+  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
+    while (k < nt && ready[torder[k]] < c) ++k;
+    w->res_lo[c] = k;
+  }
+  std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) { return x.step < y.step; });
+  w->part_lo.assign(nch + 1, 0);
+  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
+    while (k < parts.size() && parts[k].step < c) ++k;
+    w->part_lo[c] = k;
+  }
+  w->tile_base.resize(parts.size() + 1);
+  w->tile_base[0] = 0;
+  for (size_t k = 0; k < parts.size(); ++k)
+    w->tile_base[k + 1] = w->tile_base[k] + tiles_for(parts[k].e - parts[k].b, w->elem);
+  std::vector<uint64_t> det(nsites);
+  {
+    std::vector<uint64_t> sidx(nsites);
+    std::iota(sidx.begin(), sidx.end(), 0);
+    std::vector<uint64_t> srel(nsites);
+    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[chunk_of(b, sites[s])];
+    std::stable_sort(sidx.begin(), sidx.end(), [&](uint64_t x, uint64_t y) { return srel[x] < srel[y]; });
+    w->det_lo.assign(nch + 1, 0);
+    for (uint64_t c = 0, k = 0; c <= nch; ++c) {
+      while (k < nsites && srel[sidx[k]] < c) ++k;
+      w->det_lo[c] = k;
+    }
+    for (uint64_t k = 0; k < nsites; ++k) det[k] = sites[sidx[k]];
+  }
+  w->released.assign(nch, {});
+  for (uint64_t c = 0; c < nch; ++c) w->released[release[c]].push_back(uint32_t(c));
+
+  // ---- table block: sites | det | level | ordinal | parts | tile_base
+  auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
+  w->off_sites = 0;
+  w->off_det = al8(w->off_sites + nsites * 8);
+  w->off_level = al8(w->off_det + nsites * 8);
+  w->off_ord = al8(w->off_level + nt * 4);
+  w->off_parts = al8(w->off_ord + nt * 8);
+  w->off_tb = al8(w->off_parts + parts.size() * 24);
+  w->tab_bytes = al8(w->off_tb + (parts.size() + 1) * 8);
+  cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
+  if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
+  if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
+  if (ce == cudaSuccess) ce = cudaMalloc(&w->d_count, std::max<uint64_t>(nt, 1) * 4);
+  if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "window tables: %s", cudaGetErrorString(ce)); }
+  memcpy(w->h_tab + w->off_sites, sites, nsites * 8);
+  memcpy(w->h_tab + w->off_det, det.data(), nsites * 8);
+  int32_t* lv = reinterpret_cast<int32_t*>(w->h_tab + w->off_level);
+  uint64_t* od = reinterpret_cast<uint64_t*>(w->h_tab + w->off_ord);
+  for (uint64_t k = 0; k < nt; ++k) {
+    const int64_t a = desc->h_targets[torder[k]];
+    lv[k] = t->arr_level[a];
+    od[k] = t->arr_ordinal[a];
+  }
+  uint64_t* pp = reinterpret_cast<uint64_t*>(w->h_tab + w->off_parts);
+  for (size_t k = 0; k < parts.size(); ++k) {
+    pp[3 * k] = tpos[parts[k].t];
+    pp[3 * k + 1] = parts[k].b;
+    pp[3 * k + 2] = parts[k].e;
+  }
+  memcpy(w->h_tab + w->off_tb, w->tile_base.data(), (parts.size() + 1) * 8);
+  // the device mirror starts valid so runs without CF_WIN_TABLES work
+  ce = cudaMemcpy(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "table upload: %s", cudaGetErrorString(ce)); }
+
+  // ---- events
+  auto mk = [](cudaEvent_t* e, unsigned f) { return cudaEventCreateWithFlags(e, f); };
+  w->ev_h2d.resize(nch);
+  w->ev_rel.resize(nch);
+  w->ev_k0.resize(nch);
+  w->ev_k1.resize(nch);
+  bool ok = mk(&w->ev_start, cudaEventDefault) == cudaSuccess && mk(&w->ev_end, cudaEventDefault) == cudaSuccess &&
+            mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess;
+  for (uint64_t c = 0; c < nch && ok; ++c)
+    ok = mk(&w->ev_h2d[c], cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_rel[c], cudaEventDisableTiming) == cudaSuccess &&
+         mk(&w->ev_k0[c], cudaEventDefault) == cudaSuccess && mk(&w->ev_k1[c], cudaEventDefault) == cudaSuccess;
+  if (!ok) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "event creation failed"); }
+  *out = w;
+  return CF_OK;
+}
+
+int cf_window_set_scale(cf_window* w, double scale) {
+  if (!w) return fail(CF_E_INVALID, "null window");
+  w->d.scale = scale;
+  return CF_OK;
+}
+
+int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
+  if (!w) return fail(CF_E_INVALID, "null window");
+  cf_ctx* c = w->ctx;
+  CfDevice g(c);
+  const cf_window_desc& d = w->d;
+  const uint32_t fl = d.flags;
+  const uint64_t nch = w->bounds.size() - 1;
+  const uint64_t launches0 = c->launches.load();
+  uint8_t* img = static_cast<uint8_t*>(d.image);
+  const uint8_t* src = static_cast<const uint8_t*>(d.host_src);
+  uint8_t* dst = static_cast<uint8_t*>(d.host_dst);
+  const uint64_t dimg = reinterpret_cast<uint64_t>(d.image);
+  cudaStream_t cs = c->compute;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  const bool timing = sync != 0 && st != nullptr;
+
+  CF_CUDA(cudaEventRecord(w->ev_start, cs));
+  for (auto s : c->h2d) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
+  CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_start, 0));
+  if (fl & CF_WIN_TABLES) {
+    CF_CUDA(cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, cs));
+    h2d_bytes += w->tab_bytes;
+  }
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, cs));
+  const uint64_t* dsites = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_sites);
+  const uint64_t* ddet = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_det);
+  const int32_t* dlv = reinterpret_cast<const int32_t*>(w->d_tab + w->off_level);
+  const uint64_t* dod = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_ord);
+  const uint64_t* dparts = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_parts);
+  const uint64_t* dtb = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
+  const bool chase = d.mode == CF_MODE_CHASE;
+
+  for (uint64_t k = 0; k < nch; ++k) {
+    const uint64_t lo = w->bounds[k], hi = w->bounds[k + 1];
+    if (fl & CF_WIN_H2D) {
+      cudaStream_t s = c->h2d[k % c->h2d.size()];
+      CF_CUDA(cudaMemcpyAsync(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
+      CF_CUDA(cudaEventRecord(w->ev_h2d[k], s));
+      CF_CUDA(cudaStreamWaitEvent(cs, w->ev_h2d[k], 0));
+      h2d_bytes += hi - lo;
+    }
+    if (fl & CF_WIN_ATTACH)
+      CF_TRY(launch_relocate(c, img, w->bounds.back(), dsites + w->reloc_lo[k],
+                             w->reloc_lo[k + 1] - w->reloc_lo[k], d.host_base, dimg, c->d_bad, cs));
+    if ((fl & CF_WIN_RESOLVE) && !chase)
+      CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], w->res_lo[k + 1] - w->res_lo[k],
+                            w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
+    if (fl & CF_WIN_SCALE) {
+      const uint64_t p0 = w->part_lo[k], p1 = w->part_lo[k + 1];
+      if (p1 > p0) {
+        if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
+        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, dparts + 3 * p0, p1 - p0,
+                            dtb + p0, w->tile_base[p0], w->tile_base[p1], d.scale, c->d_bad, cs));
+        if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
+      }
+    }
+    if (fl & CF_WIN_DETACH)
+      CF_TRY(launch_relocate(c, img, w->bounds.back(), ddet + w->det_lo[k], w->det_lo[k + 1] - w->det_lo[k], dimg,
+                             d.host_base, c->d_bad, cs));
+    if ((fl & CF_WIN_D2H) && !w->released[k].empty()) {
+      CF_CUDA(cudaEventRecord(w->ev_rel[k], cs));
+      CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_rel[k], 0));
+      for (uint32_t r : w->released[k]) {
+        const uint64_t rlo = w->bounds[r], rhi = w->bounds[r + 1];
+        CF_CUDA(cudaMemcpyAsync(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
+        d2h_bytes += rhi - rlo;
+      }
+    }
+  }
+  // join the copy streams back into the compute stream
+  for (auto s : c->h2d) {
+    CF_CUDA(cudaEventRecord(w->ev_join, s));
+    CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
+  }
+  CF_CUDA(cudaEventRecord(w->ev_join, c->d2h));
+  CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
+  // the error word is the step's result read back to the host
+  CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, cs));
+  d2h_bytes += 8;
+  CF_CUDA(cudaEventRecord(w->ev_end, cs));
+  if (!sync) return CF_OK;
+  CF_CUDA(cudaEventSynchronize(w->ev_end));
+  const uint64_t bad = c->h_bad[0];
+  if (st) {
+    memset(st, 0, sizeof *st);
+    CF_CUDA(cudaEventElapsedTime(&st->ms_total, w->ev_start, w->ev_end));
+    float ks = 0;
+    for (uint64_t k = 0; k < nch; ++k) {
+      if (!(fl & CF_WIN_SCALE) || w->part_lo[k + 1] == w->part_lo[k]) continue;
+      float ms = 0;
+      CF_CUDA(cudaEventElapsedTime(&ms, w->ev_k0[k], w->ev_k1[k]));
+      ks += ms;
+    }
+    st->ms_kernel = ks;
+    st->h2d_bytes = h2d_bytes;
+    st->d2h_bytes = d2h_bytes;
+    st->launches = c->launches.load() - launches0;
+    st->bad = bad;
+    st->nchunks = nch;
+    st->nsteps = nch;
+  }
+  if (bad != NO_BAD)
+    return fail(CF_E_OUTSIDE_ARENA, "window: relocation/resolve/scale reported index %llu", (unsigned long long)bad);
+  return CF_OK;
+}
+
+int cf_window_free(cf_window* w) {
+  destroy(w);
+  return CF_OK;
+}
+
+}  // extern "C"

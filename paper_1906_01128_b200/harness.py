@@ -1,0 +1,453 @@
+"""End-to-end execution of one benchmark case per transfer scheme, on a B200.
+
+Drop-in for the reference harness (harness.py:1-427).  The metered window
+(``transfer_to_device -> kernel_scale -> copy_back``, harness.py:369-373) runs on the GPU:
+
+* ``marshalling``  pinned arena -> chunked multi-stream H2D -> relocation kernel per chunk;
+                   device pointerchain resolve + leaf kernel; detach kernel -> D2H.
+* ``naive``        one batched per-object copy submission + interval-map fix-up kernel.
+* ``pointerchain`` host-resolved selective copies of the targeted arrays (the reference's
+                   semantics, harness.py:228-238) + resolved leaf kernel.
+* ``uvm``          the tree lives in cudaMallocManaged memory; the kernels walk it in place.
+
+The logical counters (bytes, ops, attaches, page faults) and the simulated cost-model columns
+are computed exactly as the reference does, so rows stay comparable; measured wall time of
+the window is added (``wall_us``).  Leaf-kernel modes: ``mode="resolved"`` (effective address
+from the resolve kernel) or ``mode="chase"`` (chain re-walked per access).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import statistics
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .errors import SchemeError, VerificationFailed
+from .memory import DATA_OP_KINDS, AddressMap, Arena, Machine
+from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, LinearSpec,
+                        TreeHandle, build_tree, marshal_tree, payload_values, targeted_arrays)
+
+SCHEMES = ("uvm", "marshalling", "pointerchain", "naive")
+MODES = ("resolved", "chase")
+
+# single-loop kernel instruction model of the reference (harness.py:38-43)
+KERNEL_BASE_INSTRUCTIONS = 60
+PLAIN_STEP_INSTRUCTIONS = 2
+INDEXED_STEP_INSTRUCTIONS = 6
+FINAL_ARRAY_LOAD_INSTRUCTIONS = 2
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Constants turning counted events into the reference's simulated times.
+
+    Kept so ``sim_*`` columns stay comparable with the reference; the B200 backend reports
+    measured times beside them.
+    """
+
+    latency_us_per_op: float = 10.0
+    bandwidth_gib_s: float = 12.0
+    page_size: int = 4096
+    elem_op_ns: float = 0.5
+    deref_ns: float = 5.0
+    l2_bytes: int = 6 << 20
+    spill_penalty: float = 3.0
+
+    def __post_init__(self):
+        positive = ("latency_us_per_op", "bandwidth_gib_s", "page_size", "elem_op_ns", "deref_ns", "l2_bytes")
+        bad = [k for k in positive if not getattr(self, k) > 0]
+        if bad:
+            raise ValueError(f"{bad[0]} must be positive")
+        if self.spill_penalty < 1:
+            raise ValueError("spill_penalty must be >= 1")
+
+    @classmethod
+    def from_file(cls, path) -> "CostModel":
+        """Overrides from `key = value` lines; '#' starts a comment."""
+        kw = {}
+        for line in Path(path).read_text().splitlines():
+            text = line.split("#", 1)[0].strip()
+            if not text:
+                continue
+            key, _, val = (p.strip() for p in text.partition("="))
+            fld = cls.__dataclass_fields__.get(key)
+            if fld is None:
+                raise ValueError(f"unknown cost-model key {key!r}")
+            kw[key] = int(val) if fld.type in ("int", int) else float(val)
+        return cls(**kw)
+
+
+P100_COST_MODEL = CostModel(l2_bytes=4 << 20)
+
+
+@dataclass(frozen=True)
+class ChainShape:
+    steps: tuple = ()
+    count_final_array_load: bool = False
+
+
+def chain_shape(spec, scheme: str) -> ChainShape:
+    if scheme == "pointerchain":
+        return ChainShape()
+    if isinstance(spec, LinearSpec):
+        return ChainShape(("plain",) * (spec.k - 1), False)
+    return ChainShape(("indexed",) * spec.depth, True)
+
+
+def estimate_instructions(shape: ChainShape) -> int:
+    per = {"indexed": INDEXED_STEP_INSTRUCTIONS, "plain": PLAIN_STEP_INSTRUCTIONS}
+    total = KERNEL_BASE_INSTRUCTIONS + sum(per.get(s, PLAIN_STEP_INSTRUCTIONS) for s in shape.steps)
+    return total + (FINAL_ARRAY_LOAD_INSTRUCTIONS if shape.count_final_array_load else 0)
+
+
+@dataclass
+class RunMetrics:
+    scenario: str
+    scheme: str
+    layout: str
+    k_or_q: int
+    n: int
+    bytes_h2d: int = 0
+    bytes_d2h: int = 0
+    transfer_ops: int = 0
+    attach_ops: int = 0
+    page_faults: int = 0
+    instr_estimate: int = 0
+    sim_kernel_us: float = 0.0
+    sim_wall_us: float = 0.0
+    iterations: int = 1
+    verified: bool = False
+    # measured on the B200 (not in the reference)
+    wall_us: float = 0.0
+    mode: str = "resolved"
+    gpu_launches: int = 0
+
+    def sort_key(self):
+        return (self.scenario, self.scheme, self.layout, self.k_or_q, self.n)
+
+
+@dataclass
+class KernelStats:
+    elements_touched: int = 0
+    chain_derefs: int = 0
+
+
+@dataclass
+class RepeatResult:
+    mean: float
+    iterations: int
+    converged: bool
+
+
+def adaptive_repeat(run_closure, min_iters: int = 3, cv_threshold: float = 0.02,
+                    max_iters: int = 100) -> RepeatResult:
+    """Repeat until the coefficient of variation settles (harness.py:165-185 semantics)."""
+    if min_iters < 3:
+        raise ValueError("min_iters must be >= 3")
+    samples = [float(run_closure()) for _ in range(min_iters)]
+    while True:
+        mean = statistics.fmean(samples)
+        cv = 0.0 if mean == 0 else statistics.pstdev(samples) / abs(mean)
+        if cv < cv_threshold:
+            return RepeatResult(mean, len(samples), True)
+        if len(samples) >= max_iters:
+            return RepeatResult(mean, len(samples), False)
+        samples.append(float(run_closure()))
+
+
+def simulate_times(entries, elements_touched: int, chain_derefs: int, cost_model: CostModel,
+                   working_set_bytes: int) -> tuple[float, float]:
+    """Deterministic (kernel_us, wall_us) of the reference cost model (harness.py:188-205)."""
+    cm = cost_model
+    penalty = cm.spill_penalty if working_set_bytes > cm.l2_bytes else 1.0
+    kernel_us = (elements_touched * cm.elem_op_ns * penalty + chain_derefs * cm.deref_ns) / 1000.0
+    us_per_byte = 1e6 / (cm.bandwidth_gib_s * (1 << 30))
+    if isinstance(entries, tuple):  # (dirs, kinds, bytes) columns of data-moving entries
+        _, _, nbytes = entries
+        wall = kernel_us
+        for b in nbytes.tolist():   # same summation order as the reference
+            wall += cm.latency_us_per_op + b * us_per_byte
+        return kernel_us, wall
+    wall = kernel_us
+    for e in entries:
+        if e.op_kind in DATA_OP_KINDS:
+            wall += cm.latency_us_per_op + e.bytes * us_per_byte
+    return kernel_us, wall
+
+
+# -- scheme execution ---------------------------------------------------------
+
+@dataclass
+class DevicePrep:
+    scheme: str
+    device_root: int = 0
+    buffers: list = field(default_factory=list)  # (device_addr, ArrayRef)
+    arena: Arena | None = None
+    amap: AddressMap | None = None
+    policy: str = "ref"
+    image: int = 0
+    image_bytes: int = 0
+
+
+def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena: Arena | None = None,
+                       policy: str = "ref") -> DevicePrep:
+    if scheme == "marshalling":
+        if arena is None:
+            raise ValueError("marshalling needs the arena returned by marshal_tree")
+        image = machine.marshal_transfer_and_attach(arena)
+        return DevicePrep(scheme, device_root=image + (handle.root_addr - arena.buffer_host_addr), arena=arena,
+                          policy=policy, image=image, image_bytes=arena.total_bytes)
+    if scheme == "naive":
+        root, amap = machine.naive_deep_copy(handle)
+        base, span = machine._naive_span
+        return DevicePrep(scheme, device_root=root, amap=amap, policy=policy, image=base, image_bytes=span)
+    if scheme == "pointerchain":
+        buffers = []
+        for ref in targeted_arrays(handle, policy):
+            if ref.count == 0:
+                continue
+            nbytes = ref.count * handle.spec.elem
+            dev = machine.device.allocate(nbytes)
+            machine.transfer_range(machine.host, ref.addr, machine.device, dev, nbytes, "bulk")
+            buffers.append((dev, ref))
+        return DevicePrep(scheme, buffers=buffers, policy=policy)
+    if scheme == "uvm":
+        return DevicePrep(scheme, device_root=handle.root_addr, policy=policy, image=handle.base,
+                          image_bytes=handle.total_bytes)
+    raise SchemeError(f"unknown transfer scheme {scheme!r}")
+
+
+def _reference_derefs(handle: TreeHandle, policy: str, idx: np.ndarray) -> int:
+    """chain_derefs exactly as the reference walk counts them (harness.py:264-304)."""
+    spec = handle.spec
+    if policy == "ref":
+        if isinstance(spec, LinearSpec):
+            return (spec.k if spec.all_levels_used else 1) + (spec.k - 1)
+        return spec.depth + 1
+    return int((handle.arr_level[idx].astype(np.int64) + 1).sum())
+
+
+def _level_nodes(handle: TreeHandle, level: int) -> np.ndarray:
+    return handle.node_off[handle.node_level == level]
+
+
+def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int) -> tuple[set, set]:
+    """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394).
+
+    Used for the logical page-fault counters; the data itself migrates under the CUDA driver.
+    """
+    spec = handle.spec
+    base, e = handle.base, spec.elem
+    linear = isinstance(spec, LinearSpec)
+    q = 1 if linear else spec.q
+    owner = {int(o): (int(a), int(c)) for o, a, c in zip(handle.arr_owner, handle.arr_off, handle.arr_count)}
+    touched, dirty = set(), set()
+
+    def node_at(level: int, ordinal: int) -> int:
+        return int(_level_nodes(handle, level)[ordinal])
+
+    def visit_terminal(node: int, a_off: int) -> None:
+        touched.add((base + node + a_off) // page)
+        arr = owner.get(node)
+        if arr and arr[1]:
+            a, n = base + arr[0], arr[1]
+            touched.add((base + node + OFF_NA) // page)
+            pages = range(a // page, (a + e * (n - 1)) // page + 1)
+            touched.update(pages)
+            dirty.update(pages)
+
+    if policy == "ref" and linear:
+        for level in range(spec.k):
+            node = node_at(level, 0)
+            if spec.all_levels_used or level == spec.k - 1:
+                visit_terminal(node, OFF_A)
+            if level < spec.k - 1:
+                touched.add((base + node + OFF_LNEXT) // page)
+    elif policy == "ref":
+        for level in range(spec.depth):
+            touched.add((base + node_at(level, q ** level - 1) + OFF_LNEXT) // page)
+        visit_terminal(node_at(spec.depth, q ** spec.depth - 1), LEAF_OFF_A)
+    else:
+        for i in idx.tolist():
+            L, ordv = int(handle.arr_level[i]), int(handle.arr_ordinal[i])
+            for lv in range(L):
+                touched.add((base + node_at(lv, 0 if linear else ordv // q ** (L - lv)) + OFF_LNEXT) // page)
+            leaf = (not linear) and L == spec.depth
+            visit_terminal(node_at(L, 0 if linear else ordv), LEAF_OFF_A if leaf else OFF_A)
+    return touched, dirty
+
+
+def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: float,
+                 mode: str = "resolved") -> KernelStats:
+    """Scale the targeted arrays where the scheme left them, on the GPU."""
+    if mode not in MODES:
+        raise ValueError(f"unknown kernel mode {mode!r}")
+    stats = KernelStats()
+    elem = handle.spec.elem
+    ctx = machine.ctx.handle
+    if prep.scheme == "pointerchain":
+        if prep.buffers:
+            ea = np.array([d for d, _ in prep.buffers], np.uint64)
+            cnt = np.array([r.count for _, r in prep.buffers], np.uint64)
+            N.check(N.lib().cf_scale_resolved(ctx, elem, N.ptr(ea), N.ptr(cnt), len(ea), float(scale)),
+                    "kernel_scale")
+            stats.elements_touched = int(cnt.sum())
+        return stats
+
+    idx = handle.target_indices(prep.policy)
+    idx = idx[handle.arr_count[idx] > 0]
+    stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
+    if prep.scheme == "uvm":
+        touched, dirty = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
+        machine.uvm_touch_pages(sorted(touched), "read", "device")
+        for p in dirty:
+            machine.uvm.page_table[p].dirty = True
+    if len(idx) == 0:
+        return stats
+    sh = handle.chain_shape()
+    sh.root_off = prep.device_root - prep.image
+    sh.image_bytes = prep.image_bytes
+    lv = np.ascontiguousarray(handle.arr_level[idx], np.int32)
+    od = np.ascontiguousarray(handle.arr_ordinal[idx], np.uint64)
+    cnt = np.ascontiguousarray(handle.arr_count[idx], np.uint64)
+    bad = N.U64(0)
+    rc = N.lib().cf_kernel_scale(ctx, elem, N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
+                                 prep.image, C.byref(sh), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
+                                 float(scale), None, C.byref(bad))
+    N.check(rc, "kernel_scale")
+    stats.elements_touched = int(cnt.sum())
+    return stats
+
+
+def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
+    if prep.scheme == "marshalling":
+        machine.demarshal(prep.arena)
+    elif prep.scheme == "naive":
+        machine.naive_copy_back(handle, prep.amap)
+    elif prep.scheme == "pointerchain":
+        for dev, ref in prep.buffers:
+            machine.transfer_range(machine.device, dev, machine.host, ref.addr, ref.count * handle.spec.elem, "bulk")
+    elif prep.scheme == "uvm":
+        machine.ctx.sync()
+        dirty = machine.uvm.dirty_pages()
+        machine.uvm_touch_pages(dirty, "read", "host")
+
+
+def verify_tree(machine: Machine, handle: TreeHandle, scale: float, policy: str = "ref") -> None:
+    """Check every element and pointer field on the host after copy-back (harness.py:328-345)."""
+    spec = handle.spec
+    e = spec.elem
+    dt = np.dtype("<f8") if e == 8 else np.dtype("<f4")
+    view = N.host_view(handle.base, handle.total_bytes)
+    targeted = np.zeros(len(handle.arr_off), bool)
+    targeted[handle.target_indices(policy)] = True
+    s = np.float64(scale) if e == 8 else np.float32(scale)
+    for lv in np.unique(handle.arr_level).tolist() if len(handle.arr_level) else []:
+        sel = np.nonzero(handle.arr_level == lv)[0]
+        for flag in (False, True):
+            group = sel[targeted[sel] == flag]
+            if len(group) == 0:
+                continue
+            for n in np.unique(handle.arr_count[group]).tolist():
+                if n == 0:
+                    continue
+                g = group[handle.arr_count[group] == n]
+                expected = payload_values(handle.seed, lv, n, e)
+                if flag:
+                    expected = (expected * s).astype(dt)
+                exp_bytes = np.frombuffer(expected.astype(dt).tobytes(), np.uint8)
+                nb = n * e
+                step = max(1, (64 << 20) // max(nb, 1))
+                for c0 in range(0, len(g), step):
+                    offs = handle.arr_off[g[c0:c0 + step]].astype(np.int64)
+                    got = view[offs[:, None] + np.arange(nb, dtype=np.int64)[None, :]]
+                    rows = np.nonzero((got != exp_bytes[None, :]).any(axis=1))[0]
+                    if len(rows):
+                        a = handle.base + int(offs[rows[0]])
+                        raise VerificationFailed(f"array at 0x{a:x} (level {lv}) does not match")
+    fields, targets = handle.site_off.astype(np.int64), handle.site_target + np.uint64(handle.base)
+    if len(fields):
+        got = view[fields[:, None] + np.arange(8, dtype=np.int64)[None, :]].copy().view("<u8").ravel()
+        bad = np.nonzero(got != targets)[0]
+        if len(bad):
+            raise VerificationFailed(f"pointer field at 0x{handle.base + int(fields[bad[0]]):x} not restored")
+
+
+# -- one full case -------------------------------------------------------------
+
+def _describe(spec) -> tuple[str, str, int, int]:
+    if isinstance(spec, LinearSpec):
+        return "linear", spec.layout, spec.k, spec.n
+    return "dense", "dense", spec.q, spec.n
+
+
+def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale: float = 2.0,
+                 mode: str = "resolved", policy: str = "ref", align: int | None = None,
+                 device: int = 0) -> tuple[RunMetrics, Machine]:
+    """Run one case once on the GPU; returns the metrics and the machine (for its log)."""
+    if scheme not in SCHEMES:
+        raise SchemeError(f"unknown transfer scheme {scheme!r}")
+    machine = Machine(page_size=cost_model.page_size, device=device)
+    if scheme == "uvm":
+        machine.enable_uvm(cost_model.page_size)
+    arena = None
+    if scheme == "marshalling":
+        arena, handle = marshal_tree(machine, spec, seed=seed, align=align or 1)
+    else:
+        handle = build_tree(machine, spec, seed=seed, align=align)
+    launches0 = machine.ctx.launches()
+    mark = machine.log.mark()
+    t0 = time.perf_counter()
+    prep = transfer_to_device(machine, handle, scheme, arena, policy=policy)
+    stats = kernel_scale(machine, handle, prep, scale, mode=mode)
+    copy_back(machine, handle, prep)
+    machine.ctx.sync()
+    wall_us = (time.perf_counter() - t0) * 1e6
+    kernel_us, sim_wall = simulate_times(machine.log.data_entries_since(mark), stats.elements_touched,
+                                         stats.chain_derefs, cost_model, handle.served_bytes)
+    verify_tree(machine, handle, scale, policy)  # outside the metered window
+    scenario, layout, k_or_q, n = _describe(spec)
+    metrics = RunMetrics(
+        scenario=scenario, scheme=scheme, layout=layout, k_or_q=k_or_q, n=n,
+        bytes_h2d=machine.log.bytes_moved("H2D", mark), bytes_d2h=machine.log.bytes_moved("D2H", mark),
+        transfer_ops=machine.log.data_ops(mark), attach_ops=machine.log.count("attach", mark),
+        page_faults=machine.log.count("page_migration", mark),
+        instr_estimate=estimate_instructions(chain_shape(spec, scheme)),
+        sim_kernel_us=kernel_us, sim_wall_us=sim_wall, iterations=1, verified=True,
+        wall_us=wall_us, mode=mode, gpu_launches=machine.ctx.launches() - launches0)
+    return metrics, machine
+
+
+def run_case(spec, scheme: str, cost_model: CostModel | None = None, seed: int = 0, scale: float = 2.0,
+             min_iters: int = 3, cv_threshold: float = 0.02, max_iters: int = 50,
+             mode: str = "resolved", policy: str = "ref") -> RunMetrics:
+    """Execute one cell with adaptive repetition over the simulated wall time (as the reference)."""
+    if scheme not in SCHEMES:
+        raise SchemeError(f"unknown transfer scheme {scheme!r}")
+    cm = cost_model or CostModel()
+    runs: list[RunMetrics] = []
+
+    def one_run():
+        metrics, machine = execute_case(spec, scheme, cm, seed, scale, mode=mode, policy=policy)
+        machine.close()
+        runs.append(metrics)
+        return metrics.sim_wall_us
+
+    result = adaptive_repeat(one_run, min_iters, cv_threshold, max_iters)
+    metrics = runs[-1]
+    metrics.sim_wall_us = result.mean
+    metrics.sim_kernel_us = statistics.fmean(r.sim_kernel_us for r in runs)
+    metrics.wall_us = statistics.fmean(r.wall_us for r in runs)
+    metrics.iterations = result.iterations
+    return metrics
+
+
+def sweep(cases, cost_model: CostModel | None = None, seed: int = 0, min_iters: int = 3) -> list[RunMetrics]:
+    """Run (spec, scheme) pairs and merge results in deterministic order."""
+    rows = [run_case(spec, scheme, cost_model, seed=seed, min_iters=min_iters) for spec, scheme in cases]
+    rows.sort(key=RunMetrics.sort_key)
+    return rows

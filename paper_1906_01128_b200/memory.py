@@ -1,0 +1,681 @@
+"""Host and device memory spaces backed by real pinned memory and HBM.
+
+Drop-in for the reference's simulated machine (memory.py:1-419): same class and method names,
+argument meaning and exceptions, but a ``Machine`` owns a B200 context, its host space is
+pinned (``cudaHostAlloc``) or managed (UVM mode) memory, its device space is HBM, and every
+transfer, attach and detach is executed by libchainforge_b200 (multi-stream copies and sm_100a
+relocation kernels).  The transfer log keeps the reference's *logical* accounting
+(memory.py:60-98): one marshalled arena is one ``bulk`` entry however many streams carried
+it, and each relocated site is one ``attach`` entry.
+
+Addresses are real virtual addresses.  Bounds are still enforced per allocation (WildAccess),
+so a fix-up that escapes the arena fails loudly as in the reference.
+"""
+from __future__ import annotations
+
+import bisect
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import (AttachOutsideArena, OutOfSimMemory, SimMemoryError,  # noqa: F401
+                     WildAccess)
+
+HOST_BASE = 0x1000_0000        # reference constants (memory.py:27-35), kept for API parity
+DEVICE_BASE = 0xD0_0000_0000
+DEFAULT_CAPACITY = 8 << 30
+ALIGNMENT = 8
+NULL_ADDR = 0
+DEFAULT_PAGE_SIZE = 4096
+
+H2D = "H2D"
+D2H = "D2H"
+DATA_OP_KINDS = ("bulk", "per_object", "page_migration")
+
+_DIRS = (H2D, D2H)
+_KINDS = ("bulk", "per_object", "page_migration", "attach", "detach")
+_DATA_KIND_IDS = (0, 1, 2)
+
+# marshalled arenas are uploaded in chunks of this many bytes over the context's copy streams
+MARSHAL_CHUNK = 32 << 20
+# host/device spaces carve small allocations out of slabs of this size
+SLAB_BYTES = 64 << 20
+
+
+@dataclass
+class TransferEntry:
+    direction: str
+    op_kind: str
+    bytes: int
+    order: int
+
+
+class TransferLog:
+    """Append-only logical transfer log (memory.py:68-98) stored column-wise.
+
+    A marshalled C4 tree logs a million attach entries; they are kept as numpy columns and
+    appended in bulk, and ``entries`` materialises ``TransferEntry`` objects only on demand.
+    """
+
+    def __init__(self):
+        self._dir = np.zeros(0, np.uint8)
+        self._kind = np.zeros(0, np.uint8)
+        self._bytes = np.zeros(0, np.int64)
+        self._pending: list = []  # small appends, folded lazily
+
+    def _fold(self) -> None:
+        if self._pending:
+            d, k, b = zip(*self._pending)
+            self._dir = np.concatenate([self._dir, np.array(d, np.uint8)])
+            self._kind = np.concatenate([self._kind, np.array(k, np.uint8)])
+            self._bytes = np.concatenate([self._bytes, np.array(b, np.int64)])
+            self._pending = []
+
+    def append(self, direction: str, op_kind: str, nbytes: int) -> None:
+        if nbytes <= 0:
+            raise ValueError("log entries must move at least one byte")
+        self._pending.append((_DIRS.index(direction), _KINDS.index(op_kind), int(nbytes)))
+
+    def append_many(self, direction: str, op_kind: str, nbytes) -> None:
+        """Append one entry per element of ``nbytes`` (an int count pair or an array)."""
+        b = np.asarray(nbytes, dtype=np.int64).ravel()
+        if b.size == 0:
+            return
+        if (b <= 0).any():
+            raise ValueError("log entries must move at least one byte")
+        self._fold()
+        self._dir = np.concatenate([self._dir, np.full(b.size, _DIRS.index(direction), np.uint8)])
+        self._kind = np.concatenate([self._kind, np.full(b.size, _KINDS.index(op_kind), np.uint8)])
+        self._bytes = np.concatenate([self._bytes, b])
+
+    @property
+    def entries(self) -> list[TransferEntry]:
+        self._fold()
+        return [TransferEntry(_DIRS[d], _KINDS[k], int(b), i)
+                for i, (d, k, b) in enumerate(zip(self._dir.tolist(), self._kind.tolist(),
+                                                  self._bytes.tolist()))]
+
+    def mark(self) -> int:
+        self._fold()
+        return int(self._dir.size)
+
+    def since(self, mark: int) -> list[TransferEntry]:
+        return self.entries[mark:]
+
+    def _cols(self, since: int):
+        self._fold()
+        return self._dir[since:], self._kind[since:], self._bytes[since:]
+
+    def bytes_moved(self, direction: str, since: int = 0) -> int:
+        d, k, b = self._cols(since)
+        m = (d == _DIRS.index(direction)) & (k <= 2)
+        return int(b[m].sum())
+
+    def data_ops(self, since: int = 0) -> int:
+        _, k, _ = self._cols(since)
+        return int((k <= 2).sum())
+
+    def count(self, op_kind: str, since: int = 0) -> int:
+        _, k, _ = self._cols(since)
+        return int((k == _KINDS.index(op_kind)).sum())
+
+    def dump(self) -> str:
+        """Stable newline-delimited `direction,op_kind,bytes,order` records."""
+        return "\n".join(f"{e.direction},{e.op_kind},{e.bytes},{e.order}" for e in self.entries)
+
+    def data_entries_since(self, mark: int):
+        """(direction, op_kind, bytes) arrays of data-moving entries (for simulate_times)."""
+        d, k, b = self._cols(mark)
+        m = k <= 2
+        return d[m], k[m], b[m]
+
+
+class _Segment:
+    """A contiguous storage block holding one or many allocations (sorted sub-offsets)."""
+
+    __slots__ = ("base", "size", "offs", "sizes")
+
+    def __init__(self, base: int, size: int, offs=None, sizes=None):
+        self.base = base
+        self.size = size
+        self.offs = np.zeros(1, np.uint64) if offs is None else offs
+        self.sizes = np.array([size], np.uint64) if sizes is None else sizes
+
+    def locate(self, addr: int, nbytes: int):
+        rel = addr - self.base
+        if rel < 0 or rel + nbytes > self.size:
+            return None
+        i = int(np.searchsorted(self.offs, np.uint64(rel), side="right")) - 1
+        if i < 0:
+            return None
+        if rel + nbytes <= int(self.offs[i]) + int(self.sizes[i]):
+            return i
+        return None
+
+
+class MemorySpace:
+    """One memory space with a bump allocator over real storage (memory.py:101-190).
+
+    kind="host": pinned host memory (managed memory once the machine is in UVM mode; pageable
+    memory when no GPU is visible, which only the host-side builder uses).
+    kind="device": HBM of the machine's GPU.
+    Storage is taken in slabs; allocations are 8-byte aligned and adjacent within a slab.
+    """
+
+    def __init__(self, kind: str, machine: "Machine" = None, capacity: int = DEFAULT_CAPACITY):
+        if kind not in ("host", "device"):
+            raise ValueError(f"unknown space kind {kind!r}")
+        self.kind = kind
+        self.machine = machine
+        self.capacity = capacity
+        self.bump_offset = 0
+        self._segs: list[_Segment] = []
+        self._seg_bases: list[int] = []
+        self._storage: list[tuple[int, int, int]] = []  # (addr, bytes, memkind)
+        self._slab: tuple[int, int] | None = None        # (addr, bytes)
+        self._slab_used = 0
+        self._last = None
+
+    # -- storage -------------------------------------------------------------------------
+    def _memkind(self) -> int:
+        if self.kind == "device":
+            return -1
+        if self.machine is not None and self.machine.uvm is not None:
+            return N.CF_MEM_MANAGED
+        return N.CF_MEM_PINNED if self.machine is not None and self.machine.has_device else N.CF_MEM_PAGEABLE
+
+    def _raw_alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        kind = self._memkind()
+        if kind < 0:
+            N.check(N.lib().cf_dev_alloc(self.machine.ctx.handle, nbytes, C.byref(p)), "device allocate")
+            N.check(N.lib().cf_memset(self.machine.ctx.handle, p, 0, nbytes))
+        else:
+            N.check(N.lib().cf_host_alloc(nbytes, kind, C.byref(p)), "host allocate")
+        self._storage.append((p.value, nbytes, kind))
+        return p.value
+
+    @property
+    def base(self) -> int:
+        return self._segs[0].base if self._segs else (HOST_BASE if self.kind == "host" else DEVICE_BASE)
+
+    @property
+    def end(self) -> int:
+        return self.base + self.capacity
+
+    def _reserve(self, aligned: int, size_bytes: int) -> None:
+        if self.bump_offset + aligned > self.capacity:
+            raise OutOfSimMemory(
+                f"{self.kind} space exhausted: want {size_bytes} bytes, "
+                f"{self.capacity - self.bump_offset} remain")
+        self.bump_offset += aligned
+
+    def _register(self, seg: _Segment) -> None:
+        i = bisect.bisect_left(self._seg_bases, seg.base)
+        self._seg_bases.insert(i, seg.base)
+        self._segs.insert(i, seg)
+
+    def allocate(self, size_bytes: int) -> int:
+        if size_bytes <= 0:
+            raise ValueError("allocation size must be positive")
+        aligned = (size_bytes + ALIGNMENT - 1) & ~(ALIGNMENT - 1)
+        self._reserve(aligned, size_bytes)
+        if aligned > SLAB_BYTES // 4:
+            addr = self._raw_alloc(aligned)
+        else:
+            if self._slab is None or self._slab_used + aligned > self._slab[1]:
+                self._slab = (self._raw_alloc(SLAB_BYTES), SLAB_BYTES)
+                self._slab_used = 0
+            addr = self._slab[0] + self._slab_used
+            self._slab_used += aligned
+        self._register(_Segment(addr, size_bytes))
+        return addr
+
+    def allocate_span(self, total: int, offs: np.ndarray, sizes: np.ndarray) -> int:
+        """One storage block holding a whole tree's allocations (offsets relative to the block).
+
+        Used by the native builder so a million-object tree is one pinned block while each
+        object stays a separately bounds-checked allocation.
+        """
+        if total <= 0:
+            raise ValueError("allocation size must be positive")
+        aligned = (total + 4095) & ~4095
+        self._reserve((total + ALIGNMENT - 1) & ~(ALIGNMENT - 1), total)
+        addr = self._raw_alloc(aligned)
+        order = np.argsort(offs, kind="stable")
+        self._register(_Segment(addr, total, np.ascontiguousarray(offs[order], np.uint64),
+                                np.ascontiguousarray(sizes[order], np.uint64)))
+        return addr
+
+    def free_all(self) -> None:
+        lib = N._lib
+        for addr, nbytes, kind in self._storage:
+            if lib is None:
+                break
+            if kind < 0:
+                lib.cf_dev_free(self.machine.ctx.handle, addr)
+            else:
+                lib.cf_host_free_sized(addr, nbytes, kind)
+        self._storage.clear()
+        self._segs.clear()
+        self._seg_bases.clear()
+        self._slab = None
+
+    # -- bounds-checked access (memory.py:139-184) ---------------------------------------
+    def _check(self, addr: int, nbytes: int) -> None:
+        seg = self._last
+        if seg is not None and seg.locate(addr, nbytes) is not None:
+            return
+        i = bisect.bisect_right(self._seg_bases, addr) - 1
+        if i >= 0 and self._segs[i].locate(addr, nbytes) is not None:
+            self._last = self._segs[i]
+            return
+        raise WildAccess(f"{self.kind} access at 0x{addr:x} (+{nbytes}) hits no live allocation")
+
+    def contains_range(self, addr: int, nbytes: int) -> bool:
+        try:
+            self._check(addr, nbytes)
+            return True
+        except WildAccess:
+            return False
+
+    def read_bytes(self, addr: int, nbytes: int) -> bytes:
+        self._check(addr, nbytes)
+        if self.kind == "host":
+            return N.read_bytes(addr, nbytes)
+        out = np.empty(nbytes, np.uint8)
+        N.check(N.lib().cf_memcpy(self.machine.ctx.handle, N.ptr(out), addr, nbytes), "read")
+        return out.tobytes()
+
+    def write_bytes(self, addr: int, data: bytes) -> None:
+        self._check(addr, len(data))
+        if self.kind == "host":
+            N.write_bytes(addr, data)
+        else:
+            src = np.frombuffer(bytes(data), np.uint8)
+            N.check(N.lib().cf_memcpy(self.machine.ctx.handle, addr, N.ptr(src), len(data)), "write")
+
+    def read_word(self, addr: int) -> int:
+        return int.from_bytes(self.read_bytes(addr, 8), "little")
+
+    def write_word(self, addr: int, value: int) -> None:
+        self.write_bytes(addr, (value & 0xFFFF_FFFF_FFFF_FFFF).to_bytes(8, "little"))
+
+    def read_u32(self, addr: int) -> int:
+        return int.from_bytes(self.read_bytes(addr, 4), "little")
+
+    def write_u32(self, addr: int, value: int) -> None:
+        self.write_bytes(addr, (value & 0xFFFF_FFFF).to_bytes(4, "little"))
+
+    def read_f64(self, addr: int) -> float:
+        return float(np.frombuffer(self.read_bytes(addr, 8), "<f8")[0])
+
+    def write_f64(self, addr: int, value: float) -> None:
+        self.write_bytes(addr, np.array([value], "<f8").tobytes())
+
+    def allocations(self) -> list[tuple[int, int]]:
+        out = []
+        for s in self._segs:
+            out.extend((s.base + int(o), int(z)) for o, z in zip(s.offs, s.sizes))
+        return out
+
+    def snapshot(self, addr: int, nbytes: int) -> bytes:
+        return self.read_bytes(addr, nbytes)
+
+
+@dataclass
+class AllocationRequest:
+    host_addr: int
+    size_bytes: int
+    order: int
+
+
+class Arena:
+    """One contiguous pinned host buffer serving a whole tree (memory.py:200-230).
+
+    ``align=1`` packs sub-allocations back to back exactly like the reference (the arena size
+    equals the closed form); ``align=16`` is the production layout whose arrays are 16-byte
+    aligned for 128-bit vector access.
+    """
+
+    def __init__(self, space: MemorySpace, total_bytes: int, align: int = 1):
+        self.space = space
+        self.total_bytes = total_bytes
+        self.align = align
+        self.buffer_host_addr = space.allocate(total_bytes)
+        self.served_offset = 0
+        self._req: list = []             # (offset, size) appended by allocate()
+        self._req_arr = None             # numpy (m, 2) set by the native builder
+        self._site_off = np.zeros(0, np.uint64)   # DFS order, relative to the arena
+        self._sorted = None
+        self.device_image_addr = NULL_ADDR
+
+    def allocate(self, size_bytes: int) -> int:
+        if size_bytes <= 0:
+            raise ValueError("allocation size must be positive")
+        off = self.served_offset
+        if self.align > 1:
+            off = (off + self.align - 1) // self.align * self.align
+        if off + size_bytes > self.total_bytes:
+            raise OutOfSimMemory(
+                f"arena exhausted: want {size_bytes} bytes, "
+                f"{self.total_bytes - self.served_offset} remain")
+        self.served_offset = off + size_bytes
+        self._req.append((off, size_bytes))
+        return self.buffer_host_addr + off
+
+    @property
+    def request_list(self) -> list[AllocationRequest]:
+        rows = self._req_arr.tolist() if self._req_arr is not None else self._req
+        return [AllocationRequest(self.buffer_host_addr + int(o), int(z), i)
+                for i, (o, z) in enumerate(rows)]
+
+    @property
+    def pointer_sites(self) -> list[int]:
+        return (self._site_off + np.uint64(self.buffer_host_addr)).tolist()
+
+    @pointer_sites.setter
+    def pointer_sites(self, sites) -> None:
+        arr = np.asarray(list(sites), dtype=np.uint64)
+        self._site_off = arr - np.uint64(self.buffer_host_addr) if arr.size else arr
+        self._sorted = None
+
+    def set_site_offsets(self, site_off: np.ndarray, sorted_off: np.ndarray | None = None) -> None:
+        self._site_off = np.ascontiguousarray(site_off, np.uint64)
+        self._sorted = None if sorted_off is None else np.ascontiguousarray(sorted_off, np.uint64)
+
+    @property
+    def site_offsets(self) -> np.ndarray:
+        return self._site_off
+
+    @property
+    def sorted_site_offsets(self) -> np.ndarray:
+        if self._sorted is None:
+            self._sorted = np.sort(self._site_off)
+        return self._sorted
+
+    def contains(self, addr: int) -> bool:
+        return self.buffer_host_addr <= addr < self.buffer_host_addr + self.total_bytes
+
+
+@dataclass
+class PageState:
+    resident: str  # "host" | "device"
+    dirty: bool = False
+
+
+class UvmState:
+    """Logical page table of the unified-memory mode (memory.py:239-261).
+
+    The real data lives in ``cudaMallocManaged`` memory and migrates under the CUDA driver;
+    this table keeps the reference's single-residence accounting (page_faults, migrations)
+    so RunMetrics stay comparable with the reference.
+    """
+
+    def __init__(self, page_size: int = DEFAULT_PAGE_SIZE):
+        self.page_size = page_size
+        self.page_table: dict[int, PageState] = {}
+
+    def register_range(self, addr: int, size: int) -> None:
+        first = addr // self.page_size
+        last = (addr + size - 1) // self.page_size
+        for page in range(first, last + 1):
+            self.page_table.setdefault(page, PageState("host"))
+
+    def resident_pages(self, side: str) -> list[int]:
+        return sorted(p for p, st in self.page_table.items() if st.resident == side)
+
+    def dirty_pages(self) -> list[int]:
+        return sorted(p for p, st in self.page_table.items() if st.dirty)
+
+
+class Machine:
+    """A pinned host space, an HBM device space, one logical transfer log, optional UVM mode.
+
+    ``device`` selects the GPU; all device work goes through the shared per-process context.
+    Without a visible GPU the machine can still plan and build trees in pageable host memory,
+    but every transfer or kernel raises ``NativeUnavailable``.
+    """
+
+    def __init__(self, capacity: int = DEFAULT_CAPACITY, page_size: int = DEFAULT_PAGE_SIZE,
+                 device: int = 0):
+        self.has_device = N.device_count() > device
+        self._device = device
+        self._ctx = None
+        self.host = MemorySpace("host", self, capacity)
+        self.device = MemorySpace("device", self, capacity)
+        self.log = TransferLog()
+        self.uvm: UvmState | None = None
+        self._default_page_size = page_size
+
+    @property
+    def ctx(self) -> N.DeviceContext:
+        if self._ctx is None:
+            if not self.has_device:
+                raise N.NativeUnavailable("no CUDA device visible: device operations need a B200")
+            self._ctx = N.DeviceContext.get(self._device)
+        return self._ctx
+
+    def space(self, kind: str) -> MemorySpace:
+        return self.host if kind == "host" else self.device
+
+    def alloc_host(self, size_bytes: int) -> int:
+        addr = self.host.allocate(size_bytes)
+        if self.uvm is not None:
+            self.uvm.register_range(addr, size_bytes)
+        return addr
+
+    def enable_uvm(self, page_size: int = None) -> UvmState:
+        self.uvm = UvmState(page_size or self._default_page_size)
+        return self.uvm
+
+    def create_arena(self, total_bytes: int, align: int = 1) -> Arena:
+        return Arena(self.host, total_bytes, align)
+
+    def close(self) -> None:
+        self.host.free_all()
+        self.device.free_all()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- transfers (memory.py:294-303) ------------------------------------------------------
+    def transfer_range(self, src: MemorySpace, src_addr: int, dst: MemorySpace, dst_addr: int,
+                       nbytes: int, op_kind: str = "bulk") -> None:
+        """Copy nbytes between spaces (snapshot semantics) and log one entry."""
+        if src.kind == dst.kind:
+            raise ValueError("transfer_range requires distinct memory spaces")
+        src._check(src_addr, nbytes)
+        dst._check(dst_addr, nbytes)
+        N.check(N.lib().cf_memcpy(self.ctx.handle, dst_addr, src_addr, nbytes), "transfer_range")
+        self.log.append(H2D if dst.kind == "device" else D2H, op_kind, nbytes)
+
+    # -- marshalling (memory.py:307-345) ----------------------------------------------------
+    def marshal_transfer_and_attach(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> int:
+        """Ship the arena in one logical bulk op (chunked over copy streams) and relocate every
+        pointer field on the device as its chunk lands."""
+        image = self.device.allocate(arena.total_bytes)
+        sites = arena.sorted_site_offsets
+        bad = N.U64(0)
+        rc = N.lib().cf_marshal_transfer_and_attach(
+            self.ctx.handle, arena.buffer_host_addr, arena.total_bytes, image, N.ptr(sites),
+            len(sites), chunk_bytes, C.byref(bad))
+        if rc == N.CF_E_OUTSIDE_ARENA:
+            raise AttachOutsideArena(N.last_error())
+        N.check(rc, "marshal_transfer_and_attach")
+        self.log.append(H2D, "bulk", arena.total_bytes)
+        self.log.append_many(H2D, "attach", np.full(len(sites), 8, np.int64))
+        arena.device_image_addr = image
+        return image
+
+    def demarshal(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> None:
+        """Detach on the device (inverse relocation kernel), then bulk copy the image back."""
+        image = arena.device_image_addr
+        if image == NULL_ADDR:
+            raise SimMemoryError("demarshal before marshal_transfer_and_attach")
+        sites = arena.sorted_site_offsets
+        bad = N.U64(0)
+        rc = N.lib().cf_demarshal(self.ctx.handle, arena.buffer_host_addr, arena.total_bytes, image,
+                                  N.ptr(sites), len(sites), chunk_bytes, C.byref(bad))
+        if rc == N.CF_E_OUTSIDE_ARENA:
+            raise AttachOutsideArena(N.last_error())
+        N.check(rc, "demarshal")
+        self.log.append(D2H, "bulk", arena.total_bytes)
+        self.log.append_many(D2H, "detach", np.full(len(sites), 8, np.int64))
+        arena.device_image_addr = NULL_ADDR
+
+    # -- naive per-object deep copy (memory.py:349-374) -------------------------------------
+    def naive_deep_copy(self, tree) -> tuple[int, "AddressMap"]:
+        """Copy every object individually (one batched submission), then fix every pointer
+        field on the device through the sorted interval map."""
+        allocs = tree.allocation_array()          # (m, 2) host addr, size in allocation order
+        m = len(allocs)
+        sizes = allocs[:, 1].astype(np.uint64)
+        aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
+        span = int(aligned.sum())
+        dev_off = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64)
+        dev_base = self.device.allocate_span(span, dev_off, sizes)
+        dev = dev_off + np.uint64(dev_base)
+        host = allocs[:, 0].astype(np.uint64)
+        ctx = self.ctx.handle
+        N.check(N.lib().cf_memcpy_batch(ctx, N.ptr(dev), N.ptr(host), N.ptr(sizes), m, None),
+                "naive per-object copies")
+        amap = AddressMap.from_arrays(host, sizes, dev)
+        fields, targets = tree.site_field_target_arrays()
+        self._device_fixup(amap, fields, targets)
+        self.log.append_many(H2D, "per_object", sizes.astype(np.int64))
+        self.log.append_many(H2D, "attach", np.full(len(fields), 8, np.int64))
+        self._naive_span = (dev_base, span)
+        return amap.translate(tree.root_addr), amap
+
+    def _device_fixup(self, amap: "AddressMap", fields: np.ndarray, targets: np.ndarray) -> None:
+        hb, sz, db = amap.arrays()
+        ctx = self.ctx.handle
+        n = len(fields)
+        if n == 0:
+            return
+        blob = np.concatenate([fields, targets, hb, sz, db, np.array([N.NO_BAD], np.uint64)]).astype(np.uint64)
+        dptr = C.c_void_p()
+        N.check(N.lib().cf_dev_alloc(ctx, blob.nbytes, C.byref(dptr)))
+        try:
+            N.check(N.lib().cf_memcpy(ctx, dptr.value, N.ptr(blob), blob.nbytes))
+            base = dptr.value
+            k = len(hb)
+            N.check(N.lib().cf_naive_fixup(ctx, base, base + 8 * n, n, base + 16 * n, base + 16 * n + 8 * k,
+                                           base + 16 * n + 16 * k, k, base + 16 * n + 24 * k, None))
+            bad = np.zeros(1, np.uint64)
+            N.check(N.lib().cf_memcpy(ctx, N.ptr(bad), base + 16 * n + 24 * k, 8))
+        finally:
+            N.lib().cf_dev_free(ctx, dptr.value)
+        if int(bad[0]) != N.NO_BAD:
+            raise WildAccess(f"fixup target 0x{int(targets[int(bad[0])]):x} was never copied to the device")
+
+    def naive_copy_back(self, tree, amap: "AddressMap") -> None:
+        """Per-object copy back (one batched submission) plus host-side pointer restore."""
+        allocs = tree.allocation_array()
+        host = allocs[:, 0].astype(np.uint64)
+        sizes = allocs[:, 1].astype(np.uint64)
+        dev = amap.translate_many(host)
+        N.check(N.lib().cf_memcpy_batch(self.ctx.handle, N.ptr(host), N.ptr(dev), N.ptr(sizes),
+                                        len(host), None), "naive copy back")
+        N.check(N.lib().cf_ctx_sync(self.ctx.handle))
+        fields, targets = tree.site_field_target_arrays()
+        _poke_words(fields, targets)
+        self.log.append_many(D2H, "per_object", sizes.astype(np.int64))
+        self.log.append_many(D2H, "detach", np.full(len(fields), 8, np.int64))
+
+    # -- unified memory (memory.py:378-394) -------------------------------------------------
+    def uvm_touch(self, addr: int, access: str, actor: str) -> int:
+        """Route one access through the logical page table; returns migrations (0/1)."""
+        if self.uvm is None:
+            raise SimMemoryError("uvm_touch outside UVM mode")
+        state = self.uvm.page_table.get(addr // self.uvm.page_size)
+        if state is None:
+            raise WildAccess(f"unified access at 0x{addr:x} hits no registered page")
+        migrated = 0
+        if state.resident != actor:
+            self.log.append(H2D if actor == "device" else D2H, "page_migration", self.uvm.page_size)
+            state.resident = actor
+            state.dirty = False
+            migrated = 1
+        if access == "write":
+            state.dirty = True
+        return migrated
+
+    def uvm_touch_pages(self, pages, access: str, actor: str) -> int:
+        """Vectorised uvm_touch over a set of page numbers (one touch per page)."""
+        if self.uvm is None:
+            raise SimMemoryError("uvm_touch outside UVM mode")
+        table = self.uvm.page_table
+        migrated = 0
+        for page in pages:
+            state = table.get(int(page))
+            if state is None:
+                raise WildAccess(f"unified access at page {int(page)} hits no registered page")
+            if state.resident != actor:
+                state.resident = actor
+                state.dirty = False
+                migrated += 1
+            if access == "write":
+                state.dirty = True
+        if migrated:
+            self.log.append_many(H2D if actor == "device" else D2H, "page_migration",
+                                 np.full(migrated, self.uvm.page_size, np.int64))
+        return migrated
+
+
+def _poke_words(fields: np.ndarray, values: np.ndarray) -> None:
+    """Write 8-byte values at arbitrary (4-aligned) host addresses."""
+    for f, v in zip(fields.tolist(), values.tolist()):
+        C.memmove(f, int(v).to_bytes(8, "little"), 8)
+
+
+class AddressMap:
+    """Interval map translating host addresses into a copied device image (memory.py:397-419)."""
+
+    def __init__(self):
+        self._hb = np.zeros(0, np.uint64)
+        self._sz = np.zeros(0, np.uint64)
+        self._db = np.zeros(0, np.uint64)
+        self._pending: list = []
+
+    @classmethod
+    def from_arrays(cls, host_base, size, dev_base) -> "AddressMap":
+        m = cls()
+        order = np.argsort(host_base, kind="stable")
+        m._hb = np.ascontiguousarray(np.asarray(host_base, np.uint64)[order])
+        m._sz = np.ascontiguousarray(np.asarray(size, np.uint64)[order])
+        m._db = np.ascontiguousarray(np.asarray(dev_base, np.uint64)[order])
+        return m
+
+    def add(self, host_base: int, size: int, dev_base: int) -> None:
+        self._pending.append((host_base, size, dev_base))
+
+    def arrays(self):
+        if self._pending:
+            hb, sz, db = (np.array(c, np.uint64) for c in zip(*self._pending))
+            self._pending = []
+            merged = AddressMap.from_arrays(np.concatenate([self._hb, hb]), np.concatenate([self._sz, sz]),
+                                            np.concatenate([self._db, db]))
+            self._hb, self._sz, self._db = merged._hb, merged._sz, merged._db
+        return self._hb, self._sz, self._db
+
+    def translate(self, addr: int) -> int:
+        hb, sz, db = self.arrays()
+        i = int(np.searchsorted(hb, np.uint64(addr), side="right")) - 1
+        if i >= 0 and addr < int(hb[i]) + int(sz[i]):
+            return int(db[i]) + (addr - int(hb[i]))
+        raise WildAccess(f"fixup target 0x{addr:x} was never copied to the device")
+
+    def translate_many(self, addrs: np.ndarray) -> np.ndarray:
+        hb, sz, db = self.arrays()
+        a = np.asarray(addrs, np.uint64)
+        i = np.searchsorted(hb, a, side="right").astype(np.int64) - 1
+        if (i < 0).any() or (a >= hb[i] + sz[i]).any():
+            raise WildAccess("fixup target was never copied to the device")
+        return db[i] + (a - hb[i])

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path against the reference golden vectors and the CPU oracle.
+
+Bar (north_star): relocated pointers / offsets bit-exact; leaf outputs bit-exact (the scale is
+a single IEEE multiply, __fmul_rn/__dmul_rn, so no FMA contraction is possible -- tolerance 0).
+"""
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+NO_BAD = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1906_01128_b200 as cf
+    from paper_1906_01128_b200 import _native as N
+    if N.device_count() == 0:
+        pytest.fail("no GPU visible: GPU tests must run on a B200 box")
+    return cf
+
+
+def _spec(cf, j, elem=8, leaf_only=False):
+    if j["kind"] == "linear":
+        return cf.LinearSpec(j["k"], j["n"], j["layout"], elem=elem)
+    return cf.DenseSpec(j["q"], j["n"], j["depth"], elem=elem, leaf_only=leaf_only)
+
+
+def test_attach_image_matches_reference_kats(cf, kats, oracle):
+    """Device image after the relocation kernel == the reference's device image (offset-normalised)."""
+    for r in kats["marshal"]:
+        m = cf.Machine()
+        arena, handle = cf.marshal_tree(m, _spec(cf, r["spec"]), seed=r["seed"])
+        image = m.marshal_transfer_and_attach(arena)
+        dev = np.frombuffer(m.device.read_bytes(image, arena.total_bytes), np.uint8)
+        sites = np.array(r["sites"], np.uint64)
+        # relocated pointers bit-exact: device value - image base == reference target offset
+        vals = [int.from_bytes(dev[s:s + 8].tobytes(), "little") - image for s in r["sites"]]
+        assert vals == r["site_targets"], r["spec"]
+        assert hashlib.sha256(oracle.normalised(dev, sites, image)).hexdigest() == r["image_sha"]
+        assert m.log.count("attach") == len(r["sites"])
+        bulk = [e for e in m.log.entries if e.op_kind == "bulk"]
+        assert len(bulk) == 1 and bulk[0].bytes == r["total_bytes"]
+        # byte-exact demarshal round trip (test_memory.py:153-160)
+        before = m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes)
+        m.demarshal(arena)
+        assert m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes) == before
+        assert m.log.count("detach") == m.log.count("attach")
+        m.close()
+
+
+def test_execute_case_counters_match_reference(cf, kats):
+    """Every scheme's RunMetrics counters and sim columns equal the reference's (seed 1)."""
+    cm = cf.CostModel()
+    for row in kats["counters"]:
+        spec = _spec(cf, row["spec"])
+        for scheme, want in row["schemes"].items():
+            m, machine = cf.execute_case(spec, scheme, cm, seed=1)
+            got = [m.bytes_h2d, m.bytes_d2h, m.transfer_ops, m.attach_ops, m.page_faults, m.instr_estimate,
+                   m.verified]
+            assert got == want[:7], (row["spec"], scheme, got, want)
+            assert m.sim_kernel_us == pytest.approx(want[7], rel=1e-12, abs=1e-12)
+            assert m.sim_wall_us == pytest.approx(want[8], rel=1e-12)
+            machine.close()
+
+
+def test_after_window_bytes_match_reference(cf, kats, oracle):
+    """Host arena after transfer -> scale(2.0) -> copy_back == the reference's (normalised)."""
+    for r in kats["marshal"]:
+        m = cf.Machine()
+        spec = _spec(cf, r["spec"])
+        arena, handle = cf.marshal_tree(m, spec, seed=r["seed"])
+        for mode in ("resolved", "chase"):
+            prep = cf.transfer_to_device(m, handle, "marshalling", arena)
+            cf.kernel_scale(m, handle, prep, 2.0 if mode == "resolved" else 0.5, mode=mode)
+            cf.copy_back(m, handle, prep)
+        # x * 2 * 0.5 == x exactly; run once more with 2.0 for the golden comparison
+        prep = cf.transfer_to_device(m, handle, "marshalling", arena)
+        cf.kernel_scale(m, handle, prep, 2.0)
+        cf.copy_back(m, handle, prep)
+        raw = np.frombuffer(m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes), np.uint8)
+        norm = oracle.normalised(raw, np.array(r["sites"], np.uint64), arena.buffer_host_addr)
+        assert hashlib.sha256(norm).hexdigest() == r["after_window_sha"], r["spec"]
+        cf.verify_tree(m, handle, 2.0)
+        m.close()
+
+
+def test_attach_rejects_targets_outside_the_arena(cf):
+    m = cf.Machine()
+    arena, _ = cf.marshal_tree(m, cf.LinearSpec(2, 10, "allinit_allused"))
+    stray = m.host.allocate(8)
+    m.host.write_word(arena.pointer_sites[0], stray)
+    with pytest.raises(cf.AttachOutsideArena):
+        m.marshal_transfer_and_attach(arena)
+    m.close()
+
+
+def test_demarshal_rejects_corrupted_device_pointer(cf):
+    m = cf.Machine()
+    arena, _ = cf.marshal_tree(m, cf.LinearSpec(2, 10, "allinit_allused"))
+    image = m.marshal_transfer_and_attach(arena)
+    site = arena.pointer_sites[0] - arena.buffer_host_addr
+    m.device.write_word(image + site, 0xDEAD_BEEF)
+    with pytest.raises(cf.AttachOutsideArena):
+        m.demarshal(arena)
+    m.close()
+
+
+def test_demarshal_before_marshal_raises(cf):
+    m = cf.Machine()
+    arena, _ = cf.marshal_tree(m, cf.LinearSpec(2, 10))
+    with pytest.raises(cf.SimMemoryError):
+        m.demarshal(arena)
+    m.close()
+
+
+def test_device_side_chain_chase_after_attach(cf):
+    m = cf.Machine()
+    arena, handle = cf.marshal_tree(m, cf.LinearSpec(3, 4, "allinit_allused"), seed=7)
+    image = m.marshal_transfer_and_attach(arena)
+    node = image + (handle.root_addr - arena.buffer_host_addr)
+    for _ in range(2):
+        node = m.device.read_word(node + 16)
+    aptr = m.device.read_word(node + 8)
+    assert m.device.read_f64(aptr) == m.host.read_f64(handle.arrays[-1].addr)
+    m.close()
+
+
+def test_naive_and_marshalled_trees_agree_after_copy_back(cf):
+    spec = cf.LinearSpec(3, 40, "allinit_allused")
+    dumps = []
+    for scheme in ("marshalling", "naive", "uvm", "pointerchain"):
+        m = cf.Machine()
+        if scheme == "uvm":
+            m.enable_uvm()
+        if scheme == "marshalling":
+            arena, h = cf.marshal_tree(m, spec, seed=9)
+        else:
+            arena, h = None, cf.build_tree(m, spec, seed=9)
+        prep = cf.transfer_to_device(m, h, scheme, arena)
+        cf.kernel_scale(m, h, prep, 2.0)
+        cf.copy_back(m, h, prep)
+        dumps.append([m.host.read_bytes(a.addr, a.count * 8) for a in h.arrays])
+        m.close()
+    assert all(d == dumps[0] for d in dumps[1:])
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+@pytest.mark.parametrize("mode", ["resolved", "chase"])
+def test_pipelined_window_matches_oracle_random_specs(cf, oracle, elem, mode):
+    """Random trees, packed and aligned layouts, small chunks: the pipelined window's copy-back
+    equals the oracle's expected arena bit-for-bit (every dependency path exercised)."""
+    rng = random.Random(1234 + elem + len(mode))
+    for trial in range(24):
+        if rng.random() < 0.5:
+            j = {"kind": "linear", "k": rng.randint(1, 9), "n": rng.randint(0, 5000),
+                 "layout": rng.choice(["allinit_allused", "allinit_LLused", "LLinit_LLused"])}
+            leaf_only = False
+        else:
+            j = {"kind": "dense", "q": rng.randint(1, 5), "n": rng.randint(0, 3000), "depth": rng.randint(0, 3)}
+            leaf_only = rng.random() < 0.4
+        align = rng.choice([1, 8, 16])
+        policy = rng.choice(["ref", "all_leaves", "all_arrays"])
+        chunk = rng.choice([0, 256, 4096, 1 << 16])
+        spec = _spec(cf, j, elem, leaf_only)
+        w = cf.DeepCopyWindow(spec, seed=trial, policy=policy, mode=mode, align=align, chunk_bytes=chunk)
+        try:
+            if w.total == 0:
+                continue
+            st = w.run(scale=2.0)
+            assert st.bad == NO_BAD
+            ot = oracle.build(oracle.spec_from_json(j, elem=elem, align=align, leaf_only=leaf_only), trial,
+                              ptr_base=w.src)
+            pol = {"ref": oracle.TARGET_REF, "all_leaves": oracle.TARGET_ALL_LEAVES,
+                   "all_arrays": oracle.TARGET_ALL_ARRAYS}[policy]
+            idx = oracle.targets(ot, pol)
+            want = oracle.expected_after_window(ot, idx, 2.0)[:w.total]
+            assert np.array_equal(w.host_dst(), want), (j, align, policy, chunk)
+            # resident path on the same image: attach -> resolve -> scale -> detach
+            w.upload_raw()
+            st = w.run_resident(scale=2.0)
+            assert st.bad == NO_BAD
+            assert np.array_equal(w.image_bytes(), want), (j, align, policy, "resident")
+        finally:
+            w.close()
+
+
+def test_kernel_scale_counts_and_derefs(cf):
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.LinearSpec(3, 4, "allinit_allused"))
+    prep = cf.transfer_to_device(m, h, "naive")
+    st = cf.kernel_scale(m, h, prep, 2.0)
+    assert st.elements_touched == 12 and st.chain_derefs == 5
+    m.close()
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.DenseSpec(3, 5, 3))
+    prep = cf.transfer_to_device(m, h, "naive")
+    st = cf.kernel_scale(m, h, prep, 2.0)
+    assert st.elements_touched == 5 and st.chain_derefs == 4
+    m.close()
+
+
+def test_verification_catches_corruption(cf):
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.LinearSpec(2, 8, "allinit_allused"), seed=3)
+    prep = cf.transfer_to_device(m, h, "naive")
+    cf.kernel_scale(m, h, prep, 2.0)
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0)
+    m.host.write_f64(h.arrays[0].addr, -1.0)
+    with pytest.raises(cf.VerificationFailed):
+        cf.verify_tree(m, h, 2.0)
+    m.close()

@@ -245,6 +245,9 @@ typedef struct {
 int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
 /* Enqueue one window; if sync != 0 wait and fill stats (ms from CUDA events). */
 int cf_window_run(cf_window* w, int sync, cf_window_stats* stats);
+/* Enqueue nruns windows back to back (scale alternating scale_even / scale_odd, e.g. 2.0 / 0.5
+ * so the data stays bounded), then wait: stats cover the whole sequence (benchmark timing). */
+int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd, cf_window_stats* stats);
 int cf_window_set_scale(cf_window* w, double scale);
 int cf_window_free(cf_window* w);
 

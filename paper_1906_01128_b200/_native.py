@@ -44,7 +44,7 @@ EXPORTED = (
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup",
-    "cf_window_plan", "cf_window_run", "cf_window_set_scale", "cf_window_free",
+    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_set_scale", "cf_window_free",
 )
 
 
@@ -122,6 +122,7 @@ def _declare(L):
         "cf_naive_fixup": (C.c_int, [P, P, P, U64, P, P, P, U64, P, P]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
+        "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
         "cf_window_free": (C.c_int, [P]),
     }
@@ -185,7 +186,7 @@ class DeviceContext:
 
     _cache: dict = {}
 
-    def __init__(self, device: int = 0, nstreams: int = 4):
+    def __init__(self, device: int = 0, nstreams: int = 1):
         h = P()
         check(lib().cf_ctx_create(device, nstreams, C.byref(h)), "cf_ctx_create")
         self.handle = h
@@ -193,10 +194,10 @@ class DeviceContext:
         self.sm_count = lib().cf_ctx_sm_count(h)
 
     @classmethod
-    def get(cls, device: int = 0) -> "DeviceContext":
-        ctx = cls._cache.get(device)
+    def get(cls, device: int = 0, nstreams: int = 1) -> "DeviceContext":
+        ctx = cls._cache.get((device, nstreams))
         if ctx is None:
-            ctx = cls._cache[device] = cls(device)
+            ctx = cls._cache[(device, nstreams)] = cls(device, nstreams)
         return ctx
 
     def launches(self) -> int:

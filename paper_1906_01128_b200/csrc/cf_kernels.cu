@@ -336,9 +336,10 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
   if (tile_end <= tile_begin || nparts == 0) return CF_OK;
   const uint64_t ntiles = tile_end - tile_begin;
   ScaleArgs a{image, sh, level, ordinal, ea, count, parts, nparts, tile_base, tile_begin, tile_end, bad};
-  // persistent grid: 148 SMs x 8 resident CTAs of 256 threads (2048 threads / SM)
-  const unsigned cap = unsigned((ctx->sm_count > 0 ? ctx->sm_count : 148) * 8);
-  const unsigned grid = unsigned(std::min<uint64_t>(ntiles, cap));
+  // one CTA per 16 KiB tile: measured faster than a persistent grid-stride grid on B200
+  // (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware CTA launcher
+  // keeps more independent loads in flight than a loop that re-locates its part every tile
+  const unsigned grid = unsigned(std::min<uint64_t>(ntiles, 0x7FFFFFFFull));
   if (elem == 4) {
     if (mode == CF_MODE_CHASE) k_scale<float, true><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
     else k_scale<float, false><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));

@@ -44,7 +44,7 @@ struct cf_window {
   uint64_t* d_ea = nullptr;
   uint32_t* d_count = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rel;
-  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr, ev_first = nullptr, ev_tables = nullptr;
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
 };
@@ -69,6 +69,8 @@ void destroy(cf_window* w) {
   if (w->ev_start) cudaEventDestroy(w->ev_start);
   if (w->ev_end) cudaEventDestroy(w->ev_end);
   if (w->ev_join) cudaEventDestroy(w->ev_join);
+  if (w->ev_first) cudaEventDestroy(w->ev_first);
+  if (w->ev_tables) cudaEventDestroy(w->ev_tables);
   delete w;
 }
 
@@ -254,7 +256,8 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->ev_k0.resize(nch);
   w->ev_k1.resize(nch);
   bool ok = mk(&w->ev_start, cudaEventDefault) == cudaSuccess && mk(&w->ev_end, cudaEventDefault) == cudaSuccess &&
-            mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess;
+            mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_first, cudaEventDefault) == cudaSuccess &&
+            mk(&w->ev_tables, cudaEventDisableTiming) == cudaSuccess;
   for (uint64_t c = 0; c < nch && ok; ++c)
     ok = mk(&w->ev_h2d[c], cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_rel[c], cudaEventDisableTiming) == cudaSuccess &&
          mk(&w->ev_k0[c], cudaEventDefault) == cudaSuccess && mk(&w->ev_k1[c], cudaEventDefault) == cudaSuccess;
@@ -269,30 +272,66 @@ int cf_window_set_scale(cf_window* w, double scale) {
   return CF_OK;
 }
 
+namespace {
+int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out);
+int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, uint64_t d2h, bool kernel_times,
+           cudaEvent_t first);
+}  // namespace
+
 int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
   if (!w) return fail(CF_E_INVALID, "null window");
+  CfDevice g(w->ctx);
+  const uint64_t launches0 = w->ctx->launches.load();
+  uint64_t h2d = 0, d2h = 0;
+  const bool timing = sync != 0 && st != nullptr;
+  CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
+  CF_TRY(enqueue(w, timing, &h2d, &d2h));
+  if (!sync) return CF_OK;
+  return finish(w, st, launches0, h2d, d2h, timing, w->ev_first);
+}
+
+int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd, cf_window_stats* st) {
+  if (!w || nruns < 1) return fail(CF_E_INVALID, "bad arguments");
+  CfDevice g(w->ctx);
+  const uint64_t launches0 = w->ctx->launches.load();
+  uint64_t h2d = 0, d2h = 0;
+  CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
+  for (int r = 0; r < nruns; ++r) {
+    w->d.scale = (r & 1) ? scale_odd : scale_even;
+    uint64_t a = 0, b = 0;
+    CF_TRY(enqueue(w, false, &a, &b));
+    h2d += a;
+    d2h += b;
+  }
+  return finish(w, st, launches0, h2d, d2h, false, w->ev_first);
+}
+
+namespace {
+int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   cf_ctx* c = w->ctx;
-  CfDevice g(c);
   const cf_window_desc& d = w->d;
   const uint32_t fl = d.flags;
   const uint64_t nch = w->bounds.size() - 1;
-  const uint64_t launches0 = c->launches.load();
   uint8_t* img = static_cast<uint8_t*>(d.image);
   const uint8_t* src = static_cast<const uint8_t*>(d.host_src);
   uint8_t* dst = static_cast<uint8_t*>(d.host_dst);
   const uint64_t dimg = reinterpret_cast<uint64_t>(d.image);
   cudaStream_t cs = c->compute;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
-  const bool timing = sync != 0 && st != nullptr;
 
   CF_CUDA(cudaEventRecord(w->ev_start, cs));
   for (auto s : c->h2d) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
   CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_start, 0));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, cs));
   if (fl & CF_WIN_TABLES) {
-    CF_CUDA(cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, cs));
+    // the relocation / chain tables travel with the arena, first on the H2D copy stream
+    // (an H2D copy on the compute stream serialises badly against the D2H engine)
+    cudaStream_t s0 = c->h2d[0];
+    CF_CUDA(cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, s0));
+    CF_CUDA(cudaEventRecord(w->ev_tables, s0));
+    CF_CUDA(cudaStreamWaitEvent(cs, w->ev_tables, 0));
     h2d_bytes += w->tab_bytes;
   }
-  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, cs));
   const uint64_t* dsites = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_sites);
   const uint64_t* ddet = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_det);
   const int32_t* dlv = reinterpret_cast<const int32_t*>(w->d_tab + w->off_level);
@@ -349,22 +388,32 @@ int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
   CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, cs));
   d2h_bytes += 8;
   CF_CUDA(cudaEventRecord(w->ev_end, cs));
-  if (!sync) return CF_OK;
+  *h2d_out = h2d_bytes;
+  *d2h_out = d2h_bytes;
+  return CF_OK;
+}
+
+int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, uint64_t d2h, bool kernel_times,
+           cudaEvent_t first) {
+  cf_ctx* c = w->ctx;
   CF_CUDA(cudaEventSynchronize(w->ev_end));
   const uint64_t bad = c->h_bad[0];
+  const uint64_t nch = w->bounds.size() - 1;
   if (st) {
     memset(st, 0, sizeof *st);
-    CF_CUDA(cudaEventElapsedTime(&st->ms_total, w->ev_start, w->ev_end));
+    CF_CUDA(cudaEventElapsedTime(&st->ms_total, first, w->ev_end));
     float ks = 0;
-    for (uint64_t k = 0; k < nch; ++k) {
-      if (!(fl & CF_WIN_SCALE) || w->part_lo[k + 1] == w->part_lo[k]) continue;
-      float ms = 0;
-      CF_CUDA(cudaEventElapsedTime(&ms, w->ev_k0[k], w->ev_k1[k]));
-      ks += ms;
+    if (kernel_times) {
+      for (uint64_t k = 0; k < nch; ++k) {
+        if (!(w->d.flags & CF_WIN_SCALE) || w->part_lo[k + 1] == w->part_lo[k]) continue;
+        float ms = 0;
+        CF_CUDA(cudaEventElapsedTime(&ms, w->ev_k0[k], w->ev_k1[k]));
+        ks += ms;
+      }
     }
     st->ms_kernel = ks;
-    st->h2d_bytes = h2d_bytes;
-    st->d2h_bytes = d2h_bytes;
+    st->h2d_bytes = h2d;
+    st->d2h_bytes = d2h;
     st->launches = c->launches.load() - launches0;
     st->bad = bad;
     st->nchunks = nch;
@@ -374,6 +423,7 @@ int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
     return fail(CF_E_OUTSIDE_ARENA, "window: relocation/resolve/scale reported index %llu", (unsigned long long)bad);
   return CF_OK;
 }
+}  // namespace
 
 int cf_window_free(cf_window* w) {
   destroy(w);

@@ -24,8 +24,8 @@ from .scenarios import TARGET_POLICIES
 class DeepCopyWindow:
     def __init__(self, spec, seed: int = 1, policy: str = "all_leaves", mode: str = "resolved",
                  align: int = 16, chunk_bytes: int = 16 << 20, device: int = 0,
-                 separate_output: bool = True, scale: float = 2.0):
-        self.ctx = N.DeviceContext.get(device)
+                 separate_output: bool = True, scale: float = 2.0, nstreams: int = 1):
+        self.ctx = N.DeviceContext.get(device, nstreams)
         self.spec = spec
         self.seed = seed
         self.plan = N.NativeTree(spec.native(align))
@@ -79,6 +79,19 @@ class DeepCopyWindow:
             chunk_bytes: int | None = None, flags: int = N.CF_WIN_FULL):
         """Full window from host buffers (H2D + tables + attach + resolve + scale + detach + D2H)."""
         return self._run(flags, self.chunk_bytes if chunk_bytes is None else chunk_bytes, mode, scale, sync)
+
+    def run_n(self, nruns: int, flags: int = N.CF_WIN_FULL, chunk_bytes: int | None = None,
+              mode: str | None = None, scales: tuple = (2.0, 0.5)):
+        """Enqueue ``nruns`` windows back to back (scale alternating 2.0 / 0.5, exact in IEEE so
+        the data stays bounded) and wait once; stats cover the whole sequence."""
+        cb = self.chunk_bytes if chunk_bytes is None else chunk_bytes
+        if flags == N.CF_WIN_RESIDENT:
+            cb = 0
+        w = self._window(flags, cb, mode or self.mode)
+        st = N.CfWindowStats()
+        N.check(N.lib().cf_window_run_n(w, int(nruns), float(scales[0]), float(scales[1]), C.byref(st)),
+                "cf_window_run_n")
+        return st
 
     def upload_raw(self) -> None:
         """Put the un-relocated arena bytes into the device image (prepares run_resident)."""

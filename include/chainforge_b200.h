@@ -162,16 +162,26 @@ int cf_relocate(cf_ctx* ctx, void* image, uint64_t image_bytes, const uint64_t* 
 int cf_resolve(cf_ctx* ctx, const void* image, const cf_chain_shape* shape,
                const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets,
                uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad, void* stream);
-/* Leaf kernel (kernel_scale / _scale_block, harness.py:244-309): x *= scale over
- * [begin, end) of every target, elem = 4 (f32) or 8 (f64).
- * mode CF_MODE_RESOLVED reads d_ea (from cf_resolve); CF_MODE_CHASE re-walks the chain from
- * the image root on every 16-byte access with non-hoistable loads (d_ea unused).
- * parts: (target, elem_begin, elem_end) triples, u64[3*nparts]; NULL = whole arrays of
- * d_count. d_bad is raised if a part exceeds the count read from the node. */
+/* Leaf-kernel work list (device pointers).  A launch covers big parts
+ * [big_begin, big_begin + big_count) -- one CTA per 16 KiB tile, tiles [tile_begin, tile_end) --
+ * and small-part groups [group_begin, group_end) -- one CTA per group, one warp per part. */
+typedef struct {
+  const uint64_t* parts;      /* (target, elem_begin, elem_end) triples */
+  const uint64_t* tile_base;  /* per part: first tile number (meaningful for big parts) */
+  const uint32_t* groups;     /* (first part, end part) pairs */
+  uint64_t big_begin, big_count;
+  uint64_t tile_begin, tile_end;
+  uint64_t group_begin, group_end;
+} cf_scale_work;
+
+/* Leaf kernel (kernel_scale / _scale_block, harness.py:244-309): x *= scale over every part,
+ * elem = 4 (f32) or 8 (f64).  mode CF_MODE_RESOLVED reads d_ea (from cf_resolve);
+ * CF_MODE_CHASE re-walks the chain from the image root on every 16-byte access with
+ * non-hoistable loads (d_ea unused).  d_bad is raised if a part exceeds the count read from
+ * the node or the array pointer is null. */
 int cf_scale(cf_ctx* ctx, int elem, int mode, const void* image, const cf_chain_shape* shape,
              const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
-             const uint32_t* d_count, uint64_t ntargets, const uint64_t* d_parts, uint64_t nparts,
-             const uint64_t* d_part_tile_base, uint64_t ntiles, double scale, uint64_t* d_bad,
+             const uint32_t* d_count, const cf_scale_work* work, double scale, uint64_t* d_bad,
              void* stream);
 
 /* ---------------- reference-named composite operations ---------------- */

@@ -45,9 +45,8 @@ int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh,
                    uint32_t* count, uint64_t* bad, cudaStream_t s);
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
-                 const uint32_t* count, const uint64_t* parts, uint64_t nparts,
-                 const uint64_t* tile_base, uint64_t tile_begin, uint64_t tile_end, double scale,
-                 uint64_t* bad, cudaStream_t s);
+                 const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
+                 cudaStream_t s);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);
@@ -57,6 +56,58 @@ inline uint64_t tiles_for(uint64_t elems, int elem) {
   const uint64_t per = TILE_BYTES / uint64_t(elem);
   return (elems + per - 1) / per;
 }
+
+// Small parts (< one tile) are packed into groups of at most GROUP_BYTES / GROUP_PARTS and
+// processed one warp per part, so 1M 1 KiB leaves do not become 1M mostly idle CTAs.
+constexpr uint64_t GROUP_BYTES = TILE_BYTES;
+constexpr uint32_t GROUP_PARTS = 32;
+
+// Host-side builder of the leaf-kernel work list (see cf_scale_work in the header).
+struct ScaleWork {
+  int elem = 4;
+  std::vector<uint64_t> parts;      // (target, elem_begin, elem_end) per part
+  std::vector<uint64_t> tile_base;  // per part: first tile (big parts), 0 for small parts
+  std::vector<uint32_t> groups;     // (first part, end part) per group
+  uint64_t next_tile = 0;
+
+  uint64_t nparts() const { return parts.size() / 3; }
+  uint64_t ngroups() const { return groups.size() / 2; }
+
+  // Append one launch segment: big parts first (one CTA per 16 KiB tile), then the small
+  // parts packed into groups.  Descriptor pointers are left null (filled per launch).
+  cf_scale_work append(const std::vector<uint64_t>& tri) {
+    cf_scale_work w{};
+    const uint64_t tile_elems = TILE_BYTES / uint64_t(elem);
+    w.big_begin = nparts();
+    w.tile_begin = next_tile;
+    for (size_t i = 0; i < tri.size(); i += 3) {
+      if (tri[i + 2] - tri[i + 1] < tile_elems) continue;
+      parts.insert(parts.end(), {tri[i], tri[i + 1], tri[i + 2]});
+      tile_base.push_back(next_tile);
+      next_tile += tiles_for(tri[i + 2] - tri[i + 1], elem);
+    }
+    w.big_count = nparts() - w.big_begin;
+    w.tile_end = next_tile;
+    w.group_begin = ngroups();
+    uint64_t first = nparts(), bytes = 0;
+    for (size_t i = 0; i < tri.size(); i += 3) {
+      const uint64_t n = tri[i + 2] - tri[i + 1];
+      if (n >= tile_elems || n == 0) continue;
+      const uint64_t b = n * uint64_t(elem);
+      if (nparts() > first && (bytes + b > GROUP_BYTES || nparts() - first >= GROUP_PARTS)) {
+        groups.insert(groups.end(), {uint32_t(first), uint32_t(nparts())});
+        first = nparts();
+        bytes = 0;
+      }
+      parts.insert(parts.end(), {tri[i], tri[i + 1], tri[i + 2]});
+      tile_base.push_back(0);
+      bytes += b;
+    }
+    if (nparts() > first) groups.insert(groups.end(), {uint32_t(first), uint32_t(nparts())});
+    w.group_end = ngroups();
+    return w;
+  }
+};
 
 }  // namespace cf
 

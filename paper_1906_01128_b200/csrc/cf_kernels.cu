@@ -183,79 +183,111 @@ struct ScaleArgs {
   const uint64_t* ordinal;
   const uint64_t* ea;
   const uint32_t* count;
-  const uint64_t* parts;      // (target, begin, end) x nparts
-  uint64_t nparts;
-  const uint64_t* tile_base;  // per-part first tile (absolute tile numbers)
-  uint64_t tile_begin;        // tiles [tile_begin, tile_end) belong to these parts
-  uint64_t tile_end;
+  cf_scale_work w;
   uint64_t* bad;
 };
 
-template <typename T, bool CHASE>
-__global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
+// Array base + element count of target t: from the resolved table, or re-walked (CHASE).
+template <bool CHASE>
+__device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uint8_t*& arr, uint64_t& cnt) {
+  if (CHASE) {
+    Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+    if (!w.node) return false;
+    arr = reinterpret_cast<uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
+    cnt = ld_u32_any(w.node + OFF_NA);
+  } else {
+    arr = reinterpret_cast<uint8_t*>(a.ea[t]);
+    cnt = a.count[t];
+  }
+  return arr != nullptr;
+}
+
+// Re-derive the array address through the chain (CHASE: one walk per 16-byte access).
+template <bool CHASE>
+__device__ __forceinline__ uint8_t* chase_base(const ScaleArgs& a, uint64_t t, uint8_t* resolved) {
+  if (!CHASE) return resolved;
+  Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+  return reinterpret_cast<uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
+}
+
+// Scale elements [e0, e1) of arr with `lanes` cooperating threads (rank `me`): scalar head up to
+// 16-byte alignment, UNROLL independent 128-bit loads in flight per thread, scalar tail.
+template <typename T, bool CHASE, int UNROLL>
+__device__ __forceinline__ void scale_range(const ScaleArgs& a, uint64_t t, uint8_t* arr, uint64_t e0, uint64_t e1,
+                                            T s, unsigned me, unsigned lanes) {
   using VT = Vec<T>;
   using V = typename VT::V;
-  constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
   constexpr uint64_t VN = VT::N;
-  for (uint64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-    // locate the part owning this tile (uniform across the CTA; loads are broadcast)
-    uint64_t lo = 0, hi = a.nparts;
+  const uintptr_t first = reinterpret_cast<uintptr_t>(arr + e0 * sizeof(T));
+  uint64_t v0 = e1, v1 = e1;
+  if ((first % sizeof(T)) == 0) {
+    const uint64_t head = ((16 - (first & 15)) & 15) / sizeof(T);
+    v0 = min(e1, e0 + head);
+    v1 = v0 + (e1 - v0) / VN * VN;
+  }
+  for (uint64_t i = e0 + me; i < v0; i += lanes)
+    scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+  for (uint64_t i = v1 + me; i < e1; i += lanes)
+    scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+  const uint64_t nv = (v1 - v0) / VN;
+  uint64_t j = me;
+  if (CHASE) {
+    for (; j < nv; j += lanes) {
+      V* p = reinterpret_cast<V*>(chase_base<true>(a, t, arr) + v0 * sizeof(T)) + j;
+      VT::st(p, VT::mul(VT::ld(p), s));
+    }
+    return;
+  }
+  V* p = reinterpret_cast<V*>(arr + v0 * sizeof(T));
+  for (; j + (UNROLL - 1) * lanes < nv; j += UNROLL * lanes) {
+    V r[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) r[u] = VT::ld(p + j + u * lanes);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) VT::st(p + j + u * lanes, VT::mul(r[u], s));
+  }
+  for (; j < nv; j += lanes) VT::st(p + j, VT::mul(VT::ld(p + j), s));
+}
+
+// One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
+// blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part.
+template <typename T, bool CHASE>
+__global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
+  constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
+  const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
+  if (blockIdx.x < ntiles) {
+    const uint64_t tile = a.w.tile_begin + blockIdx.x;
+    uint64_t lo = a.w.big_begin, hi = a.w.big_begin + a.w.big_count;
     while (hi - lo > 1) {
       const uint64_t mid = (lo + hi) >> 1;
-      if (a.tile_base[mid] <= tile) lo = mid; else hi = mid;
+      if (a.w.tile_base[mid] <= tile) lo = mid; else hi = mid;
     }
-    const uint64_t t = a.parts[3 * lo];
-    const uint64_t pb = a.parts[3 * lo + 1], pe = a.parts[3 * lo + 2];
-    const uint64_t e0 = pb + (tile - a.tile_base[lo]) * TILE;
-    const uint64_t e1 = min(pe, e0 + TILE);
-    const uint8_t* arr;
+    const uint64_t t = a.w.parts[3 * lo];
+    const uint64_t e0 = a.w.parts[3 * lo + 1] + (tile - a.w.tile_base[lo]) * TILE;
+    const uint64_t e1 = min(a.w.parts[3 * lo + 2], e0 + TILE);
+    uint8_t* arr;
     uint64_t cnt;
-    if (CHASE) {
-      Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
-      if (!w.node) { if (threadIdx.x == 0) raise_bad(a.bad, t); continue; }
-      arr = reinterpret_cast<const uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
-      cnt = ld_u32_any(w.node + OFF_NA);
-    } else {
-      arr = reinterpret_cast<const uint8_t*>(a.ea[t]);
-      cnt = a.count[t];
+    if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
+      if (threadIdx.x == 0) raise_bad(a.bad, t);
+      return;
     }
-    if (arr == nullptr || e1 > cnt) { if (threadIdx.x == 0) raise_bad(a.bad, t); continue; }
-    uint8_t* base = const_cast<uint8_t*>(arr);
-    const uintptr_t first = reinterpret_cast<uintptr_t>(base + e0 * sizeof(T));
-    // vector body [v0, v1) in elements; scalar head/tail
-    uint64_t v0 = e1, v1 = e1;
-    if ((first % sizeof(T)) == 0) {
-      const uint64_t head = ((16 - (first & 15)) & 15) / sizeof(T);
-      v0 = min(e1, e0 + head);
-      v1 = v0 + (e1 - v0) / VN * VN;
+    scale_range<T, CHASE, SCALE_UNROLL>(a, t, arr, e0, e1, s, threadIdx.x, SCALE_THREADS);
+    return;
+  }
+  const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
+  if (g >= a.w.group_end) return;
+  const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t p = p0 + warp; p < p1; p += SCALE_THREADS / 32) {
+    const uint64_t t = a.w.parts[3ull * p];
+    const uint64_t e0 = a.w.parts[3ull * p + 1], e1 = a.w.parts[3ull * p + 2];
+    uint8_t* arr;
+    uint64_t cnt;
+    if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
+      if (lane == 0) raise_bad(a.bad, t);
+      continue;
     }
-    for (uint64_t i = e0 + threadIdx.x; i < v0; i += SCALE_THREADS)
-      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
-    for (uint64_t i = v1 + threadIdx.x; i < e1; i += SCALE_THREADS)
-      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
-    const uint64_t nv = (v1 - v0) / VN;
-    if (nv == 0) continue;
-    if (CHASE) {
-      // every 16-byte access re-derives its address through the chain (Listing 2 semantics)
-      for (uint64_t j = threadIdx.x; j < nv; j += SCALE_THREADS) {
-        Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
-        const uint8_t* A = reinterpret_cast<const uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
-        V* p = reinterpret_cast<V*>(const_cast<uint8_t*>(A) + v0 * sizeof(T)) + j;
-        VT::st(p, VT::mul(VT::ld(p), s));
-      }
-    } else {
-      V* p = reinterpret_cast<V*>(base + v0 * sizeof(T));
-      uint64_t j = threadIdx.x;
-      // full tiles: SCALE_UNROLL independent 16-byte loads in flight per thread
-      for (; j + (SCALE_UNROLL - 1) * SCALE_THREADS < nv; j += SCALE_UNROLL * SCALE_THREADS) {
-        V r[SCALE_UNROLL];
-#pragma unroll
-        for (int u = 0; u < int(SCALE_UNROLL); ++u) r[u] = VT::ld(p + j + u * SCALE_THREADS);
-#pragma unroll
-        for (int u = 0; u < int(SCALE_UNROLL); ++u) VT::st(p + j + u * SCALE_THREADS, VT::mul(r[u], s));
-      }
-      for (; j < nv; j += SCALE_THREADS) VT::st(p + j, VT::mul(VT::ld(p + j), s));
-    }
+    scale_range<T, CHASE, 2>(a, t, arr, e0, e1, s, lane, 32);
   }
 }
 
@@ -331,15 +363,16 @@ int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, 
 
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const int32_t* level, const uint64_t* ordinal, const uint64_t* ea, const uint32_t* count,
-                 const uint64_t* parts, uint64_t nparts, const uint64_t* tile_base, uint64_t tile_begin,
-                 uint64_t tile_end, double scale, uint64_t* bad, cudaStream_t s) {
-  if (tile_end <= tile_begin || nparts == 0) return CF_OK;
-  const uint64_t ntiles = tile_end - tile_begin;
-  ScaleArgs a{image, sh, level, ordinal, ea, count, parts, nparts, tile_base, tile_begin, tile_end, bad};
-  // one CTA per 16 KiB tile: measured faster than a persistent grid-stride grid on B200
-  // (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware CTA launcher
-  // keeps more independent loads in flight than a loop that re-locates its part every tile
-  const unsigned grid = unsigned(std::min<uint64_t>(ntiles, 0x7FFFFFFFull));
+                 const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s) {
+  const uint64_t units = (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin);
+  if (units == 0) return CF_OK;
+  if (units > 0x7FFFFFFFull) return fail(CF_E_INVALID, "leaf kernel: %llu work units exceed one grid",
+                                         (unsigned long long)units);
+  ScaleArgs a{image, sh, level, ordinal, ea, count, work, bad};
+  // one CTA per 16 KiB tile / small-part group: measured faster than a persistent grid-stride
+  // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware
+  // CTA launcher keeps more independent loads in flight than a loop re-locating its part
+  const unsigned grid = unsigned(units);
   if (elem == 4) {
     if (mode == CF_MODE_CHASE) k_scale<float, true><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
     else k_scale<float, false><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));

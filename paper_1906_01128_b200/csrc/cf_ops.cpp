@@ -63,6 +63,21 @@ std::vector<uint64_t> chunk_bounds(uint64_t total, uint64_t chunk, const uint64_
   return b;
 }
 
+// Upload a host ScaleWork into `dst` (device) and point `w` at it.
+uint64_t work_bytes(const ScaleWork& sw) {
+  return sw.parts.size() * 8 + sw.tile_base.size() * 8 + ((sw.groups.size() * 4 + 7) / 8) * 8;
+}
+int upload_work(const ScaleWork& sw, uint8_t* dst, cudaStream_t s, cf_scale_work* w) {
+  const uint64_t n1 = sw.parts.size() * 8, n2 = sw.tile_base.size() * 8, n3 = sw.groups.size() * 4;
+  if (n1) CF_CUDA(cudaMemcpyAsync(dst, sw.parts.data(), n1, cudaMemcpyHostToDevice, s));
+  if (n2) CF_CUDA(cudaMemcpyAsync(dst + n1, sw.tile_base.data(), n2, cudaMemcpyHostToDevice, s));
+  if (n3) CF_CUDA(cudaMemcpyAsync(dst + n1 + n2, sw.groups.data(), n3, cudaMemcpyHostToDevice, s));
+  w->parts = reinterpret_cast<const uint64_t*>(dst);
+  w->tile_base = reinterpret_cast<const uint64_t*>(dst + n1);
+  w->groups = reinterpret_cast<const uint32_t*>(dst + n1 + n2);
+  return CF_OK;
+}
+
 int read_bad(cf_ctx* c, const uint64_t* d_bad, cudaStream_t s, uint64_t* out) {
   CF_CUDA(cudaMemcpyAsync(c->h_bad, d_bad, 8, cudaMemcpyDeviceToHost, s));
   CF_CUDA(cudaStreamSynchronize(s));
@@ -93,15 +108,14 @@ int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const 
 
 int cf_scale(cf_ctx* c, int elem, int mode, const void* image, const cf_chain_shape* shape,
              const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea, const uint32_t* d_count,
-             uint64_t ntargets, const uint64_t* d_parts, uint64_t nparts, const uint64_t* d_part_tile_base,
-             uint64_t ntiles, double scale, uint64_t* d_bad, void* stream) {
-  (void)ntargets;
-  if (!c || !shape) return fail(CF_E_INVALID, "null argument");
+             const cf_scale_work* work, double scale, uint64_t* d_bad, void* stream) {
+  if (!c || !shape || !work) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
-  if (!d_parts || !d_part_tile_base) return fail(CF_E_INVALID, "parts and tile bases are required");
+  if (!work->parts || (work->big_count && !work->tile_base) || (work->group_end > work->group_begin && !work->groups))
+    return fail(CF_E_INVALID, "incomplete work list");
   CfDevice g(c);
-  return launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, d_ea,
-                      d_count, d_parts, nparts, d_part_tile_base, 0, ntiles, scale, d_bad, pick(c, stream));
+  return launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, d_ea, d_count,
+                      *work, scale, d_bad, pick(c, stream));
 }
 
 int cf_marshal_transfer_and_attach(cf_ctx* c, const void* host_arena, uint64_t total, void* image,
@@ -197,32 +211,25 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   CfDevice g(c);
   if (bad) *bad = NO_BAD;
   if (ntargets == 0) return CF_OK;
-  // parts: whole arrays; tile prefix from the planned counts
-  std::vector<uint64_t> parts, tb;
-  uint64_t nt = 0;
-  for (uint64_t t = 0; t < ntargets; ++t) {
-    if (h_count[t] == 0) continue;
-    parts.insert(parts.end(), {t, 0, h_count[t]});
-    tb.push_back(nt);
-    nt += tiles_for(h_count[t], elem);
-  }
-  const uint64_t np = tb.size();
-  // one device block: level | ordinal | ea | count | parts | tile_base
+  // parts: whole arrays with their planned counts
+  ScaleWork sw;
+  sw.elem = elem;
+  std::vector<uint64_t> tri;
+  for (uint64_t t = 0; t < ntargets; ++t)
+    if (h_count[t]) tri.insert(tri.end(), {t, 0, h_count[t]});
+  cf_scale_work work = sw.append(tri);
+  // one device block: level | ordinal | ea | count | work list
   const uint64_t off_ord = ((ntargets * 4 + 7) / 8) * 8;
   const uint64_t off_ea = off_ord + ntargets * 8;
   const uint64_t off_cnt = off_ea + ntargets * 8;
-  const uint64_t off_parts = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
-  const uint64_t off_tb = off_parts + np * 24;
+  const uint64_t off_work = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
   DevBuf blk;
-  CF_TRY(blk.alloc(off_tb + np * 8 + 8));
+  CF_TRY(blk.alloc(off_work + work_bytes(sw) + 8));
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;
   CF_CUDA(cudaMemcpyAsync(d, h_level, ntargets * 4, cudaMemcpyHostToDevice, s));
   CF_CUDA(cudaMemcpyAsync(d + off_ord, h_ordinal, ntargets * 8, cudaMemcpyHostToDevice, s));
-  if (np) {
-    CF_CUDA(cudaMemcpyAsync(d + off_parts, parts.data(), np * 24, cudaMemcpyHostToDevice, s));
-    CF_CUDA(cudaMemcpyAsync(d + off_tb, tb.data(), np * 8, cudaMemcpyHostToDevice, s));
-  }
+  CF_TRY(upload_work(sw, d + off_work, s, &work));
   CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   const int32_t* lv = reinterpret_cast<const int32_t*>(d);
   const uint64_t* od = reinterpret_cast<const uint64_t*>(d + off_ord);
@@ -235,11 +242,8 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
     if (bad) *bad = rb;
     return fail(CF_E_WILD, "chain walk for target %llu left the device image", (unsigned long long)rb);
   }
-  if (np) {
-    CF_TRY(launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, lv, od, ea, cnt,
-                        reinterpret_cast<const uint64_t*>(d + off_parts), np,
-                        reinterpret_cast<const uint64_t*>(d + off_tb), 0, nt, scale, c->d_bad, s));
-  }
+  CF_TRY(launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, lv, od, ea, cnt, work, scale,
+                      c->d_bad, s));
   if (h_ea_out) CF_CUDA(cudaMemcpyAsync(h_ea_out, ea, ntargets * 8, cudaMemcpyDeviceToHost, s));
   CF_TRY(read_bad(c, c->d_bad, s, &rb));
   if (rb != NO_BAD) {
@@ -254,34 +258,31 @@ int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t*
   if (!c || (n && (!h_ea || !h_count))) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
   CfDevice g(c);
-  std::vector<uint64_t> parts, tb;
   std::vector<uint32_t> cnt(n);
-  uint64_t nt = 0;
+  ScaleWork sw;
+  sw.elem = elem;
+  std::vector<uint64_t> tri;
   for (uint64_t t = 0; t < n; ++t) {
     if (h_count[t] >> 32) return fail(CF_E_INVALID, "count does not fit the u32 nA field");
     cnt[t] = uint32_t(h_count[t]);
     if (h_count[t] == 0 || h_ea[t] == 0) continue;
-    parts.insert(parts.end(), {t, 0, h_count[t]});
-    tb.push_back(nt);
-    nt += tiles_for(h_count[t], elem);
+    tri.insert(tri.end(), {t, 0, h_count[t]});
   }
-  const uint64_t np = tb.size();
-  if (np == 0) return CF_OK;
-  const uint64_t off_cnt = n * 8, off_parts = off_cnt + ((n * 4 + 7) / 8) * 8, off_tb = off_parts + np * 24;
+  cf_scale_work work = sw.append(tri);
+  if (sw.nparts() == 0) return CF_OK;
+  const uint64_t off_cnt = n * 8, off_work = off_cnt + ((n * 4 + 7) / 8) * 8;
   DevBuf blk;
-  CF_TRY(blk.alloc(off_tb + np * 8));
+  CF_TRY(blk.alloc(off_work + work_bytes(sw) + 8));
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;
   CF_CUDA(cudaMemcpyAsync(d, h_ea, n * 8, cudaMemcpyHostToDevice, s));
   CF_CUDA(cudaMemcpyAsync(d + off_cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice, s));
-  CF_CUDA(cudaMemcpyAsync(d + off_parts, parts.data(), np * 24, cudaMemcpyHostToDevice, s));
-  CF_CUDA(cudaMemcpyAsync(d + off_tb, tb.data(), np * 8, cudaMemcpyHostToDevice, s));
+  CF_TRY(upload_work(sw, d + off_work, s, &work));
   CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   cf_chain_shape sh;
   memset(&sh, 0, sizeof sh);
   CF_TRY(launch_scale(c, elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, reinterpret_cast<const uint64_t*>(d),
-                      reinterpret_cast<const uint32_t*>(d + off_cnt), reinterpret_cast<const uint64_t*>(d + off_parts), np,
-                      reinterpret_cast<const uint64_t*>(d + off_tb), 0, nt, scale, c->d_bad, s));
+                      reinterpret_cast<const uint32_t*>(d + off_cnt), work, scale, c->d_bad, s));
   uint64_t rb = NO_BAD;
   CF_TRY(read_bad(c, c->d_bad, s, &rb));
   if (rb != NO_BAD) return fail(CF_E_WILD, "leaf kernel: buffer %llu rejected", (unsigned long long)rb);

@@ -32,15 +32,14 @@ struct cf_window {
   std::vector<uint64_t> bounds;        // chunk boundaries, nchunks + 1
   std::vector<uint64_t> reloc_lo;      // sorted-site ranges per chunk, nchunks + 1
   std::vector<uint64_t> res_lo;        // resolve-target ranges per step, nchunks + 1
-  std::vector<uint64_t> part_lo;       // part ranges per step, nchunks + 1
+  std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step, nchunks + 1
   std::vector<std::vector<uint32_t>> released;  // chunks whose copy-back may start after step c
-  std::vector<uint64_t> tile_base;     // per part (+ sentinel): absolute first tile
   // one pinned table block and its device mirror
   uint8_t* h_tab = nullptr;
   uint8_t* d_tab = nullptr;
   uint64_t tab_bytes = 0;
-  uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_parts = 0, off_tb = 0;
+  uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_parts = 0, off_tb = 0, off_grp = 0;
   uint64_t* d_ea = nullptr;
   uint32_t* d_count = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rel;
@@ -188,16 +187,16 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     while (k < nt && ready[torder[k]] < c) ++k;
     w->res_lo[c] = k;
   }
+  // per step: the pieces ready at that step, as one leaf-kernel launch (big tiles + small groups)
   std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) { return x.step < y.step; });
-  w->part_lo.assign(nch + 1, 0);
-  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
-    while (k < parts.size() && parts[k].step < c) ++k;
-    w->part_lo[c] = k;
+  ScaleWork sw;
+  sw.elem = w->elem;
+  w->seg.resize(nch);
+  for (uint64_t c = 0, k = 0; c < nch; ++c) {
+    std::vector<uint64_t> tri;
+    for (; k < parts.size() && parts[k].step == c; ++k) tri.insert(tri.end(), {tpos[parts[k].t], parts[k].b, parts[k].e});
+    w->seg[c] = sw.append(tri);
   }
-  w->tile_base.resize(parts.size() + 1);
-  w->tile_base[0] = 0;
-  for (size_t k = 0; k < parts.size(); ++k)
-    w->tile_base[k + 1] = w->tile_base[k] + tiles_for(parts[k].e - parts[k].b, w->elem);
   std::vector<uint64_t> det(nsites);
   {
     std::vector<uint64_t> sidx(nsites);
@@ -215,15 +214,16 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->released.assign(nch, {});
   for (uint64_t c = 0; c < nch; ++c) w->released[release[c]].push_back(uint32_t(c));
 
-  // ---- table block: sites | det | level | ordinal | parts | tile_base
+  // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->off_sites = 0;
   w->off_det = al8(w->off_sites + nsites * 8);
   w->off_level = al8(w->off_det + nsites * 8);
   w->off_ord = al8(w->off_level + nt * 4);
   w->off_parts = al8(w->off_ord + nt * 8);
-  w->off_tb = al8(w->off_parts + parts.size() * 24);
-  w->tab_bytes = al8(w->off_tb + (parts.size() + 1) * 8);
+  w->off_tb = al8(w->off_parts + sw.parts.size() * 8);
+  w->off_grp = al8(w->off_tb + sw.tile_base.size() * 8);
+  w->tab_bytes = al8(w->off_grp + sw.groups.size() * 4 + 8);
   cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
@@ -238,13 +238,14 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     lv[k] = t->arr_level[a];
     od[k] = t->arr_ordinal[a];
   }
-  uint64_t* pp = reinterpret_cast<uint64_t*>(w->h_tab + w->off_parts);
-  for (size_t k = 0; k < parts.size(); ++k) {
-    pp[3 * k] = tpos[parts[k].t];
-    pp[3 * k + 1] = parts[k].b;
-    pp[3 * k + 2] = parts[k].e;
+  if (!sw.parts.empty()) memcpy(w->h_tab + w->off_parts, sw.parts.data(), sw.parts.size() * 8);
+  if (!sw.tile_base.empty()) memcpy(w->h_tab + w->off_tb, sw.tile_base.data(), sw.tile_base.size() * 8);
+  if (!sw.groups.empty()) memcpy(w->h_tab + w->off_grp, sw.groups.data(), sw.groups.size() * 4);
+  for (auto& sg : w->seg) {
+    sg.parts = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_parts);
+    sg.tile_base = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
+    sg.groups = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_grp);
   }
-  memcpy(w->h_tab + w->off_tb, w->tile_base.data(), (parts.size() + 1) * 8);
   // the device mirror starts valid so runs without CF_WIN_TABLES work
   ce = cudaMemcpy(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "table upload: %s", cudaGetErrorString(ce)); }
@@ -336,8 +337,6 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   const uint64_t* ddet = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_det);
   const int32_t* dlv = reinterpret_cast<const int32_t*>(w->d_tab + w->off_level);
   const uint64_t* dod = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_ord);
-  const uint64_t* dparts = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_parts);
-  const uint64_t* dtb = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
   const bool chase = d.mode == CF_MODE_CHASE;
 
   for (uint64_t k = 0; k < nch; ++k) {
@@ -356,11 +355,10 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], w->res_lo[k + 1] - w->res_lo[k],
                             w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
     if (fl & CF_WIN_SCALE) {
-      const uint64_t p0 = w->part_lo[k], p1 = w->part_lo[k + 1];
-      if (p1 > p0) {
+      const cf_scale_work& sg = w->seg[k];
+      if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, dparts + 3 * p0, p1 - p0,
-                            dtb + p0, w->tile_base[p0], w->tile_base[p1], d.scale, c->d_bad, cs));
+        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
@@ -405,7 +403,8 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
     float ks = 0;
     if (kernel_times) {
       for (uint64_t k = 0; k < nch; ++k) {
-        if (!(w->d.flags & CF_WIN_SCALE) || w->part_lo[k + 1] == w->part_lo[k]) continue;
+        const cf_scale_work& sg = w->seg[k];
+        if (!(w->d.flags & CF_WIN_SCALE) || (sg.tile_end == sg.tile_begin && sg.group_end == sg.group_begin)) continue;
         float ms = 0;
         CF_CUDA(cudaEventElapsedTime(&ms, w->ev_k0[k], w->ev_k1[k]));
         ks += ms;

@@ -235,19 +235,20 @@ def run_ours(args, dist: Dist) -> None:
     clocks = ClockSampler(device)
     clocks.start()
     # ---- e2e: host buffers in, copy-back out, through the C-ABI window
-    w.run_n(args.warmup, flags=N.CF_WIN_FULL)
+    gflag = 0 if args.no_graph else N.CF_WIN_GRAPH
+    w.run_n(args.warmup, flags=N.CF_WIN_FULL | gflag)
     dist.barrier()
     N.check(N.lib().cf_ctx_sync(w.ctx.handle))
-    st_e2e = w.run_n(args.steps, flags=N.CF_WIN_FULL)
+    st_e2e = w.run_n(args.steps, flags=N.CF_WIN_FULL | gflag)
     N.check(N.lib().cf_ctx_sync(w.ctx.handle))
     dist.barrier()
     e2e_ms = dist.max(st_e2e.ms_total) / args.steps
     # ---- value: image resident in HBM
     w.upload_raw()
-    w.run_n(args.warmup, flags=N.CF_WIN_RESIDENT)
+    w.run_n(args.warmup, flags=N.CF_WIN_RESIDENT | gflag)
     dist.barrier()
     N.check(N.lib().cf_ctx_sync(w.ctx.handle))
-    st_res = w.run_n(args.steps, flags=N.CF_WIN_RESIDENT)
+    st_res = w.run_n(args.steps, flags=N.CF_WIN_RESIDENT | gflag)
     N.check(N.lib().cf_ctx_sync(w.ctx.handle))
     dist.barrier()
     res_ms = dist.max(st_res.ms_total) / args.steps
@@ -295,7 +296,7 @@ def run_ours(args, dist: Dist) -> None:
         "data": "synthetic (payload_values of the reference, seed 1+rank)",
         "config": {"workload": desc, "graph_bytes_per_gpu": total, "leaf_bytes_per_gpu": leaf_bytes,
                    "layout": "aligned16 arena", "targets": policy, "chunk_bytes": args.chunk_mb << 20,
-                   "h2d_streams": 1, "d2h_streams": 1, "l2": "inputs >= 1 GiB per GPU exceed the 126 MB L2 (no flush needed)"
+                   "h2d_streams": 1, "d2h_streams": 1, "cuda_graph": not args.no_graph, "l2": "inputs >= 1 GiB per GPU exceed the 126 MB L2 (no flush needed)"
                    if total > (256 << 20) else "working set fits L2: value is L2-assisted",
                    "parallelism": f"dp{n} (one subtree shard per GPU, no data-path collective)"},
         "e2e": {"value": round(e2e, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
@@ -338,6 +339,7 @@ def main(argv=None):
     ap.add_argument("--chunk-mb", type=int, default=16)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-chase", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="enqueue every window directly (no CUDA graph)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -43,10 +43,18 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh,
                    const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea,
                    uint32_t* count, uint64_t* bad, cudaStream_t s);
+// A relocation job that can ride along in a leaf-kernel launch (extra CTAs).
+struct RelocArgs {
+  uint8_t* image;
+  uint64_t total;
+  const uint64_t* sites;
+  uint64_t n;
+  uint64_t from, to;
+};
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
                  const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
-                 cudaStream_t s);
+                 cudaStream_t s, const RelocArgs* fused_reloc = nullptr);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);

@@ -75,19 +75,24 @@ __device__ __forceinline__ void raise_bad(uint64_t* bad, uint64_t idx) {
 }
 
 // ---------------------------------------------------------------- relocation (attach/detach)
+__device__ __forceinline__ void relocate_one(uint8_t* __restrict__ image, uint64_t total,
+                                             const uint64_t* __restrict__ sites, uint64_t i, uint64_t from,
+                                             uint64_t to, uint64_t* bad) {
+  const uint64_t s = sites[i];  // coalesced table read
+  if (s + 8 > total) { raise_bad(bad, i); return; }
+  uint8_t* p = image + s;
+  const uint64_t v = ld_u64_any(p);
+  const uint64_t d = v - from;  // wraps when v < from
+  if (d >= total) { raise_bad(bad, i); return; }
+  st_u64_any(p, to + d);
+}
+
 __global__ void __launch_bounds__(256) k_relocate(uint8_t* __restrict__ image, uint64_t total,
                                                   const uint64_t* __restrict__ sites, uint64_t n,
                                                   uint64_t from, uint64_t to, uint64_t* bad) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t s = sites[i];  // coalesced table read
-    if (s + 8 > total) { raise_bad(bad, i); continue; }
-    uint8_t* p = image + s;
-    const uint64_t v = ld_u64_any(p);
-    const uint64_t d = v - from;  // wraps when v < from
-    if (d >= total) { raise_bad(bad, i); continue; }
-    st_u64_any(p, to + d);
-  }
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    relocate_one(image, total, sites, i, from, to, bad);
 }
 
 // ---------------------------------------------------------------- chain walk
@@ -185,6 +190,7 @@ struct ScaleArgs {
   const uint32_t* count;
   cf_scale_work w;
   uint64_t* bad;
+  RelocArgs reloc;   // optional fused relocation (reloc.n == 0: none)
 };
 
 // Array base + element count of target t: from the resolved table, or re-walked (CHASE).
@@ -274,8 +280,14 @@ __global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
     scale_range<T, CHASE, SCALE_UNROLL>(a, t, arr, e0, e1, s, threadIdx.x, SCALE_THREADS);
     return;
   }
+  const uint64_t ngroups = a.w.group_end - a.w.group_begin;
+  if (blockIdx.x >= ntiles + ngroups) {
+    // fused relocation CTAs (detach riding in the leaf-kernel launch)
+    const uint64_t i = (blockIdx.x - ntiles - ngroups) * uint64_t(SCALE_THREADS) + threadIdx.x;
+    if (i < a.reloc.n) relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad);
+    return;
+  }
   const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
-  if (g >= a.w.group_end) return;
   const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (uint32_t p = p0 + warp; p < p1; p += SCALE_THREADS / 32) {
@@ -363,12 +375,16 @@ int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, 
 
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const int32_t* level, const uint64_t* ordinal, const uint64_t* ea, const uint32_t* count,
-                 const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s) {
-  const uint64_t units = (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin);
+                 const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s,
+                 const RelocArgs* fused_reloc) {
+  const uint64_t nreloc = fused_reloc ? fused_reloc->n : 0;
+  const uint64_t units = (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin) +
+                         (nreloc + SCALE_THREADS - 1) / SCALE_THREADS;
   if (units == 0) return CF_OK;
   if (units > 0x7FFFFFFFull) return fail(CF_E_INVALID, "leaf kernel: %llu work units exceed one grid",
                                          (unsigned long long)units);
-  ScaleArgs a{image, sh, level, ordinal, ea, count, work, bad};
+  ScaleArgs a{image, sh, level, ordinal, ea, count, work, bad, RelocArgs{}};
+  if (nreloc) a.reloc = *fused_reloc;
   // one CTA per 16 KiB tile / small-part group: measured faster than a persistent grid-stride
   // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware
   // CTA launcher keeps more independent loads in flight than a loop re-locating its part

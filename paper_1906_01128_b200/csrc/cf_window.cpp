@@ -46,6 +46,9 @@ struct cf_window {
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr, ev_first = nullptr, ev_tables = nullptr;
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
+  // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
+  struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
+  std::vector<Graph> graphs;
 };
 
 namespace {
@@ -70,6 +73,7 @@ void destroy(cf_window* w) {
   if (w->ev_join) cudaEventDestroy(w->ev_join);
   if (w->ev_first) cudaEventDestroy(w->ev_first);
   if (w->ev_tables) cudaEventDestroy(w->ev_tables);
+  for (auto& gr : w->graphs) cudaGraphExecDestroy(gr.exec);
   delete w;
 }
 
@@ -275,6 +279,7 @@ int cf_window_set_scale(cf_window* w, double scale) {
 
 namespace {
 int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out);
+int one_run(cf_window* w, bool timing, uint64_t* h2d, uint64_t* d2h);
 int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, uint64_t d2h, bool kernel_times,
            cudaEvent_t first);
 }  // namespace
@@ -284,9 +289,10 @@ int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
   CfDevice g(w->ctx);
   const uint64_t launches0 = w->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
-  const bool timing = sync != 0 && st != nullptr;
+  const bool timing = sync != 0 && st != nullptr && !(w->d.flags & CF_WIN_GRAPH);
   CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
-  CF_TRY(enqueue(w, timing, &h2d, &d2h));
+  CF_TRY(one_run(w, timing, &h2d, &d2h));
+  CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
   if (!sync) return CF_OK;
   return finish(w, st, launches0, h2d, d2h, timing, w->ev_first);
 }
@@ -300,14 +306,47 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
   for (int r = 0; r < nruns; ++r) {
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;
-    CF_TRY(enqueue(w, false, &a, &b));
+    CF_TRY(one_run(w, false, &a, &b));
     h2d += a;
     d2h += b;
   }
+  CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
   return finish(w, st, launches0, h2d, d2h, false, w->ev_first);
 }
 
 namespace {
+// Direct enqueue, or (CF_WIN_GRAPH) capture the whole multi-stream sequence once per scale value
+// into a CUDA graph and replay it: one launch call instead of ~100 per window.
+int one_run(cf_window* w, bool timing, uint64_t* h2d, uint64_t* d2h) {
+  if (!(w->d.flags & CF_WIN_GRAPH)) return enqueue(w, timing, h2d, d2h);
+  cf_ctx* c = w->ctx;
+  cf_window::Graph* gr = nullptr;
+  for (auto& g : w->graphs)
+    if (g.scale == w->d.scale) gr = &g;
+  if (!gr) {
+    cf_window::Graph g{w->d.scale, nullptr, 0, 0, 0};
+    const uint64_t l0 = c->launches.load();
+    CF_CUDA(cudaStreamBeginCapture(c->compute, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue(w, false, &g.h2d, &g.d2h);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(c->compute, &graph);
+    if (rc != CF_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (ce != cudaSuccess) return fail(CF_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(CF_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    g.launches = c->launches.load() - l0;
+    c->launches.fetch_sub(g.launches);  // counted when the graph actually runs
+    w->graphs.push_back(g);
+    gr = &w->graphs.back();
+  }
+  CF_CUDA(cudaGraphLaunch(gr->exec, c->compute));
+  c->launches.fetch_add(gr->launches);
+  *h2d = gr->h2d;
+  *d2h = gr->d2h;
+  return CF_OK;
+}
+
 int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   cf_ctx* c = w->ctx;
   const cf_window_desc& d = w->d;
@@ -354,15 +393,21 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     if ((fl & CF_WIN_RESOLVE) && !chase)
       CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], w->res_lo[k + 1] - w->res_lo[k],
                             w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
+    // In RESOLVED mode the leaf kernel never reads pointer fields, and every resolve that reads
+    // the fields detached at this step has already run: the detach rides in the same launch.
+    const bool fuse_detach = (fl & CF_WIN_DETACH) && (fl & CF_WIN_SCALE) && !chase && !timing;
     if (fl & CF_WIN_SCALE) {
       const cf_scale_work& sg = w->seg[k];
-      if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin) {
+      const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
+      if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs));
+        RelocArgs det{img, w->bounds.back(), ddet + w->det_lo[k], nd, dimg, d.host_base};
+        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
+                            nd ? &det : nullptr));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
-    if (fl & CF_WIN_DETACH)
+    if ((fl & CF_WIN_DETACH) && !fuse_detach)
       CF_TRY(launch_relocate(c, img, w->bounds.back(), ddet + w->det_lo[k], w->det_lo[k + 1] - w->det_lo[k], dimg,
                              d.host_base, c->d_bad, cs));
     if ((fl & CF_WIN_D2H) && !w->released[k].empty()) {
@@ -385,7 +430,6 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   // the error word is the step's result read back to the host
   CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, cs));
   d2h_bytes += 8;
-  CF_CUDA(cudaEventRecord(w->ev_end, cs));
   *h2d_out = h2d_bytes;
   *d2h_out = d2h_bytes;
   return CF_OK;

@@ -85,7 +85,7 @@ class DeepCopyWindow:
         """Enqueue ``nruns`` windows back to back (scale alternating 2.0 / 0.5, exact in IEEE so
         the data stays bounded) and wait once; stats cover the whole sequence."""
         cb = self.chunk_bytes if chunk_bytes is None else chunk_bytes
-        if flags == N.CF_WIN_RESIDENT:
+        if not flags & (N.CF_WIN_H2D | N.CF_WIN_D2H):
             cb = 0
         w = self._window(flags, cb, mode or self.mode)
         st = N.CfWindowStats()
@@ -97,9 +97,10 @@ class DeepCopyWindow:
         """Put the un-relocated arena bytes into the device image (prepares run_resident)."""
         N.check(N.lib().cf_memcpy(self.ctx.handle, self.image, self.src, self.total), "upload")
 
-    def run_resident(self, scale: float | None = None, mode: str | None = None, sync: bool = True):
+    def run_resident(self, scale: float | None = None, mode: str | None = None, sync: bool = True,
+                     graph: bool = False):
         """attach -> resolve -> scale -> detach on the HBM-resident image (one chunk)."""
-        return self._run(N.CF_WIN_RESIDENT, 0, mode, scale, sync)
+        return self._run(N.CF_WIN_RESIDENT | (N.CF_WIN_GRAPH if graph else 0), 0, mode, scale, sync)
 
     # -- inspection ----------------------------------------------------------------------
     def host_src(self) -> np.ndarray:

@@ -9,6 +9,8 @@ import random
 import numpy as np
 import pytest
 
+from paper_1906_01128_b200 import _native as N
+
 pytestmark = pytest.mark.gpu
 
 NO_BAD = (1 << 64) - 1
@@ -179,11 +181,20 @@ def test_pipelined_window_matches_oracle_random_specs(cf, oracle, elem, mode):
             idx = oracle.targets(ot, pol)
             want = oracle.expected_after_window(ot, idx, 2.0)[:w.total]
             assert np.array_equal(w.host_dst(), want), (j, align, policy, chunk)
+            # same window replayed from a captured CUDA graph (detach fused into the leaf launch)
+            st = w.run(scale=2.0, flags=N.CF_WIN_FULL | N.CF_WIN_GRAPH)
+            st = w.run(scale=2.0, flags=N.CF_WIN_FULL | N.CF_WIN_GRAPH)
+            assert st.bad == NO_BAD
+            assert np.array_equal(w.host_dst(), want), (j, align, policy, chunk, "graph")
             # resident path on the same image: attach -> resolve -> scale -> detach
             w.upload_raw()
             st = w.run_resident(scale=2.0)
             assert st.bad == NO_BAD
             assert np.array_equal(w.image_bytes(), want), (j, align, policy, "resident")
+            w.upload_raw()
+            st = w.run_resident(scale=2.0, graph=True)
+            assert st.bad == NO_BAD
+            assert np.array_equal(w.image_bytes(), want), (j, align, policy, "resident graph")
         finally:
             w.close()
 

@@ -1,0 +1,69 @@
+"""Multi-process (gloo, world_size 2, CPU) checks of the sharded benchmark plumbing: shard
+assignment, barrier, max-over-ranks timing, whole-job aggregation, and the reference arm's
+rank-0-only rule.  The GPU data path has no collective, so this covers all cross-rank logic."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import REPO
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(REPO))
+    import bench
+    from paper_1906_01128_b200 import DenseSpec
+    from paper_1906_01128_b200.shard import aggregate_gbs, shard_for
+    d = bench.Dist()
+    spec = DenseSpec(4, 4 << 20, 3, elem=4, leaf_only=True)
+    sh = shard_for(spec, d.rank, d.world)
+    strong = shard_for(DenseSpec(4, 268_435_456, 3, elem=4, leaf_only=True), d.rank, d.world, "strong")
+    d.barrier()
+    ms = d.max(10.0 + 5.0 * d.rank)
+    total = d.sum(1000.0)
+    with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
+        json.dump({"seed": sh.seed, "n": sh.spec.n, "strong_n": strong.spec.n, "max_ms": ms, "sum": total,
+                   "gbs": aggregate_gbs([1 << 30] * d.world, ms)}, f)
+    d.close()
+
+
+def test_two_rank_gloo_plumbing(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r = [json.loads((tmp_path / f"r{i}.json").read_text()) for i in range(2)]
+    assert [x["seed"] for x in r] == [1, 2]                 # distinct shards
+    assert all(x["n"] == 4 << 20 for x in r)                # weak: fixed per-GPU work
+    assert all(x["strong_n"] == 268_435_456 // 2 for x in r)  # strong: split payload
+    assert all(x["max_ms"] == 15.0 for x in r)              # max over ranks
+    assert all(x["sum"] == 2000.0 for x in r)
+    assert r[0]["gbs"] == pytest.approx(2 * (1 << 30) / 15e-3 / 1e9)
+
+
+def test_reference_arm_under_torchrun_rank1_is_silent(tmp_path):
+    """`torchrun --nproc-per-node 2 bench.py --impl reference`: rank 0 prints one line, rank 1 nothing."""
+    port = _free_port()
+    env = dict(os.environ, CF_ORACLE_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(REPO / "bench.py"),
+           "--impl", "reference", "--config", "C1", "--steps", "2", "--warmup", "3", "--gpus", "2"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=str(tmp_path))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

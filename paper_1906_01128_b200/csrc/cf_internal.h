@@ -40,6 +40,12 @@ void clear_error();
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
                     uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s);
+// One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).
+constexpr uint64_t SMALL_FUSED = 4096;
+int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const int32_t* level,
+                          const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
+                          cudaStream_t s);
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh,
                    const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea,
                    uint32_t* count, uint64_t* bad, cudaStream_t s);

@@ -142,6 +142,30 @@ __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ ima
   count[i] = ld_u32_any(w.node + OFF_NA);
 }
 
+// Small windows (C2: 85 sites, 64 chains): attach and resolve in ONE CTA -- the barrier between
+// them is a __syncthreads instead of a kernel boundary.
+__global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ image, uint64_t total,
+                                                         const uint64_t* __restrict__ sites, uint64_t nsites,
+                                                         uint64_t from, uint64_t to, cf_chain_shape sh,
+                                                         const int32_t* __restrict__ level,
+                                                         const uint64_t* __restrict__ ordinal, uint64_t ntargets,
+                                                         uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
+                                                         uint64_t* bad) {
+  for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
+  __syncthreads();
+  for (uint64_t i = threadIdx.x; i < ntargets; i += blockDim.x) {
+    Walk w = walk_chain<false>(image, sh, level[i], ordinal[i]);
+    if (!w.node) {
+      ea[i] = 0;
+      count[i] = 0;
+      raise_bad(bad, i);
+      continue;
+    }
+    ea[i] = ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A));
+    count[i] = ld_u32_any(w.node + OFF_NA);
+  }
+}
+
 // ---------------------------------------------------------------- leaf kernel
 template <typename T> struct Vec;
 template <> struct Vec<float> {
@@ -255,6 +279,97 @@ __device__ __forceinline__ void scale_range(const ScaleArgs& a, uint64_t t, uint
   for (; j < nv; j += lanes) VT::st(p + j, VT::mul(VT::ld(p + j), s));
 }
 
+// A group of small parts (<= GROUP_PARTS arrays, <= 16 KiB): warp 0 loads every part's
+// metadata once (one dependent-load round per group, not per part) and prefix-sums the vector
+// counts into shared memory; then all 256 threads stream the group's 16-byte vectors as one
+// flattened range, 4 independent loads in flight per thread.  Scalar heads/tails (only in
+// packed layouts) are handled per part afterwards.
+template <typename T, bool CHASE>
+__device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s) {
+  using VT = Vec<T>;
+  using V = typename VT::V;
+  constexpr uint64_t VN = VT::N;
+  __shared__ uint8_t* s_base[GROUP_PARTS];    // array base (resolved), nullptr if rejected
+  __shared__ uint64_t s_v0[GROUP_PARTS];      // first 16-byte-aligned element
+  __shared__ uint32_t s_pre[GROUP_PARTS + 1]; // exclusive prefix of vector counts
+  __shared__ uint64_t s_t[GROUP_PARTS];
+  const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
+  const uint32_t np = p1 - p0;
+  const unsigned lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    uint32_t nv = 0;
+    if (lane < np) {
+      const uint64_t p = p0 + lane;
+      const uint64_t t = a.w.parts[3 * p], e0 = a.w.parts[3 * p + 1], e1 = a.w.parts[3 * p + 2];
+      uint8_t* arr;
+      uint64_t cnt;
+      s_t[lane] = t;
+      if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
+        raise_bad(a.bad, t);
+        s_base[lane] = nullptr;
+        s_v0[lane] = e1;
+      } else {
+        const uintptr_t first = reinterpret_cast<uintptr_t>(arr + e0 * sizeof(T));
+        uint64_t v0 = e1;
+        if ((first % sizeof(T)) == 0) v0 = min(e1, e0 + ((16 - (first & 15)) & 15) / sizeof(T));
+        nv = uint32_t((e1 - v0) / VN);
+        s_base[lane] = arr;
+        s_v0[lane] = v0;
+      }
+    }
+    uint32_t inc = nv;  // warp inclusive scan -> exclusive prefix
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= unsigned(d)) inc += o;
+    }
+    if (lane < np) s_pre[lane] = inc - nv;
+    if (lane == np - 1) s_pre[np] = inc;
+  }
+  __syncthreads();
+  const uint32_t total = s_pre[np];
+  // address of flattened vector j (CHASE: through a freshly walked chain per access)
+  auto vec_ptr = [&](uint32_t j) -> V* {
+    uint32_t lo = 0, hi = np;  // largest k with s_pre[k] <= j
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= j) lo = mid; else hi = mid;
+    }
+    uint8_t* base = CHASE ? chase_base<true>(a, s_t[lo], nullptr) : s_base[lo];
+    return reinterpret_cast<V*>(base + s_v0[lo] * sizeof(T)) + (j - s_pre[lo]);
+  };
+  constexpr int U = 4;
+  uint32_t j = threadIdx.x;
+  for (; j + (U - 1) * SCALE_THREADS < total; j += U * SCALE_THREADS) {
+    V* ptr[U];
+    V r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ptr[u] = vec_ptr(j + u * SCALE_THREADS);
+      r[u] = VT::ld(ptr[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) VT::st(ptr[u], VT::mul(r[u], s));
+  }
+  for (; j < total; j += SCALE_THREADS) {
+    V* p = vec_ptr(j);
+    VT::st(p, VT::mul(VT::ld(p), s));
+  }
+  // scalar heads / tails (non-empty only in packed layouts); one warp per part
+  const unsigned warp = threadIdx.x >> 5;
+  for (uint32_t k = warp; k < np; k += SCALE_THREADS / 32) {
+    uint8_t* base = s_base[k];
+    if (base == nullptr) continue;
+    const uint64_t p = p0 + k;
+    const uint64_t e0 = a.w.parts[3 * p + 1], e1 = a.w.parts[3 * p + 2];
+    const uint64_t v0 = s_v0[k], v1 = v0 + uint64_t(s_pre[k + 1] - s_pre[k]) * VN;
+    for (uint64_t i = e0 + lane; i < v0; i += 32)
+      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
+    for (uint64_t i = v1 + lane; i < e1; i += 32)
+      scalar_st<T>(base + i * sizeof(T), mul_rn<T>(scalar_ld<T>(base + i * sizeof(T)), s));
+  }
+}
+
 // One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
 // blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part.
 template <typename T, bool CHASE>
@@ -288,19 +403,7 @@ __global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
     return;
   }
   const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
-  const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
-  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t p = p0 + warp; p < p1; p += SCALE_THREADS / 32) {
-    const uint64_t t = a.w.parts[3ull * p];
-    const uint64_t e0 = a.w.parts[3ull * p + 1], e1 = a.w.parts[3ull * p + 2];
-    uint8_t* arr;
-    uint64_t cnt;
-    if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
-      if (lane == 0) raise_bad(a.bad, t);
-      continue;
-    }
-    scale_range<T, CHASE, 2>(a, t, arr, e0, e1, s, lane, 32);
-  }
+  scale_group<T, CHASE>(a, g, s);
 }
 
 // ---------------------------------------------------------------- naive fix-up
@@ -360,6 +463,18 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
                     uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, n, from, to, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const int32_t* level,
+                          const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
+                          cudaStream_t s) {
+  if (nsites == 0 && ntargets == 0) return CF_OK;
+  const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
+  k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, level, ordinal, ntargets, ea,
+                                        count, bad);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -291,7 +291,11 @@ int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
   uint64_t h2d = 0, d2h = 0;
   const bool timing = sync != 0 && st != nullptr && !(w->d.flags & CF_WIN_GRAPH);
   CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
+  CF_CUDA(cudaMemsetAsync(w->ctx->d_bad, 0xFF, 8, w->ctx->compute));
   CF_TRY(one_run(w, timing, &h2d, &d2h));
+  // the error word (sticky over the batch) is read back once, after the last window
+  CF_CUDA(cudaMemcpyAsync(w->ctx->h_bad, w->ctx->d_bad, 8, cudaMemcpyDeviceToHost, w->ctx->compute));
+  d2h += 8;
   CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
   if (!sync) return CF_OK;
   return finish(w, st, launches0, h2d, d2h, timing, w->ev_first);
@@ -303,6 +307,7 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
   const uint64_t launches0 = w->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
   CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
+  CF_CUDA(cudaMemsetAsync(w->ctx->d_bad, 0xFF, 8, w->ctx->compute));
   for (int r = 0; r < nruns; ++r) {
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;
@@ -310,6 +315,8 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
     h2d += a;
     d2h += b;
   }
+  CF_CUDA(cudaMemcpyAsync(w->ctx->h_bad, w->ctx->d_bad, 8, cudaMemcpyDeviceToHost, w->ctx->compute));
+  d2h += 8;
   CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
   return finish(w, st, launches0, h2d, d2h, false, w->ev_first);
 }
@@ -359,10 +366,13 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   cudaStream_t cs = c->compute;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
-  CF_CUDA(cudaEventRecord(w->ev_start, cs));
-  for (auto s : c->h2d) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
-  CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_start, 0));
-  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, cs));
+  // copy streams join only when this window copies anything (a resident window is kernels only)
+  const bool copies = (fl & (CF_WIN_H2D | CF_WIN_D2H | CF_WIN_TABLES)) != 0;
+  if (copies) {
+    CF_CUDA(cudaEventRecord(w->ev_start, cs));
+    for (auto s : c->h2d) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
+    CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_start, 0));
+  }
   if (fl & CF_WIN_TABLES) {
     // the relocation / chain tables travel with the arena, first on the H2D copy stream
     // (an H2D copy on the compute stream serialises badly against the D2H engine)
@@ -387,12 +397,19 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_CUDA(cudaStreamWaitEvent(cs, w->ev_h2d[k], 0));
       h2d_bytes += hi - lo;
     }
-    if (fl & CF_WIN_ATTACH)
-      CF_TRY(launch_relocate(c, img, w->bounds.back(), dsites + w->reloc_lo[k],
-                             w->reloc_lo[k + 1] - w->reloc_lo[k], d.host_base, dimg, c->d_bad, cs));
-    if ((fl & CF_WIN_RESOLVE) && !chase)
-      CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], w->res_lo[k + 1] - w->res_lo[k],
-                            w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
+    const uint64_t ns = w->reloc_lo[k + 1] - w->reloc_lo[k], nr = w->res_lo[k + 1] - w->res_lo[k];
+    const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
+    if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
+      CF_TRY(launch_attach_resolve(c, img, w->bounds.back(), dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
+                                   dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
+                                   w->d_count + w->res_lo[k], c->d_bad, cs));
+    } else {
+      if (do_attach)
+        CF_TRY(launch_relocate(c, img, w->bounds.back(), dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));
+      if (do_resolve)
+        CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
+                              w->d_count + w->res_lo[k], c->d_bad, cs));
+    }
     // In RESOLVED mode the leaf kernel never reads pointer fields, and every resolve that reads
     // the fields detached at this step has already run: the detach rides in the same launch.
     const bool fuse_detach = (fl & CF_WIN_DETACH) && (fl & CF_WIN_SCALE) && !chase && !timing;
@@ -421,15 +438,14 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     }
   }
   // join the copy streams back into the compute stream
-  for (auto s : c->h2d) {
-    CF_CUDA(cudaEventRecord(w->ev_join, s));
+  if (copies) {
+    for (auto s : c->h2d) {
+      CF_CUDA(cudaEventRecord(w->ev_join, s));
+      CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
+    }
+    CF_CUDA(cudaEventRecord(w->ev_join, c->d2h));
     CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
   }
-  CF_CUDA(cudaEventRecord(w->ev_join, c->d2h));
-  CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
-  // the error word is the step's result read back to the host
-  CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, cs));
-  d2h_bytes += 8;
   *h2d_out = h2d_bytes;
   *d2h_out = d2h_bytes;
   return CF_OK;

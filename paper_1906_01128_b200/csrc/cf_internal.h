@@ -73,7 +73,10 @@ inline uint64_t tiles_for(uint64_t elems, int elem) {
 
 // Small parts (< one tile) are packed into groups of at most GROUP_BYTES / GROUP_PARTS and
 // processed one warp per part, so 1M 1 KiB leaves do not become 1M mostly idle CTAs.
-constexpr uint64_t GROUP_BYTES = TILE_BYTES;
+#ifndef CF_GROUP_KB
+#define CF_GROUP_KB 32
+#endif
+constexpr uint64_t GROUP_BYTES = uint64_t(CF_GROUP_KB) << 10;
 constexpr uint32_t GROUP_PARTS = 32;
 
 // Host-side builder of the leaf-kernel work list (see cf_scale_work in the header).

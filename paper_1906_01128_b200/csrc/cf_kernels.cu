@@ -22,6 +22,14 @@
 
 #include <algorithm>
 
+// tuning knobs (design experiments: tools/build_variants.sh)
+#ifndef CF_SCALE_MINB
+#define CF_SCALE_MINB 8
+#endif
+#ifndef CF_GROUP_U
+#define CF_GROUP_U 4
+#endif
+
 namespace cf {
 namespace {
 
@@ -338,7 +346,7 @@ __device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s)
     uint8_t* base = CHASE ? chase_base<true>(a, s_t[lo], nullptr) : s_base[lo];
     return reinterpret_cast<V*>(base + s_v0[lo] * sizeof(T)) + (j - s_pre[lo]);
   };
-  constexpr int U = 4;
+  constexpr int U = CF_GROUP_U;
   uint32_t j = threadIdx.x;
   for (; j + (U - 1) * SCALE_THREADS < total; j += U * SCALE_THREADS) {
     V* ptr[U];
@@ -373,7 +381,7 @@ __device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s)
 // One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
 // blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part.
 template <typename T, bool CHASE>
-__global__ void __launch_bounds__(SCALE_THREADS) k_scale(ScaleArgs a, T s) {
+__global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArgs a, T s) {
   constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
   const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
   if (blockIdx.x < ntiles) {

@@ -202,6 +202,50 @@ def cpu_window(spec, policy: str, seed: int, steps: int, warmup: int, threads: i
     return times, t.total
 
 
+def compare_schemes(spec, policy: str, reps: int, device: int) -> dict:
+    """The four transfer schemes of the reference (harness.py:219-325) through the drop-in API on
+    the same graph: window = transfer_to_device -> kernel_scale -> copy_back, host wall clock
+    with device syncs, median of `reps` after one warm-up.  UVM is measured without hints and
+    with a whole-tree prefetch; GB/s are graph bytes over the window."""
+    import paper_1906_01128_b200 as cf
+    out = {}
+    plans = (("marshalling", "marshalling", {}), ("pointerchain", "pointerchain", {}), ("naive", "naive", {}),
+             ("uvm", "uvm", {"uvm_hints": "none"}), ("uvm_prefetch", "uvm", {"uvm_hints": "prefetch"}))
+    for name, scheme, kw in plans:
+        m = cf.Machine(device=device)
+        try:
+            if scheme == "uvm":
+                m.enable_uvm()
+            if scheme == "marshalling":
+                arena, h = cf.marshal_tree(m, spec, seed=1, align=16)
+            else:
+                arena, h = None, cf.build_tree(m, spec, seed=1, align=16)
+            times, h2d = [], 0
+            for r in range(reps + 1):
+                m.ctx.sync()
+                mark = m.log.mark()
+                t0 = time.perf_counter()
+                prep = cf.transfer_to_device(m, h, scheme, arena, policy=policy, **kw)
+                cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5)
+                cf.copy_back(m, h, prep)
+                m.ctx.sync()
+                if r:
+                    times.append(time.perf_counter() - t0)
+                    h2d = m.log.bytes_moved("H2D", mark)
+            med = statistics.median(times)
+            out[name] = {"window_ms": round(med * 1e3, 3), "graph_gbs": round(h.total_bytes / med / 1e9, 3),
+                         "h2d_bytes": int(h2d)}
+        except Exception as exc:  # a scheme failing must not hide the others; it is reported
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+        finally:
+            m.close()
+    if "uvm" in out and "window_ms" in out["uvm"]:
+        for v in out.values():
+            if "window_ms" in v:
+                v["normalized_to_uvm"] = round(v["window_ms"] / out["uvm"]["window_ms"], 4)
+    return out
+
+
 def run_reference(args, dist: Dist) -> None:
     if dist.rank != 0:
         return
@@ -343,6 +387,8 @@ def run_ours(args, dist: Dist) -> None:
         "clocks": clk,
         "build_s": round(t_build, 2),
     }
+    if dist.rank == 0 and not args.skip_schemes:
+        line["schemes"] = compare_schemes(spec, policy, 3, device)
     if dist.rank == 0 and not args.skip_cpu_baseline:
         from oracle import oracle as O
         threads = O.default_threads()
@@ -370,6 +416,7 @@ def main(argv=None):
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-chase", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="enqueue every window directly (no CUDA graph)")
+    ap.add_argument("--skip-schemes", action="store_true", help="skip the 4-scheme drop-in API comparison")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -125,7 +125,8 @@ int cf_host_free(void* p, int kind);            /* PINNED / MANAGED */
 int cf_host_free_sized(void* p, uint64_t bytes, int kind); /* any kind */
 int cf_dev_alloc(cf_ctx* ctx, uint64_t bytes, void** out);
 int cf_dev_free(cf_ctx* ctx, void* p);
-/* Synchronous copy between any two spaces (Machine.transfer_range, memory.py:294-303). */
+/* Synchronous copy between any two spaces (Machine.transfer_range, memory.py:294-303), ordered
+ * after all work already enqueued on the context's compute stream. */
 int cf_memcpy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int cf_memcpy_async(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, void* stream);
 int cf_memset(cf_ctx* ctx, void* dst, int value, uint64_t bytes);
@@ -215,6 +216,14 @@ int cf_memcpy_batch(cf_ctx* ctx, void* const* dsts, const void* const* srcs,
 int cf_naive_fixup(cf_ctx* ctx, const uint64_t* d_site_field_host, const uint64_t* d_site_target_host,
                    uint64_t nsites, const uint64_t* d_map_host_base, const uint64_t* d_map_size,
                    const uint64_t* d_map_dev_base, uint64_t nmap, uint64_t* d_bad, void* stream);
+
+/* ---------------- unified memory (memory.py:239-261, 378-394) ---------------- */
+/* Managed-memory hints for the UVM scheme. dst_device < 0 prefetches to the host (the
+ * reference's copy-back re-touch of dirty pages, harness.py:321-325). advice: 0 = none,
+ * 1 = SetPreferredLocation(device), 2 = SetAccessedBy(device), 3 = SetReadMostly. */
+enum { CF_UVM_ADVISE_NONE = 0, CF_UVM_PREFERRED_DEVICE = 1, CF_UVM_ACCESSED_BY = 2, CF_UVM_READ_MOSTLY = 3 };
+int cf_uvm_prefetch(cf_ctx* ctx, const void* p, uint64_t bytes, int dst_device, void* stream);
+int cf_uvm_advise(cf_ctx* ctx, const void* p, uint64_t bytes, int advice);
 
 /* ---------------- pipelined metered window (harness.py:369-373) ---------------- */
 /* Flags for the window */

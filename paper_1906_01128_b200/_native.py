@@ -24,6 +24,7 @@ CF_LINEAR, CF_DENSE = 0, 1
 CF_MEM_PAGEABLE, CF_MEM_PINNED, CF_MEM_MANAGED = 0, 1, 2
 CF_TARGET_REF, CF_TARGET_ALL_LEAVES, CF_TARGET_ALL_ARRAYS = 0, 1, 2
 CF_MODE_RESOLVED, CF_MODE_CHASE = 0, 1
+CF_UVM_ADVISE_NONE, CF_UVM_PREFERRED_DEVICE, CF_UVM_ACCESSED_BY, CF_UVM_READ_MOSTLY = 0, 1, 2, 3
 (CF_TAB_ALLOC_OFF, CF_TAB_ALLOC_SIZE, CF_TAB_NODE_OFF, CF_TAB_NODE_LEVEL, CF_TAB_NODE_SIZE,
  CF_TAB_ARR_LEVEL, CF_TAB_ARR_OWNER, CF_TAB_ARR_OFF, CF_TAB_ARR_COUNT, CF_TAB_SITE_OFF,
  CF_TAB_SITE_TARGET, CF_TAB_SITE_SORTED, CF_TAB_ARR_ORDINAL) = range(13)
@@ -45,6 +46,7 @@ EXPORTED = (
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_set_scale", "cf_window_free",
+    "cf_uvm_prefetch", "cf_uvm_advise",
 )
 
 
@@ -125,6 +127,8 @@ def _declare(L):
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
         "cf_window_free": (C.c_int, [P]),
+        "cf_uvm_prefetch": (C.c_int, [P, P, U64, C.c_int, P]),
+        "cf_uvm_advise": (C.c_int, [P, P, U64, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -137,6 +137,10 @@ struct cf_ctx {
   uint64_t* d_bad = nullptr;   // device scratch error word
   uint64_t* h_bad = nullptr;   // pinned mirror
   std::atomic<uint64_t> launches{0};
+  // grow-only device scratch for the synchronous reference-named operations (avoids a
+  // cudaMalloc/cudaFree -- and the implicit device sync of cudaFree -- per call)
+  void* scratch = nullptr;
+  uint64_t scratch_bytes = 0;
 };
 
 struct cf_tree {

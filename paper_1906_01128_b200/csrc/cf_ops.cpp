@@ -15,19 +15,31 @@ namespace {
 
 cudaStream_t pick(cf_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->compute; }
 
-// RAII device buffer
+// Device scratch taken from the context's grow-only buffer (callers are synchronous, one
+// operation at a time per context).
 struct DevBuf {
+  cf_ctx* c;
   void* p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
+  explicit DevBuf(cf_ctx* ctx) : c(ctx) {}
   int alloc(uint64_t bytes) {
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      p = nullptr;
-      return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "cudaMalloc(%llu): %s",
-                  (unsigned long long)bytes, cudaGetErrorString(e));
+    if (bytes > c->scratch_bytes) {
+      if (c->scratch) {
+        cudaStreamSynchronize(c->compute);
+        cudaFree(c->scratch);
+        c->scratch = nullptr;
+        c->scratch_bytes = 0;
+      }
+      const uint64_t want = std::max<uint64_t>(bytes, 1ull << 20);
+      cudaError_t e = cudaMalloc(&c->scratch, want);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "cudaMalloc(%llu): %s",
+                    (unsigned long long)want, cudaGetErrorString(e));
+      }
+      c->scratch_bytes = want;
     }
+    p = c->scratch;
     return CF_OK;
   }
   template <typename T> T* as() const { return static_cast<T*>(p); }
@@ -125,7 +137,7 @@ int cf_marshal_transfer_and_attach(cf_ctx* c, const void* host_arena, uint64_t t
   if (total == 0) return fail(CF_E_INVALID, "empty arena");
   CfDevice g(c);
   if (bad_site) *bad_site = NO_BAD;
-  DevBuf d_sites;
+  DevBuf d_sites(c);
   CF_TRY(d_sites.alloc(nsites * 8));
   const uint64_t base = reinterpret_cast<uint64_t>(host_arena);
   const uint64_t dimg = reinterpret_cast<uint64_t>(image);
@@ -175,7 +187,7 @@ int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const
   if (!c || !host_arena || !image || (nsites && !h_sites)) return fail(CF_E_INVALID, "null argument");
   CfDevice g(c);
   if (bad_site) *bad_site = NO_BAD;
-  DevBuf d_sites;
+  DevBuf d_sites(c);
   CF_TRY(d_sites.alloc(nsites * 8));
   const uint64_t base = reinterpret_cast<uint64_t>(host_arena);
   const uint64_t dimg = reinterpret_cast<uint64_t>(image);
@@ -223,7 +235,7 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   const uint64_t off_ea = off_ord + ntargets * 8;
   const uint64_t off_cnt = off_ea + ntargets * 8;
   const uint64_t off_work = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
-  DevBuf blk;
+  DevBuf blk(c);
   CF_TRY(blk.alloc(off_work + work_bytes(sw) + 8));
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;
@@ -271,7 +283,7 @@ int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t*
   cf_scale_work work = sw.append(tri);
   if (sw.nparts() == 0) return CF_OK;
   const uint64_t off_cnt = n * 8, off_work = off_cnt + ((n * 4 + 7) / 8) * 8;
-  DevBuf blk;
+  DevBuf blk(c);
   CF_TRY(blk.alloc(off_work + work_bytes(sw) + 8));
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;

@@ -80,6 +80,7 @@ int cf_ctx_destroy(cf_ctx* c) {
   for (auto s : c->h2d) cudaStreamDestroy(s);
   cudaFree(c->d_bad);
   cudaFreeHost(c->h_bad);
+  if (c->scratch) cudaFree(c->scratch);
   delete c;
   return CF_OK;
 }
@@ -173,8 +174,12 @@ int cf_dev_free(cf_ctx* c, void* p) {
 
 int cf_memcpy(cf_ctx* c, void* dst, const void* src, uint64_t bytes) {
   if (bytes == 0) return CF_OK;
+  if (!c) return fail(CF_E_INVALID, "null ctx");
   CfDevice g(c);
-  CF_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  // ordered after everything already on the compute stream (the context's streams are
+  // non-blocking, so the legacy default stream would not order against them), then waited for
+  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->compute));
+  CF_CUDA(cudaStreamSynchronize(c->compute));
   return CF_OK;
 }
 
@@ -187,8 +192,10 @@ int cf_memcpy_async(cf_ctx* c, void* dst, const void* src, uint64_t bytes, void*
 }
 
 int cf_memset(cf_ctx* c, void* dst, int value, uint64_t bytes) {
+  if (!c) return fail(CF_E_INVALID, "null ctx");
   CfDevice g(c);
-  CF_CUDA(cudaMemset(dst, value, bytes));
+  CF_CUDA(cudaMemsetAsync(dst, value, bytes, c->compute));
+  CF_CUDA(cudaStreamSynchronize(c->compute));
   return CF_OK;
 }
 
@@ -219,6 +226,40 @@ int cf_memcpy_batch(cf_ctx* c, void* const* dsts, const void* const* srcs, const
         CF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));
     }
   }
+  return CF_OK;
+}
+
+int cf_uvm_prefetch(cf_ctx* c, const void* p, uint64_t bytes, int dst_device, void* stream) {
+  if (!c || !p) return fail(CF_E_INVALID, "null argument");
+  if (bytes == 0) return CF_OK;
+  CfDevice g(c);
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->compute;
+#if CUDART_VERSION >= 12080
+  cudaMemLocation loc;
+  loc.type = dst_device < 0 ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
+  loc.id = dst_device < 0 ? 0 : c->device;
+  CF_CUDA(cudaMemPrefetchAsync_v2(p, bytes, loc, 0, s));
+#else
+  CF_CUDA(cudaMemPrefetchAsync(p, bytes, dst_device < 0 ? cudaCpuDeviceId : c->device, s));
+#endif
+  return CF_OK;
+}
+
+int cf_uvm_advise(cf_ctx* c, const void* p, uint64_t bytes, int advice) {
+  if (!c || !p) return fail(CF_E_INVALID, "null argument");
+  if (advice == CF_UVM_ADVISE_NONE || bytes == 0) return CF_OK;
+  CfDevice g(c);
+  cudaMemoryAdvise a = advice == CF_UVM_PREFERRED_DEVICE ? cudaMemAdviseSetPreferredLocation
+                       : advice == CF_UVM_ACCESSED_BY    ? cudaMemAdviseSetAccessedBy
+                                                         : cudaMemAdviseSetReadMostly;
+#if CUDART_VERSION >= 12080
+  cudaMemLocation loc;
+  loc.type = cudaMemLocationTypeDevice;
+  loc.id = c->device;
+  CF_CUDA(cudaMemAdvise_v2(p, bytes, a, loc));
+#else
+  CF_CUDA(cudaMemAdvise(p, bytes, a, c->device));
+#endif
   return CF_OK;
 }
 

@@ -251,7 +251,8 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     sg.groups = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_grp);
   }
   // the device mirror starts valid so runs without CF_WIN_TABLES work
-  ce = cudaMemcpy(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice);
+  ce = cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, ctx->compute);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->compute);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "table upload: %s", cudaGetErrorString(ce)); }
 
   // ---- events

@@ -191,10 +191,14 @@ class DevicePrep:
     policy: str = "ref"
     image: int = 0
     image_bytes: int = 0
+    uvm_hints: str = "none"
+
+
+UVM_HINTS = ("none", "prefetch", "advise")
 
 
 def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena: Arena | None = None,
-                       policy: str = "ref") -> DevicePrep:
+                       policy: str = "ref", uvm_hints: str = "none") -> DevicePrep:
     if scheme == "marshalling":
         if arena is None:
             raise ValueError("marshalling needs the arena returned by marshal_tree")
@@ -206,18 +210,29 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         base, span = machine._naive_span
         return DevicePrep(scheme, device_root=root, amap=amap, policy=policy, image=base, image_bytes=span)
     if scheme == "pointerchain":
+        # host-side chain resolution, then one selective bulk copy per targeted array
+        # (harness.py:228-238), submitted together as one batched copy
         buffers = []
         for ref in targeted_arrays(handle, policy):
             if ref.count == 0:
                 continue
-            nbytes = ref.count * handle.spec.elem
-            dev = machine.device.allocate(nbytes)
-            machine.transfer_range(machine.host, ref.addr, machine.device, dev, nbytes, "bulk")
-            buffers.append((dev, ref))
+            buffers.append((machine.device.allocate(ref.count * handle.spec.elem), ref))
+        e = handle.spec.elem
+        machine.transfer_ranges(machine.host, [r.addr for _, r in buffers], machine.device,
+                                [d for d, _ in buffers], [r.count * e for _, r in buffers], "bulk")
         return DevicePrep(scheme, buffers=buffers, policy=policy)
     if scheme == "uvm":
+        # the tree already lives in managed memory (harness.py:239-240: no copy); optional
+        # driver hints: migrate the whole tree ahead of the kernel, or map it for remote access
+        if uvm_hints not in UVM_HINTS:
+            raise ValueError(f"unknown uvm hint {uvm_hints!r}")
+        ctx = machine.ctx.handle
+        if uvm_hints == "prefetch":
+            N.check(N.lib().cf_uvm_prefetch(ctx, handle.base, handle.total_bytes, machine.ctx.device, None))
+        elif uvm_hints == "advise":
+            N.check(N.lib().cf_uvm_advise(ctx, handle.base, handle.total_bytes, N.CF_UVM_ACCESSED_BY))
         return DevicePrep(scheme, device_root=handle.root_addr, policy=policy, image=handle.base,
-                          image_bytes=handle.total_bytes)
+                          image_bytes=handle.total_bytes, uvm_hints=uvm_hints)
     raise SchemeError(f"unknown transfer scheme {scheme!r}")
 
 
@@ -235,30 +250,27 @@ def _level_nodes(handle: TreeHandle, level: int) -> np.ndarray:
     return handle.node_off[handle.node_level == level]
 
 
-def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int) -> tuple[set, set]:
-    """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394).
-
-    Used for the logical page-fault counters; the data itself migrates under the CUDA driver.
-    """
+def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int):
+    """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394),
+    as sorted numpy arrays.  Used for the logical page-fault counters; the data itself migrates
+    under the CUDA driver."""
     spec = handle.spec
     base, e = handle.base, spec.elem
     linear = isinstance(spec, LinearSpec)
     q = 1 if linear else spec.q
     owner = {int(o): (int(a), int(c)) for o, a, c in zip(handle.arr_owner, handle.arr_off, handle.arr_count)}
-    touched, dirty = set(), set()
+    fields: list[int] = []
+    spans: list[tuple[int, int]] = []
 
     def node_at(level: int, ordinal: int) -> int:
         return int(_level_nodes(handle, level)[ordinal])
 
     def visit_terminal(node: int, a_off: int) -> None:
-        touched.add((base + node + a_off) // page)
+        fields.append(base + node + a_off)
         arr = owner.get(node)
         if arr and arr[1]:
-            a, n = base + arr[0], arr[1]
-            touched.add((base + node + OFF_NA) // page)
-            pages = range(a // page, (a + e * (n - 1)) // page + 1)
-            touched.update(pages)
-            dirty.update(pages)
+            fields.append(base + node + OFF_NA)
+            spans.append((base + arr[0], arr[1]))
 
     if policy == "ref" and linear:
         for level in range(spec.k):
@@ -266,18 +278,22 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
             if spec.all_levels_used or level == spec.k - 1:
                 visit_terminal(node, OFF_A)
             if level < spec.k - 1:
-                touched.add((base + node + OFF_LNEXT) // page)
+                fields.append(base + node + OFF_LNEXT)
     elif policy == "ref":
         for level in range(spec.depth):
-            touched.add((base + node_at(level, q ** level - 1) + OFF_LNEXT) // page)
+            fields.append(base + node_at(level, q ** level - 1) + OFF_LNEXT)
         visit_terminal(node_at(spec.depth, q ** spec.depth - 1), LEAF_OFF_A)
     else:
         for i in idx.tolist():
             L, ordv = int(handle.arr_level[i]), int(handle.arr_ordinal[i])
             for lv in range(L):
-                touched.add((base + node_at(lv, 0 if linear else ordv // q ** (L - lv)) + OFF_LNEXT) // page)
+                fields.append(base + node_at(lv, 0 if linear else ordv // q ** (L - lv)) + OFF_LNEXT)
             leaf = (not linear) and L == spec.depth
             visit_terminal(node_at(L, 0 if linear else ordv), LEAF_OFF_A if leaf else OFF_A)
+    # every element touch hits the page of its first byte (uvm_touch(aptr + e*i))
+    dirty = [np.arange(a // page, (a + e * (n - 1)) // page + 1, dtype=np.int64) for a, n in spans]
+    dirty = np.unique(np.concatenate(dirty)) if dirty else np.zeros(0, np.int64)
+    touched = np.union1d(np.array(fields, np.int64) // page, dirty)
     return touched, dirty
 
 
@@ -303,9 +319,9 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
     if prep.scheme == "uvm":
         touched, dirty = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
-        machine.uvm_touch_pages(sorted(touched), "read", "device")
-        for p in dirty:
-            machine.uvm.page_table[p].dirty = True
+        machine.uvm_touch_pages(touched, "read", "device")
+        if dirty.size:
+            machine.uvm_touch_pages(dirty, "write", "device")
     if len(idx) == 0:
         return stats
     sh = handle.chain_shape()
@@ -329,9 +345,17 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     elif prep.scheme == "naive":
         machine.naive_copy_back(handle, prep.amap)
     elif prep.scheme == "pointerchain":
-        for dev, ref in prep.buffers:
-            machine.transfer_range(machine.device, dev, machine.host, ref.addr, ref.count * handle.spec.elem, "bulk")
+        e = handle.spec.elem
+        machine.transfer_ranges(machine.device, [d for d, _ in prep.buffers], machine.host,
+                                [r.addr for _, r in prep.buffers], [r.count * e for _, r in prep.buffers], "bulk")
     elif prep.scheme == "uvm":
+        # the host re-touches every page the kernel dirtied (harness.py:321-325): migrate the
+        # targeted arrays back explicitly, then account the logical page migrations
+        ctx = machine.ctx.handle
+        for i in handle.target_indices(prep.policy).tolist():
+            n = int(handle.arr_count[i]) * handle.spec.elem
+            if n:
+                N.check(N.lib().cf_uvm_prefetch(ctx, handle.base + int(handle.arr_off[i]), n, -1, None))
         machine.ctx.sync()
         dirty = machine.uvm.dirty_pages()
         machine.uvm_touch_pages(dirty, "read", "host")
@@ -387,7 +411,7 @@ def _describe(spec) -> tuple[str, str, int, int]:
 
 def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale: float = 2.0,
                  mode: str = "resolved", policy: str = "ref", align: int | None = None,
-                 device: int = 0) -> tuple[RunMetrics, Machine]:
+                 device: int = 0, uvm_hints: str = "none") -> tuple[RunMetrics, Machine]:
     """Run one case once on the GPU; returns the metrics and the machine (for its log)."""
     if scheme not in SCHEMES:
         raise SchemeError(f"unknown transfer scheme {scheme!r}")
@@ -402,7 +426,7 @@ def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale:
     launches0 = machine.ctx.launches()
     mark = machine.log.mark()
     t0 = time.perf_counter()
-    prep = transfer_to_device(machine, handle, scheme, arena, policy=policy)
+    prep = transfer_to_device(machine, handle, scheme, arena, policy=policy, uvm_hints=uvm_hints)
     stats = kernel_scale(machine, handle, prep, scale, mode=mode)
     copy_back(machine, handle, prep)
     machine.ctx.sync()

@@ -410,25 +410,50 @@ class UvmState:
     """Logical page table of the unified-memory mode (memory.py:239-261).
 
     The real data lives in ``cudaMallocManaged`` memory and migrates under the CUDA driver;
-    this table keeps the reference's single-residence accounting (page_faults, migrations)
-    so RunMetrics stay comparable with the reference.
+    this table keeps the reference's single-residence accounting (page_faults, migrations) so
+    RunMetrics stay comparable.  Stored as sorted numpy columns (a 1 GiB tree is 262,144
+    pages); ``page_table`` materialises the reference's dict view on demand.
     """
 
     def __init__(self, page_size: int = DEFAULT_PAGE_SIZE):
         self.page_size = page_size
-        self.page_table: dict[int, PageState] = {}
+        self._pages = np.zeros(0, np.int64)
+        self._device = np.zeros(0, bool)
+        self._dirty = np.zeros(0, bool)
 
     def register_range(self, addr: int, size: int) -> None:
         first = addr // self.page_size
         last = (addr + size - 1) // self.page_size
-        for page in range(first, last + 1):
-            self.page_table.setdefault(page, PageState("host"))
+        self.register_pages(np.arange(first, last + 1, dtype=np.int64))
+
+    def register_pages(self, pages: np.ndarray) -> None:
+        new = np.setdiff1d(np.asarray(pages, np.int64), self._pages, assume_unique=False)
+        if new.size == 0:
+            return
+        allp = np.concatenate([self._pages, new])
+        order = np.argsort(allp, kind="stable")
+        self._pages = allp[order]
+        self._device = np.concatenate([self._device, np.zeros(new.size, bool)])[order]
+        self._dirty = np.concatenate([self._dirty, np.zeros(new.size, bool)])[order]
+
+    def index(self, pages) -> np.ndarray:
+        pages = np.asarray(pages, np.int64)
+        i = np.searchsorted(self._pages, pages)
+        ok = (i < self._pages.size) & (self._pages[np.minimum(i, max(self._pages.size - 1, 0))] == pages) \
+            if self._pages.size else np.zeros(pages.shape, bool)
+        return np.where(ok, i, -1)
+
+    @property
+    def page_table(self) -> dict:
+        return {int(p): PageState("device" if d else "host", bool(y))
+                for p, d, y in zip(self._pages, self._device, self._dirty)}
 
     def resident_pages(self, side: str) -> list[int]:
-        return sorted(p for p, st in self.page_table.items() if st.resident == side)
+        m = self._device if side == "device" else ~self._device
+        return self._pages[m].tolist()
 
     def dirty_pages(self) -> list[int]:
-        return sorted(p for p, st in self.page_table.items() if st.dirty)
+        return self._pages[self._dirty].tolist()
 
 
 class Machine:
@@ -494,6 +519,24 @@ class Machine:
         dst._check(dst_addr, nbytes)
         N.check(N.lib().cf_memcpy(self.ctx.handle, dst_addr, src_addr, nbytes), "transfer_range")
         self.log.append(H2D if dst.kind == "device" else D2H, op_kind, nbytes)
+
+    def transfer_ranges(self, src: MemorySpace, src_addrs, dst: MemorySpace, dst_addrs, sizes,
+                        op_kind: str = "bulk") -> None:
+        """Several transfer_range calls submitted as one batched copy (one log entry each)."""
+        if src.kind == dst.kind:
+            raise ValueError("transfer_range requires distinct memory spaces")
+        sa = np.ascontiguousarray(src_addrs, np.uint64)
+        da = np.ascontiguousarray(dst_addrs, np.uint64)
+        sz = np.ascontiguousarray(sizes, np.uint64)
+        if sa.size == 0:
+            return
+        for a, d, n in zip(sa.tolist(), da.tolist(), sz.tolist()):
+            src._check(a, n)
+            dst._check(d, n)
+        ctx = self.ctx.handle
+        N.check(N.lib().cf_memcpy_batch(ctx, N.ptr(da), N.ptr(sa), N.ptr(sz), sa.size, None), "transfer_ranges")
+        N.check(N.lib().cf_ctx_sync(ctx))
+        self.log.append_many(H2D if dst.kind == "device" else D2H, op_kind, sz.astype(np.int64))
 
     # -- marshalling (memory.py:307-345) ----------------------------------------------------
     def marshal_transfer_and_attach(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> int:
@@ -594,39 +637,32 @@ class Machine:
         """Route one access through the logical page table; returns migrations (0/1)."""
         if self.uvm is None:
             raise SimMemoryError("uvm_touch outside UVM mode")
-        state = self.uvm.page_table.get(addr // self.uvm.page_size)
-        if state is None:
+        (i,) = self.uvm.index([addr // self.uvm.page_size])
+        if i < 0:
             raise WildAccess(f"unified access at 0x{addr:x} hits no registered page")
-        migrated = 0
-        if state.resident != actor:
-            self.log.append(H2D if actor == "device" else D2H, "page_migration", self.uvm.page_size)
-            state.resident = actor
-            state.dirty = False
-            migrated = 1
-        if access == "write":
-            state.dirty = True
-        return migrated
+        return self._touch(np.array([i]), access, actor)
 
     def uvm_touch_pages(self, pages, access: str, actor: str) -> int:
         """Vectorised uvm_touch over a set of page numbers (one touch per page)."""
         if self.uvm is None:
             raise SimMemoryError("uvm_touch outside UVM mode")
-        table = self.uvm.page_table
-        migrated = 0
-        for page in pages:
-            state = table.get(int(page))
-            if state is None:
-                raise WildAccess(f"unified access at page {int(page)} hits no registered page")
-            if state.resident != actor:
-                state.resident = actor
-                state.dirty = False
-                migrated += 1
-            if access == "write":
-                state.dirty = True
-        if migrated:
-            self.log.append_many(H2D if actor == "device" else D2H, "page_migration",
-                                 np.full(migrated, self.uvm.page_size, np.int64))
-        return migrated
+        idx = self.uvm.index(np.unique(np.asarray(pages, np.int64)))
+        if (idx < 0).any():
+            raise WildAccess("unified access hits no registered page")
+        return self._touch(idx, access, actor)
+
+    def _touch(self, idx: np.ndarray, access: str, actor: str) -> int:
+        u = self.uvm
+        on_device = actor == "device"
+        move = idx[u._device[idx] != on_device]
+        if move.size:
+            u._device[move] = on_device
+            u._dirty[move] = False
+            self.log.append_many(H2D if on_device else D2H, "page_migration",
+                                 np.full(move.size, u.page_size, np.int64))
+        if access == "write":
+            u._dirty[idx] = True
+        return int(move.size)
 
 
 def _poke_words(fields: np.ndarray, values: np.ndarray) -> None:

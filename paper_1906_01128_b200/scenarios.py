@@ -257,8 +257,12 @@ def _build(machine: Machine, spec, arena: Arena | None, seed: int, align: int | 
         arena.served_offset = total
         arena.set_site_offsets(handle.site_off, plan.table(N.CF_TAB_SITE_SORTED))
     elif machine.uvm is not None:
-        for off, size in zip(handle.alloc_off.tolist(), handle.alloc_size.tolist()):
-            machine.uvm.register_range(base + off, size)
+        ps = machine.uvm.page_size
+        first = (np.uint64(base) + handle.alloc_off) // np.uint64(ps)
+        last = (np.uint64(base) + handle.alloc_off + handle.alloc_size - np.uint64(1)) // np.uint64(ps)
+        pages = np.unique(np.concatenate([np.arange(int(a), int(b) + 1, dtype=np.int64)
+                                          for a, b in zip(first, last)]))
+        machine.uvm.register_pages(pages)
     return handle
 
 

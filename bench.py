@@ -40,6 +40,9 @@ CONFIGS = {
            "C1: depth-1 struct with one float32 leaf array of 1M elements"),
     "C2": ("dense", (4, 4 << 20, 3), 4, True, "all_leaves",
            "C2: depth-4 pointer chain, dense q=4 layout, 64 leaf arrays x 4Mi float32 (leaves only)"),
+    "C3": ("forest", (4, 4 << 20, "LLinit_LLused"), 4, False, "all_leaves",
+           "C3: 64 x depth-4 linear chains (LLinit_LLused), 64 leaves x 4Mi float32, 320 objects scattered "
+           "over the slab (seeded permutation)"),
     "C4": ("dense", (100, 256, 3), 4, False, "all_leaves",
            "C4: 1,010,101 structs, 1M leaves x 256 float32, depth 3, relocation-bound"),
     "C5": ("dense", (4, 268_435_456, 3), 4, True, "all_leaves",
@@ -48,8 +51,10 @@ CONFIGS = {
 
 
 def make_spec(name: str):
-    from paper_1906_01128_b200 import DenseSpec, LinearSpec
+    from paper_1906_01128_b200 import DenseSpec, ForestSpec, LinearSpec
     kind, args, elem, leaf_only, policy, desc = CONFIGS[name]
+    if kind == "forest":
+        return ForestSpec(LinearSpec(*args, elem=elem), 64, scatter_seed=0xC3), policy, desc
     if kind == "linear":
         return LinearSpec(*args, elem=elem), policy, desc
     return DenseSpec(*args, elem=elem, leaf_only=leaf_only), policy, desc
@@ -180,6 +185,9 @@ def cpu_window(spec, policy: str, seed: int, steps: int, warmup: int, threads: i
     """The oracle's restatement of the metered window (host cores): copy in, attach, resolve,
     scale, detach, copy out.  Returns (seconds per step list, graph bytes)."""
     from oracle import oracle as O
+    trees = 1
+    if spec.__class__.__name__ == "ForestSpec":   # the reference has no forest: one tree x count
+        spec, trees = spec.tree, spec.count
     ospec = O.OSpec(O.DENSE if spec.__class__.__name__ == "DenseSpec" else O.LINEAR,
                     getattr(spec, "q", getattr(spec, "k", 1)), spec.n, getattr(spec, "depth", 0),
                     getattr(spec, "layout", "allinit_allused"), spec.elem, getattr(spec, "leaf_only", False), 16)
@@ -199,7 +207,7 @@ def cpu_window(spec, policy: str, seed: int, steps: int, warmup: int, threads: i
             raise RuntimeError(f"oracle window reported site {rc}")
         if i >= warmup:
             times.append(dt)
-    return times, t.total
+    return [x * trees for x in times], t.total * trees
 
 
 def compare_schemes(spec, policy: str, reps: int, device: int) -> dict:

@@ -55,7 +55,9 @@ typedef struct cf_window cf_window; /* a planned, pipelined metered window */
  * elem: 8 = float64 (reference), 4 = float32 (BASELINE configs).
  * align: 1 = packed arena (Arena.allocate, memory.py:217-227), 8 = host bump allocator
  *        (MemorySpace.allocate, memory.py:124-137), 16 = aligned production arena.
- * leaf_only: dense trees with arrays on the depth-D leaves only (BASELINE C2/C5). */
+ * leaf_only: dense trees with arrays on the depth-D leaves only (BASELINE C2/C5).
+ * forest / scatter_seed: BASELINE C3 -- many independent trees whose objects are scattered
+ * over the slab instead of laid out in DFS order (the reference builds single trees only). */
 typedef struct {
   int32_t kind;
   int32_t layout;
@@ -65,12 +67,13 @@ typedef struct {
   int32_t elem;
   int32_t leaf_only;
   int32_t align;
-  int32_t reserved;
+  int32_t forest;         /* number of independent trees (0 or 1: a single tree); C3 = 64 chains */
+  uint64_t scatter_seed;  /* != 0: allocations placed in a seeded random order (sparse layout) */
 } cf_spec;
 
 typedef struct {
   uint64_t total_bytes;   /* arena bytes (== closed form when align == 1) */
-  uint64_t nallocs, nnodes, narrays, nsites;
+  uint64_t nallocs, nnodes, narrays, nsites, ntrees;
   uint64_t root_off;      /* offset of the root node */
   uint64_t payload_bytes; /* sum of array bytes */
   uint64_t padding_bytes; /* total_bytes - sum of allocation sizes */
@@ -90,7 +93,9 @@ enum {
   CF_TAB_SITE_OFF = 9,    /* u64[nsites]    DFS order (Arena.pointer_sites)           */
   CF_TAB_SITE_TARGET = 10,/* u64[nsites]    target offset of each pointer field      */
   CF_TAB_SITE_SORTED = 11,/* u64[nsites]    ascending offsets (the relocation table)  */
-  CF_TAB_ARR_ORDINAL = 12 /* u64[narrays]   owner's ordinal among nodes of its level  */
+  CF_TAB_ARR_ORDINAL = 12,/* u64[narrays]   owner's ordinal among nodes of its level  */
+  CF_TAB_ARR_ROOT = 13,   /* u64[narrays]   root offset of the tree owning the array   */
+  CF_TAB_TREE_ROOT = 14   /* u64[ntrees]    root offset of every tree                  */
 };
 
 /* Chain shape walked by the resolve / chase kernels (kernel_scale walk, harness.py:285-304).
@@ -157,10 +162,11 @@ int cf_tree_free(cf_tree* tree);
 int cf_relocate(cf_ctx* ctx, void* image, uint64_t image_bytes, const uint64_t* d_sites,
                 uint64_t nsites, uint64_t from_base, uint64_t to_base, uint64_t* d_bad,
                 void* stream);
-/* Pointerchain resolve kernel: one thread per chain, walks it once in the relocated image and
+/* Pointerchain resolve kernel: one thread per chain (d_root: per-target root offset, NULL =
+ * shape->root_off), walks it once in the relocated image and
  * writes its effective address + node count (targeted_arrays, scenarios.py:270-284, done on
  * the device; harness.py:228-238 pointerchain buffers). */
-int cf_resolve(cf_ctx* ctx, const void* image, const cf_chain_shape* shape,
+int cf_resolve(cf_ctx* ctx, const void* image, const cf_chain_shape* shape, const uint64_t* d_root,
                const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets,
                uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad, void* stream);
 /* Leaf-kernel work list (device pointers).  A launch covers big parts
@@ -181,7 +187,7 @@ typedef struct {
  * non-hoistable loads (d_ea unused).  d_bad is raised if a part exceeds the count read from
  * the node or the array pointer is null. */
 int cf_scale(cf_ctx* ctx, int elem, int mode, const void* image, const cf_chain_shape* shape,
-             const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
+             const uint64_t* d_root, const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
              const uint32_t* d_count, const cf_scale_work* work, double scale, uint64_t* d_bad,
              void* stream);
 
@@ -202,7 +208,8 @@ int cf_demarshal(cf_ctx* ctx, void* host_arena, uint64_t total, void* image,
  * the targets' chain keys and planned element counts. Synchronous; d_ea_out (optional,
  * device) receives the effective addresses. */
 int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain_shape* shape,
-                    const int32_t* h_level, const uint64_t* h_ordinal, const uint64_t* h_count,
+                    const uint64_t* h_root, const int32_t* h_level, const uint64_t* h_ordinal,
+                    const uint64_t* h_count,
                     uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad);
 /* Pointerchain scheme leaf kernel over host-resolved buffers (harness.py:255-259): every
  * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */

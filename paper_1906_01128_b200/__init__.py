@@ -13,7 +13,7 @@ from .harness import (ChainShape, CostModel, DevicePrep, KernelStats, P100_COST_
                       transfer_to_device, verify_tree)
 from .memory import (AddressMap, Arena, Machine, MemorySpace, TransferEntry, TransferLog,
                      UvmState)
-from .scenarios import (ArrayRef, DenseSpec, LinearSpec, TreeHandle, build_dense_tree,
+from .scenarios import (ArrayRef, DenseSpec, ForestSpec, LinearSpec, TreeHandle, build_dense_tree,
                         build_linear_tree, build_tree, dense_data_size, linear_data_size,
                         marshal_tree, payload_values, targeted_arrays, tree_total_bytes)
 from .engine import DeepCopyWindow

@@ -27,7 +27,7 @@ CF_MODE_RESOLVED, CF_MODE_CHASE = 0, 1
 CF_UVM_ADVISE_NONE, CF_UVM_PREFERRED_DEVICE, CF_UVM_ACCESSED_BY, CF_UVM_READ_MOSTLY = 0, 1, 2, 3
 (CF_TAB_ALLOC_OFF, CF_TAB_ALLOC_SIZE, CF_TAB_NODE_OFF, CF_TAB_NODE_LEVEL, CF_TAB_NODE_SIZE,
  CF_TAB_ARR_LEVEL, CF_TAB_ARR_OWNER, CF_TAB_ARR_OFF, CF_TAB_ARR_COUNT, CF_TAB_SITE_OFF,
- CF_TAB_SITE_TARGET, CF_TAB_SITE_SORTED, CF_TAB_ARR_ORDINAL) = range(13)
+ CF_TAB_SITE_TARGET, CF_TAB_SITE_SORTED, CF_TAB_ARR_ORDINAL, CF_TAB_ARR_ROOT, CF_TAB_TREE_ROOT) = range(15)
 CF_WIN_H2D, CF_WIN_TABLES, CF_WIN_ATTACH, CF_WIN_RESOLVE, CF_WIN_SCALE, CF_WIN_DETACH, CF_WIN_D2H, \
     CF_WIN_GRAPH = (1 << i for i in range(8))
 CF_WIN_FULL = (CF_WIN_H2D | CF_WIN_TABLES | CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE
@@ -53,17 +53,24 @@ EXPORTED = (
 class CfSpec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("layout", C.c_int32), ("k_or_q", C.c_int64),
                 ("n", C.c_int64), ("depth", C.c_int64), ("elem", C.c_int32),
-                ("leaf_only", C.c_int32), ("align", C.c_int32), ("reserved", C.c_int32)]
+                ("leaf_only", C.c_int32), ("align", C.c_int32), ("forest", C.c_int32),
+                ("scatter_seed", C.c_uint64)]
 
 
 class CfTreeInfo(C.Structure):
-    _fields_ = [(n, C.c_uint64) for n in ("total_bytes", "nallocs", "nnodes", "narrays", "nsites",
+    _fields_ = [(n, C.c_uint64) for n in ("total_bytes", "nallocs", "nnodes", "narrays", "nsites", "ntrees",
                                          "root_off", "payload_bytes", "padding_bytes")]
 
 
 class CfChainShape(C.Structure):
     _fields_ = [("kind", C.c_int32), ("depth", C.c_int32), ("q", C.c_uint32),
                 ("reserved", C.c_uint32), ("root_off", C.c_uint64), ("image_bytes", C.c_uint64)]
+
+
+class CfScaleWork(C.Structure):
+    _fields_ = [("parts", C.c_void_p), ("tile_base", C.c_void_p), ("groups", C.c_void_p),
+                ("big_begin", C.c_uint64), ("big_count", C.c_uint64), ("tile_begin", C.c_uint64),
+                ("tile_end", C.c_uint64), ("group_begin", C.c_uint64), ("group_end", C.c_uint64)]
 
 
 class CfWindowDesc(C.Structure):
@@ -112,12 +119,12 @@ def _declare(L):
         "cf_tree_chain_shape": (C.c_int, [P, C.POINTER(CfChainShape)]),
         "cf_tree_free": (C.c_int, [P]),
         "cf_relocate": (C.c_int, [P, P, U64, P, U64, U64, U64, P, P]),
-        "cf_resolve": (C.c_int, [P, P, C.POINTER(CfChainShape), P, P, U64, P, P, P, P]),
-        "cf_scale": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(CfChainShape), P, P, P, P, U64,
-                               P, U64, P, U64, C.c_double, P, P]),
+        "cf_resolve": (C.c_int, [P, P, C.POINTER(CfChainShape), P, P, P, U64, P, P, P, P]),
+        "cf_scale": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(CfChainShape), P, P, P, P, P,
+                               C.POINTER(CfScaleWork), C.c_double, P, P]),
         "cf_marshal_transfer_and_attach": (C.c_int, [P, P, U64, P, P, U64, U64, C.POINTER(U64)]),
         "cf_demarshal": (C.c_int, [P, P, U64, P, P, U64, U64, C.POINTER(U64)]),
-        "cf_kernel_scale": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(CfChainShape), P, P, P,
+        "cf_kernel_scale": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(CfChainShape), P, P, P, P,
                                       U64, C.c_double, P, C.POINTER(U64)]),
         "cf_scale_resolved": (C.c_int, [P, C.c_int, P, P, U64, C.c_double]),
         "cf_memcpy_batch": (C.c_int, [P, P, P, P, U64, P]),

@@ -43,10 +43,10 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 // One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).
 constexpr uint64_t SMALL_FUSED = 4096;
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
-                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const int32_t* level,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
                           cudaStream_t s);
-int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh,
+int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
                    const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea,
                    uint32_t* count, uint64_t* bad, cudaStream_t s);
 // A relocation job that can ride along in a leaf-kernel launch (extra CTAs).
@@ -58,13 +58,15 @@ struct RelocArgs {
   uint64_t from, to;
 };
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
-                 const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
+                 const uint64_t* root, const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
                  const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
                  cudaStream_t s, const RelocArgs* fused_reloc = nullptr);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);
 int launch_fill_u64(cf_ctx* ctx, uint64_t* p, uint64_t value, uint64_t n, cudaStream_t s);
+// (lo, hi) byte segments copied src+lo -> dst+lo by the SMs (mapped host memory allowed).
+int launch_seg_copy(cf_ctx* ctx, const uint64_t* segs, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t s);
 
 inline uint64_t tiles_for(uint64_t elems, int elem) {
   const uint64_t per = TILE_BYTES / uint64_t(elem);
@@ -154,9 +156,11 @@ struct cf_tree {
   std::vector<uint32_t> node_na;      // value of the nA field
   std::vector<int64_t> node_nlnext;   // value of nLnext, -1 when the node has no such field
   std::vector<int32_t> arr_level;
-  std::vector<uint64_t> arr_owner, arr_off, arr_count, arr_ordinal;
+  std::vector<uint64_t> arr_owner, arr_off, arr_count, arr_ordinal, arr_tree, arr_root;
   std::vector<uint64_t> site_off, site_target, site_sorted;
-  std::vector<std::vector<uint64_t>> level_nodes;  // per level: node offsets by ordinal
+  std::vector<uint64_t> tree_root;
+  // per tree, per level: node offsets by ordinal (pre-order within a level)
+  std::vector<std::vector<std::vector<uint64_t>>> level_nodes;
 };
 
 // RAII: make ctx's device current on this thread.

@@ -110,9 +110,9 @@ struct Walk {
 };
 
 template <bool CHASE>
-__device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_shape& sh, int level,
-                                           uint64_t ordinal) {
-  const uint8_t* p = image + sh.root_off;
+__device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_shape& sh, uint64_t root_off,
+                                           int level, uint64_t ordinal) {
+  const uint8_t* p = image + root_off;
   const bool dense = sh.kind == CF_DENSE;
   uint64_t qpow = 1;
   if (dense)
@@ -133,13 +133,14 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
 }
 
 __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ image, cf_chain_shape sh,
+                                                 const uint64_t* __restrict__ root,
                                                  const int32_t* __restrict__ level,
                                                  const uint64_t* __restrict__ ordinal, uint64_t n,
                                                  uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
                                                  uint64_t* bad) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  Walk w = walk_chain<false>(image, sh, level[i], ordinal[i]);
+  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i]);
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ ima
 __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ image, uint64_t total,
                                                          const uint64_t* __restrict__ sites, uint64_t nsites,
                                                          uint64_t from, uint64_t to, cf_chain_shape sh,
+                                                         const uint64_t* __restrict__ root,
                                                          const int32_t* __restrict__ level,
                                                          const uint64_t* __restrict__ ordinal, uint64_t ntargets,
                                                          uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
   __syncthreads();
   for (uint64_t i = threadIdx.x; i < ntargets; i += blockDim.x) {
-    Walk w = walk_chain<false>(image, sh, level[i], ordinal[i]);
+    Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i]);
     if (!w.node) {
       ea[i] = 0;
       count[i] = 0;
@@ -216,6 +218,7 @@ template <> __device__ __forceinline__ double mul_rn<double>(double a, double b)
 struct ScaleArgs {
   const uint8_t* image;
   cf_chain_shape sh;
+  const uint64_t* root;       // per-target root offsets (forests), nullptr = sh.root_off
   const int32_t* level;
   const uint64_t* ordinal;
   const uint64_t* ea;
@@ -229,7 +232,7 @@ struct ScaleArgs {
 template <bool CHASE>
 __device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uint8_t*& arr, uint64_t& cnt) {
   if (CHASE) {
-    Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+    Walk w = walk_chain<true>(a.image, a.sh, a.root ? a.root[t] : a.sh.root_off, a.level[t], a.ordinal[t]);
     if (!w.node) return false;
     arr = reinterpret_cast<uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
     cnt = ld_u32_any(w.node + OFF_NA);
@@ -244,7 +247,7 @@ __device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uin
 template <bool CHASE>
 __device__ __forceinline__ uint8_t* chase_base(const ScaleArgs& a, uint64_t t, uint8_t* resolved) {
   if (!CHASE) return resolved;
-  Walk w = walk_chain<true>(a.image, a.sh, a.level[t], a.ordinal[t]);
+  Walk w = walk_chain<true>(a.image, a.sh, a.root ? a.root[t] : a.sh.root_off, a.level[t], a.ordinal[t]);
   return reinterpret_cast<uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
 }
 
@@ -445,6 +448,24 @@ __global__ void __launch_bounds__(256) k_naive_fixup(const uint64_t* __restrict_
   }
 }
 
+// Zero-copy segment copy: one warp per (lo, hi) segment, src and dst at the same offsets from
+// their bases; either side may be mapped pinned host memory (PCIe loads/stores issued by the
+// SMs).  Moves hundreds of scattered node records in one launch instead of one DMA each.
+__global__ void __launch_bounds__(256) k_seg_copy(const uint64_t* __restrict__ segs, uint64_t n,
+                                                  const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+  const uint64_t wid = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  const uint64_t lo = segs[2 * wid], hi = segs[2 * wid + 1];
+  uint64_t i = lo;
+  if (((lo | hi) & 3) == 0) {
+    for (uint64_t k = lo / 4 + lane; k < hi / 4; k += 32)
+      reinterpret_cast<uint32_t*>(dst)[k] = reinterpret_cast<const uint32_t*>(src)[k];
+    return;
+  }
+  for (i = lo + lane; i < hi; i += 32) dst[i] = src[i];
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t v, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -476,28 +497,29 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 }
 
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
-                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const int32_t* level,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
                           cudaStream_t s) {
   if (nsites == 0 && ntargets == 0) return CF_OK;
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
-  k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, level, ordinal, ntargets, ea,
-                                        count, bad);
+  k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level, ordinal, ntargets,
+                                        ea, count, bad);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
 
-int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const int32_t* level,
-                   const uint64_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                   cudaStream_t s) {
+int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
+                   const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count,
+                   uint64_t* bad, cudaStream_t s) {
   if (n == 0) return CF_OK;
-  k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, level, ordinal, n, ea, count, bad);
+  k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, root, level, ordinal, n, ea, count, bad);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
 
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
-                 const int32_t* level, const uint64_t* ordinal, const uint64_t* ea, const uint32_t* count,
+                 const uint64_t* root, const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
+                 const uint32_t* count,
                  const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s,
                  const RelocArgs* fused_reloc) {
   const uint64_t nreloc = fused_reloc ? fused_reloc->n : 0;
@@ -506,7 +528,7 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
   if (units == 0) return CF_OK;
   if (units > 0x7FFFFFFFull) return fail(CF_E_INVALID, "leaf kernel: %llu work units exceed one grid",
                                          (unsigned long long)units);
-  ScaleArgs a{image, sh, level, ordinal, ea, count, work, bad, RelocArgs{}};
+  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, RelocArgs{}};
   if (nreloc) a.reloc = *fused_reloc;
   // one CTA per 16 KiB tile / small-part group: measured faster than a persistent grid-stride
   // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware
@@ -528,6 +550,13 @@ int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* 
                        uint64_t* bad, cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_naive_fixup<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(field_host, target_host, n, hb, sz, db, nmap, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_seg_copy(cf_ctx* ctx, const uint64_t* segs, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_seg_copy<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(segs, n, src, dst);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -109,25 +109,26 @@ int cf_relocate(cf_ctx* c, void* image, uint64_t image_bytes, const uint64_t* d_
                          d_bad, pick(c, stream));
 }
 
-int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const int32_t* d_level,
-               const uint64_t* d_ordinal, uint64_t ntargets, uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad,
-               void* stream) {
+int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const uint64_t* d_root,
+               const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets, uint64_t* d_ea,
+               uint32_t* d_count, uint64_t* d_bad, void* stream) {
   if (!c || !shape) return fail(CF_E_INVALID, "null argument");
   CfDevice g(c);
-  return launch_resolve(c, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, ntargets, d_ea,
+  return launch_resolve(c, static_cast<const uint8_t*>(image), *shape, d_root, d_level, d_ordinal, ntargets, d_ea,
                         d_count, d_bad, pick(c, stream));
 }
 
 int cf_scale(cf_ctx* c, int elem, int mode, const void* image, const cf_chain_shape* shape,
-             const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea, const uint32_t* d_count,
+             const uint64_t* d_root, const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
+             const uint32_t* d_count,
              const cf_scale_work* work, double scale, uint64_t* d_bad, void* stream) {
   if (!c || !shape || !work) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
   if (!work->parts || (work->big_count && !work->tile_base) || (work->group_end > work->group_begin && !work->groups))
     return fail(CF_E_INVALID, "incomplete work list");
   CfDevice g(c);
-  return launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, d_level, d_ordinal, d_ea, d_count,
-                      *work, scale, d_bad, pick(c, stream));
+  return launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, d_root, d_level, d_ordinal, d_ea,
+                      d_count, *work, scale, d_bad, pick(c, stream));
 }
 
 int cf_marshal_transfer_and_attach(cf_ctx* c, const void* host_arena, uint64_t total, void* image,
@@ -216,8 +217,8 @@ int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const
 }
 
 int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_shape* shape,
-                    const int32_t* h_level, const uint64_t* h_ordinal, const uint64_t* h_count, uint64_t ntargets,
-                    double scale, uint64_t* h_ea_out, uint64_t* bad) {
+                    const uint64_t* h_root, const int32_t* h_level, const uint64_t* h_ordinal,
+                    const uint64_t* h_count, uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad) {
   if (!c || !shape || (ntargets && (!h_level || !h_ordinal || !h_count))) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
   CfDevice g(c);
@@ -230,31 +231,34 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   for (uint64_t t = 0; t < ntargets; ++t)
     if (h_count[t]) tri.insert(tri.end(), {t, 0, h_count[t]});
   cf_scale_work work = sw.append(tri);
-  // one device block: level | ordinal | ea | count | work list
+  // one device block: level | ordinal | ea | count | roots | work list
   const uint64_t off_ord = ((ntargets * 4 + 7) / 8) * 8;
   const uint64_t off_ea = off_ord + ntargets * 8;
   const uint64_t off_cnt = off_ea + ntargets * 8;
-  const uint64_t off_work = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_root = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_work = off_root + (h_root ? ntargets * 8 : 0);
   DevBuf blk(c);
   CF_TRY(blk.alloc(off_work + work_bytes(sw) + 8));
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;
   CF_CUDA(cudaMemcpyAsync(d, h_level, ntargets * 4, cudaMemcpyHostToDevice, s));
   CF_CUDA(cudaMemcpyAsync(d + off_ord, h_ordinal, ntargets * 8, cudaMemcpyHostToDevice, s));
+  if (h_root) CF_CUDA(cudaMemcpyAsync(d + off_root, h_root, ntargets * 8, cudaMemcpyHostToDevice, s));
+  const uint64_t* droot = h_root ? reinterpret_cast<const uint64_t*>(d + off_root) : nullptr;
   CF_TRY(upload_work(sw, d + off_work, s, &work));
   CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   const int32_t* lv = reinterpret_cast<const int32_t*>(d);
   const uint64_t* od = reinterpret_cast<const uint64_t*>(d + off_ord);
   uint64_t* ea = reinterpret_cast<uint64_t*>(d + off_ea);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(d + off_cnt);
-  CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, lv, od, ntargets, ea, cnt, c->d_bad, s));
+  CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, droot, lv, od, ntargets, ea, cnt, c->d_bad, s));
   uint64_t rb = NO_BAD;
   CF_TRY(read_bad(c, c->d_bad, s, &rb));
   if (rb != NO_BAD) {
     if (bad) *bad = rb;
     return fail(CF_E_WILD, "chain walk for target %llu left the device image", (unsigned long long)rb);
   }
-  CF_TRY(launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, lv, od, ea, cnt, work, scale,
+  CF_TRY(launch_scale(c, elem, mode, static_cast<const uint8_t*>(image), *shape, droot, lv, od, ea, cnt, work, scale,
                       c->d_bad, s));
   if (h_ea_out) CF_CUDA(cudaMemcpyAsync(h_ea_out, ea, ntargets * 8, cudaMemcpyDeviceToHost, s));
   CF_TRY(read_bad(c, c->d_bad, s, &rb));
@@ -293,7 +297,7 @@ int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t*
   CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   cf_chain_shape sh;
   memset(&sh, 0, sizeof sh);
-  CF_TRY(launch_scale(c, elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, reinterpret_cast<const uint64_t*>(d),
+  CF_TRY(launch_scale(c, elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, nullptr, reinterpret_cast<const uint64_t*>(d),
                       reinterpret_cast<const uint32_t*>(d + off_cnt), work, scale, c->d_bad, s));
   uint64_t rb = NO_BAD;
   CF_TRY(read_bad(c, c->d_bad, s, &rb));

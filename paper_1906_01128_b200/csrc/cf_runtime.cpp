@@ -105,7 +105,8 @@ int cf_host_alloc(uint64_t bytes, int kind, void** out) {
     p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) return fail(CF_E_OOM, "host mmap of %llu bytes failed", (unsigned long long)bytes);
   } else if (kind == CF_MEM_PINNED) {
-    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+    // mapped: under UVA the same pointer is usable by kernels (zero-copy node transfers)
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA,

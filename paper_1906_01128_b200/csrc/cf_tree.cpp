@@ -30,6 +30,8 @@ uint64_t round_up(uint64_t x, uint64_t a) { return a <= 1 ? x : (x + a - 1) / a 
 struct Planner {
   cf_tree* t;
   uint64_t cursor = 0;
+  uint64_t tree = 0;   // index of the tree being planned
+  uint64_t root = 0;   // its root offset
 
   uint64_t alloc(uint64_t size, int64_t array_index) {
     uint64_t off = round_up(cursor, uint64_t(t->spec.align));
@@ -47,8 +49,9 @@ struct Planner {
     t->node_size.push_back(size);
     t->node_na.push_back(na);
     t->node_nlnext.push_back(nlnext);
-    if (int(t->level_nodes.size()) <= level) t->level_nodes.resize(level + 1);
-    t->level_nodes[level].push_back(off);
+    auto& ln = t->level_nodes[tree];
+    if (int(ln.size()) <= level) ln.resize(level + 1);
+    ln[level].push_back(off);
   }
 
   int64_t array(int level, uint64_t owner, uint64_t count, uint64_t ordinal) {
@@ -59,6 +62,8 @@ struct Planner {
     t->arr_off.push_back(off);
     t->arr_count.push_back(count);
     t->arr_ordinal.push_back(ordinal);
+    t->arr_tree.push_back(tree);
+    t->arr_root.push_back(root);
     t->payload_bytes += uint64_t(t->spec.elem) * count;
     return idx;
   }
@@ -77,6 +82,7 @@ struct Planner {
     std::vector<int64_t> arr(k, -1);
     for (int64_t lv = 0; lv < k; ++lv) {
       nodes[lv] = alloc(NODE_SIZE, -1);
+      if (lv == 0) root = nodes[0];
       if (s.n > 0 && (allinit || lv == k - 1)) arr[lv] = array(int(lv), nodes[lv], uint64_t(s.n), 0);
     }
     for (int64_t lv = 0; lv < k; ++lv) {
@@ -95,8 +101,7 @@ struct Planner {
     struct Frame { uint64_t off; int level; uint64_t ordinal; };
     std::vector<Frame> stack;
     std::vector<uint64_t> per_level(D + 1, 0);
-    uint64_t root = alloc(D > 0 ? NODE_SIZE : LEAF_NODE_SIZE, -1);
-    t->root_off = root;
+    root = alloc(D > 0 ? NODE_SIZE : LEAF_NODE_SIZE, -1);
     stack.push_back({root, 0, 0});
     while (!stack.empty()) {
       Frame f = stack.back();
@@ -119,6 +124,45 @@ struct Planner {
     }
   }
 };
+
+uint64_t splitmix(uint64_t& x) {
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Sparse layout: place the allocations in a seeded random order (same sizes / alignment) and
+// move every recorded offset with its allocation.
+void scatter(cf_tree* t, uint64_t seed) {
+  const size_t m = t->alloc_off.size();
+  std::vector<size_t> perm(m);
+  for (size_t i = 0; i < m; ++i) perm[i] = i;
+  uint64_t st = seed;
+  for (size_t i = m; i > 1; --i) std::swap(perm[i - 1], perm[splitmix(st) % i]);
+  std::vector<uint64_t> neu(m);
+  uint64_t cur = 0;
+  for (size_t k = 0; k < m; ++k) {
+    const size_t i = perm[k];
+    const uint64_t off = round_up(cur, uint64_t(t->spec.align));
+    neu[i] = off;
+    cur = off + t->alloc_size[i];
+  }
+  const std::vector<uint64_t> old = t->alloc_off;  // ascending (bump order)
+  auto remap = [&](uint64_t off) {
+    const size_t i = size_t(std::upper_bound(old.begin(), old.end(), off) - old.begin()) - 1;
+    return neu[i] + (off - old[i]);
+  };
+  for (auto* v : {&t->node_off, &t->arr_owner, &t->arr_off, &t->arr_root, &t->site_off, &t->site_target,
+                  &t->tree_root})
+    for (auto& x : *v) x = remap(x);
+  for (auto& tree : t->level_nodes)
+    for (auto& lv : tree)
+      for (auto& x : lv) x = remap(x);
+  t->root_off = remap(t->root_off);
+  t->alloc_off = neu;
+  t->total = cur;
+}
 
 void fill_payload(uint8_t* host, const cf_tree* t, uint64_t seed31, int nthreads) {
   // payload_values (scenarios.py:152-155): raw_i = (seed*16777619 + level*1000003 + i) mod 2^31,
@@ -178,14 +222,18 @@ int cf_tree_plan(const cf_spec* spec, cf_tree** out) {
   cf_tree* t = new (std::nothrow) cf_tree();
   if (!t) return fail(CF_E_OOM, "out of host memory");
   t->spec = s;
+  const uint64_t ntrees = s.forest > 1 ? uint64_t(s.forest) : 1;
+  t->level_nodes.resize(ntrees);
   Planner pl{t};
-  if (s.kind == CF_LINEAR) {
-    pl.linear();
-    t->root_off = t->node_off.empty() ? 0 : t->node_off[0];
-  } else {
-    pl.dense();
+  for (uint64_t f = 0; f < ntrees; ++f) {
+    pl.tree = f;
+    if (s.kind == CF_LINEAR) pl.linear();
+    else pl.dense();
+    t->tree_root.push_back(pl.root);
   }
+  t->root_off = t->tree_root[0];
   t->total = pl.cursor;
+  if (s.scatter_seed) scatter(t, s.scatter_seed);
   t->site_sorted = t->site_off;
   std::sort(t->site_sorted.begin(), t->site_sorted.end());
   *out = t;
@@ -199,6 +247,7 @@ int cf_tree_info_get(const cf_tree* t, cf_tree_info* out) {
   out->nnodes = t->node_off.size();
   out->narrays = t->arr_off.size();
   out->nsites = t->site_off.size();
+  out->ntrees = t->tree_root.size();
   out->root_off = t->root_off;
   out->payload_bytes = t->payload_bytes;
   out->padding_bytes = t->total - t->served;
@@ -226,6 +275,8 @@ int cf_tree_table(const cf_tree* t, int which, const void** ptr, uint64_t* count
     TAB(CF_TAB_SITE_TARGET, t->site_target)
     TAB(CF_TAB_SITE_SORTED, t->site_sorted)
     TAB(CF_TAB_ARR_ORDINAL, t->arr_ordinal)
+    TAB(CF_TAB_ARR_ROOT, t->arr_root)
+    TAB(CF_TAB_TREE_ROOT, t->tree_root)
     default:
       return fail(CF_E_INVALID, "unknown table %d", which);
   }
@@ -237,8 +288,11 @@ int cf_tree_build(const cf_tree* t, void* host, uint64_t ptr_base, uint64_t seed
   uint8_t* h = static_cast<uint8_t*>(host);
   // 1. zero everything that is not array payload: node blocks and alignment gaps
   //    (the reference storage is zero-filled, memory.py:135)
+  std::vector<size_t> order(t->alloc_off.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t x, size_t y) { return t->alloc_off[x] < t->alloc_off[y]; });
   uint64_t prev_end = 0;
-  for (size_t i = 0; i < t->alloc_off.size(); ++i) {
+  for (size_t i : order) {
     const uint64_t off = t->alloc_off[i];
     if (off > prev_end) memset(h + prev_end, 0, off - prev_end);
     if (t->alloc_array[i] < 0) memset(h + off, 0, t->alloc_size[i]);
@@ -277,11 +331,13 @@ int cf_tree_targets(const cf_tree* t, int policy, int64_t* out, uint64_t cap, ui
     for (size_t i = 0; i < na; ++i)
       if (t->arr_level[i] == s.depth) idx.push_back(int64_t(i));
   } else if (policy == CF_TARGET_REF) {
-    // the leaf reached by always taking the last child (scenarios.py:277-284)
-    const uint64_t last = (s.depth > 0) ? t->level_nodes[s.depth].size() - 1 : 0;
-    const uint64_t node = t->level_nodes[s.depth][last];
-    for (size_t i = 0; i < na; ++i)
-      if (t->arr_owner[i] == node) idx.push_back(int64_t(i));
+    // per tree: the leaf reached by always taking the last child (scenarios.py:277-284)
+    for (size_t f = 0; f < t->tree_root.size(); ++f) {
+      const auto& leaves = t->level_nodes[f][s.depth];
+      const uint64_t node = leaves.back();
+      for (size_t i = 0; i < na; ++i)
+        if (t->arr_tree[i] == f && t->arr_owner[i] == node) idx.push_back(int64_t(i));
+    }
   } else {
     return fail(CF_E_INVALID, "unknown target policy %d", policy);
   }

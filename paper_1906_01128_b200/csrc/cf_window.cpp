@@ -2,12 +2,15 @@
 // (harness.py:369-373, marshalling scheme + device pointerchain) as one planned, multi-stream
 // schedule on a B200.
 //
-// The arena is cut into chunks (boundaries never split a pointer field).  Step c of the
-// schedule, on the compute stream, after chunk c has landed:
-//   1. relocate (attach) the sites inside chunk c                       memory.py:316-323
-//   2. resolve the targets whose chain fields are all in chunks <= c     scenarios.py:270-284
+// The arena is cut into segments (boundaries never split a pointer field) grouped into steps
+// that are uploaded in order.  When the graph has few node allocations, all node records are
+// hoisted into step 0 (tiny copies) so every chain is resolvable before the first array chunk
+// lands, whatever the placement (scattered C3 layouts); array data follows in 16 MiB chunks.
+// Step c of the schedule, on the compute stream, after step c's segments have landed:
+//   1. relocate (attach) the sites inside them                          memory.py:316-323
+//   2. resolve the targets whose chain fields have all landed            scenarios.py:270-284
 //   3. scale the array pieces that are ready at step c                   harness.py:307-309
-//   4. detach every chunk whose last reader ran at step <= c, then
+//   4. detach every segment whose last reader ran at step <= c, then
 //      copy it home on the D2H stream                                    memory.py:327-345
 // H2D copies alternate over the context's copy streams, D2H runs concurrently on its own
 // stream, so copy-in, compute and copy-out overlap over the full-duplex host link.  All
@@ -29,17 +32,27 @@ struct cf_window {
   cf_window_desc d{};
   cf_chain_shape sh{};
   int elem = 8;
-  std::vector<uint64_t> bounds;        // chunk boundaries, nchunks + 1
-  std::vector<uint64_t> reloc_lo;      // sorted-site ranges per chunk, nchunks + 1
-  std::vector<uint64_t> res_lo;        // resolve-target ranges per step, nchunks + 1
+  uint64_t total = 0;
+  uint64_t nsteps = 0;
+  std::vector<uint64_t> seg_lo, seg_hi;          // segments in upload order
+  std::vector<uint64_t> step_seg_lo;             // segments of step k: [step_seg_lo[k], step_seg_lo[k+1])
+  std::vector<uint64_t> reloc_lo;      // attach-site ranges per step (sites grouped by step)
+  std::vector<uint64_t> res_lo;        // resolve-target ranges per step
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
-  std::vector<uint64_t> det_lo;        // detach-site ranges per step, nchunks + 1
-  std::vector<std::vector<uint32_t>> released;  // chunks whose copy-back may start after step c
+  std::vector<uint64_t> det_lo;        // detach-site ranges per step
+  std::vector<std::vector<uint32_t>> released;  // segments whose copy-back may start after step k
+  // zero-copy node transfers (scattered layouts): step 0's node segments are pulled from the
+  // mapped host arena by one kernel, and pushed back by one kernel per release step
+  bool zc = false;
+  uint64_t zc_n = 0;                   // node segments in step 0
+  std::vector<uint64_t> zc_rel_lo;     // per step: range in the release-ordered node-seg list
+  uint64_t off_zc_h2d = 0, off_zc_d2h = 0;
   // one pinned table block and its device mirror
   uint8_t* h_tab = nullptr;
   uint8_t* d_tab = nullptr;
   uint64_t tab_bytes = 0;
-  uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_parts = 0, off_tb = 0, off_grp = 0;
+  uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_root = 0, off_parts = 0, off_tb = 0,
+           off_grp = 0;
   uint64_t* d_ea = nullptr;
   uint32_t* d_count = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rel;
@@ -53,9 +66,20 @@ struct cf_window {
 
 namespace {
 
-uint64_t chunk_of(const std::vector<uint64_t>& b, uint64_t off) {
-  return uint64_t(std::upper_bound(b.begin(), b.end(), off) - b.begin()) - 1;
-}
+// Address -> segment lookup over segments sorted by start address.
+struct SegIndex {
+  std::vector<uint64_t> lo;    // sorted starts
+  std::vector<uint32_t> seg;   // segment id of each start
+  uint32_t at(uint64_t off) const {
+    return seg[size_t(std::upper_bound(lo.begin(), lo.end(), off) - lo.begin()) - 1];
+  }
+};
+
+// Hoist node records into their own leading step when there are few node allocations.
+constexpr uint64_t HOIST_MAX_NODE_ALLOCS = 4096;
+constexpr uint64_t HOIST_MERGE_GAP = 64;
+// More hoisted node segments than this move by zero-copy kernels instead of one DMA each.
+constexpr uint64_t ZC_MIN_SEGS = 16;
 
 void destroy(cf_window* w) {
   if (!w) return;
@@ -100,55 +124,119 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->nsites = nsites;
   const uint64_t* sites = t->site_sorted.data();
 
-  // ---- chunks (no pointer field straddles a boundary)
-  std::vector<uint64_t>& b = w->bounds;
-  b.push_back(0);
+  // ---- segments and steps (no pointer field straddles a segment boundary)
+  w->total = total;
   const uint64_t ch = desc->chunk_bytes;
-  if (ch && ch < total) {
-    for (uint64_t x = ch; x < total; x += ch) {
-      uint64_t y = x;
-      const uint64_t* it = std::lower_bound(sites, sites + nsites, x >= 7 ? x - 7 : 0);
-      if (it != sites + nsites && *it < x && *it + 8 > x) y = *it;
-      if (y > b.back()) b.push_back(y);
-    }
+  std::vector<std::pair<uint64_t, uint64_t>> node_ranges;
+  for (size_t i = 0; i < t->alloc_off.size(); ++i)
+    if (t->alloc_array[i] < 0) node_ranges.push_back({t->alloc_off[i], t->alloc_off[i] + t->alloc_size[i]});
+  // hoist only when address order would make arrays wait for their chains, i.e. some chain
+  // node lies after the array it leads to (scattered layouts; DFS layouts never do)
+  bool late_nodes = false;
+  for (uint64_t i = 0; i < desc->ntargets && !late_nodes; ++i) {
+    const int64_t a = desc->h_targets[i];
+    if (a < 0 || uint64_t(a) >= t->arr_off.size()) break;
+    late_nodes = t->arr_owner[a] > t->arr_off[a] || t->arr_root[a] > t->arr_off[a];
   }
-  b.push_back(total);
-  const uint64_t nch = b.size() - 1;
-  w->reloc_lo.resize(nch + 1);
-  for (uint64_t c = 0; c <= nch; ++c)
-    w->reloc_lo[c] = uint64_t(std::lower_bound(sites, sites + nsites, b[c]) - sites);
+  const bool hoist = ch && ch < total && late_nodes && !node_ranges.empty() &&
+                     node_ranges.size() <= HOIST_MAX_NODE_ALLOCS;
+  auto cut = [&](uint64_t a, uint64_t b, bool check_sites) {   // [a, b) into <= ch pieces, one step each
+    uint64_t x = a;
+    while (x < b) {
+      uint64_t y = (ch && ch < total) ? std::min(b, (x / ch + 1) * ch) : b;
+      if (check_sites && y < b) {
+        const uint64_t* it = std::lower_bound(sites, sites + nsites, y >= 7 ? y - 7 : 0);
+        if (it != sites + nsites && *it < y && *it + 8 > y && *it > x) y = *it;
+      }
+      w->seg_lo.push_back(x);
+      w->seg_hi.push_back(y);
+      w->step_seg_lo.push_back(w->seg_lo.size() - 1);
+      x = y;
+    }
+  };
+  if (hoist) {
+    std::sort(node_ranges.begin(), node_ranges.end());
+    std::vector<std::pair<uint64_t, uint64_t>> merged;
+    for (auto& r : node_ranges) {
+      if (!merged.empty() && r.first <= merged.back().second + HOIST_MERGE_GAP) merged.back().second = std::max(merged.back().second, r.second);
+      else merged.push_back(r);
+    }
+    w->step_seg_lo.push_back(0);                       // step 0: every node segment
+    for (auto& r : merged) { w->seg_lo.push_back(r.first); w->seg_hi.push_back(r.second); }
+    // then the data between them: pieces on the chunk grid, consecutive pieces packed into
+    // steps of about one chunk (a scattered layout leaves many short gaps)
+    uint64_t x = 0, acc = ch;
+    auto add = [&](uint64_t a, uint64_t b) {
+      while (a < b) {
+        const uint64_t y = std::min(b, (a / ch + 1) * ch);
+        if (acc + (y - a) > ch) { w->step_seg_lo.push_back(w->seg_lo.size()); acc = 0; }
+        w->seg_lo.push_back(a);
+        w->seg_hi.push_back(y);
+        acc += y - a;
+        a = y;
+      }
+    };
+    for (auto& r : merged) { if (r.first > x) add(x, r.first); x = r.second; }
+    if (x < total) add(x, total);
+  } else {
+    cut(0, total, true);
+  }
+  const uint64_t nseg = w->seg_lo.size();
+  const uint64_t nch = w->step_seg_lo.size();
+  w->nsteps = nch;
+  w->step_seg_lo.push_back(nseg);
+  std::vector<uint64_t> seg_step(nseg);
+  for (uint64_t k = 0; k < nch; ++k)
+    for (uint64_t j = w->step_seg_lo[k]; j < w->step_seg_lo[k + 1]; ++j) seg_step[j] = k;
+  SegIndex six;
+  {
+    std::vector<uint32_t> ord(nseg);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return w->seg_lo[x] < w->seg_lo[y]; });
+    for (uint32_t j : ord) { six.lo.push_back(w->seg_lo[j]); six.seg.push_back(j); }
+  }
+  auto step_of = [&](uint64_t off) { return seg_step[six.at(off)]; };
+  // attach sites grouped by the step that uploads them (address order within a step)
+  std::vector<uint64_t> reloc(sites, sites + nsites);
+  std::stable_sort(reloc.begin(), reloc.end(), [&](uint64_t x, uint64_t y) { return step_of(x) < step_of(y); });
+  w->reloc_lo.assign(nch + 1, 0);
+  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
+    while (k < nsites && step_of(reloc[k]) < c) ++k;
+    w->reloc_lo[c] = k;
+  }
 
   // ---- per target: chain fields -> ready step
   const uint64_t nt = desc->ntargets;
   const bool dense = t->spec.kind == CF_DENSE;
   const uint64_t q = dense ? uint64_t(t->spec.k_or_q) : 1;
   std::vector<uint64_t> ready(nt, 0), max_step(nt, 0);
-  std::vector<std::vector<uint64_t>> field_chunks(nt);
-  std::vector<uint64_t> release(nch);
-  std::iota(release.begin(), release.end(), 0);
+  std::vector<std::vector<uint32_t>> field_segs(nt);
+  std::vector<uint64_t> release(seg_step);   // per segment: last step that reads it
   for (uint64_t i = 0; i < nt; ++i) {
     const int64_t a = desc->h_targets[i];
     if (a < 0 || uint64_t(a) >= t->arr_off.size()) { destroy(w); return fail(CF_E_INVALID, "target %lld out of range", (long long)a); }
     const int L = t->arr_level[a];
     const uint64_t ord = t->arr_ordinal[a];
+    const auto& lnodes = t->level_nodes[t->arr_tree[a]];
     uint64_t r = 0;
     for (int l = 0; l <= L; ++l) {
       // ancestor at level l: ordinal prefix ord / q^(L-l) (pre-order within a level)
       uint64_t pw = 1;
       for (int m = l; m < L; ++m) pw *= q;
-      const uint64_t node = t->level_nodes[l][dense ? ord / pw : 0];
+      const uint64_t node = lnodes[l][dense ? ord / pw : 0];
       const bool leaf = dense && l == t->spec.depth;
       uint64_t lo, hi;  // byte range read at this level
       if (l < L) { lo = node + OFF_LNEXT; hi = lo + 8; }
       else { lo = node + OFF_NA; hi = node + (leaf ? LEAF_NODE_SIZE : OFF_LNEXT); }
-      const uint64_t c0 = chunk_of(b, lo), c1 = chunk_of(b, hi - 1);
-      for (uint64_t c = c0; c <= c1; ++c) field_chunks[i].push_back(c);
-      r = std::max(r, c1);
+      for (uint64_t x : {lo, hi - 1}) {
+        field_segs[i].push_back(six.at(x));
+        r = std::max(r, step_of(x));
+      }
     }
     ready[i] = r;
   }
-  // ---- parts: each target's array cut at chunk boundaries; element i belongs to the chunk
-  //      holding its last byte
+  // ---- parts: each target's array cut at segment boundaries; element i belongs to the
+  //      segment holding its last byte
   struct Part { uint64_t t, b, e, step; };
   std::vector<Part> parts;
   const uint64_t e = uint64_t(w->elem);
@@ -162,23 +250,29 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
       if (x <= off + e - 1) return 0;
       return std::min(n, (x - (off + e - 1) + e - 1) / e);
     };
-    const uint64_t c_first = chunk_of(b, off + e - 1), c_last = chunk_of(b, end - 1);
-    for (uint64_t c = c_first; c <= c_last; ++c) {
-      const uint64_t i0 = first_i(b[c]);
-      const uint64_t i1 = (c == c_last) ? n : first_i(b[c + 1]);
+    // walk the segments under the array in address order
+    size_t pos = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e - 1) - six.lo.begin()) - 1;
+    for (; pos < six.lo.size() && six.lo[pos] < end; ++pos) {
+      const uint32_t sg = six.seg[pos];
+      const uint64_t i0 = first_i(w->seg_lo[sg]);
+      const uint64_t i1 = (w->seg_hi[sg] >= end) ? n : first_i(w->seg_hi[sg]);
       if (i1 <= i0) continue;
-      const uint64_t step = std::max(c, ready[i]);
+      // the piece's bytes may reach into neighbouring segments (elements straddling a
+      // boundary): it runs once all of them have landed and its chain is resolved
+      const size_t pb = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i0) - six.lo.begin()) - 1;
+      const size_t pe = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i1 - 1) - six.lo.begin()) - 1;
+      uint64_t step = ready[i];
+      for (size_t x = pb; x <= pe; ++x) step = std::max(step, seg_step[six.seg[x]]);
       parts.push_back({i, i0, i1, step});
       max_step[i] = std::max(max_step[i], step);
-      // every chunk this piece touches is copied back no earlier than its step
-      const uint64_t cb = chunk_of(b, off + e * i0), ce = chunk_of(b, off + e * i1 - 1);
-      for (uint64_t x = cb; x <= ce; ++x) release[x] = std::max(release[x], step);
+      // every segment this piece touches is copied back no earlier than its step
+      for (size_t x = pb; x <= pe; ++x) release[six.seg[x]] = std::max(release[six.seg[x]], step);
     }
   }
   const bool chase = desc->mode == CF_MODE_CHASE;
   for (uint64_t i = 0; i < nt; ++i)
-    for (uint64_t c : field_chunks[i])
-      release[c] = std::max(release[c], chase ? std::max(ready[i], max_step[i]) : ready[i]);
+    for (uint32_t sg : field_segs[i])
+      release[sg] = std::max(release[sg], chase ? std::max(ready[i], max_step[i]) : ready[i]);
 
   // ---- order targets by ready step, parts by step, detach sites by release step
   std::vector<uint64_t> torder(nt);
@@ -206,7 +300,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     std::vector<uint64_t> sidx(nsites);
     std::iota(sidx.begin(), sidx.end(), 0);
     std::vector<uint64_t> srel(nsites);
-    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[chunk_of(b, sites[s])];
+    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[six.at(sites[s])];
     std::stable_sort(sidx.begin(), sidx.end(), [&](uint64_t x, uint64_t y) { return srel[x] < srel[y]; });
     w->det_lo.assign(nch + 1, 0);
     for (uint64_t c = 0, k = 0; c <= nch; ++c) {
@@ -216,7 +310,32 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     for (uint64_t k = 0; k < nsites; ++k) det[k] = sites[sidx[k]];
   }
   w->released.assign(nch, {});
-  for (uint64_t c = 0; c < nch; ++c) w->released[release[c]].push_back(uint32_t(c));
+  const uint64_t nnode_seg = hoist ? w->step_seg_lo[1] : 0;
+  {
+    void* dp = nullptr;
+    const bool mapped = desc->host_src && cudaHostGetDevicePointer(&dp, const_cast<void*>(desc->host_src), 0) == cudaSuccess &&
+                        dp == desc->host_src &&
+                        (!desc->host_dst || (cudaHostGetDevicePointer(&dp, desc->host_dst, 0) == cudaSuccess && dp == desc->host_dst));
+    cudaGetLastError();
+    w->zc = hoist && mapped && nnode_seg > ZC_MIN_SEGS;
+  }
+  std::vector<uint64_t> zc_rel;   // node segments ordered by release step
+  for (uint64_t sg = 0; sg < nseg; ++sg) {
+    if (w->zc && sg < nnode_seg) continue;
+    w->released[release[sg]].push_back(uint32_t(sg));
+  }
+  if (w->zc) {
+    w->zc_n = nnode_seg;
+    std::vector<uint64_t> ids(nnode_seg);
+    std::iota(ids.begin(), ids.end(), 0);
+    std::stable_sort(ids.begin(), ids.end(), [&](uint64_t x, uint64_t y) { return release[x] < release[y]; });
+    w->zc_rel_lo.assign(nch + 1, 0);
+    for (uint64_t c = 0, k = 0; c <= nch; ++c) {
+      while (k < nnode_seg && release[ids[k]] < c) ++k;
+      w->zc_rel_lo[c] = k;
+    }
+    for (uint64_t id : ids) zc_rel.insert(zc_rel.end(), {w->seg_lo[id], w->seg_hi[id]});
+  }
 
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
@@ -224,27 +343,37 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->off_det = al8(w->off_sites + nsites * 8);
   w->off_level = al8(w->off_det + nsites * 8);
   w->off_ord = al8(w->off_level + nt * 4);
-  w->off_parts = al8(w->off_ord + nt * 8);
+  w->off_root = al8(w->off_ord + nt * 8);
+  w->off_parts = al8(w->off_root + nt * 8);
   w->off_tb = al8(w->off_parts + sw.parts.size() * 8);
   w->off_grp = al8(w->off_tb + sw.tile_base.size() * 8);
-  w->tab_bytes = al8(w->off_grp + sw.groups.size() * 4 + 8);
+  w->off_zc_h2d = al8(w->off_grp + sw.groups.size() * 4 + 8);
+  w->off_zc_d2h = w->off_zc_h2d + (w->zc ? w->zc_n * 16 : 0);
+  w->tab_bytes = al8(w->off_zc_d2h + (w->zc ? w->zc_n * 16 : 0) + 8);
   cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_count, std::max<uint64_t>(nt, 1) * 4);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "window tables: %s", cudaGetErrorString(ce)); }
-  memcpy(w->h_tab + w->off_sites, sites, nsites * 8);
+  if (nsites) memcpy(w->h_tab + w->off_sites, reloc.data(), nsites * 8);
   memcpy(w->h_tab + w->off_det, det.data(), nsites * 8);
   int32_t* lv = reinterpret_cast<int32_t*>(w->h_tab + w->off_level);
   uint64_t* od = reinterpret_cast<uint64_t*>(w->h_tab + w->off_ord);
+  uint64_t* rt = reinterpret_cast<uint64_t*>(w->h_tab + w->off_root);
   for (uint64_t k = 0; k < nt; ++k) {
     const int64_t a = desc->h_targets[torder[k]];
     lv[k] = t->arr_level[a];
     od[k] = t->arr_ordinal[a];
+    rt[k] = t->arr_root[a];
   }
   if (!sw.parts.empty()) memcpy(w->h_tab + w->off_parts, sw.parts.data(), sw.parts.size() * 8);
   if (!sw.tile_base.empty()) memcpy(w->h_tab + w->off_tb, sw.tile_base.data(), sw.tile_base.size() * 8);
   if (!sw.groups.empty()) memcpy(w->h_tab + w->off_grp, sw.groups.data(), sw.groups.size() * 4);
+  if (w->zc) {
+    uint64_t* zh = reinterpret_cast<uint64_t*>(w->h_tab + w->off_zc_h2d);
+    for (uint64_t j = 0; j < w->zc_n; ++j) { zh[2 * j] = w->seg_lo[j]; zh[2 * j + 1] = w->seg_hi[j]; }
+    memcpy(w->h_tab + w->off_zc_d2h, zc_rel.data(), zc_rel.size() * 8);
+  }
   for (auto& sg : w->seg) {
     sg.parts = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_parts);
     sg.tile_base = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
@@ -359,7 +488,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   cf_ctx* c = w->ctx;
   const cf_window_desc& d = w->d;
   const uint32_t fl = d.flags;
-  const uint64_t nch = w->bounds.size() - 1;
+  const uint64_t nch = w->nsteps;
   uint8_t* img = static_cast<uint8_t*>(d.image);
   const uint8_t* src = static_cast<const uint8_t*>(d.host_src);
   uint8_t* dst = static_cast<uint8_t*>(d.host_dst);
@@ -387,28 +516,36 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   const uint64_t* ddet = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_det);
   const int32_t* dlv = reinterpret_cast<const int32_t*>(w->d_tab + w->off_level);
   const uint64_t* dod = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_ord);
+  const uint64_t* drt = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_root);
   const bool chase = d.mode == CF_MODE_CHASE;
 
   for (uint64_t k = 0; k < nch; ++k) {
-    const uint64_t lo = w->bounds[k], hi = w->bounds[k + 1];
-    if (fl & CF_WIN_H2D) {
+    if ((fl & CF_WIN_H2D) && k == 0 && w->zc) {
+      // node records straight from the mapped host arena, one kernel for all of them
+      CF_TRY(launch_seg_copy(c, reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zc_h2d), w->zc_n, src, img, cs));
+      for (uint64_t j = 0; j < w->zc_n; ++j) h2d_bytes += w->seg_hi[j] - w->seg_lo[j];
+    } else if (fl & CF_WIN_H2D) {
       cudaStream_t s = c->h2d[k % c->h2d.size()];
-      CF_CUDA(cudaMemcpyAsync(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
+      for (uint64_t j = w->step_seg_lo[k]; j < w->step_seg_lo[k + 1]; ++j) {
+        const uint64_t lo = w->seg_lo[j], hi = w->seg_hi[j];
+        CF_CUDA(cudaMemcpyAsync(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
+        h2d_bytes += hi - lo;
+      }
       CF_CUDA(cudaEventRecord(w->ev_h2d[k], s));
       CF_CUDA(cudaStreamWaitEvent(cs, w->ev_h2d[k], 0));
-      h2d_bytes += hi - lo;
     }
     const uint64_t ns = w->reloc_lo[k + 1] - w->reloc_lo[k], nr = w->res_lo[k + 1] - w->res_lo[k];
     const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
     if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
-      CF_TRY(launch_attach_resolve(c, img, w->bounds.back(), dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
-                                   dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
+      CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
+                                   drt + w->res_lo[k], dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
                                    w->d_count + w->res_lo[k], c->d_bad, cs));
     } else {
       if (do_attach)
-        CF_TRY(launch_relocate(c, img, w->bounds.back(), dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));
+        CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));
       if (do_resolve)
-        CF_TRY(launch_resolve(c, img, w->sh, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
+        CF_TRY(launch_resolve(c, img, w->sh, drt + w->res_lo[k], dlv + w->res_lo[k], dod + w->res_lo[k], nr,
+                              w->d_ea + w->res_lo[k],
                               w->d_count + w->res_lo[k], c->d_bad, cs));
     }
     // In RESOLVED mode the leaf kernel never reads pointer fields, and every resolve that reads
@@ -419,20 +556,28 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
       if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        RelocArgs det{img, w->bounds.back(), ddet + w->det_lo[k], nd, dimg, d.host_base};
-        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
+        RelocArgs det{img, w->total, ddet + w->det_lo[k], nd, dimg, d.host_base};
+        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
                             nd ? &det : nullptr));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
     if ((fl & CF_WIN_DETACH) && !fuse_detach)
-      CF_TRY(launch_relocate(c, img, w->bounds.back(), ddet + w->det_lo[k], w->det_lo[k + 1] - w->det_lo[k], dimg,
+      CF_TRY(launch_relocate(c, img, w->total, ddet + w->det_lo[k], w->det_lo[k + 1] - w->det_lo[k], dimg,
                              d.host_base, c->d_bad, cs));
+    if ((fl & CF_WIN_D2H) && w->zc && w->zc_rel_lo[k + 1] > w->zc_rel_lo[k]) {
+      const uint64_t* zs = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zc_d2h) + 2 * w->zc_rel_lo[k];
+      CF_TRY(launch_seg_copy(c, zs, w->zc_rel_lo[k + 1] - w->zc_rel_lo[k], img, dst, cs));
+      for (uint64_t j = w->zc_rel_lo[k]; j < w->zc_rel_lo[k + 1]; ++j) {
+        const uint64_t* hz = reinterpret_cast<const uint64_t*>(w->h_tab + w->off_zc_d2h);
+        d2h_bytes += hz[2 * j + 1] - hz[2 * j];
+      }
+    }
     if ((fl & CF_WIN_D2H) && !w->released[k].empty()) {
       CF_CUDA(cudaEventRecord(w->ev_rel[k], cs));
       CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_rel[k], 0));
       for (uint32_t r : w->released[k]) {
-        const uint64_t rlo = w->bounds[r], rhi = w->bounds[r + 1];
+        const uint64_t rlo = w->seg_lo[r], rhi = w->seg_hi[r];
         CF_CUDA(cudaMemcpyAsync(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
         d2h_bytes += rhi - rlo;
       }
@@ -457,7 +602,7 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
   cf_ctx* c = w->ctx;
   CF_CUDA(cudaEventSynchronize(w->ev_end));
   const uint64_t bad = c->h_bad[0];
-  const uint64_t nch = w->bounds.size() - 1;
+  const uint64_t nch = w->nsteps;
   if (st) {
     memset(st, 0, sizeof *st);
     CF_CUDA(cudaEventElapsedTime(&st->ms_total, first, w->ev_end));
@@ -476,7 +621,7 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
     st->d2h_bytes = d2h;
     st->launches = c->launches.load() - launches0;
     st->bad = bad;
-    st->nchunks = nch;
+    st->nchunks = w->seg_lo.size();
     st->nsteps = nch;
   }
   if (bad != NO_BAD)

@@ -28,8 +28,8 @@ import numpy as np
 from . import _native as N
 from .errors import SchemeError, VerificationFailed
 from .memory import DATA_OP_KINDS, AddressMap, Arena, Machine
-from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, LinearSpec,
-                        TreeHandle, build_tree, marshal_tree, payload_values, targeted_arrays)
+from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, ForestSpec,
+                        LinearSpec, TreeHandle, build_tree, marshal_tree, payload_values, targeted_arrays)
 
 SCHEMES = ("uvm", "marshalling", "pointerchain", "naive")
 MODES = ("resolved", "chase")
@@ -91,6 +91,8 @@ class ChainShape:
 
 
 def chain_shape(spec, scheme: str) -> ChainShape:
+    if isinstance(spec, ForestSpec):
+        spec = spec.tree
     if scheme == "pointerchain":
         return ChainShape()
     if isinstance(spec, LinearSpec):
@@ -239,10 +241,13 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
 def _reference_derefs(handle: TreeHandle, policy: str, idx: np.ndarray) -> int:
     """chain_derefs exactly as the reference walk counts them (harness.py:264-304)."""
     spec = handle.spec
+    trees = 1
+    if isinstance(spec, ForestSpec):
+        spec, trees = spec.tree, spec.count
     if policy == "ref":
         if isinstance(spec, LinearSpec):
-            return (spec.k if spec.all_levels_used else 1) + (spec.k - 1)
-        return spec.depth + 1
+            return trees * ((spec.k if spec.all_levels_used else 1) + (spec.k - 1))
+        return trees * (spec.depth + 1)
     return int((handle.arr_level[idx].astype(np.int64) + 1).sum())
 
 
@@ -256,8 +261,10 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
     under the CUDA driver."""
     spec = handle.spec
     base, e = handle.base, spec.elem
-    linear = isinstance(spec, LinearSpec)
-    q = 1 if linear else spec.q
+    forest = isinstance(spec, ForestSpec)
+    tree = spec.tree if forest else spec
+    linear = isinstance(tree, LinearSpec)
+    q = 1 if linear else tree.q
     owner = {int(o): (int(a), int(c)) for o, a, c in zip(handle.arr_owner, handle.arr_off, handle.arr_count)}
     fields: list[int] = []
     spans: list[tuple[int, int]] = []
@@ -272,7 +279,19 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
             fields.append(base + node + OFF_NA)
             spans.append((base + arr[0], arr[1]))
 
-    if policy == "ref" and linear:
+    if forest:
+        # walk every targeted chain through the (host-resident) tree itself
+        view = N.host_view(base, handle.total_bytes)
+        rd = lambda off: int.from_bytes(view[off:off + 8].tobytes(), "little") - base  # noqa: E731
+        for i in idx.tolist():
+            L, ordv, node = int(handle.arr_level[i]), int(handle.arr_ordinal[i]), int(handle.arr_root[i])
+            for lv in range(1, L + 1):
+                fields.append(base + node + OFF_LNEXT)
+                child = 0 if linear else (NODE_SIZE if lv < tree.depth else LEAF_NODE_SIZE)
+                node = rd(node + OFF_LNEXT) + child * (0 if linear else (ordv // q ** (L - lv)) % q)
+            leaf = (not linear) and L == tree.depth
+            visit_terminal(node, LEAF_OFF_A if leaf else OFF_A)
+    elif policy == "ref" and linear:
         for level in range(spec.k):
             node = node_at(level, 0)
             if spec.all_levels_used or level == spec.k - 1:
@@ -330,9 +349,15 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     lv = np.ascontiguousarray(handle.arr_level[idx], np.int32)
     od = np.ascontiguousarray(handle.arr_ordinal[idx], np.uint64)
     cnt = np.ascontiguousarray(handle.arr_count[idx], np.uint64)
+    # per-target chain roots inside the image (several for a forest)
+    if prep.amap is not None:   # naive: objects were re-placed on the device
+        roots = prep.amap.translate_many(handle.arr_root[idx] + np.uint64(handle.base)) - np.uint64(prep.image)
+    else:                       # marshalling image / managed tree: same offsets as the host layout
+        roots = handle.arr_root[idx]
+    roots = np.ascontiguousarray(roots, np.uint64)
     bad = N.U64(0)
     rc = N.lib().cf_kernel_scale(ctx, elem, N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
-                                 prep.image, C.byref(sh), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
+                                 prep.image, C.byref(sh), N.ptr(roots), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
                                  float(scale), None, C.byref(bad))
     N.check(rc, "kernel_scale")
     stats.elements_touched = int(cnt.sum())
@@ -404,6 +429,9 @@ def verify_tree(machine: Machine, handle: TreeHandle, scale: float, policy: str 
 # -- one full case -------------------------------------------------------------
 
 def _describe(spec) -> tuple[str, str, int, int]:
+    if isinstance(spec, ForestSpec):
+        scen, layout, k_or_q, n = _describe(spec.tree)
+        return f"forest{spec.count}-{scen}", layout, k_or_q, n
     if isinstance(spec, LinearSpec):
         return "linear", spec.layout, spec.k, spec.n
     return "dense", "dense", spec.q, spec.n

@@ -65,7 +65,7 @@ class LinearSpec:
         return self.layout.endswith("allused")
 
     def native(self, align: int) -> N.CfSpec:
-        return N.CfSpec(N.CF_LINEAR, LAYOUTS.index(self.layout), self.k, self.n, 0, self.elem, 0, align, 0)
+        return N.CfSpec(N.CF_LINEAR, LAYOUTS.index(self.layout), self.k, self.n, 0, self.elem, 0, align, 1, 0)
 
 
 @dataclass(frozen=True)
@@ -86,7 +86,40 @@ class DenseSpec:
         _check_elem(self.elem)
 
     def native(self, align: int) -> N.CfSpec:
-        return N.CfSpec(N.CF_DENSE, 0, self.q, self.n, self.depth, self.elem, int(self.leaf_only), align, 0)
+        return N.CfSpec(N.CF_DENSE, 0, self.q, self.n, self.depth, self.elem, int(self.leaf_only), align, 1, 0)
+
+
+@dataclass(frozen=True)
+class ForestSpec:
+    """``count`` independent copies of one tree spec, optionally scattered over the slab.
+
+    BASELINE C3 (64 x LinearSpec(4, 4Mi, LLinit_LLused), sparse allocations).  Not in the
+    reference, which builds one tree per case; each tree is byte-for-byte a reference tree.
+    """
+
+    tree: object
+    count: int
+    scatter_seed: int = 0
+
+    def __post_init__(self):
+        if self.count < 1:
+            raise ValueError("count must be >= 1")
+        if not isinstance(self.tree, (LinearSpec, DenseSpec)):
+            raise ValueError("tree must be a LinearSpec or DenseSpec")
+
+    @property
+    def elem(self) -> int:
+        return self.tree.elem
+
+    @property
+    def n(self) -> int:
+        return self.tree.n
+
+    def native(self, align: int) -> N.CfSpec:
+        s = self.tree.native(align)
+        s.forest = self.count
+        s.scatter_seed = self.scatter_seed
+        return s
 
 
 @dataclass
@@ -119,6 +152,8 @@ class TreeHandle:
         self.arr_level, self.arr_owner, self.arr_off, self.arr_count, self.arr_ordinal = (
             t(N.CF_TAB_ARR_LEVEL), t(N.CF_TAB_ARR_OWNER), t(N.CF_TAB_ARR_OFF), t(N.CF_TAB_ARR_COUNT),
             t(N.CF_TAB_ARR_ORDINAL))
+        self.arr_root, self.tree_root = t(N.CF_TAB_ARR_ROOT), t(N.CF_TAB_TREE_ROOT)
+        self.ntrees = int(info.ntrees)
         self.site_off, self.site_target = t(N.CF_TAB_SITE_OFF), t(N.CF_TAB_SITE_TARGET)
         self.root_off = int(info.root_off)
 

@@ -110,3 +110,23 @@ def test_spec_validation_matches_reference():
                 lambda: DenseSpec(0, 10), lambda: DenseSpec(2, 10, -1), lambda: DenseSpec(2, 1, 1, elem=2)):
         with pytest.raises(ValueError):
             bad()
+
+
+def test_sass_chase_mode_keeps_per_access_chain_loads():
+    """CHASE must re-load the chain per access (non-hoistable ld.global.nc ->
+    LDG.E.64.CONSTANT in SASS) while RESOLVED issues none and streams with 128-bit accesses."""
+    import shutil
+    import subprocess
+    import sys
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([sys.executable, str(REPO / "tools" / "sass_report.py")], capture_output=True,
+                         text=True, check=True, cwd=str(REPO)).stdout
+    rows = {}
+    for line in out.splitlines()[2:]:
+        t, mode, total, ld128, st128, chain = [x.strip() for x in line.strip("|").split("|")]
+        rows[(t, mode)] = (int(total), int(ld128), int(st128), int(chain))
+    for t in ("float", "double"):
+        assert rows[(t, "resolved")][3] == 0
+        assert rows[(t, "chase")][3] > 0
+        assert rows[(t, "resolved")][1] > 0 and rows[(t, "resolved")][2] > 0

@@ -187,13 +187,26 @@ def simulate_times(entries, elements_touched: int, chain_derefs: int, cost_model
 class DevicePrep:
     scheme: str
     device_root: int = 0
-    buffers: list = field(default_factory=list)  # (device_addr, ArrayRef)
     arena: Arena | None = None
     amap: AddressMap | None = None
     policy: str = "ref"
     image: int = 0
     image_bytes: int = 0
     uvm_hints: str = "none"
+    # pointerchain selective buffers, column-wise: device address, host address, count, index
+    buf_dev: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    buf_host: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    buf_count: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    buf_array: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    handle: TreeHandle | None = None
+
+    @property
+    def buffers(self) -> list:
+        """(device_addr, ArrayRef) pairs as in the reference (harness.py:210-216)."""
+        if self.handle is None:
+            return []
+        arrays = self.handle.arrays
+        return [(int(d), arrays[int(i)]) for d, i in zip(self.buf_dev, self.buf_array)]
 
 
 UVM_HINTS = ("none", "prefetch", "advise")
@@ -213,16 +226,20 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         return DevicePrep(scheme, device_root=root, amap=amap, policy=policy, image=base, image_bytes=span)
     if scheme == "pointerchain":
         # host-side chain resolution, then one selective bulk copy per targeted array
-        # (harness.py:228-238), submitted together as one batched copy
-        buffers = []
-        for ref in targeted_arrays(handle, policy):
-            if ref.count == 0:
-                continue
-            buffers.append((machine.device.allocate(ref.count * handle.spec.elem), ref))
+        # (harness.py:228-238), submitted together as one batched copy into one device span
+        idx = handle.target_indices(policy)
+        idx = idx[handle.arr_count[idx] > 0]
         e = handle.spec.elem
-        machine.transfer_ranges(machine.host, [r.addr for _, r in buffers], machine.device,
-                                [d for d, _ in buffers], [r.count * e for _, r in buffers], "bulk")
-        return DevicePrep(scheme, buffers=buffers, policy=policy)
+        sizes = handle.arr_count[idx] * np.uint64(e)
+        aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
+        offs = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64) if len(idx) else aligned
+        prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx,
+                          buf_host=handle.arr_off[idx] + np.uint64(handle.base), buf_count=handle.arr_count[idx])
+        if len(idx):
+            dev_base = machine.device.allocate_span(int(aligned.sum()), offs, sizes)
+            prep.buf_dev = offs + np.uint64(dev_base)
+            machine.transfer_ranges(machine.host, prep.buf_host, machine.device, prep.buf_dev, sizes, "bulk")
+        return prep
     if scheme == "uvm":
         # the tree already lives in managed memory (harness.py:239-240: no copy); optional
         # driver hints: migrate the whole tree ahead of the kernel, or map it for remote access
@@ -255,65 +272,105 @@ def _level_nodes(handle: TreeHandle, level: int) -> np.ndarray:
     return handle.node_off[handle.node_level == level]
 
 
+def _pages_of_spans(starts: np.ndarray, counts: np.ndarray, e: int, page: int) -> np.ndarray:
+    """Distinct pages hit by the element touches aptr + e*i, i < n, of every span."""
+    starts = np.asarray(starts, np.int64)
+    counts = np.asarray(counts, np.int64)
+    keep = counts > 0
+    first = starts[keep] // page
+    last = (starts[keep] + e * (counts[keep] - 1)) // page
+    k = last - first + 1
+    if k.size == 0:
+        return np.zeros(0, np.int64)
+    rep = np.repeat(first - np.concatenate([[0], np.cumsum(k)[:-1]]), k)
+    return np.unique(rep + np.arange(int(k.sum()), dtype=np.int64))
+
+
 def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int):
     """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394),
     as sorted numpy arrays.  Used for the logical page-fault counters; the data itself migrates
-    under the CUDA driver."""
+    under the CUDA driver.  Chains are walked level by level for all targets at once."""
     spec = handle.spec
     base, e = handle.base, spec.elem
     forest = isinstance(spec, ForestSpec)
     tree = spec.tree if forest else spec
     linear = isinstance(tree, LinearSpec)
-    q = 1 if linear else tree.q
-    owner = {int(o): (int(a), int(c)) for o, a, c in zip(handle.arr_owner, handle.arr_off, handle.arr_count)}
-    fields: list[int] = []
-    spans: list[tuple[int, int]] = []
+    view = N.host_view(base, handle.total_bytes)
 
-    def node_at(level: int, ordinal: int) -> int:
-        return int(_level_nodes(handle, level)[ordinal])
+    def rd(offs: np.ndarray) -> np.ndarray:   # 8-byte pointer fields -> arena offsets
+        ix = offs.astype(np.int64)[:, None] + np.arange(8, dtype=np.int64)[None, :]
+        return view[ix].copy().view("<u8").ravel().astype(np.int64) - base
 
-    def visit_terminal(node: int, a_off: int) -> None:
-        fields.append(base + node + a_off)
-        arr = owner.get(node)
-        if arr and arr[1]:
-            fields.append(base + node + OFF_NA)
-            spans.append((base + arr[0], arr[1]))
-
-    if forest:
-        # walk every targeted chain through the (host-resident) tree itself
-        view = N.host_view(base, handle.total_bytes)
-        rd = lambda off: int.from_bytes(view[off:off + 8].tobytes(), "little") - base  # noqa: E731
-        for i in idx.tolist():
-            L, ordv, node = int(handle.arr_level[i]), int(handle.arr_ordinal[i]), int(handle.arr_root[i])
-            for lv in range(1, L + 1):
-                fields.append(base + node + OFF_LNEXT)
-                child = 0 if linear else (NODE_SIZE if lv < tree.depth else LEAF_NODE_SIZE)
-                node = rd(node + OFF_LNEXT) + child * (0 if linear else (ordv // q ** (L - lv)) % q)
-            leaf = (not linear) and L == tree.depth
-            visit_terminal(node, LEAF_OFF_A if leaf else OFF_A)
-    elif policy == "ref" and linear:
-        for level in range(spec.k):
-            node = node_at(level, 0)
-            if spec.all_levels_used or level == spec.k - 1:
-                visit_terminal(node, OFF_A)
-            if level < spec.k - 1:
-                fields.append(base + node + OFF_LNEXT)
-    elif policy == "ref":
-        for level in range(spec.depth):
-            fields.append(base + node_at(level, q ** level - 1) + OFF_LNEXT)
-        visit_terminal(node_at(spec.depth, q ** spec.depth - 1), LEAF_OFF_A)
+    if policy == "ref" and not forest and not linear:
+        # always take the last child: the last node of every level in pre-order
+        path = [int(handle.node_off[handle.node_level == lv][-1]) for lv in range(spec.depth + 1)]
+        fields = [np.array(path[:-1], np.int64) + OFF_LNEXT, np.array([path[-1] + LEAF_OFF_A], np.int64)]
+        t_nodes = np.array([path[-1]], np.int64)
+    elif policy == "ref" and not forest and linear:
+        # the reference walk reads A on every used level and Lnext on every level but the last
+        nodes = _level_nodes_all(handle)
+        used = np.arange(spec.k) if spec.all_levels_used else np.array([spec.k - 1])
+        fields = [nodes[:-1] + OFF_LNEXT, nodes[used] + OFF_A]
+        t_nodes = nodes[used]
     else:
-        for i in idx.tolist():
-            L, ordv = int(handle.arr_level[i]), int(handle.arr_ordinal[i])
-            for lv in range(L):
-                fields.append(base + node_at(lv, 0 if linear else ordv // q ** (L - lv)) + OFF_LNEXT)
-            leaf = (not linear) and L == spec.depth
-            visit_terminal(node_at(L, 0 if linear else ordv), LEAF_OFF_A if leaf else OFF_A)
-    # every element touch hits the page of its first byte (uvm_touch(aptr + e*i))
-    dirty = [np.arange(a // page, (a + e * (n - 1)) // page + 1, dtype=np.int64) for a, n in spans]
-    dirty = np.unique(np.concatenate(dirty)) if dirty else np.zeros(0, np.int64)
-    touched = np.union1d(np.array(fields, np.int64) // page, dirty)
+        sel = idx if policy != "ref" or forest else handle.target_indices("ref")
+        L = handle.arr_level[sel].astype(np.int64)
+        fields, t_nodes = [], []
+        node = handle.arr_root[sel].astype(np.int64)
+        ords = handle.arr_ordinal[sel].astype(np.int64)
+        depth = 0 if linear else tree.depth
+        q = 1 if linear else tree.q
+        for lv in range(1, int(L.max()) + 1 if L.size else 1):
+            act = L >= lv
+            fields.append(node[act] + OFF_LNEXT)
+            blk = rd(node[act] + OFF_LNEXT)
+            if linear:
+                node[act] = blk
+            else:
+                child = NODE_SIZE if lv < depth else LEAF_NODE_SIZE
+                digit = (ords[act] // q ** (L[act] - lv)) % q
+                node[act] = blk + child * digit
+        leaf = (~np.asarray(linear)) & (L == depth) if not linear else np.zeros(L.shape, bool)
+        fields.append(node + np.where(leaf, LEAF_OFF_A, OFF_A))
+        t_nodes = node
+    # terminal nodes with an array also read their count
+    t_nodes = np.asarray(t_nodes, np.int64)
+    owner_sorted = np.argsort(handle.arr_owner, kind="stable")
+    pos = np.searchsorted(handle.arr_owner[owner_sorted], t_nodes.astype(np.uint64))
+    pos = np.minimum(pos, max(len(owner_sorted) - 1, 0))
+    has = (len(owner_sorted) > 0) & (handle.arr_owner[owner_sorted][pos] == t_nodes.astype(np.uint64)) \
+        if len(owner_sorted) else np.zeros(t_nodes.shape, bool)
+    arr = owner_sorted[pos][has] if len(owner_sorted) else np.zeros(0, np.int64)
+    cnt = handle.arr_count[arr].astype(np.int64)
+    fields.append(t_nodes[has][cnt > 0] + OFF_NA)
+    dirty = _pages_of_spans(handle.arr_off[arr].astype(np.int64) + base, cnt, e, page)
+    f = np.concatenate([np.asarray(x, np.int64) for x in fields]) if fields else np.zeros(0, np.int64)
+    touched = np.union1d((f + base) // page, dirty)
     return touched, dirty
+
+
+def _merged_ranges(handle: TreeHandle, idx: np.ndarray, gap: int) -> list:
+    """Byte ranges of the given arrays, merged when closer than `gap` (few prefetch calls)."""
+    idx = idx[handle.arr_count[idx] > 0]
+    if len(idx) == 0:
+        return []
+    lo = handle.arr_off[idx].astype(np.int64)
+    hi = lo + handle.arr_count[idx].astype(np.int64) * handle.spec.elem
+    order = np.argsort(lo)
+    lo, hi = lo[order], hi[order]
+    out = [[int(lo[0]), int(hi[0])]]
+    for a, b in zip(lo[1:].tolist(), hi[1:].tolist()):
+        if a <= out[-1][1] + gap:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def _level_nodes_all(handle: TreeHandle) -> np.ndarray:
+    """Node offsets of a single linear tree, level order."""
+    order = np.argsort(handle.node_level, kind="stable")
+    return handle.node_off[order].astype(np.int64)
 
 
 def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: float,
@@ -325,9 +382,9 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     elem = handle.spec.elem
     ctx = machine.ctx.handle
     if prep.scheme == "pointerchain":
-        if prep.buffers:
-            ea = np.array([d for d, _ in prep.buffers], np.uint64)
-            cnt = np.array([r.count for _, r in prep.buffers], np.uint64)
+        if len(prep.buf_dev):
+            ea = np.ascontiguousarray(prep.buf_dev, np.uint64)
+            cnt = np.ascontiguousarray(prep.buf_count, np.uint64)
             N.check(N.lib().cf_scale_resolved(ctx, elem, N.ptr(ea), N.ptr(cnt), len(ea), float(scale)),
                     "kernel_scale")
             stats.elements_touched = int(cnt.sum())
@@ -370,17 +427,14 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     elif prep.scheme == "naive":
         machine.naive_copy_back(handle, prep.amap)
     elif prep.scheme == "pointerchain":
-        e = handle.spec.elem
-        machine.transfer_ranges(machine.device, [d for d, _ in prep.buffers], machine.host,
-                                [r.addr for _, r in prep.buffers], [r.count * e for _, r in prep.buffers], "bulk")
+        machine.transfer_ranges(machine.device, prep.buf_dev, machine.host, prep.buf_host,
+                                prep.buf_count * np.uint64(handle.spec.elem), "bulk")
     elif prep.scheme == "uvm":
         # the host re-touches every page the kernel dirtied (harness.py:321-325): migrate the
         # targeted arrays back explicitly, then account the logical page migrations
         ctx = machine.ctx.handle
-        for i in handle.target_indices(prep.policy).tolist():
-            n = int(handle.arr_count[i]) * handle.spec.elem
-            if n:
-                N.check(N.lib().cf_uvm_prefetch(ctx, handle.base + int(handle.arr_off[i]), n, -1, None))
+        for lo, hi in _merged_ranges(handle, handle.target_indices(prep.policy), machine.uvm.page_size):
+            N.check(N.lib().cf_uvm_prefetch(ctx, handle.base + lo, hi - lo, -1, None))
         machine.ctx.sync()
         dirty = machine.uvm.dirty_pages()
         machine.uvm_touch_pages(dirty, "read", "host")

@@ -274,6 +274,26 @@ class MemorySpace:
             return
         raise WildAccess(f"{self.kind} access at 0x{addr:x} (+{nbytes}) hits no live allocation")
 
+    def _check_many(self, addrs: np.ndarray, sizes: np.ndarray) -> None:
+        """Vectorised _check: every [addr, addr+size) inside one live allocation."""
+        addrs = np.asarray(addrs, np.uint64)
+        sizes = np.asarray(sizes, np.uint64)
+        if addrs.size <= 64:
+            for a, n in zip(addrs.tolist(), sizes.tolist()):
+                self._check(a, n)
+            return
+        bases = np.array(self._seg_bases, np.uint64)
+        si = np.searchsorted(bases, addrs, side="right").astype(np.int64) - 1
+        if (si < 0).any():
+            raise WildAccess(f"{self.kind} access hits no live allocation")
+        for k in np.unique(si).tolist():
+            seg = self._segs[k]
+            m = si == k
+            rel = addrs[m] - np.uint64(seg.base)
+            j = np.searchsorted(seg.offs, rel, side="right").astype(np.int64) - 1
+            if (j < 0).any() or (rel + sizes[m] > seg.offs[np.maximum(j, 0)] + seg.sizes[np.maximum(j, 0)]).any():
+                raise WildAccess(f"{self.kind} access hits no live allocation")
+
     def contains_range(self, addr: int, nbytes: int) -> bool:
         try:
             self._check(addr, nbytes)
@@ -530,9 +550,8 @@ class Machine:
         sz = np.ascontiguousarray(sizes, np.uint64)
         if sa.size == 0:
             return
-        for a, d, n in zip(sa.tolist(), da.tolist(), sz.tolist()):
-            src._check(a, n)
-            dst._check(d, n)
+        src._check_many(sa, sz)
+        dst._check_many(da, sz)
         ctx = self.ctx.handle
         N.check(N.lib().cf_memcpy_batch(ctx, N.ptr(da), N.ptr(sa), N.ptr(sz), sa.size, None), "transfer_ranges")
         N.check(N.lib().cf_ctx_sync(ctx))
@@ -666,9 +685,14 @@ class Machine:
 
 
 def _poke_words(fields: np.ndarray, values: np.ndarray) -> None:
-    """Write 8-byte values at arbitrary (4-aligned) host addresses."""
-    for f, v in zip(fields.tolist(), values.tolist()):
-        C.memmove(f, int(v).to_bytes(8, "little"), 8)
+    """Write 8-byte values at arbitrary (4-aligned) host addresses (vectorised over one span)."""
+    fields = np.asarray(fields, np.uint64)
+    if fields.size == 0:
+        return
+    lo, hi = int(fields.min()), int(fields.max()) + 8
+    view = N.host_view(lo, hi - lo)
+    idx = (fields - np.uint64(lo)).astype(np.int64)[:, None] + np.arange(8, dtype=np.int64)[None, :]
+    view[idx] = np.ascontiguousarray(values, np.uint64).view(np.uint8).reshape(-1, 8)
 
 
 class AddressMap:

@@ -292,12 +292,10 @@ def _build(machine: Machine, spec, arena: Arena | None, seed: int, align: int | 
         arena.served_offset = total
         arena.set_site_offsets(handle.site_off, plan.table(N.CF_TAB_SITE_SORTED))
     elif machine.uvm is not None:
-        ps = machine.uvm.page_size
-        first = (np.uint64(base) + handle.alloc_off) // np.uint64(ps)
-        last = (np.uint64(base) + handle.alloc_off + handle.alloc_size - np.uint64(1)) // np.uint64(ps)
-        pages = np.unique(np.concatenate([np.arange(int(a), int(b) + 1, dtype=np.int64)
-                                          for a, b in zip(first, last)]))
-        machine.uvm.register_pages(pages)
+        from .harness import _pages_of_spans
+        starts = handle.alloc_off.astype(np.int64) + base
+        machine.uvm.register_pages(_pages_of_spans(starts, handle.alloc_size.astype(np.int64), 1,
+                                                   machine.uvm.page_size))
     return handle
 
 

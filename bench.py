@@ -218,7 +218,8 @@ def compare_schemes(spec, policy: str, reps: int, device: int) -> dict:
     import paper_1906_01128_b200 as cf
     out = {}
     plans = (("marshalling", "marshalling", {}), ("pointerchain", "pointerchain", {}), ("naive", "naive", {}),
-             ("uvm", "uvm", {"uvm_hints": "none"}), ("uvm_prefetch", "uvm", {"uvm_hints": "prefetch"}))
+             ("uvm", "uvm", {"uvm_hints": "none"}), ("uvm_prefetch", "uvm", {"uvm_hints": "prefetch"}),
+             ("uvm_advise", "uvm", {"uvm_hints": "advise"}))
     for name, scheme, kw in plans:
         m = cf.Machine(device=device)
         try:
@@ -288,7 +289,10 @@ def run_ours(args, dist: Dist) -> None:
 
     from paper_1906_01128_b200.shard import shard_for
 
-    device = dist.local_rank
+    from paper_1906_01128_b200 import _native as Nn
+    ndev = Nn.device_count()
+    # one rank per GPU; ranks beyond the visible GPUs share them (plumbing runs on small boxes)
+    device = dist.local_rank % max(ndev, 1)
     spec, policy, desc = make_spec(args.config)
     scaling = "strong" if args.config == "C5" else "weak"
     shard = shard_for(spec, dist.rank, dist.world, scaling)

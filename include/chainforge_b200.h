@@ -274,6 +274,11 @@ int cf_window_run(cf_window* w, int sync, cf_window_stats* stats);
 /* Enqueue nruns windows back to back (scale alternating scale_even / scale_odd, e.g. 2.0 / 0.5
  * so the data stays bounded), then wait: stats cover the whole sequence (benchmark timing). */
 int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd, cf_window_stats* stats);
+/* As cf_window_run_n, alternating two windows planned alike over different images / copy-back
+ * buffers: window r+1 starts copying in while window r is still copying out (each window runs on
+ * its own stream; the copy engines' streams are shared). */
+int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_even, double scale_odd,
+                       cf_window_stats* stats);
 int cf_window_set_scale(cf_window* w, double scale);
 int cf_window_free(cf_window* w);
 

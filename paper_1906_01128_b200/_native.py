@@ -45,7 +45,8 @@ EXPORTED = (
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup",
-    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_set_scale", "cf_window_free",
+    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
+    "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
 )
 
@@ -132,6 +133,7 @@ def _declare(L):
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
+        "cf_window_run_pair": (C.c_int, [P, P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
         "cf_window_free": (C.c_int, [P]),
         "cf_uvm_prefetch": (C.c_int, [P, P, U64, C.c_int, P]),

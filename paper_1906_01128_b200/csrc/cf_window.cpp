@@ -29,6 +29,8 @@ using namespace cf;
 
 struct cf_window {
   cf_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;       // the window's own compute stream (pairs overlap)
+  cudaEvent_t ev_fan = nullptr;        // fan-in/fan-out with the context's compute stream
   cf_window_desc d{};
   cf_chain_shape sh{};
   int elem = 8;
@@ -98,6 +100,8 @@ void destroy(cf_window* w) {
   if (w->ev_first) cudaEventDestroy(w->ev_first);
   if (w->ev_tables) cudaEventDestroy(w->ev_tables);
   for (auto& gr : w->graphs) cudaGraphExecDestroy(gr.exec);
+  if (w->ev_fan) cudaEventDestroy(w->ev_fan);
+  if (w->stream) cudaStreamDestroy(w->stream);
   delete w;
 }
 
@@ -392,7 +396,9 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->ev_k1.resize(nch);
   bool ok = mk(&w->ev_start, cudaEventDefault) == cudaSuccess && mk(&w->ev_end, cudaEventDefault) == cudaSuccess &&
             mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_first, cudaEventDefault) == cudaSuccess &&
-            mk(&w->ev_tables, cudaEventDisableTiming) == cudaSuccess;
+            mk(&w->ev_tables, cudaEventDisableTiming) == cudaSuccess &&
+            mk(&w->ev_fan, cudaEventDisableTiming) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) == cudaSuccess;
   for (uint64_t c = 0; c < nch && ok; ++c)
     ok = mk(&w->ev_h2d[c], cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_rel[c], cudaEventDisableTiming) == cudaSuccess &&
          mk(&w->ev_k0[c], cudaEventDefault) == cudaSuccess && mk(&w->ev_k1[c], cudaEventDefault) == cudaSuccess;
@@ -414,41 +420,66 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
            cudaEvent_t first);
 }  // namespace
 
+namespace {
+// Batch prologue/epilogue on the context's compute stream: the windows' own streams fan out
+// from it (ordered after earlier context work) and join back (ordered before later work).
+int batch_begin(cf_ctx* c, cf_window* const* ws, int nw, cudaEvent_t first) {
+  CF_CUDA(cudaEventRecord(first, c->compute));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, c->compute));
+  CF_CUDA(cudaEventRecord(ws[0]->ev_fan, c->compute));
+  for (int i = 0; i < nw; ++i) CF_CUDA(cudaStreamWaitEvent(ws[i]->stream, ws[0]->ev_fan, 0));
+  return CF_OK;
+}
+int batch_end(cf_ctx* c, cf_window* const* ws, int nw, uint64_t* d2h, cudaEvent_t end) {
+  for (int i = 0; i < nw; ++i) {
+    CF_CUDA(cudaEventRecord(ws[i]->ev_fan, ws[i]->stream));
+    CF_CUDA(cudaStreamWaitEvent(c->compute, ws[i]->ev_fan, 0));
+  }
+  // the error word (sticky over the batch) is read back once, after the last window
+  CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, c->compute));
+  *d2h += 8;
+  CF_CUDA(cudaEventRecord(end, c->compute));
+  return CF_OK;
+}
+}  // namespace
+
 int cf_window_run(cf_window* w, int sync, cf_window_stats* st) {
   if (!w) return fail(CF_E_INVALID, "null window");
   CfDevice g(w->ctx);
   const uint64_t launches0 = w->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
   const bool timing = sync != 0 && st != nullptr && !(w->d.flags & CF_WIN_GRAPH);
-  CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
-  CF_CUDA(cudaMemsetAsync(w->ctx->d_bad, 0xFF, 8, w->ctx->compute));
+  CF_TRY(batch_begin(w->ctx, &w, 1, w->ev_first));
   CF_TRY(one_run(w, timing, &h2d, &d2h));
-  // the error word (sticky over the batch) is read back once, after the last window
-  CF_CUDA(cudaMemcpyAsync(w->ctx->h_bad, w->ctx->d_bad, 8, cudaMemcpyDeviceToHost, w->ctx->compute));
-  d2h += 8;
-  CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
+  CF_TRY(batch_end(w->ctx, &w, 1, &d2h, w->ev_end));
   if (!sync) return CF_OK;
   return finish(w, st, launches0, h2d, d2h, timing, w->ev_first);
 }
 
 int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd, cf_window_stats* st) {
-  if (!w || nruns < 1) return fail(CF_E_INVALID, "bad arguments");
-  CfDevice g(w->ctx);
-  const uint64_t launches0 = w->ctx->launches.load();
+  return cf_window_run_pair(w, nullptr, nruns, scale_even, scale_odd, st);
+}
+
+int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_even, double scale_odd,
+                       cf_window_stats* st) {
+  if (!w0 || nruns < 1) return fail(CF_E_INVALID, "bad arguments");
+  if (w1 && (w1->ctx != w0->ctx || w1->d.flags != w0->d.flags)) return fail(CF_E_INVALID, "mismatched window pair");
+  CfDevice g(w0->ctx);
+  cf_window* ws[2] = {w0, w1 ? w1 : w0};
+  const int nw = w1 ? 2 : 1;
+  const uint64_t launches0 = w0->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
-  CF_CUDA(cudaEventRecord(w->ev_first, w->ctx->compute));
-  CF_CUDA(cudaMemsetAsync(w->ctx->d_bad, 0xFF, 8, w->ctx->compute));
+  CF_TRY(batch_begin(w0->ctx, ws, nw, w0->ev_first));
   for (int r = 0; r < nruns; ++r) {
+    cf_window* w = ws[r % nw];
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;
     CF_TRY(one_run(w, false, &a, &b));
     h2d += a;
     d2h += b;
   }
-  CF_CUDA(cudaMemcpyAsync(w->ctx->h_bad, w->ctx->d_bad, 8, cudaMemcpyDeviceToHost, w->ctx->compute));
-  d2h += 8;
-  CF_CUDA(cudaEventRecord(w->ev_end, w->ctx->compute));
-  return finish(w, st, launches0, h2d, d2h, false, w->ev_first);
+  CF_TRY(batch_end(w0->ctx, ws, nw, &d2h, w0->ev_end));
+  return finish(w0, st, launches0, h2d, d2h, false, w0->ev_first);
 }
 
 namespace {
@@ -463,10 +494,10 @@ int one_run(cf_window* w, bool timing, uint64_t* h2d, uint64_t* d2h) {
   if (!gr) {
     cf_window::Graph g{w->d.scale, nullptr, 0, 0, 0};
     const uint64_t l0 = c->launches.load();
-    CF_CUDA(cudaStreamBeginCapture(c->compute, cudaStreamCaptureModeThreadLocal));
+    CF_CUDA(cudaStreamBeginCapture(w->stream, cudaStreamCaptureModeThreadLocal));
     int rc = enqueue(w, false, &g.h2d, &g.d2h);
     cudaGraph_t graph = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(c->compute, &graph);
+    cudaError_t ce = cudaStreamEndCapture(w->stream, &graph);
     if (rc != CF_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ce != cudaSuccess) return fail(CF_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
     ce = cudaGraphInstantiate(&g.exec, graph, 0);
@@ -477,7 +508,7 @@ int one_run(cf_window* w, bool timing, uint64_t* h2d, uint64_t* d2h) {
     w->graphs.push_back(g);
     gr = &w->graphs.back();
   }
-  CF_CUDA(cudaGraphLaunch(gr->exec, c->compute));
+  CF_CUDA(cudaGraphLaunch(gr->exec, w->stream));
   c->launches.fetch_add(gr->launches);
   *h2d = gr->h2d;
   *d2h = gr->d2h;
@@ -493,7 +524,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   const uint8_t* src = static_cast<const uint8_t*>(d.host_src);
   uint8_t* dst = static_cast<uint8_t*>(d.host_dst);
   const uint64_t dimg = reinterpret_cast<uint64_t>(d.image);
-  cudaStream_t cs = c->compute;
+  cudaStream_t cs = w->stream;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
   // copy streams join only when this window copies anything (a resident window is kernels only)

@@ -54,6 +54,31 @@ class DeepCopyWindow:
         self.chunk_bytes = chunk_bytes
         self._windows: dict = {}
 
+    def twin(self) -> "DeepCopyWindow":
+        """A second window over the same source arena and plan, with its own device image and
+        copy-back buffer: alternating the two lets window r+1 copy in while window r copies out."""
+        t = object.__new__(DeepCopyWindow)
+        t.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("_owned", "_windows")})
+        t._owned, t._windows = [], {}
+        lib = N.lib()
+        dst, img = C.c_void_p(), C.c_void_p()
+        N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(dst)), "pinned copy-back buffer")
+        t._owned.append(("host", dst.value, self.total))
+        N.check(lib.cf_dev_alloc(self.ctx.handle, self.total, C.byref(img)), "device image")
+        t._owned.append(("dev", img.value, self.total))
+        t.dst, t.image = dst.value, img.value
+        return t
+
+    def run_pair_n(self, other: "DeepCopyWindow", nruns: int, flags: int = N.CF_WIN_FULL,
+                   scales: tuple = (2.0, 0.5)):
+        """Alternate this window and its twin for ``nruns`` windows (see cf_window_run_pair)."""
+        a = self._window(flags, self.chunk_bytes, self.mode)
+        b = other._window(flags, other.chunk_bytes, other.mode)
+        st = N.CfWindowStats()
+        N.check(N.lib().cf_window_run_pair(a, b, int(nruns), float(scales[0]), float(scales[1]), C.byref(st)),
+                "cf_window_run_pair")
+        return st
+
     # -- planning ---------------------------------------------------------------------------
     def _window(self, flags: int, chunk_bytes: int, mode: str):
         key = (flags, chunk_bytes, mode)

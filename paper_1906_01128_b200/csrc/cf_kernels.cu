@@ -24,10 +24,13 @@
 
 // tuning knobs (design experiments: tools/build_variants.sh)
 #ifndef CF_SCALE_MINB
-#define CF_SCALE_MINB 8
+#define CF_SCALE_MINB 6
 #endif
 #ifndef CF_GROUP_U
 #define CF_GROUP_U 4
+#endif
+#ifndef CF_GROUP_WARP
+#define CF_GROUP_WARP 1
 #endif
 
 namespace cf {
@@ -381,6 +384,99 @@ __device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s)
   }
 }
 
+// Small-part group, warp-local version: warp w owns parts p0+w, p0+w+8, ... (<= 4 with 32-part
+// groups).  Lanes 0..3 fetch those parts' metadata in parallel (one dependent-load round per
+// warp, no CTA barrier), the warp prefix-sums their vector counts in registers, and then streams
+// the flattened (part, vector) sequence with 4 independent 128-bit loads in flight per lane.
+template <typename T, bool CHASE>
+__device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g, T s) {
+  using VT = Vec<T>;
+  using V = typename VT::V;
+  constexpr uint64_t VN = VT::N;
+  constexpr unsigned WARPS = SCALE_THREADS / 32;
+  constexpr unsigned PER = (GROUP_PARTS + WARPS - 1) / WARPS;  // parts per warp
+  const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // lane j < PER: metadata of part p0 + warp + WARPS * j
+  uint8_t* base = nullptr;
+  uint64_t v0 = 0, e0 = 0, e1 = 0, t = 0;
+  uint32_t nv = 0;
+  const uint64_t pj = uint64_t(p0) + warp + uint64_t(WARPS) * lane;
+  if (lane < PER && pj < p1) {
+    t = a.w.parts[3 * pj];
+    e0 = a.w.parts[3 * pj + 1];
+    e1 = a.w.parts[3 * pj + 2];
+    uint64_t cnt;
+    if (!target_array<CHASE>(a, t, base, cnt) || e1 > cnt) {
+      raise_bad(a.bad, t);
+      base = nullptr;
+      v0 = e1;
+    } else {
+      const uintptr_t first = reinterpret_cast<uintptr_t>(base + e0 * sizeof(T));
+      v0 = e1;
+      if ((first % sizeof(T)) == 0) v0 = min(e1, e0 + ((16 - (first & 15)) & 15) / sizeof(T));
+      nv = uint32_t((e1 - v0) / VN);
+    }
+  }
+  // exclusive prefix of nv over lanes 0..PER-1, broadcast to the warp
+  uint32_t pre[PER + 1];
+  pre[0] = 0;
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
+  uint8_t* bj[PER];
+  uint64_t tj[PER], oj[PER];
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j) {
+    bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
+    tj[j] = __shfl_sync(0xffffffffu, t, j);
+    oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
+  }
+  const uint32_t total = pre[PER];
+  auto vptr = [&](uint32_t f) -> V* {
+    unsigned j = 0;
+#pragma unroll
+    for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
+    uint8_t* b = bj[0];
+    uint32_t off = pre[0];
+    uint64_t tt = tj[0], bo = oj[0];
+#pragma unroll
+    for (unsigned k = 1; k < PER; ++k)
+      if (j == k) { b = bj[k]; off = pre[k]; tt = tj[k]; bo = oj[k]; }
+    if (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
+    return reinterpret_cast<V*>(b) + (f - off);
+  };
+  constexpr int U = 4;
+  uint32_t f = lane;
+  for (; f + (U - 1) * 32 < total; f += U * 32) {
+    V* ptr[U];
+    V r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ptr[u] = vptr(f + u * 32);
+      r[u] = VT::ld(ptr[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) VT::st(ptr[u], VT::mul(r[u], s));
+  }
+  for (; f < total; f += 32) {
+    V* p = vptr(f);
+    VT::st(p, VT::mul(VT::ld(p), s));
+  }
+  // scalar heads / tails (packed layouts only)
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j) {
+    const uint64_t ej0 = __shfl_sync(0xffffffffu, e0, j), ej1 = __shfl_sync(0xffffffffu, e1, j);
+    const uint64_t vj0 = __shfl_sync(0xffffffffu, v0, j);
+    uint8_t* arr = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base), j));
+    if (arr == nullptr) continue;
+    const uint64_t vj1 = vj0 + uint64_t(pre[j + 1] - pre[j]) * VN;
+    for (uint64_t i = ej0 + lane; i < vj0; i += 32)
+      scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+    for (uint64_t i = vj1 + lane; i < ej1; i += 32)
+      scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+  }
+}
+
 // One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
 // blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part.
 template <typename T, bool CHASE>
@@ -414,7 +510,11 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
     return;
   }
   const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
+#if CF_GROUP_WARP
+  scale_group_warp<T, CHASE>(a, g, s);
+#else
   scale_group<T, CHASE>(a, g, s);
+#endif
 }
 
 // ---------------------------------------------------------------- naive fix-up

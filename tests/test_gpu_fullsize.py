@@ -1,0 +1,83 @@
+"""Full-size GPU checks: BASELINE C2 / C4 windows bit-exact against the oracle restatement, and a
+compute-sanitizer memcheck pass over every kernel on small windows."""
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1906_01128_b200 as cf
+    from paper_1906_01128_b200 import _native as N
+    if N.device_count() == 0:
+        pytest.skip("no GPU visible: run `pytest -m gpu` on a B200 box (gpurun)")
+    return cf
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_full_size_window_matches_oracle(cf, oracle, cfg):
+    """The BASELINE config at full size (1 GiB): e2e window copy-back and resident image equal
+    the oracle's expected arena byte for byte (relocated pointers restored, leaves x2)."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    spec, policy, _ = bench.make_spec(cfg)
+    w = cf.DeepCopyWindow(spec, seed=1, policy=policy, align=16)
+    try:
+        st = w.run(scale=2.0)
+        assert st.bad == (1 << 64) - 1
+        ospec = oracle.OSpec(oracle.DENSE, spec.q, spec.n, spec.depth, elem=spec.elem, leaf_only=spec.leaf_only,
+                             align=16)
+        ot = oracle.build(ospec, 1, ptr_base=w.src)
+        idx = oracle.targets(ot, oracle.TARGET_ALL_LEAVES)
+        want = oracle.expected_after_window(ot, idx, 2.0)[:w.total]
+        assert np.array_equal(w.host_dst(), want)
+        assert np.array_equal(w.host_src(), ot.buf[:w.total])   # source untouched
+        w.upload_raw()
+        st = w.run_resident(scale=2.0, graph=True)
+        assert st.bad == (1 << 64) - 1
+        assert np.array_equal(w.image_bytes(), want)
+    finally:
+        w.close()
+
+
+SANITIZE = r'''
+import sys
+sys.path.insert(0, ".")
+import paper_1906_01128_b200 as cf
+specs = [cf.DenseSpec(3, 301, 2, elem=4), cf.DenseSpec(4, 5000, 3, elem=4, leaf_only=True),
+         cf.LinearSpec(4, 777, "allinit_allused"), cf.DenseSpec(3, 17, 2),
+         cf.ForestSpec(cf.LinearSpec(3, 1000, "LLinit_LLused", elem=4), 20, scatter_seed=5)]
+for spec in specs:
+    for align in (1, 16):
+        for mode in ("resolved", "chase"):
+            w = cf.DeepCopyWindow(spec, seed=2, policy="all_arrays", mode=mode, align=align, chunk_bytes=4096)
+            w.run(scale=2.0)
+            w.upload_raw()
+            w.run_resident(scale=0.5)
+            w.close()
+for scheme in ("marshalling", "naive", "pointerchain", "uvm"):
+    m, mach = cf.execute_case(cf.DenseSpec(2, 64, 3), scheme, cf.CostModel(), seed=1)
+    mach.close()
+print("sanitized ok")
+'''
+
+
+def test_compute_sanitizer_memcheck(cf, tmp_path):
+    tool = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(tool):
+        pytest.skip("compute-sanitizer not installed")
+    script = tmp_path / "san.py"
+    script.write_text(SANITIZE)
+    out = subprocess.run([tool, "--tool", "memcheck", "--error-exitcode", "99", sys.executable, str(script)],
+                         capture_output=True, text=True, timeout=900, cwd=str(REPO))
+    assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
+    assert "sanitized ok" in out.stdout
+    assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr

@@ -167,16 +167,18 @@ int cf_relocate(cf_ctx* ctx, void* image, uint64_t image_bytes, const uint64_t* 
  * writes its effective address + node count (targeted_arrays, scenarios.py:270-284, done on
  * the device; harness.py:228-238 pointerchain buffers). */
 int cf_resolve(cf_ctx* ctx, const void* image, const cf_chain_shape* shape, const uint64_t* d_root,
-               const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets,
+               const int32_t* d_level, const uint32_t* d_ordinal, uint64_t ntargets,
                uint64_t* d_ea, uint32_t* d_count, uint64_t* d_bad, void* stream);
 /* Leaf-kernel work list (device pointers).  A launch covers big parts
- * [big_begin, big_begin + big_count) -- one CTA per 16 KiB tile, tiles [tile_begin, tile_end) --
+ * [big_begin, big_begin + big_count) -- one CTA per 16 KiB tile, tiles [tile_begin, tile_end), their
+ * first tiles at tile_base[tb_begin ..) --
  * and small-part groups [group_begin, group_end) -- one CTA per group, one warp per part. */
 typedef struct {
-  const uint64_t* parts;      /* (target, elem_begin, elem_end) triples */
-  const uint64_t* tile_base;  /* per part: first tile number (meaningful for big parts) */
+  const uint32_t* parts;      /* (target, elem_begin, elem_end) u32 triples (nA is u32) */
+  const uint64_t* tile_base;  /* first tile number of every big part, big parts only */
   const uint32_t* groups;     /* (first part, end part) pairs */
-  uint64_t big_begin, big_count;
+  uint64_t big_begin, big_count; /* big parts: parts[big_begin ..), tile_base[tb_begin ..) */
+  uint64_t tb_begin;
   uint64_t tile_begin, tile_end;
   uint64_t group_begin, group_end;
 } cf_scale_work;
@@ -187,7 +189,7 @@ typedef struct {
  * non-hoistable loads (d_ea unused).  d_bad is raised if a part exceeds the count read from
  * the node or the array pointer is null. */
 int cf_scale(cf_ctx* ctx, int elem, int mode, const void* image, const cf_chain_shape* shape,
-             const uint64_t* d_root, const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
+             const uint64_t* d_root, const int32_t* d_level, const uint32_t* d_ordinal, const uint64_t* d_ea,
              const uint32_t* d_count, const cf_scale_work* work, double scale, uint64_t* d_bad,
              void* stream);
 
@@ -208,7 +210,7 @@ int cf_demarshal(cf_ctx* ctx, void* host_arena, uint64_t total, void* image,
  * the targets' chain keys and planned element counts. Synchronous; d_ea_out (optional,
  * device) receives the effective addresses. */
 int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain_shape* shape,
-                    const uint64_t* h_root, const int32_t* h_level, const uint64_t* h_ordinal,
+                    const uint64_t* h_root, const int32_t* h_level, const uint32_t* h_ordinal,
                     const uint64_t* h_count,
                     uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad);
 /* Pointerchain scheme leaf kernel over host-resolved buffers (harness.py:255-259): every

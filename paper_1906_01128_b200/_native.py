@@ -70,8 +70,9 @@ class CfChainShape(C.Structure):
 
 class CfScaleWork(C.Structure):
     _fields_ = [("parts", C.c_void_p), ("tile_base", C.c_void_p), ("groups", C.c_void_p),
-                ("big_begin", C.c_uint64), ("big_count", C.c_uint64), ("tile_begin", C.c_uint64),
-                ("tile_end", C.c_uint64), ("group_begin", C.c_uint64), ("group_end", C.c_uint64)]
+                ("big_begin", C.c_uint64), ("big_count", C.c_uint64), ("tb_begin", C.c_uint64),
+                ("tile_begin", C.c_uint64), ("tile_end", C.c_uint64), ("group_begin", C.c_uint64),
+                ("group_end", C.c_uint64)]
 
 
 class CfWindowDesc(C.Structure):

@@ -39,26 +39,28 @@ void clear_error();
 
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
-                    uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s);
+                    uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s,
+                    const uint32_t* idx = nullptr);
 // One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).
 constexpr uint64_t SMALL_FUSED = 4096;
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
-                          const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
+                          const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
                           cudaStream_t s);
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
-                   const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea,
+                   const int32_t* level, const uint32_t* ordinal, uint64_t n, uint64_t* ea,
                    uint32_t* count, uint64_t* bad, cudaStream_t s);
 // A relocation job that can ride along in a leaf-kernel launch (extra CTAs).
 struct RelocArgs {
   uint8_t* image;
   uint64_t total;
   const uint64_t* sites;
+  const uint32_t* idx;   // optional indirection: site = sites[idx[i]]
   uint64_t n;
   uint64_t from, to;
 };
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
-                 const uint64_t* root, const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
+                 const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
                  cudaStream_t s, const RelocArgs* fused_reloc = nullptr);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
@@ -84,24 +86,25 @@ constexpr uint32_t GROUP_PARTS = 32;
 // Host-side builder of the leaf-kernel work list (see cf_scale_work in the header).
 struct ScaleWork {
   int elem = 4;
-  std::vector<uint64_t> parts;      // (target, elem_begin, elem_end) per part
-  std::vector<uint64_t> tile_base;  // per part: first tile (big parts), 0 for small parts
+  std::vector<uint32_t> parts;      // (target, elem_begin, elem_end) per part
+  std::vector<uint64_t> tile_base;  // first tile of every big part (big parts only)
   std::vector<uint32_t> groups;     // (first part, end part) per group
   uint64_t next_tile = 0;
 
   uint64_t nparts() const { return parts.size() / 3; }
   uint64_t ngroups() const { return groups.size() / 2; }
 
-  // Append one launch segment: big parts first (one CTA per 16 KiB tile), then the small
-  // parts packed into groups.  Descriptor pointers are left null (filled per launch).
+  // Append one launch segment from (target, begin, end) triples: big parts first (one CTA per
+  // 16 KiB tile), then the small parts packed into groups.  Device pointers are left null.
   cf_scale_work append(const std::vector<uint64_t>& tri) {
     cf_scale_work w{};
     const uint64_t tile_elems = TILE_BYTES / uint64_t(elem);
     w.big_begin = nparts();
+    w.tb_begin = tile_base.size();
     w.tile_begin = next_tile;
     for (size_t i = 0; i < tri.size(); i += 3) {
       if (tri[i + 2] - tri[i + 1] < tile_elems) continue;
-      parts.insert(parts.end(), {tri[i], tri[i + 1], tri[i + 2]});
+      parts.insert(parts.end(), {uint32_t(tri[i]), uint32_t(tri[i + 1]), uint32_t(tri[i + 2])});
       tile_base.push_back(next_tile);
       next_tile += tiles_for(tri[i + 2] - tri[i + 1], elem);
     }
@@ -118,8 +121,7 @@ struct ScaleWork {
         first = nparts();
         bytes = 0;
       }
-      parts.insert(parts.end(), {tri[i], tri[i + 1], tri[i + 2]});
-      tile_base.push_back(0);
+      parts.insert(parts.end(), {uint32_t(tri[i]), uint32_t(tri[i + 1]), uint32_t(tri[i + 2])});
       bytes += b;
     }
     if (nparts() > first) groups.insert(groups.end(), {uint32_t(first), uint32_t(nparts())});

@@ -88,8 +88,8 @@ __device__ __forceinline__ void raise_bad(uint64_t* bad, uint64_t idx) {
 // ---------------------------------------------------------------- relocation (attach/detach)
 __device__ __forceinline__ void relocate_one(uint8_t* __restrict__ image, uint64_t total,
                                              const uint64_t* __restrict__ sites, uint64_t i, uint64_t from,
-                                             uint64_t to, uint64_t* bad) {
-  const uint64_t s = sites[i];  // coalesced table read
+                                             uint64_t to, uint64_t* bad, const uint32_t* __restrict__ idx = nullptr) {
+  const uint64_t s = sites[idx ? idx[i] : i];  // coalesced table read
   if (s + 8 > total) { raise_bad(bad, i); return; }
   uint8_t* p = image + s;
   const uint64_t v = ld_u64_any(p);
@@ -99,11 +99,12 @@ __device__ __forceinline__ void relocate_one(uint8_t* __restrict__ image, uint64
 }
 
 __global__ void __launch_bounds__(256) k_relocate(uint8_t* __restrict__ image, uint64_t total,
-                                                  const uint64_t* __restrict__ sites, uint64_t n,
+                                                  const uint64_t* __restrict__ sites,
+                                                  const uint32_t* __restrict__ idx, uint64_t n,
                                                   uint64_t from, uint64_t to, uint64_t* bad) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    relocate_one(image, total, sites, i, from, to, bad);
+    relocate_one(image, total, sites, i, from, to, bad, idx);
 }
 
 // ---------------------------------------------------------------- chain walk
@@ -138,7 +139,7 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
 __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ image, cf_chain_shape sh,
                                                  const uint64_t* __restrict__ root,
                                                  const int32_t* __restrict__ level,
-                                                 const uint64_t* __restrict__ ordinal, uint64_t n,
+                                                 const uint32_t* __restrict__ ordinal, uint64_t n,
                                                  uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
                                                  uint64_t* bad) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
                                                          uint64_t from, uint64_t to, cf_chain_shape sh,
                                                          const uint64_t* __restrict__ root,
                                                          const int32_t* __restrict__ level,
-                                                         const uint64_t* __restrict__ ordinal, uint64_t ntargets,
+                                                         const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                          uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
                                                          uint64_t* bad) {
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
@@ -223,7 +224,7 @@ struct ScaleArgs {
   cf_chain_shape sh;
   const uint64_t* root;       // per-target root offsets (forests), nullptr = sh.root_off
   const int32_t* level;
-  const uint64_t* ordinal;
+  const uint32_t* ordinal;
   const uint64_t* ea;
   const uint32_t* count;
   cf_scale_work w;
@@ -485,14 +486,16 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
   const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
   if (blockIdx.x < ntiles) {
     const uint64_t tile = a.w.tile_begin + blockIdx.x;
-    uint64_t lo = a.w.big_begin, hi = a.w.big_begin + a.w.big_count;
+    uint64_t lo = 0, hi = a.w.big_count;   // big part index within this launch
+    const uint64_t* tb = a.w.tile_base + a.w.tb_begin;
     while (hi - lo > 1) {
       const uint64_t mid = (lo + hi) >> 1;
-      if (a.w.tile_base[mid] <= tile) lo = mid; else hi = mid;
+      if (tb[mid] <= tile) lo = mid; else hi = mid;
     }
-    const uint64_t t = a.w.parts[3 * lo];
-    const uint64_t e0 = a.w.parts[3 * lo + 1] + (tile - a.w.tile_base[lo]) * TILE;
-    const uint64_t e1 = min(a.w.parts[3 * lo + 2], e0 + TILE);
+    const uint32_t* pt = a.w.parts + 3 * (a.w.big_begin + lo);
+    const uint64_t t = pt[0];
+    const uint64_t e0 = uint64_t(pt[1]) + (tile - tb[lo]) * TILE;
+    const uint64_t e1 = min(uint64_t(pt[2]), e0 + TILE);
     uint8_t* arr;
     uint64_t cnt;
     if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
@@ -506,7 +509,8 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
   if (blockIdx.x >= ntiles + ngroups) {
     // fused relocation CTAs (detach riding in the leaf-kernel launch)
     const uint64_t i = (blockIdx.x - ntiles - ngroups) * uint64_t(SCALE_THREADS) + threadIdx.x;
-    if (i < a.reloc.n) relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad);
+    if (i < a.reloc.n)
+      relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad, a.reloc.idx);
     return;
   }
   const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
@@ -589,16 +593,16 @@ unsigned grid_for(cf_ctx* ctx, uint64_t work, unsigned threads, unsigned per_sm)
   } while (0)
 
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t n,
-                    uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s) {
+                    uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s, const uint32_t* idx) {
   if (n == 0) return CF_OK;
-  k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, n, from, to, bad);
+  k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, idx, n, from, to, bad);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
 
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
-                          const uint64_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
+                          const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
                           cudaStream_t s) {
   if (nsites == 0 && ntargets == 0) return CF_OK;
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
@@ -609,7 +613,7 @@ int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uin
 }
 
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
-                   const int32_t* level, const uint64_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count,
+                   const int32_t* level, const uint32_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count,
                    uint64_t* bad, cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, root, level, ordinal, n, ea, count, bad);
@@ -618,7 +622,7 @@ int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, 
 }
 
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
-                 const uint64_t* root, const int32_t* level, const uint64_t* ordinal, const uint64_t* ea,
+                 const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count,
                  const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s,
                  const RelocArgs* fused_reloc) {

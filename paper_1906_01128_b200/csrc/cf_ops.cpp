@@ -77,14 +77,14 @@ std::vector<uint64_t> chunk_bounds(uint64_t total, uint64_t chunk, const uint64_
 
 // Upload a host ScaleWork into `dst` (device) and point `w` at it.
 uint64_t work_bytes(const ScaleWork& sw) {
-  return sw.parts.size() * 8 + sw.tile_base.size() * 8 + ((sw.groups.size() * 4 + 7) / 8) * 8;
+  return ((sw.parts.size() * 4 + 7) / 8) * 8 + sw.tile_base.size() * 8 + sw.groups.size() * 4 + 8;
 }
 int upload_work(const ScaleWork& sw, uint8_t* dst, cudaStream_t s, cf_scale_work* w) {
-  const uint64_t n1 = sw.parts.size() * 8, n2 = sw.tile_base.size() * 8, n3 = sw.groups.size() * 4;
-  if (n1) CF_CUDA(cudaMemcpyAsync(dst, sw.parts.data(), n1, cudaMemcpyHostToDevice, s));
+  const uint64_t n1 = ((sw.parts.size() * 4 + 7) / 8) * 8, n2 = sw.tile_base.size() * 8, n3 = sw.groups.size() * 4;
+  if (!sw.parts.empty()) CF_CUDA(cudaMemcpyAsync(dst, sw.parts.data(), sw.parts.size() * 4, cudaMemcpyHostToDevice, s));
   if (n2) CF_CUDA(cudaMemcpyAsync(dst + n1, sw.tile_base.data(), n2, cudaMemcpyHostToDevice, s));
   if (n3) CF_CUDA(cudaMemcpyAsync(dst + n1 + n2, sw.groups.data(), n3, cudaMemcpyHostToDevice, s));
-  w->parts = reinterpret_cast<const uint64_t*>(dst);
+  w->parts = reinterpret_cast<const uint32_t*>(dst);
   w->tile_base = reinterpret_cast<const uint64_t*>(dst + n1);
   w->groups = reinterpret_cast<const uint32_t*>(dst + n1 + n2);
   return CF_OK;
@@ -110,7 +110,7 @@ int cf_relocate(cf_ctx* c, void* image, uint64_t image_bytes, const uint64_t* d_
 }
 
 int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const uint64_t* d_root,
-               const int32_t* d_level, const uint64_t* d_ordinal, uint64_t ntargets, uint64_t* d_ea,
+               const int32_t* d_level, const uint32_t* d_ordinal, uint64_t ntargets, uint64_t* d_ea,
                uint32_t* d_count, uint64_t* d_bad, void* stream) {
   if (!c || !shape) return fail(CF_E_INVALID, "null argument");
   CfDevice g(c);
@@ -119,7 +119,7 @@ int cf_resolve(cf_ctx* c, const void* image, const cf_chain_shape* shape, const 
 }
 
 int cf_scale(cf_ctx* c, int elem, int mode, const void* image, const cf_chain_shape* shape,
-             const uint64_t* d_root, const int32_t* d_level, const uint64_t* d_ordinal, const uint64_t* d_ea,
+             const uint64_t* d_root, const int32_t* d_level, const uint32_t* d_ordinal, const uint64_t* d_ea,
              const uint32_t* d_count,
              const cf_scale_work* work, double scale, uint64_t* d_bad, void* stream) {
   if (!c || !shape || !work) return fail(CF_E_INVALID, "null argument");
@@ -217,7 +217,7 @@ int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const
 }
 
 int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_shape* shape,
-                    const uint64_t* h_root, const int32_t* h_level, const uint64_t* h_ordinal,
+                    const uint64_t* h_root, const int32_t* h_level, const uint32_t* h_ordinal,
                     const uint64_t* h_count, uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad) {
   if (!c || !shape || (ntargets && (!h_level || !h_ordinal || !h_count))) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
@@ -233,7 +233,7 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   cf_scale_work work = sw.append(tri);
   // one device block: level | ordinal | ea | count | roots | work list
   const uint64_t off_ord = ((ntargets * 4 + 7) / 8) * 8;
-  const uint64_t off_ea = off_ord + ntargets * 8;
+  const uint64_t off_ea = off_ord + ((ntargets * 4 + 7) / 8) * 8;
   const uint64_t off_cnt = off_ea + ntargets * 8;
   const uint64_t off_root = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
   const uint64_t off_work = off_root + (h_root ? ntargets * 8 : 0);
@@ -242,13 +242,13 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   uint8_t* d = blk.as<uint8_t>();
   cudaStream_t s = c->compute;
   CF_CUDA(cudaMemcpyAsync(d, h_level, ntargets * 4, cudaMemcpyHostToDevice, s));
-  CF_CUDA(cudaMemcpyAsync(d + off_ord, h_ordinal, ntargets * 8, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + off_ord, h_ordinal, ntargets * 4, cudaMemcpyHostToDevice, s));
   if (h_root) CF_CUDA(cudaMemcpyAsync(d + off_root, h_root, ntargets * 8, cudaMemcpyHostToDevice, s));
   const uint64_t* droot = h_root ? reinterpret_cast<const uint64_t*>(d + off_root) : nullptr;
   CF_TRY(upload_work(sw, d + off_work, s, &work));
   CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   const int32_t* lv = reinterpret_cast<const int32_t*>(d);
-  const uint64_t* od = reinterpret_cast<const uint64_t*>(d + off_ord);
+  const uint32_t* od = reinterpret_cast<const uint32_t*>(d + off_ord);
   uint64_t* ea = reinterpret_cast<uint64_t*>(d + off_ea);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(d + off_cnt);
   CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, droot, lv, od, ntargets, ea, cnt, c->d_bad, s));

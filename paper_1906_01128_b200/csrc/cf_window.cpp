@@ -61,6 +61,7 @@ struct cf_window {
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr, ev_first = nullptr, ev_tables = nullptr;
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
+  bool has_roots = false;
   // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
   struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
   std::vector<Graph> graphs;
@@ -299,19 +300,20 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     for (; k < parts.size() && parts[k].step == c; ++k) tri.insert(tri.end(), {tpos[parts[k].t], parts[k].b, parts[k].e});
     w->seg[c] = sw.append(tri);
   }
-  std::vector<uint64_t> det(nsites);
+  // detach order: positions in the (step-ordered) relocation table, grouped by release step
+  std::vector<uint32_t> det(nsites);
   {
     std::vector<uint64_t> sidx(nsites);
     std::iota(sidx.begin(), sidx.end(), 0);
     std::vector<uint64_t> srel(nsites);
-    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[six.at(sites[s])];
+    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[six.at(reloc[s])];
     std::stable_sort(sidx.begin(), sidx.end(), [&](uint64_t x, uint64_t y) { return srel[x] < srel[y]; });
     w->det_lo.assign(nch + 1, 0);
     for (uint64_t c = 0, k = 0; c <= nch; ++c) {
       while (k < nsites && srel[sidx[k]] < c) ++k;
       w->det_lo[c] = k;
     }
-    for (uint64_t k = 0; k < nsites; ++k) det[k] = sites[sidx[k]];
+    for (uint64_t k = 0; k < nsites; ++k) det[k] = uint32_t(sidx[k]);
   }
   w->released.assign(nch, {});
   const uint64_t nnode_seg = hoist ? w->step_seg_lo[1] : 0;
@@ -343,13 +345,14 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
 
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
+  w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
   w->off_sites = 0;
   w->off_det = al8(w->off_sites + nsites * 8);
-  w->off_level = al8(w->off_det + nsites * 8);
+  w->off_level = al8(w->off_det + nsites * 4);
   w->off_ord = al8(w->off_level + nt * 4);
-  w->off_root = al8(w->off_ord + nt * 8);
-  w->off_parts = al8(w->off_root + nt * 8);
-  w->off_tb = al8(w->off_parts + sw.parts.size() * 8);
+  w->off_root = al8(w->off_ord + nt * 4);
+  w->off_parts = al8(w->off_root + (w->has_roots ? nt * 8 : 0));
+  w->off_tb = al8(w->off_parts + sw.parts.size() * 4);
   w->off_grp = al8(w->off_tb + sw.tile_base.size() * 8);
   w->off_zc_h2d = al8(w->off_grp + sw.groups.size() * 4 + 8);
   w->off_zc_d2h = w->off_zc_h2d + (w->zc ? w->zc_n * 16 : 0);
@@ -360,17 +363,17 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_count, std::max<uint64_t>(nt, 1) * 4);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "window tables: %s", cudaGetErrorString(ce)); }
   if (nsites) memcpy(w->h_tab + w->off_sites, reloc.data(), nsites * 8);
-  memcpy(w->h_tab + w->off_det, det.data(), nsites * 8);
+  if (nsites) memcpy(w->h_tab + w->off_det, det.data(), nsites * 4);
   int32_t* lv = reinterpret_cast<int32_t*>(w->h_tab + w->off_level);
-  uint64_t* od = reinterpret_cast<uint64_t*>(w->h_tab + w->off_ord);
+  uint32_t* od = reinterpret_cast<uint32_t*>(w->h_tab + w->off_ord);
   uint64_t* rt = reinterpret_cast<uint64_t*>(w->h_tab + w->off_root);
   for (uint64_t k = 0; k < nt; ++k) {
     const int64_t a = desc->h_targets[torder[k]];
     lv[k] = t->arr_level[a];
-    od[k] = t->arr_ordinal[a];
-    rt[k] = t->arr_root[a];
+    od[k] = uint32_t(t->arr_ordinal[a]);
+    if (w->has_roots) rt[k] = t->arr_root[a];
   }
-  if (!sw.parts.empty()) memcpy(w->h_tab + w->off_parts, sw.parts.data(), sw.parts.size() * 8);
+  if (!sw.parts.empty()) memcpy(w->h_tab + w->off_parts, sw.parts.data(), sw.parts.size() * 4);
   if (!sw.tile_base.empty()) memcpy(w->h_tab + w->off_tb, sw.tile_base.data(), sw.tile_base.size() * 8);
   if (!sw.groups.empty()) memcpy(w->h_tab + w->off_grp, sw.groups.data(), sw.groups.size() * 4);
   if (w->zc) {
@@ -379,7 +382,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     memcpy(w->h_tab + w->off_zc_d2h, zc_rel.data(), zc_rel.size() * 8);
   }
   for (auto& sg : w->seg) {
-    sg.parts = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_parts);
+    sg.parts = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_parts);
     sg.tile_base = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
     sg.groups = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_grp);
   }
@@ -544,10 +547,10 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     h2d_bytes += w->tab_bytes;
   }
   const uint64_t* dsites = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_sites);
-  const uint64_t* ddet = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_det);
+  const uint32_t* ddet = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_det);
   const int32_t* dlv = reinterpret_cast<const int32_t*>(w->d_tab + w->off_level);
-  const uint64_t* dod = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_ord);
-  const uint64_t* drt = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_root);
+  const uint32_t* dod = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_ord);
+  const uint64_t* drt = w->has_roots ? reinterpret_cast<const uint64_t*>(w->d_tab + w->off_root) : nullptr;
   const bool chase = d.mode == CF_MODE_CHASE;
 
   for (uint64_t k = 0; k < nch; ++k) {
@@ -569,13 +572,13 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
     if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
-                                   drt + w->res_lo[k], dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
+                                   drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
                                    w->d_count + w->res_lo[k], c->d_bad, cs));
     } else {
       if (do_attach)
         CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));
       if (do_resolve)
-        CF_TRY(launch_resolve(c, img, w->sh, drt + w->res_lo[k], dlv + w->res_lo[k], dod + w->res_lo[k], nr,
+        CF_TRY(launch_resolve(c, img, w->sh, drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
                               w->d_ea + w->res_lo[k],
                               w->d_count + w->res_lo[k], c->d_bad, cs));
     }
@@ -587,15 +590,15 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
       if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        RelocArgs det{img, w->total, ddet + w->det_lo[k], nd, dimg, d.host_base};
+        RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base};
         CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
                             nd ? &det : nullptr));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
     if ((fl & CF_WIN_DETACH) && !fuse_detach)
-      CF_TRY(launch_relocate(c, img, w->total, ddet + w->det_lo[k], w->det_lo[k + 1] - w->det_lo[k], dimg,
-                             d.host_base, c->d_bad, cs));
+      CF_TRY(launch_relocate(c, img, w->total, dsites, w->det_lo[k + 1] - w->det_lo[k], dimg, d.host_base, c->d_bad, cs,
+                             ddet + w->det_lo[k]));
     if ((fl & CF_WIN_D2H) && w->zc && w->zc_rel_lo[k + 1] > w->zc_rel_lo[k]) {
       const uint64_t* zs = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zc_d2h) + 2 * w->zc_rel_lo[k];
       CF_TRY(launch_seg_copy(c, zs, w->zc_rel_lo[k + 1] - w->zc_rel_lo[k], img, dst, cs));

@@ -404,7 +404,7 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     sh.root_off = prep.device_root - prep.image
     sh.image_bytes = prep.image_bytes
     lv = np.ascontiguousarray(handle.arr_level[idx], np.int32)
-    od = np.ascontiguousarray(handle.arr_ordinal[idx], np.uint64)
+    od = np.ascontiguousarray(handle.arr_ordinal[idx], np.uint32)
     cnt = np.ascontiguousarray(handle.arr_count[idx], np.uint64)
     # per-target chain roots inside the image (several for a forest)
     if prep.amap is not None:   # naive: objects were re-placed on the device

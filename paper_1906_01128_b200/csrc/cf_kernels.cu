@@ -113,16 +113,23 @@ struct Walk {
   bool leaf;
 };
 
+// A pointer field read while the attach kernel may be rewriting it concurrently (8-byte aligned
+// fields only: the 64-bit store is single-copy atomic): host values are translated on the fly.
+__device__ __forceinline__ uint64_t xlate(uint64_t v, uint64_t from, const uint8_t* image, uint64_t bytes) {
+  return (from && v - from < bytes) ? reinterpret_cast<uint64_t>(image) + (v - from) : v;
+}
+
 template <bool CHASE>
 __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_shape& sh, uint64_t root_off,
-                                           int level, uint64_t ordinal) {
+                                           int level, uint64_t ordinal, uint64_t xlate_from = 0) {
   const uint8_t* p = image + root_off;
   const bool dense = sh.kind == CF_DENSE;
   uint64_t qpow = 1;
   if (dense)
     for (int l = 1; l < level; ++l) qpow *= sh.q;
   for (int l = 1; l <= level; ++l) {
-    const uint64_t blk = CHASE ? ld_chain_u64(p + OFF_LNEXT) : ld_u64_any(p + OFF_LNEXT);
+    const uint64_t blk = xlate(CHASE ? ld_chain_u64(p + OFF_LNEXT) : ld_u64_any(p + OFF_LNEXT), xlate_from,
+                               image, sh.image_bytes);
     uint64_t child = 0, digit = 0;
     if (dense) {
       child = (l < sh.depth) ? NODE_SIZE : LEAF_NODE_SIZE;
@@ -178,6 +185,35 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
     ea[i] = ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A));
     count[i] = ld_u32_any(w.node + OFF_NA);
   }
+}
+
+// Large windows on an aligned arena (C4: 1.02M sites, 1M chains): attach and resolve in ONE
+// launch, side by side -- CTAs [0, att_blocks) relocate sites, the rest resolve chains,
+// translating any host pointer they meet that the attach CTAs have not rewritten yet.
+__global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict__ image, uint64_t total,
+                                                             const uint64_t* __restrict__ sites, uint64_t nsites,
+                                                             uint64_t from, uint64_t to, cf_chain_shape sh,
+                                                             const uint64_t* __restrict__ root,
+                                                             const int32_t* __restrict__ level,
+                                                             const uint32_t* __restrict__ ordinal, uint64_t ntargets,
+                                                             uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
+                                                             uint64_t* bad, unsigned att_blocks) {
+  if (blockIdx.x < att_blocks) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < nsites) relocate_one(image, total, sites, i, from, to, bad);
+    return;
+  }
+  const uint64_t i = uint64_t(blockIdx.x - att_blocks) * blockDim.x + threadIdx.x;
+  if (i >= ntargets) return;
+  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i], from);
+  if (!w.node) {
+    ea[i] = 0;
+    count[i] = 0;
+    raise_bad(bad, i);
+    return;
+  }
+  ea[i] = xlate(ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)), from, image, sh.image_bytes);
+  count[i] = ld_u32_any(w.node + OFF_NA);
 }
 
 // ---------------------------------------------------------------- leaf kernel
@@ -608,6 +644,19 @@ int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uin
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
   k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level, ordinal, ntargets,
                                         ea, count, bad);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
+                               uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
+                               const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
+                               uint32_t* count, uint64_t* bad, cudaStream_t s) {
+  const uint64_t ab = (nsites + 255) / 256, rb = (ntargets + 255) / 256;
+  if (ab + rb == 0) return CF_OK;
+  if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
+  k_attach_resolve_wide<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level,
+                                                         ordinal, ntargets, ea, count, bad, unsigned(ab));
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -62,6 +62,7 @@ struct cf_window {
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
   bool has_roots = false;
+  bool aligned8 = false;   // every pointer field 8-byte aligned (align >= 8): attach || resolve safe
   // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
   struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
   std::vector<Graph> graphs;
@@ -346,6 +347,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
+  w->aligned8 = t->spec.align >= 8;
   w->off_sites = 0;
   w->off_det = al8(w->off_sites + nsites * 8);
   w->off_level = al8(w->off_det + nsites * 4);
@@ -574,6 +576,10 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
                                    drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
                                    w->d_count + w->res_lo[k], c->d_bad, cs));
+    } else if (do_attach && do_resolve && w->aligned8) {
+      CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
+                                        drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
+                                        w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
     } else {
       if (do_attach)
         CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));

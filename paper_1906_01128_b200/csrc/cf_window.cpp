@@ -82,6 +82,10 @@ struct SegIndex {
 // Hoist node records into their own leading step when there are few node allocations.
 constexpr uint64_t HOIST_MAX_NODE_ALLOCS = 4096;
 constexpr uint64_t HOIST_MERGE_GAP = 64;
+#ifndef CF_HOIST_PAGE
+#define CF_HOIST_PAGE 4096
+#endif
+constexpr uint64_t HOIST_PAGE = CF_HOIST_PAGE;
 // More hoisted node segments than this move by zero-copy kernels instead of one DMA each.
 constexpr uint64_t ZC_MIN_SEGS = 16;
 
@@ -162,6 +166,14 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   };
   if (hoist) {
     std::sort(node_ranges.begin(), node_ranges.end());
+    // widen node ranges to whole pages so the bulk data copies stay page-aligned (the copy
+    // engines lose full-duplex overlap on many unaligned pieces)
+    // 64 KiB pages when that moves < 1/32 of the arena through the node step, else 4 KiB
+    const uint64_t pa = (HOIST_PAGE > 1 && node_ranges.size() * 65536 <= total / 32) ? 65536 : HOIST_PAGE;
+    for (auto& r : node_ranges) {
+      r.first = r.first / pa * pa;
+      r.second = std::min(total, (r.second + pa - 1) / pa * pa);
+    }
     std::vector<std::pair<uint64_t, uint64_t>> merged;
     for (auto& r : node_ranges) {
       if (!merged.empty() && r.first <= merged.back().second + HOIST_MERGE_GAP) merged.back().second = std::max(merged.back().second, r.second);

@@ -236,7 +236,7 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx,
                           buf_host=handle.arr_off[idx] + np.uint64(handle.base), buf_count=handle.arr_count[idx])
         if len(idx):
-            dev_base = machine.device.allocate_span(int(aligned.sum()), offs, sizes)
+            dev_base = machine.device.allocate_span(int(aligned.sum()), offs, sizes, zero=False)
             prep.buf_dev = offs + np.uint64(dev_base)
             machine.transfer_ranges(machine.host, prep.buf_host, machine.device, prep.buf_dev, sizes, "bulk")
         return prep

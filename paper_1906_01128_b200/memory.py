@@ -186,12 +186,13 @@ class MemorySpace:
             return N.CF_MEM_MANAGED
         return N.CF_MEM_PINNED if self.machine is not None and self.machine.has_device else N.CF_MEM_PAGEABLE
 
-    def _raw_alloc(self, nbytes: int) -> int:
+    def _raw_alloc(self, nbytes: int, zero: bool = True) -> int:
         p = C.c_void_p()
         kind = self._memkind()
         if kind < 0:
             N.check(N.lib().cf_dev_alloc(self.machine.ctx.handle, nbytes, C.byref(p)), "device allocate")
-            N.check(N.lib().cf_memset(self.machine.ctx.handle, p, 0, nbytes))
+            if zero:
+                N.check(N.lib().cf_memset(self.machine.ctx.handle, p, 0, nbytes))
         else:
             N.check(N.lib().cf_host_alloc(nbytes, kind, C.byref(p)), "host allocate")
         self._storage.append((p.value, nbytes, kind))
@@ -217,13 +218,15 @@ class MemorySpace:
         self._seg_bases.insert(i, seg.base)
         self._segs.insert(i, seg)
 
-    def allocate(self, size_bytes: int) -> int:
+    def allocate(self, size_bytes: int, zero: bool = True) -> int:
+        """Bump allocation.  ``zero=False`` skips the zero fill for storage the caller overwrites
+        completely (device images of an arena, selective-copy buffers)."""
         if size_bytes <= 0:
             raise ValueError("allocation size must be positive")
         aligned = (size_bytes + ALIGNMENT - 1) & ~(ALIGNMENT - 1)
         self._reserve(aligned, size_bytes)
         if aligned > SLAB_BYTES // 4:
-            addr = self._raw_alloc(aligned)
+            addr = self._raw_alloc(aligned, zero)
         else:
             if self._slab is None or self._slab_used + aligned > self._slab[1]:
                 self._slab = (self._raw_alloc(SLAB_BYTES), SLAB_BYTES)
@@ -233,7 +236,7 @@ class MemorySpace:
         self._register(_Segment(addr, size_bytes))
         return addr
 
-    def allocate_span(self, total: int, offs: np.ndarray, sizes: np.ndarray) -> int:
+    def allocate_span(self, total: int, offs: np.ndarray, sizes: np.ndarray, zero: bool = True) -> int:
         """One storage block holding a whole tree's allocations (offsets relative to the block).
 
         Used by the native builder so a million-object tree is one pinned block while each
@@ -243,7 +246,7 @@ class MemorySpace:
             raise ValueError("allocation size must be positive")
         aligned = (total + 4095) & ~4095
         self._reserve((total + ALIGNMENT - 1) & ~(ALIGNMENT - 1), total)
-        addr = self._raw_alloc(aligned)
+        addr = self._raw_alloc(aligned, zero)
         order = np.argsort(offs, kind="stable")
         self._register(_Segment(addr, total, np.ascontiguousarray(offs[order], np.uint64),
                                 np.ascontiguousarray(sizes[order], np.uint64)))
@@ -561,7 +564,7 @@ class Machine:
     def marshal_transfer_and_attach(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> int:
         """Ship the arena in one logical bulk op (chunked over copy streams) and relocate every
         pointer field on the device as its chunk lands."""
-        image = self.device.allocate(arena.total_bytes)
+        image = self.device.allocate(arena.total_bytes, zero=False)   # fully overwritten by the copy
         sites = arena.sorted_site_offsets
         bad = N.U64(0)
         rc = N.lib().cf_marshal_transfer_and_attach(
@@ -601,7 +604,7 @@ class Machine:
         aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
         span = int(aligned.sum())
         dev_off = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64)
-        dev_base = self.device.allocate_span(span, dev_off, sizes)
+        dev_base = self.device.allocate_span(span, dev_off, sizes, zero=False)
         dev = dev_off + np.uint64(dev_base)
         host = allocs[:, 0].astype(np.uint64)
         ctx = self.ctx.handle

@@ -254,3 +254,31 @@ def test_scattered_forest_window_and_schemes(cf, elem):
         m, machine = cf.execute_case(spec, scheme, cf.CostModel(), seed=3, policy="all_leaves", align=16)
         assert m.verified and m.scenario.startswith("forest9")
         machine.close()
+
+
+def test_cli_simulate_and_sweep_match_reference_counters(cf, kats, tmp_path):
+    """`python -m paper_1906_01128_b200 simulate|sweep` emit the reference CSV schema with the
+    reference's counters (golden execute_case rows); sweeps are byte-deterministic."""
+    from paper_1906_01128_b200 import cli
+    import contextlib
+    import io
+    row = next(r for r in kats["counters"] if r["spec"] == {"kind": "dense", "q": 2, "n": 10, "depth": 3})
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        assert cli.main(["simulate", "--scenario", "dense", "--q", "2", "--n", "10", "--scheme", "marshalling",
+                         "--seed", "1"]) == 0
+    header, line = buf.getvalue().strip().split("\n")
+    assert header == cli.CSV_HEADER
+    vals = dict(zip(header.split(","), line.split(",")))
+    want = row["schemes"]["marshalling"]
+    assert [int(vals[k]) for k in ("bytes_h2d", "bytes_d2h", "transfer_ops", "attach_ops", "page_faults",
+                                   "instr_estimate")] == want[:6]
+    grid = tmp_path / "grid.csv"
+    grid.write_text("scenario,scheme,layout,k_or_q,n\n" + "".join(
+        f"linear,{s},LLinit_LLused,3,100\n" for s in ("uvm", "marshalling", "pointerchain", "naive")))
+    a, b = tmp_path / "a.csv", tmp_path / "b.csv"
+    assert cli.main(["sweep", "--grid", str(grid), "--out", str(a), "--seed", "3"]) == 0
+    assert cli.main(["sweep", "--grid", str(grid), "--out", str(b), "--seed", "3"]) == 0
+    assert a.read_bytes() == b.read_bytes()
+    rows = a.read_text().strip().split("\n")
+    assert len(rows) == 5 and rows[0] == cli.CSV_HEADER

@@ -217,7 +217,8 @@ def compare_schemes(spec, policy: str, reps: int, device: int) -> dict:
     with a whole-tree prefetch; GB/s are graph bytes over the window."""
     import paper_1906_01128_b200 as cf
     out = {}
-    plans = (("marshalling", "marshalling", {}), ("pointerchain", "pointerchain", {}), ("naive", "naive", {}),
+    plans = (("marshalling", "marshalling", {}), ("marshalling_eager", "marshalling", {"fused": False}),
+             ("pointerchain", "pointerchain", {}), ("naive", "naive", {}),
              ("uvm", "uvm", {"uvm_hints": "none"}), ("uvm_prefetch", "uvm", {"uvm_hints": "prefetch"}),
              ("uvm_advise", "uvm", {"uvm_hints": "advise"}))
     for name, scheme, kw in plans:

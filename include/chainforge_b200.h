@@ -217,6 +217,12 @@ int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain
  * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */
 int cf_scale_resolved(cf_ctx* ctx, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,
                       double scale);
+/* The attach loop's bounds check (memory.py:319-321) on the host, before any transfer: every
+ * site (arena offset, table order) must hold a pointer into [ptr_base, ptr_base + total).
+ * Returns CF_E_OUTSIDE_ARENA with *bad_index = the first offending table index.  Lets a
+ * deferred (fused) marshalling window raise AttachOutsideArena at transfer_to_device time. */
+int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t* h_sites, uint64_t nsites,
+                         uint64_t ptr_base, uint64_t* bad_index);
 /* naive_deep_copy fixups (memory.py:349-365): per-object copies are issued by the caller with
  * cf_memcpy_batch; this kernel rewrites every site through a sorted interval map
  * (AddressMap.translate, memory.py:409-419) on the device. */

@@ -44,7 +44,7 @@ EXPORTED = (
     "cf_memcpy_async", "cf_memset", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
-    "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup",
+    "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -131,6 +131,7 @@ def _declare(L):
         "cf_scale_resolved": (C.c_int, [P, C.c_int, P, P, U64, C.c_double]),
         "cf_memcpy_batch": (C.c_int, [P, P, P, P, U64, P]),
         "cf_naive_fixup": (C.c_int, [P, P, P, U64, P, P, P, U64, P, P]),
+        "cf_arena_check_sites": (C.c_int, [P, U64, P, U64, U64, C.POINTER(U64)]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),

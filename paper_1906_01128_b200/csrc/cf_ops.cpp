@@ -3,6 +3,7 @@
 //   cf_demarshal                    <- Machine.demarshal                    memory.py:327-345
 //   cf_kernel_scale                 <- kernel_scale (marshalling/naive walk) harness.py:244-304
 //   cf_naive_fixup                  <- naive_deep_copy fix-up loop         memory.py:362-364
+//   cf_arena_check_sites            <- the attach loop's bounds check      memory.py:319-321
 #include "cf_internal.h"
 
 #include <algorithm>
@@ -303,6 +304,28 @@ int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t*
   CF_TRY(read_bad(c, c->d_bad, s, &rb));
   if (rb != NO_BAD) return fail(CF_E_WILD, "leaf kernel: buffer %llu rejected", (unsigned long long)rb);
   return CF_OK;
+}
+
+int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t* h_sites, uint64_t nsites,
+                         uint64_t ptr_base, uint64_t* bad_index) {
+  if (!host_arena || (nsites && !h_sites)) return fail(CF_E_INVALID, "null argument");
+  if (bad_index) *bad_index = NO_BAD;
+  const uint8_t* h = static_cast<const uint8_t*>(host_arena);
+  uint64_t first = NO_BAD;   // smallest offending index in table order
+#pragma omp parallel for schedule(static) reduction(min : first) if (nsites > (1u << 16))
+  for (int64_t i = 0; i < int64_t(nsites); ++i) {
+    const uint64_t s = h_sites[i];
+    uint64_t v;
+    if (s > total || total - s < 8) { first = std::min<uint64_t>(first, uint64_t(i)); continue; }
+    memcpy(&v, h + s, 8);
+    if (v - ptr_base >= total) first = std::min<uint64_t>(first, uint64_t(i));
+  }
+  if (first == NO_BAD) return CF_OK;
+  if (bad_index) *bad_index = first;
+  uint64_t v = 0;
+  if (h_sites[first] <= total && total - h_sites[first] >= 8) memcpy(&v, h + h_sites[first], 8);
+  return fail(CF_E_OUTSIDE_ARENA, "pointer field at arena offset %llu targets 0x%llx outside the arena",
+              (unsigned long long)h_sites[first], (unsigned long long)v);
 }
 
 int cf_naive_fixup(cf_ctx* c, const uint64_t* d_field_host, const uint64_t* d_target_host, uint64_t nsites,

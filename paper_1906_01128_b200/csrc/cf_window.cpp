@@ -20,7 +20,12 @@
 // arena.
 #include "cf_internal.h"
 
+#include <omp.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -89,6 +94,21 @@ constexpr uint64_t HOIST_PAGE = CF_HOIST_PAGE;
 // More hoisted node segments than this move by zero-copy kernels instead of one DMA each.
 constexpr uint64_t ZC_MIN_SEGS = 16;
 
+// One piece of a target's array: elements [b, e) of target t, scaled at upload step `step`.
+struct Part { uint64_t t, b, e, step; };
+
+// Stable bucket order of [0, key.size()) by key (< nk): order = indices grouped by key, lo[c] =
+// first position whose key >= c (lo has nk + 1 entries).
+void bucket_order(const std::vector<uint64_t>& key, uint64_t nk, std::vector<uint64_t>& order,
+                  std::vector<uint64_t>& lo) {
+  lo.assign(nk + 1, 0);
+  for (uint64_t k : key) ++lo[k + 1];
+  for (uint64_t c = 0; c < nk; ++c) lo[c + 1] += lo[c];
+  std::vector<uint64_t> at(lo.begin(), lo.end() - 1);
+  order.resize(key.size());
+  for (uint64_t i = 0; i < key.size(); ++i) order[at[key[i]]++] = i;
+}
+
 void destroy(cf_window* w) {
   if (!w) return;
   CfDevice g(w->ctx);
@@ -124,6 +144,15 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   if (!desc->image) return fail(CF_E_INVALID, "null image");
   if (desc->ntargets && !desc->h_targets) return fail(CF_E_INVALID, "null targets");
   CfDevice g(ctx);
+  // CF_PLAN_PROFILE=1: phase times of the planner on stderr
+  static const bool prof = getenv("CF_PLAN_PROFILE") != nullptr;
+  auto tp0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!prof) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[cf_window_plan] %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tp0).count());
+    tp0 = now;
+  };
   cf_window* w = new cf_window();
   w->ctx = ctx;
   w->d = *desc;
@@ -213,121 +242,168 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return w->seg_lo[x] < w->seg_lo[y]; });
     for (uint32_t j : ord) { six.lo.push_back(w->seg_lo[j]); six.seg.push_back(j); }
   }
+  mark("segments");
   auto step_of = [&](uint64_t off) { return seg_step[six.at(off)]; };
+  // Every ordering below is a stable bucket order on a step number (< nch), so planning is
+  // linear in sites + targets (a C4 tree has a million of each); per-item work runs in parallel.
   // attach sites grouped by the step that uploads them (address order within a step)
-  std::vector<uint64_t> reloc(sites, sites + nsites);
-  std::stable_sort(reloc.begin(), reloc.end(), [&](uint64_t x, uint64_t y) { return step_of(x) < step_of(y); });
-  w->reloc_lo.assign(nch + 1, 0);
-  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
-    while (k < nsites && step_of(reloc[k]) < c) ++k;
-    w->reloc_lo[c] = k;
-  }
+  std::vector<uint64_t> site_step(nsites);
+#pragma omp parallel for schedule(static) if (nsites > (1u << 15))
+  for (int64_t k = 0; k < int64_t(nsites); ++k) site_step[k] = step_of(sites[k]);
+  std::vector<uint64_t> reloc_order;
+  bucket_order(site_step, nch, reloc_order, w->reloc_lo);
+  std::vector<uint64_t> reloc(nsites);
+  for (uint64_t k = 0; k < nsites; ++k) reloc[k] = sites[reloc_order[k]];
 
-  // ---- per target: chain fields -> ready step
+  mark("sites");
+  // ---- per target: chain fields -> ready step (fields as (segment) pairs in CSR form)
   const uint64_t nt = desc->ntargets;
   const bool dense = t->spec.kind == CF_DENSE;
   const uint64_t q = dense ? uint64_t(t->spec.k_or_q) : 1;
-  std::vector<uint64_t> ready(nt, 0), max_step(nt, 0);
-  std::vector<std::vector<uint32_t>> field_segs(nt);
-  std::vector<uint64_t> release(seg_step);   // per segment: last step that reads it
   for (uint64_t i = 0; i < nt; ++i) {
     const int64_t a = desc->h_targets[i];
     if (a < 0 || uint64_t(a) >= t->arr_off.size()) { destroy(w); return fail(CF_E_INVALID, "target %lld out of range", (long long)a); }
+  }
+  std::vector<uint64_t> ready(nt, 0), max_step(nt, 0), fld_lo(nt + 1, 0);
+  for (uint64_t i = 0; i < nt; ++i) fld_lo[i + 1] = fld_lo[i] + 2 * uint64_t(t->arr_level[desc->h_targets[i]] + 1);
+  std::vector<uint32_t> fld_seg(fld_lo[nt]);
+#pragma omp parallel for schedule(static) if (nt > (1u << 12))
+  for (int64_t ii = 0; ii < int64_t(nt); ++ii) {
+    const uint64_t i = uint64_t(ii);
+    const int64_t a = desc->h_targets[i];
     const int L = t->arr_level[a];
     const uint64_t ord = t->arr_ordinal[a];
     const auto& lnodes = t->level_nodes[t->arr_tree[a]];
-    uint64_t r = 0;
-    for (int l = 0; l <= L; ++l) {
+    uint64_t r = 0, f = fld_lo[i];
+    uint64_t pw = 1;   // q^(L-l): q^L at the root, divided by q per level down
+    if (dense)
+      for (int l = 0; l < L; ++l) pw *= q;
+    for (int l = 0; l <= L; ++l, pw = (dense && pw >= q) ? pw / q : 1) {
       // ancestor at level l: ordinal prefix ord / q^(L-l) (pre-order within a level)
-      uint64_t pw = 1;
-      for (int m = l; m < L; ++m) pw *= q;
-      const uint64_t node = lnodes[l][dense ? ord / pw : 0];
+      const uint64_t node = lnodes[size_t(l)][dense ? ord / pw : 0];
       const bool leaf = dense && l == t->spec.depth;
       uint64_t lo, hi;  // byte range read at this level
       if (l < L) { lo = node + OFF_LNEXT; hi = lo + 8; }
       else { lo = node + OFF_NA; hi = node + (leaf ? LEAF_NODE_SIZE : OFF_LNEXT); }
       for (uint64_t x : {lo, hi - 1}) {
-        field_segs[i].push_back(six.at(x));
-        r = std::max(r, step_of(x));
+        const uint32_t sg = six.at(x);
+        fld_seg[f++] = sg;
+        r = std::max(r, seg_step[sg]);
       }
     }
     ready[i] = r;
   }
+  mark("targets");
   // ---- parts: each target's array cut at segment boundaries; element i belongs to the
   //      segment holding its last byte
-  struct Part { uint64_t t, b, e, step; };
-  std::vector<Part> parts;
   const uint64_t e = uint64_t(w->elem);
-  for (uint64_t i = 0; i < nt; ++i) {
-    const int64_t a = desc->h_targets[i];
-    const uint64_t off = t->arr_off[a], n = t->arr_count[a];
-    if (n == 0) continue;
-    const uint64_t end = off + e * n;
-    // first element whose last byte lies at or after byte x
-    auto first_i = [&](uint64_t x) -> uint64_t {
-      if (x <= off + e - 1) return 0;
-      return std::min(n, (x - (off + e - 1) + e - 1) / e);
-    };
-    // walk the segments under the array in address order
-    size_t pos = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e - 1) - six.lo.begin()) - 1;
-    for (; pos < six.lo.size() && six.lo[pos] < end; ++pos) {
-      const uint32_t sg = six.seg[pos];
-      const uint64_t i0 = first_i(w->seg_lo[sg]);
-      const uint64_t i1 = (w->seg_hi[sg] >= end) ? n : first_i(w->seg_hi[sg]);
-      if (i1 <= i0) continue;
-      // the piece's bytes may reach into neighbouring segments (elements straddling a
-      // boundary): it runs once all of them have landed and its chain is resolved
-      const size_t pb = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i0) - six.lo.begin()) - 1;
-      const size_t pe = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i1 - 1) - six.lo.begin()) - 1;
-      uint64_t step = ready[i];
-      for (size_t x = pb; x <= pe; ++x) step = std::max(step, seg_step[six.seg[x]]);
-      parts.push_back({i, i0, i1, step});
-      max_step[i] = std::max(max_step[i], step);
-      // every segment this piece touches is copied back no earlier than its step
-      for (size_t x = pb; x <= pe; ++x) release[six.seg[x]] = std::max(release[six.seg[x]], step);
+  std::vector<Part> parts;
+  std::vector<std::pair<uint32_t, uint64_t>> touched;   // (segment, step) of every piece's bytes
+  {
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = nt > (1u << 12) ? omp_get_max_threads() : 1;
+#endif
+    std::vector<std::vector<Part>> tparts(static_cast<size_t>(nthr));
+    std::vector<std::vector<std::pair<uint32_t, uint64_t>>> ttouch(static_cast<size_t>(nthr));
+#pragma omp parallel num_threads(nthr)
+    {
+      int me = 0;
+#ifdef _OPENMP
+      me = omp_get_thread_num();
+#endif
+      auto& P = tparts[size_t(me)];
+      auto& T = ttouch[size_t(me)];
+      P.reserve(nt / size_t(nthr) + 64);
+      T.reserve(nt / size_t(nthr) + 64);
+#pragma omp for schedule(static)
+      for (int64_t ii = 0; ii < int64_t(nt); ++ii) {
+        const uint64_t i = uint64_t(ii);
+        const int64_t a = desc->h_targets[i];
+        const uint64_t off = t->arr_off[a], n = t->arr_count[a];
+        if (n == 0) continue;
+        const uint64_t end = off + e * n;
+        // first element whose last byte lies at or after byte x
+        auto first_i = [&](uint64_t x) -> uint64_t {
+          if (x <= off + e - 1) return 0;
+          return std::min(n, (x - (off + e - 1) + e - 1) / e);
+        };
+        // walk the segments under the array in address order
+        size_t pos = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e - 1) - six.lo.begin()) - 1;
+        {
+          // common case: the whole array inside one segment (one piece)
+          const uint32_t sg = six.seg[pos];
+          if (w->seg_lo[sg] <= off && w->seg_hi[sg] >= end) {
+            const uint64_t step = std::max(ready[i], seg_step[sg]);
+            P.push_back({i, 0, n, step});
+            T.push_back({sg, step});
+            max_step[i] = step;
+            continue;
+          }
+        }
+        uint64_t ms = 0;
+        for (; pos < six.lo.size() && six.lo[pos] < end; ++pos) {
+          const uint32_t sg = six.seg[pos];
+          const uint64_t i0 = first_i(w->seg_lo[sg]);
+          const uint64_t i1 = (w->seg_hi[sg] >= end) ? n : first_i(w->seg_hi[sg]);
+          if (i1 <= i0) continue;
+          // the piece's bytes may reach into neighbouring segments (elements straddling a
+          // boundary): it runs once all of them have landed and its chain is resolved
+          const size_t pb = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i0) - six.lo.begin()) - 1;
+          const size_t pe = size_t(std::upper_bound(six.lo.begin(), six.lo.end(), off + e * i1 - 1) - six.lo.begin()) - 1;
+          uint64_t step = ready[i];
+          for (size_t x = pb; x <= pe; ++x) step = std::max(step, seg_step[six.seg[x]]);
+          P.push_back({i, i0, i1, step});
+          ms = std::max(ms, step);
+          // every segment this piece touches is copied back no earlier than its step
+          for (size_t x = pb; x <= pe; ++x) T.push_back({six.seg[x], step});
+        }
+        max_step[i] = ms;
+      }
     }
+    for (auto& v : tparts) parts.insert(parts.end(), v.begin(), v.end());
+    for (auto& v : ttouch) touched.insert(touched.end(), v.begin(), v.end());
   }
+  std::vector<uint64_t> release(seg_step);   // per segment: last step that reads it
+  for (auto& st : touched) release[st.first] = std::max(release[st.first], st.second);
   const bool chase = desc->mode == CF_MODE_CHASE;
-  for (uint64_t i = 0; i < nt; ++i)
-    for (uint32_t sg : field_segs[i])
-      release[sg] = std::max(release[sg], chase ? std::max(ready[i], max_step[i]) : ready[i]);
+  for (uint64_t i = 0; i < nt; ++i) {
+    const uint64_t v = chase ? std::max(ready[i], max_step[i]) : ready[i];
+    for (uint64_t f = fld_lo[i]; f < fld_lo[i + 1]; ++f) release[fld_seg[f]] = std::max(release[fld_seg[f]], v);
+  }
 
+  mark("parts");
   // ---- order targets by ready step, parts by step, detach sites by release step
-  std::vector<uint64_t> torder(nt);
-  std::iota(torder.begin(), torder.end(), 0);
-  std::stable_sort(torder.begin(), torder.end(), [&](uint64_t x, uint64_t y) { return ready[x] < ready[y]; });
+  std::vector<uint64_t> torder;
+  bucket_order(ready, nch, torder, w->res_lo);
   std::vector<uint64_t> tpos(nt);
   for (uint64_t k = 0; k < nt; ++k) tpos[torder[k]] = k;
-  w->res_lo.assign(nch + 1, 0);
-  for (uint64_t c = 0, k = 0; c <= nch; ++c) {
-    while (k < nt && ready[torder[k]] < c) ++k;
-    w->res_lo[c] = k;
-  }
   // per step: the pieces ready at that step, as one leaf-kernel launch (big tiles + small groups)
-  std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) { return x.step < y.step; });
+  std::vector<uint64_t> pstep(parts.size()), porder, plo;
+  for (size_t k = 0; k < parts.size(); ++k) pstep[k] = parts[k].step;
+  bucket_order(pstep, nch, porder, plo);
   ScaleWork sw;
   sw.elem = w->elem;
   w->seg.resize(nch);
-  for (uint64_t c = 0, k = 0; c < nch; ++c) {
+  for (uint64_t c = 0; c < nch; ++c) {
     std::vector<uint64_t> tri;
-    for (; k < parts.size() && parts[k].step == c; ++k) tri.insert(tri.end(), {tpos[parts[k].t], parts[k].b, parts[k].e});
+    tri.reserve(3 * (plo[c + 1] - plo[c]));
+    for (uint64_t k = plo[c]; k < plo[c + 1]; ++k) {
+      const Part& pp = parts[porder[k]];
+      tri.insert(tri.end(), {tpos[pp.t], pp.b, pp.e});
+    }
     w->seg[c] = sw.append(tri);
   }
   // detach order: positions in the (step-ordered) relocation table, grouped by release step
   std::vector<uint32_t> det(nsites);
   {
-    std::vector<uint64_t> sidx(nsites);
-    std::iota(sidx.begin(), sidx.end(), 0);
-    std::vector<uint64_t> srel(nsites);
-    for (uint64_t s = 0; s < nsites; ++s) srel[s] = release[six.at(reloc[s])];
-    std::stable_sort(sidx.begin(), sidx.end(), [&](uint64_t x, uint64_t y) { return srel[x] < srel[y]; });
-    w->det_lo.assign(nch + 1, 0);
-    for (uint64_t c = 0, k = 0; c <= nch; ++c) {
-      while (k < nsites && srel[sidx[k]] < c) ++k;
-      w->det_lo[c] = k;
-    }
+    std::vector<uint64_t> srel(nsites), sidx;
+#pragma omp parallel for schedule(static) if (nsites > (1u << 15))
+    for (int64_t k = 0; k < int64_t(nsites); ++k) srel[k] = release[six.at(reloc[k])];
+    bucket_order(srel, nch, sidx, w->det_lo);
     for (uint64_t k = 0; k < nsites; ++k) det[k] = uint32_t(sidx[k]);
   }
+  mark("orders");
   w->released.assign(nch, {});
   const uint64_t nnode_seg = hoist ? w->step_seg_lo[1] : 0;
   {
@@ -356,6 +432,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     for (uint64_t id : ids) zc_rel.insert(zc_rel.end(), {w->seg_lo[id], w->seg_hi[id]});
   }
 
+  mark("released");
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
@@ -405,6 +482,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->compute);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "table upload: %s", cudaGetErrorString(ce)); }
 
+  mark("tables");
   // ---- events
   auto mk = [](cudaEvent_t* e, unsigned f) { return cudaEventCreateWithFlags(e, f); };
   w->ev_h2d.resize(nch);
@@ -420,6 +498,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     ok = mk(&w->ev_h2d[c], cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_rel[c], cudaEventDisableTiming) == cudaSuccess &&
          mk(&w->ev_k0[c], cudaEventDefault) == cudaSuccess && mk(&w->ev_k1[c], cudaEventDefault) == cudaSuccess;
   if (!ok) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "event creation failed"); }
+  mark("events");
   *out = w;
   return CF_OK;
 }

@@ -26,8 +26,8 @@ from pathlib import Path
 import numpy as np
 
 from . import _native as N
-from .errors import SchemeError, VerificationFailed
-from .memory import DATA_OP_KINDS, AddressMap, Arena, Machine
+from .errors import AttachOutsideArena, SchemeError, VerificationFailed, WildAccess
+from .memory import D2H, DATA_OP_KINDS, H2D, NULL_ADDR, AddressMap, Arena, Machine
 from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, ForestSpec,
                         LinearSpec, TreeHandle, build_tree, marshal_tree, payload_values, targeted_arrays)
 
@@ -199,6 +199,7 @@ class DevicePrep:
     buf_count: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
     buf_array: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
     handle: TreeHandle | None = None
+    fused: "FusedMarshalWindow | None" = None
 
     @property
     def buffers(self) -> list:
@@ -211,9 +212,102 @@ class DevicePrep:
 
 UVM_HINTS = ("none", "prefetch", "advise")
 
+# pipeline granularity of the fused marshalling window (repo:profiles/r01_design_experiments.md)
+FUSED_CHUNK = 16 << 20
+
+
+class FusedMarshalWindow:
+    """The marshalling scheme's ``transfer_to_device -> kernel_scale -> copy_back`` deferred
+    and enqueued as ONE planned window (cf_window): chunked H2D, attach, device pointerchain
+    resolve, leaf kernel, detach and D2H overlapped chunk by chunk over the full-duplex link,
+    instead of three synchronous phases.
+
+    The calls keep the reference's observable behaviour (harness.py:219-325, memory.py:307-345):
+    each logs its logical entries when called, ``transfer_to_device`` raises
+    ``AttachOutsideArena`` up front (host-side bounds check of every site, memory.py:319-321),
+    and ``copy_back`` returns with the host arena restored and scaled.  Anything that observes or
+    mutates machine state in between (a device/host read or write, another transfer, ...)
+    calls ``Machine.flush``, which runs the window up to the stage reached so far: H2D + attach,
+    or H2D + attach + resolve + scale.  The eager primitives then carry on from there.
+    """
+
+    def __init__(self, machine: Machine, handle: TreeHandle, arena: Arena, image: int, policy: str):
+        self.machine, self.handle, self.arena, self.image, self.policy = machine, handle, arena, image, policy
+        self.scale: float | None = None     # set by kernel_scale
+        self.mode = "resolved"
+
+    def _run(self, flags: int, targets: np.ndarray, scale: float) -> None:
+        base = self.arena.buffer_host_addr
+        mode = N.CF_MODE_CHASE if self.mode == "chase" else N.CF_MODE_RESOLVED
+        lib = N.lib()
+        t0 = time.perf_counter()
+        # plans are cached per (arena, image, targets, mode, flags) on the machine: the tables
+        # depend only on the tree and the target set; the scale is set per run
+        key = (base, self.image, self.policy if len(targets) else None, mode, flags)
+        w = self.machine._plans.get(key)
+        if w is None:
+            tg = np.ascontiguousarray(targets, np.int64)
+            d = N.CfWindowDesc(self.handle.plan.handle, N.ptr(tg) if len(tg) else None, len(tg), base, base, base,
+                               self.image, mode, flags, float(scale), FUSED_CHUNK)
+            w = C.c_void_p()
+            N.check(lib.cf_window_plan(self.machine.ctx.handle, C.byref(d), C.byref(w)), "fused window plan")
+            self.machine._plans[key] = w
+        t1 = time.perf_counter()
+        N.check(lib.cf_window_set_scale(w, float(scale)))
+        rc = lib.cf_window_run(w, 1, None)   # no per-kernel events: detach fuses into the leaf launch
+        # host-side phase times of the last run (plan, enqueue + wait)
+        self.timing = {"plan_ms": (t1 - t0) * 1e3, "run_ms": (time.perf_counter() - t1) * 1e3}
+        if rc == N.CF_E_OUTSIDE_ARENA:   # sites were bounds-checked up front: a chain/count fault
+            raise WildAccess(N.last_error())
+        N.check(rc, "fused marshalling window")
+
+    def _targets(self) -> np.ndarray:
+        idx = self.handle.target_indices(self.policy)
+        return idx[self.handle.arr_count[idx] > 0]
+
+    def flush(self) -> None:
+        """Materialise the stage reached so far; later calls take the eager paths."""
+        if self.scale is None:
+            self._run(N.CF_WIN_H2D | N.CF_WIN_TABLES | N.CF_WIN_ATTACH, np.zeros(0, np.int64), 1.0)
+        else:
+            self._run(N.CF_WIN_H2D | N.CF_WIN_TABLES | N.CF_WIN_ATTACH | N.CF_WIN_RESOLVE | N.CF_WIN_SCALE,
+                      self._targets(), self.scale)
+
+    def complete(self) -> None:
+        """copy_back of a window whose kernel was recorded: the whole pipelined window."""
+        self._run(N.CF_WIN_FULL, self._targets(), self.scale)
+
+
+def _pending(machine: Machine, prep: DevicePrep) -> "FusedMarshalWindow | None":
+    f = prep.fused
+    return f if f is not None and machine._deferred is f else None
+
 
 def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena: Arena | None = None,
-                       policy: str = "ref", uvm_hints: str = "none") -> DevicePrep:
+                       policy: str = "ref", uvm_hints: str = "none", fused: bool = True) -> DevicePrep:
+    """harness.py:219-241.  ``fused=True`` (marshalling): defer the copy so that kernel_scale and
+    copy_back join it in one pipelined window (FusedMarshalWindow); ``False``: eager phases."""
+    machine.flush()
+    if scheme == "marshalling" and fused:
+        if arena is None:
+            raise ValueError("marshalling needs the arena returned by marshal_tree")
+        base, total = arena.buffer_host_addr, arena.total_bytes
+        sites = np.ascontiguousarray(arena.site_offsets, np.uint64)
+        bad = N.U64(0)
+        rc = N.lib().cf_arena_check_sites(base, total, N.ptr(sites) if len(sites) else None, len(sites), base,
+                                          C.byref(bad))
+        if rc == N.CF_E_OUTSIDE_ARENA:
+            raise AttachOutsideArena(N.last_error())
+        N.check(rc, "transfer_to_device")
+        image = arena.take_image()   # fully overwritten by the copy
+        machine.log.append(H2D, "bulk", total)
+        machine.log.append_many(H2D, "attach", np.full(len(sites), 8, np.int64))
+        arena.device_image_addr = image
+        prep = DevicePrep(scheme, device_root=image + (handle.root_addr - base), arena=arena, policy=policy,
+                          image=image, image_bytes=total)
+        prep.fused = FusedMarshalWindow(machine, handle, arena, image, policy)
+        machine._deferred = prep.fused
+        return prep
     if scheme == "marshalling":
         if arena is None:
             raise ValueError("marshalling needs the arena returned by marshal_tree")
@@ -380,6 +474,15 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
         raise ValueError(f"unknown kernel mode {mode!r}")
     stats = KernelStats()
     elem = handle.spec.elem
+    fw = _pending(machine, prep)
+    if fw is not None and fw.scale is None:
+        # joins the deferred window: the leaf kernel runs chunk by chunk as the arena lands
+        fw.scale, fw.mode = float(scale), mode
+        idx = fw._targets()
+        stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
+        stats.elements_touched = int(handle.arr_count[idx].sum())
+        return stats
+    machine.flush()
     ctx = machine.ctx.handle
     if prep.scheme == "pointerchain":
         if len(prep.buf_dev):
@@ -422,6 +525,17 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
 
 
 def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
+    fw = _pending(machine, prep)
+    if fw is not None and fw.scale is not None:
+        machine._deferred = None
+        fw.complete()
+        arena = prep.arena
+        machine.log.append(D2H, "bulk", arena.total_bytes)
+        machine.log.append_many(D2H, "detach", np.full(len(arena.site_offsets), 8, np.int64))
+        arena._spare_image = arena.device_image_addr
+        arena.device_image_addr = NULL_ADDR
+        return
+    machine.flush()
     if prep.scheme == "marshalling":
         machine.demarshal(prep.arena)
     elif prep.scheme == "naive":
@@ -493,8 +607,9 @@ def _describe(spec) -> tuple[str, str, int, int]:
 
 def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale: float = 2.0,
                  mode: str = "resolved", policy: str = "ref", align: int | None = None,
-                 device: int = 0, uvm_hints: str = "none") -> tuple[RunMetrics, Machine]:
-    """Run one case once on the GPU; returns the metrics and the machine (for its log)."""
+                 device: int = 0, uvm_hints: str = "none", fused: bool = True) -> tuple[RunMetrics, Machine]:
+    """Run one case once on the GPU; returns the metrics and the machine (for its log).
+    ``fused`` (marshalling): the metered window runs as one pipelined cf_window."""
     if scheme not in SCHEMES:
         raise SchemeError(f"unknown transfer scheme {scheme!r}")
     machine = Machine(page_size=cost_model.page_size, device=device)
@@ -508,7 +623,7 @@ def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale:
     launches0 = machine.ctx.launches()
     mark = machine.log.mark()
     t0 = time.perf_counter()
-    prep = transfer_to_device(machine, handle, scheme, arena, policy=policy, uvm_hints=uvm_hints)
+    prep = transfer_to_device(machine, handle, scheme, arena, policy=policy, uvm_hints=uvm_hints, fused=fused)
     stats = kernel_scale(machine, handle, prep, scale, mode=mode)
     copy_back(machine, handle, prep)
     machine.ctx.sync()

@@ -64,14 +64,21 @@ class TransferLog:
         self._kind = np.zeros(0, np.uint8)
         self._bytes = np.zeros(0, np.int64)
         self._pending: list = []  # small appends, folded lazily
+        self._chunks: list = []   # bulk appends (dir, kind, bytes-array), folded lazily
 
     def _fold(self) -> None:
         if self._pending:
             d, k, b = zip(*self._pending)
-            self._dir = np.concatenate([self._dir, np.array(d, np.uint8)])
-            self._kind = np.concatenate([self._kind, np.array(k, np.uint8)])
-            self._bytes = np.concatenate([self._bytes, np.array(b, np.int64)])
+            self._chunks.append((np.array(d, np.uint8), np.array(k, np.uint8), np.array(b, np.int64)))
             self._pending = []
+        if self._chunks:
+            cols = [(self._dir, self._kind, self._bytes)] + [
+                (d if isinstance(d, np.ndarray) else np.full(b.size, d, np.uint8),
+                 k if isinstance(k, np.ndarray) else np.full(b.size, k, np.uint8), b) for d, k, b in self._chunks]
+            self._dir = np.concatenate([c[0] for c in cols])
+            self._kind = np.concatenate([c[1] for c in cols])
+            self._bytes = np.concatenate([c[2] for c in cols])
+            self._chunks = []
 
     def append(self, direction: str, op_kind: str, nbytes: int) -> None:
         if nbytes <= 0:
@@ -79,16 +86,17 @@ class TransferLog:
         self._pending.append((_DIRS.index(direction), _KINDS.index(op_kind), int(nbytes)))
 
     def append_many(self, direction: str, op_kind: str, nbytes) -> None:
-        """Append one entry per element of ``nbytes`` (an int count pair or an array)."""
+        """Append one entry per element of ``nbytes`` (an array); O(len) -- columns fold on read."""
         b = np.asarray(nbytes, dtype=np.int64).ravel()
         if b.size == 0:
             return
         if (b <= 0).any():
             raise ValueError("log entries must move at least one byte")
-        self._fold()
-        self._dir = np.concatenate([self._dir, np.full(b.size, _DIRS.index(direction), np.uint8)])
-        self._kind = np.concatenate([self._kind, np.full(b.size, _KINDS.index(op_kind), np.uint8)])
-        self._bytes = np.concatenate([self._bytes, b])
+        if self._pending:   # keep order: earlier single appends go first
+            d, k, bb = zip(*self._pending)
+            self._chunks.append((np.array(d, np.uint8), np.array(k, np.uint8), np.array(bb, np.int64)))
+            self._pending = []
+        self._chunks.append((_DIRS.index(direction), _KINDS.index(op_kind), b))
 
     @property
     def entries(self) -> list[TransferEntry]:
@@ -304,7 +312,12 @@ class MemorySpace:
         except WildAccess:
             return False
 
+    def _sync_deferred(self) -> None:
+        if self.machine is not None and self.machine._deferred is not None:
+            self.machine.flush()
+
     def read_bytes(self, addr: int, nbytes: int) -> bytes:
+        self._sync_deferred()
         self._check(addr, nbytes)
         if self.kind == "host":
             return N.read_bytes(addr, nbytes)
@@ -313,6 +326,7 @@ class MemorySpace:
         return out.tobytes()
 
     def write_bytes(self, addr: int, data: bytes) -> None:
+        self._sync_deferred()
         self._check(addr, len(data))
         if self.kind == "host":
             N.write_bytes(addr, data)
@@ -374,6 +388,13 @@ class Arena:
         self._site_off = np.zeros(0, np.uint64)   # DFS order, relative to the arena
         self._sorted = None
         self.device_image_addr = NULL_ADDR
+        # image of a completed (copied-back) window, reused by the next transfer of this arena
+        # instead of a fresh 1 GiB-class allocation per window
+        self._spare_image = NULL_ADDR
+
+    def take_image(self) -> int:
+        img, self._spare_image = self._spare_image, NULL_ADDR
+        return img or self.space.machine.device.allocate(self.total_bytes, zero=False)
 
     def allocate(self, size_bytes: int) -> int:
         if size_bytes <= 0:
@@ -497,6 +518,10 @@ class Machine:
         self.log = TransferLog()
         self.uvm: UvmState | None = None
         self._default_page_size = page_size
+        # a deferred metered window (harness.FusedMarshalWindow) not yet enqueued; anything that
+        # observes or mutates device/host state runs it first (flush)
+        self._deferred = None
+        self._plans: dict = {}   # cached cf_window plans of the fused marshalling windows
 
     @property
     def ctx(self) -> N.DeviceContext:
@@ -522,7 +547,20 @@ class Machine:
     def create_arena(self, total_bytes: int, align: int = 1) -> Arena:
         return Arena(self.host, total_bytes, align)
 
+    def flush(self) -> None:
+        """Run deferred work (a fused marshalling window not yet enqueued) up to its current stage."""
+        d, self._deferred = self._deferred, None
+        if d is not None:
+            d.flush()
+
     def close(self) -> None:
+        self._deferred = None   # abandoned deferred work is dropped with the storage
+        lib = N._lib
+        if lib is not None and self._plans:
+            self.ctx.sync()
+            for w in self._plans.values():
+                lib.cf_window_free(w)
+        self._plans = {}
         self.host.free_all()
         self.device.free_all()
 
@@ -536,6 +574,7 @@ class Machine:
     def transfer_range(self, src: MemorySpace, src_addr: int, dst: MemorySpace, dst_addr: int,
                        nbytes: int, op_kind: str = "bulk") -> None:
         """Copy nbytes between spaces (snapshot semantics) and log one entry."""
+        self.flush()
         if src.kind == dst.kind:
             raise ValueError("transfer_range requires distinct memory spaces")
         src._check(src_addr, nbytes)
@@ -546,6 +585,7 @@ class Machine:
     def transfer_ranges(self, src: MemorySpace, src_addrs, dst: MemorySpace, dst_addrs, sizes,
                         op_kind: str = "bulk") -> None:
         """Several transfer_range calls submitted as one batched copy (one log entry each)."""
+        self.flush()
         if src.kind == dst.kind:
             raise ValueError("transfer_range requires distinct memory spaces")
         sa = np.ascontiguousarray(src_addrs, np.uint64)
@@ -564,7 +604,8 @@ class Machine:
     def marshal_transfer_and_attach(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> int:
         """Ship the arena in one logical bulk op (chunked over copy streams) and relocate every
         pointer field on the device as its chunk lands."""
-        image = self.device.allocate(arena.total_bytes, zero=False)   # fully overwritten by the copy
+        self.flush()
+        image = arena.take_image()   # fully overwritten by the copy
         sites = arena.sorted_site_offsets
         bad = N.U64(0)
         rc = N.lib().cf_marshal_transfer_and_attach(
@@ -580,6 +621,7 @@ class Machine:
 
     def demarshal(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> None:
         """Detach on the device (inverse relocation kernel), then bulk copy the image back."""
+        self.flush()
         image = arena.device_image_addr
         if image == NULL_ADDR:
             raise SimMemoryError("demarshal before marshal_transfer_and_attach")
@@ -592,12 +634,14 @@ class Machine:
         N.check(rc, "demarshal")
         self.log.append(D2H, "bulk", arena.total_bytes)
         self.log.append_many(D2H, "detach", np.full(len(sites), 8, np.int64))
+        arena._spare_image = image
         arena.device_image_addr = NULL_ADDR
 
     # -- naive per-object deep copy (memory.py:349-374) -------------------------------------
     def naive_deep_copy(self, tree) -> tuple[int, "AddressMap"]:
         """Copy every object individually (one batched submission), then fix every pointer
         field on the device through the sorted interval map."""
+        self.flush()
         allocs = tree.allocation_array()          # (m, 2) host addr, size in allocation order
         m = len(allocs)
         sizes = allocs[:, 1].astype(np.uint64)
@@ -642,6 +686,7 @@ class Machine:
 
     def naive_copy_back(self, tree, amap: "AddressMap") -> None:
         """Per-object copy back (one batched submission) plus host-side pointer restore."""
+        self.flush()
         allocs = tree.allocation_array()
         host = allocs[:, 0].astype(np.uint64)
         sizes = allocs[:, 1].astype(np.uint64)

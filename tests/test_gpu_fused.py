@@ -1,0 +1,177 @@
+"""The fused (deferred) marshalling window behind the drop-in calls.
+
+``transfer_to_device -> kernel_scale -> copy_back`` (harness.py:219-325) for the marshalling
+scheme is deferred into one pipelined cf_window.  These tests pin it against the eager phases
+(``fused=False``: marshal_transfer_and_attach / cf_kernel_scale / demarshal) and the oracle:
+identical host bytes after the window, identical logical logs, and the reference's observable
+behaviour when something looks at the machine between the calls (flush).
+"""
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1906_01128_b200 as cf
+    from paper_1906_01128_b200 import _native as N
+    if N.device_count() == 0:
+        pytest.skip("no GPU visible: run `pytest -m gpu` on a B200 box (gpurun)")
+    return cf
+
+
+def _window(cf, spec, fused, seed=3, scale=2.0, mode="resolved", policy="ref", align=1):
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, spec, seed=seed, align=align)
+    mark = m.log.mark()
+    prep = cf.transfer_to_device(m, h, "marshalling", arena, policy=policy, fused=fused)
+    st = cf.kernel_scale(m, h, prep, scale, mode=mode)
+    cf.copy_back(m, h, prep)
+    out = bytes(m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes))
+    log = [(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)]
+    base = arena.buffer_host_addr
+    m.close()
+    return out, log, (st.elements_touched, st.chain_derefs), base
+
+
+def _norm(cf, raw, spec, base, seed, align):
+    """Pointer fields as arena offsets, so two arenas at different addresses compare."""
+    m = cf.Machine()
+    _, h = cf.marshal_tree(m, spec, seed=seed, align=align)
+    a = np.frombuffer(raw, np.uint8).copy()
+    for f in h.site_off.tolist():
+        v = int.from_bytes(a[f:f + 8].tobytes(), "little") - base
+        a[f:f + 8] = np.frombuffer(v.to_bytes(8, "little"), np.uint8)
+    m.close()
+    return a.tobytes()
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+def test_fused_equals_eager_random_specs(cf, elem):
+    rng = random.Random(77 + elem)
+    for trial in range(16):
+        if rng.random() < 0.5:
+            spec = cf.LinearSpec(rng.randint(1, 6), rng.choice([0, 1, 7, 1000, 70001]),
+                                 rng.choice(["allinit_allused", "allinit_LLused", "LLinit_LLused"]), elem=elem)
+        else:
+            spec = cf.DenseSpec(rng.randint(1, 5), rng.choice([0, 3, 257, 40000]), rng.randint(0, 3), elem=elem,
+                                leaf_only=rng.random() < 0.3)
+        policy = rng.choice(["ref", "all_leaves", "all_arrays"])
+        mode = rng.choice(["resolved", "chase"])
+        align = rng.choice([1, 16])
+        a, la, sa, ba = _window(cf, spec, True, mode=mode, policy=policy, align=align)
+        b, lb, sb, bb = _window(cf, spec, False, mode=mode, policy=policy, align=align)
+        assert la == lb and sa == sb, (spec, policy, mode)
+        assert _norm(cf, a, spec, ba, 3, align) == _norm(cf, b, spec, bb, 3, align), (spec, policy, mode, align)
+
+
+def test_fused_window_multi_chunk_matches_oracle(cf, oracle):
+    """An arena spanning many 16 MiB chunks (C2 shape, small) through the drop-in calls."""
+    spec = cf.DenseSpec(4, 1 << 20, 3, elem=4, leaf_only=True)
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, spec, seed=1, align=16)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena, policy="all_leaves")
+    cf.kernel_scale(m, h, prep, 2.0)
+    cf.copy_back(m, h, prep)
+    got = np.frombuffer(m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes), np.uint8)
+    ospec = oracle.OSpec(oracle.DENSE, 4, 1 << 20, 3, elem=4, leaf_only=True, align=16)
+    ot = oracle.build(ospec, 1, ptr_base=arena.buffer_host_addr)
+    want = oracle.expected_after_window(ot, oracle.targets(ot, oracle.TARGET_ALL_LEAVES), 2.0)
+    assert np.array_equal(got, want[: arena.total_bytes])
+    cf.verify_tree(m, h, 2.0, policy="all_leaves")
+    m.close()
+
+
+def test_device_read_between_transfer_and_kernel_flushes(cf):
+    """Reading the device after a deferred transfer sees the attached image (test_memory.py:141-150)."""
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, cf.LinearSpec(3, 4, "allinit_allused"), seed=7)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena)
+    assert m._deferred is prep.fused
+    node = prep.device_root
+    for _ in range(2):
+        node = m.device.read_word(node + 16)
+    assert m._deferred is None
+    assert m.device.read_f64(m.device.read_word(node + 8)) == m.host.read_f64(h.arrays[-1].addr)
+    cf.kernel_scale(m, h, prep, 2.0)          # eager from here on
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0)
+    assert m.log.count("attach") == m.log.count("detach") == 5
+    m.close()
+
+
+def test_device_read_between_kernel_and_copy_back_flushes(cf):
+    m = cf.Machine()
+    spec = cf.DenseSpec(2, 16, 2)
+    arena, h = cf.marshal_tree(m, spec, seed=2)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena, policy="all_leaves")
+    cf.kernel_scale(m, h, prep, 2.0)
+    t = h.target_indices("all_leaves")[0]
+    dev_arr = prep.image + int(h.arr_off[t])
+    host_arr = h.base + int(h.arr_off[t])
+    assert m.device.read_f64(dev_arr) == 2.0 * m.host.read_f64(host_arr)
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, policy="all_leaves")
+    m.close()
+
+
+def test_host_write_before_copy_back_is_snapshotted(cf):
+    """transfer_range snapshot semantics (memory.py:294-303): a host write after the transfer call
+    does not reach the device copy (it flushes the deferred upload first)."""
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, cf.LinearSpec(2, 8, "allinit_allused"), seed=4)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena)
+    a = h.arrays[-1].addr
+    orig = m.host.read_f64(a)        # flushes
+    m.host.write_f64(a, -5.0)
+    cf.kernel_scale(m, h, prep, 2.0)
+    cf.copy_back(m, h, prep)
+    assert m.host.read_f64(a) == orig * 2.0
+    m.close()
+
+
+def test_fused_transfer_rejects_targets_outside_the_arena(cf):
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, cf.LinearSpec(2, 10, "allinit_allused"))
+    stray = m.host.allocate(8)
+    m.host.write_word(arena.pointer_sites[0], stray)
+    mark = m.log.mark()
+    with pytest.raises(cf.AttachOutsideArena):
+        cf.transfer_to_device(m, h, "marshalling", arena)
+    assert m._deferred is None and m.log.mark() == mark
+    m.close()
+
+
+def test_copy_back_without_kernel_round_trips(cf):
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, cf.DenseSpec(3, 5, 2), seed=1)
+    before = m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena)
+    cf.copy_back(m, h, prep)
+    assert m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes) == before
+    m.close()
+
+
+def test_abandoned_window_is_dropped(cf):
+    m = cf.Machine()
+    arena, h = cf.marshal_tree(m, cf.LinearSpec(2, 10), seed=1)
+    prep = cf.transfer_to_device(m, h, "marshalling", arena)
+    cf.kernel_scale(m, h, prep, 2.0)
+    m.close()
+    assert m._deferred is None
+
+
+def test_execute_case_fused_and_eager_agree(cf):
+    cm = cf.CostModel()
+    for spec in (cf.LinearSpec(5, 1000, "LLinit_LLused"), cf.DenseSpec(3, 50, 3)):
+        a, ma = cf.execute_case(spec, "marshalling", cm, seed=0, fused=True)
+        b, mb = cf.execute_case(spec, "marshalling", cm, seed=0, fused=False)
+        for k in ("bytes_h2d", "bytes_d2h", "transfer_ops", "attach_ops", "page_faults", "instr_estimate",
+                  "sim_kernel_us", "sim_wall_us", "verified"):
+            assert getattr(a, k) == getattr(b, k), k
+        assert a.gpu_launches > 0
+        ma.close()
+        mb.close()

@@ -32,6 +32,13 @@
 #ifndef CF_GROUP_WARP
 #define CF_GROUP_WARP 1
 #endif
+#ifndef CF_ROW_ALIGN
+#define CF_ROW_ALIGN 128
+#endif
+#ifndef CF_SHIFT_ALIGN
+#define CF_SHIFT_ALIGN 128
+#endif
+
 
 namespace cf {
 namespace {
@@ -291,8 +298,93 @@ __device__ __forceinline__ uint8_t* chase_base(const ScaleArgs& a, uint64_t t, u
   return reinterpret_cast<uint8_t*>(ld_chain_u64(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)));
 }
 
+// f64 arrays at 4 (mod 8) -- the packed reference layout puts them there for odd q -- cannot use
+// element-aligned vectors: every element straddles an 8-byte boundary.  One tile is streamed as
+// the aligned 16-byte words over its bytes [b0, b1) instead, in ONE pass by the whole CTA: warp
+// w loads SHIFT_ROWS consecutive rows of 32 words (a contiguous chunk), then a CTA barrier, then
+// every thread rebuilds the three elements meeting its word A = (x0, x1, x2, x3) as u32 --
+// hi(Ea) | Eb | lo(Ec) -- from its own word and its neighbours' (warp shuffles; across rows via
+// lanes 0 / 31; across warps the chunk-edge u32 was loaded before the barrier) and stores A
+// whole.  Straddling elements are thus computed twice, once by each word's owner, each writing
+// only its own word: every u32 is written by exactly one thread, always from values read
+// before any store of the tile.  Only the tile's two edge words are stored (and loaded) per
+// u32, restricted to the tile's own bytes, so neighbouring tiles (other CTAs) never race.
+constexpr int SHIFT_ROWS = 5;
+static_assert(TILE_BYTES / 16 + CF_SHIFT_ALIGN / 16 + 1 <= uint64_t(SHIFT_ROWS) * SCALE_THREADS,
+              "one pass must cover a tile");
+
+template <bool CHASE>
+__device__ __forceinline__ void scale_f64_shifted(const ScaleArgs& a, uint64_t t, uint8_t* arr, uint64_t e0,
+                                                  uint64_t e1, double s) {
+  constexpr int U = SHIFT_ROWS;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t jw = uint64_t(warp) * (U * 32);   // the warp's first word
+  uint4 x[U];
+  uintptr_t A[U], b0 = 0, b1 = 0;
+  uint32_t halo_lo = 0, halo_hi = 0;   // x3 of word jw-1 / x0 of word jw + 32U (chunk edges)
+  uint64_t nw = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    uint8_t* ar = (CHASE || u == 0) ? chase_base<CHASE>(a, t, arr) : arr;   // CHASE: one walk per row
+    b0 = reinterpret_cast<uintptr_t>(ar) + e0 * 8;
+    b1 = reinterpret_cast<uintptr_t>(ar) + e1 * 8;
+    const uintptr_t w0 = b0 & ~uintptr_t(CF_SHIFT_ALIGN - 1);
+    nw = (b1 + 15 - w0) >> 4;
+    const uint64_t j = jw + uint64_t(u) * 32 + lane;
+    A[u] = w0 + 16 * j;
+    x[u] = make_uint4(0u, 0u, 0u, 0u);
+    if (j < nw) {
+      const uintptr_t p = A[u];
+      if (p >= b0 && p + 16 <= b1) {
+        x[u] = __ldcs(reinterpret_cast<const uint4*>(p));
+      } else {   // edge word: only the u32s inside the tile
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
+        if (p >= b0 && p < b1) x[u].x = w[0];
+        if (p + 4 >= b0 && p + 4 < b1) x[u].y = w[1];
+        if (p + 8 >= b0 && p + 8 < b1) x[u].z = w[2];
+        if (p + 12 >= b0 && p + 12 < b1) x[u].w = w[3];
+      }
+    }
+  }
+  // chunk-edge neighbours owned by other warps of this CTA, read before anyone stores
+  if (lane == 0 && jw < nw && A[0] >= b0 + 4 && A[0] + 4 <= b1) halo_lo = reinterpret_cast<const uint32_t*>(A[0])[-1];
+  if (lane == 31 && jw + U * 32 < nw && A[U - 1] + 20 <= b1) halo_hi = reinterpret_cast<const uint32_t*>(A[U - 1])[4];
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    // x3 of word A-16 and x0 of word A+16
+    uint32_t lo_prev = __shfl_up_sync(0xffffffffu, x[u].w, 1);
+    uint32_t hi_next = __shfl_down_sync(0xffffffffu, x[u].x, 1);
+    const uint32_t row_prev = __shfl_sync(0xffffffffu, u > 0 ? x[u > 0 ? u - 1 : 0].w : 0u, 31);
+    const uint32_t row_next = __shfl_sync(0xffffffffu, u + 1 < U ? x[u + 1 < U ? u + 1 : 0].x : 0u, 0);
+    if (lane == 0) lo_prev = u > 0 ? row_prev : halo_lo;
+    if (lane == 31) hi_next = u + 1 < U ? row_next : halo_hi;
+    const uint64_t j = jw + uint64_t(u) * 32 + lane;
+    if (j >= nw) continue;
+    const uintptr_t p = A[u];
+    const bool own_a = p >= b0 + 4 && p + 4 <= b1;     // Ea = [A-4, A+4)
+    const bool own_b = p + 4 >= b0 && p + 12 <= b1;    // Eb = [A+4, A+12)
+    const bool own_c = p + 12 >= b0 && p + 20 <= b1;   // Ec = [A+12, A+20)
+    const double va = __dmul_rn(__hiloint2double(int(x[u].x), int(lo_prev)), s);
+    const double vb = __dmul_rn(__hiloint2double(int(x[u].z), int(x[u].y)), s);
+    const double vc = __dmul_rn(__hiloint2double(int(hi_next), int(x[u].w)), s);
+    const uint4 y = make_uint4(uint32_t(__double2hiint(va)), uint32_t(__double2loint(vb)),
+                               uint32_t(__double2hiint(vb)), uint32_t(__double2loint(vc)));
+    if (own_a && own_b && own_c) {
+      __stcs(reinterpret_cast<uint4*>(p), y);
+    } else {   // the tile's edge words: own u32s only
+      uint32_t* w = reinterpret_cast<uint32_t*>(p);
+      if (own_a) w[0] = y.x;
+      if (own_b) { w[1] = y.y; w[2] = y.z; }
+      if (own_c) w[3] = y.w;
+    }
+  }
+}
+
 // Scale elements [e0, e1) of arr with `lanes` cooperating threads (rank `me`): scalar head up to
-// 16-byte alignment, UNROLL independent 128-bit loads in flight per thread, scalar tail.
+// 128-byte alignment (so every warp's 512-byte row covers whole lines), UNROLL independent
+// 128-bit loads in flight per thread, scalar tail.  Misaligned f64 (packed layouts) streams
+// aligned words instead (scale_f64_shifted).
 template <typename T, bool CHASE, int UNROLL>
 __device__ __forceinline__ void scale_range(const ScaleArgs& a, uint64_t t, uint8_t* arr, uint64_t e0, uint64_t e1,
                                             T s, unsigned me, unsigned lanes) {
@@ -300,9 +392,15 @@ __device__ __forceinline__ void scale_range(const ScaleArgs& a, uint64_t t, uint
   using V = typename VT::V;
   constexpr uint64_t VN = VT::N;
   const uintptr_t first = reinterpret_cast<uintptr_t>(arr + e0 * sizeof(T));
+  if constexpr (sizeof(T) == 8) {
+    if ((first & 7) == 4) {   // whole CTA on one tile (the only caller): see scale_f64_shifted
+      scale_f64_shifted<CHASE>(a, t, arr, e0, e1, double(s));
+      return;
+    }
+  }
   uint64_t v0 = e1, v1 = e1;
   if ((first % sizeof(T)) == 0) {
-    const uint64_t head = ((16 - (first & 15)) & 15) / sizeof(T);
+    const uint64_t head = ((CF_ROW_ALIGN - (first & (CF_ROW_ALIGN - 1))) & (CF_ROW_ALIGN - 1)) / sizeof(T);
     v0 = min(e1, e0 + head);
     v1 = v0 + (e1 - v0) / VN * VN;
   }

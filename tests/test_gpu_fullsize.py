@@ -54,7 +54,8 @@ sys.path.insert(0, ".")
 import paper_1906_01128_b200 as cf
 specs = [cf.DenseSpec(3, 301, 2, elem=4), cf.DenseSpec(4, 5000, 3, elem=4, leaf_only=True),
          cf.LinearSpec(4, 777, "allinit_allused"), cf.DenseSpec(3, 17, 2),
-         cf.ForestSpec(cf.LinearSpec(3, 1000, "LLinit_LLused", elem=4), 20, scatter_seed=5)]
+         cf.ForestSpec(cf.LinearSpec(3, 1000, "LLinit_LLused", elem=4), 20, scatter_seed=5),
+         cf.DenseSpec(3, 4099, 2), cf.DenseSpec(5, 2500, 1, leaf_only=True)]   # packed f64 at 4 mod 8
 for spec in specs:
     for align in (1, 16):
         for mode in ("resolved", "chase"):

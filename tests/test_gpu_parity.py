@@ -282,3 +282,31 @@ def test_cli_simulate_and_sweep_match_reference_counters(cf, kats, tmp_path):
     assert a.read_bytes() == b.read_bytes()
     rows = a.read_text().strip().split("\n")
     assert len(rows) == 5 and rows[0] == cli.CSV_HEADER
+
+
+@pytest.mark.parametrize("mode", ["resolved", "chase"])
+def test_packed_f64_word_streaming_matches_oracle(cf, oracle, mode):
+    """f64 arrays at 4 (mod 8) -- the packed reference layout with odd q -- take the aligned-word
+    streaming path of the leaf kernel (scale_f64_shifted).  Multi-tile arrays cut into pieces at
+    arbitrary element offsets by odd chunk sizes must come back bit-exact."""
+    cases = [({"kind": "dense", "q": 3, "n": n, "depth": 2}, lo) for n in (2047, 2048, 2049, 4095, 10001)
+             for lo in (False, True)]
+    cases += [({"kind": "dense", "q": 5, "n": 7000, "depth": 2}, True), ({"kind": "dense", "q": 1, "n": 9999, "depth": 3}, False)]
+    for trial, (j, leaf_only) in enumerate(cases):
+        spec = _spec(cf, j, 8, leaf_only)
+        for chunk in (0, 4096, 12340, 1 << 16):
+            w = cf.DeepCopyWindow(spec, seed=trial, policy="all_arrays", mode=mode, align=1, chunk_bytes=chunk)
+            try:
+                offs = w.table(N.CF_TAB_ARR_OFF)
+                assert (offs % 8 == 4).any(), "case must exercise arrays at 4 mod 8"
+                st = w.run(scale=2.0)
+                assert st.bad == NO_BAD
+                ot = oracle.build(oracle.spec_from_json(j, elem=8, align=1, leaf_only=leaf_only), trial,
+                                  ptr_base=w.src)
+                want = oracle.expected_after_window(ot, oracle.targets(ot, oracle.TARGET_ALL_ARRAYS), 2.0)[:w.total]
+                assert np.array_equal(w.host_dst(), want), (j, leaf_only, chunk)
+                w.upload_raw()
+                st = w.run_resident(scale=2.0)
+                assert st.bad == NO_BAD and np.array_equal(w.image_bytes(), want), (j, leaf_only, "resident")
+            finally:
+                w.close()

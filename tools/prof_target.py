@@ -11,9 +11,16 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--runs", type=int, default=4)
 ap.add_argument("--mode", default="resolved")
 ap.add_argument("--full", action="store_true")
+ap.add_argument("--dense", default="", help="q,n,depth,elem: a leaves-only dense spec instead of --config")
+ap.add_argument("--align", type=int, default=16)
 a = ap.parse_args()
-spec, policy, _ = bench.make_spec(a.config)
-w = DeepCopyWindow(spec, seed=1, policy=policy, mode=a.mode, align=16, chunk_bytes=16 << 20)
+if a.dense:
+    from paper_1906_01128_b200 import DenseSpec
+    q, n, d, e = (int(x) for x in a.dense.split(","))
+    spec, policy = DenseSpec(q, n, d, elem=e, leaf_only=True), "all_leaves"
+else:
+    spec, policy, _ = bench.make_spec(a.config)
+w = DeepCopyWindow(spec, seed=1, policy=policy, mode=a.mode, align=a.align, chunk_bytes=16 << 20)
 if a.full:
     for i in range(a.runs):
         st = w.run(scale=2.0 if i % 2 == 0 else 0.5)

@@ -283,6 +283,56 @@ def run_reference(args, dist: Dist) -> None:
     print(json.dumps(line), flush=True)
 
 
+def verify_gather(w, shard, spec, dist: Dist, device: int, ndev: int, src_factor: float) -> dict:
+    """Outside the timed region: one more window (scale 2.0) from the host arena, per-leaf
+    checksums of the device image (cf_checksum_ranges), all-gathered to every rank -- over NCCL
+    when each rank has its own GPU, else gloo -- and checked on rank 0 against the checksums of
+    the whole workload (payload_values * factor, the same for every leaf of a level)."""
+    import numpy as np
+    from paper_1906_01128_b200 import _native as N
+    from paper_1906_01128_b200.shard import expected_checksum, gather_checksums, leaf_checksums
+    st = w.run(scale=2.0)
+    if st.bad != N.NO_BAD:
+        raise SystemExit("verification window reported a device error")
+    off, cnt = w.plan.table(N.CF_TAB_ARR_OFF), w.plan.table(N.CF_TAB_ARR_COUNT)
+    lvl, od = w.plan.table(N.CF_TAB_ARR_LEVEL), w.plan.table(N.CF_TAB_ARR_ORDINAL)
+    tg = w.targets
+    sums = leaf_checksums(w.ctx, w.image, off[tg], cnt[tg], spec.elem)
+    if len(set(lvl[tg].tolist())) != 1 or len(set(cnt[tg].tolist())) != 1:
+        raise SystemExit("verify_gather expects targets of one level and length")
+    nleaf_tree = int(len(tg)) if shard.scaling == "weak" else 0
+    # weak: (rank, position) -- every rank owns a whole tree; strong: the global leaf ordinal
+    keys = (np.arange(len(tg), dtype=np.int64) + np.int64(dist.rank) * (1 << 32)) if shard.scaling == "weak" \
+        else od[tg].astype(np.int64)
+    pg, dev, backend = None, None, "local"
+    if dist.world > 1:
+        import torch
+        import torch.distributed as tdist
+        backend = "gloo"
+        if ndev >= dist.world:   # one GPU per rank: the gather runs over NCCL (NVLink / NVSwitch)
+            torch.cuda.set_device(device)
+            pg, dev, backend = tdist.new_group(backend="nccl"), torch.device("cuda", device), "nccl"
+    o, v = gather_checksums(keys, sums, pg, dev)
+    out = {"backend": backend, "leaves": int(len(o)), "what": "per-leaf u32-word checksums after a "
+           "verification window (scale 2.0), gathered to all ranks"}
+    if dist.rank == 0:
+        f = 2.0 * src_factor
+        ok = True
+        seeds = {}
+        for key, val in zip(o.tolist(), v.tolist()):
+            seed = shard.seed + (key >> 32) if shard.scaling == "weak" else shard.seed
+            lv = int(lvl[tg[0]])
+            if (seed, lv) not in seeds:
+                seeds[(seed, lv)] = expected_checksum(seed, lv, int(cnt[tg[0]]), spec.elem, f)
+            ok &= int(val) == seeds[(seed, lv)]
+        want = (dist.world * nleaf_tree) if shard.scaling == "weak" else int(spec.q ** spec.depth)
+        out["complete"] = int(len(o)) == want and len(set(o.tolist())) == len(o)
+        out["checksums_match"] = bool(ok)
+        if not (ok and out["complete"]):
+            raise SystemExit(f"gathered result check failed: {out}")
+    return out
+
+
 # ------------------------------------------------------------------------------ our arm
 def run_ours(args, dist: Dist) -> None:
     from paper_1906_01128_b200 import DeepCopyWindow
@@ -295,6 +345,11 @@ def run_ours(args, dist: Dist) -> None:
     # one rank per GPU; ranks beyond the visible GPUs share them (plumbing runs on small boxes)
     device = dist.local_rank % max(ndev, 1)
     spec, policy, desc = make_spec(args.config)
+    if args.leaf_elems:   # plumbing runs only: the same shape with shorter leaves
+        from dataclasses import replace
+        spec = replace(spec, tree=replace(spec.tree, n=args.leaf_elems)) if hasattr(spec, "tree") else \
+            replace(spec, n=args.leaf_elems)
+        desc += f" [leaves shortened to {args.leaf_elems} elements: plumbing run, not a bench value]"
     scaling = "strong" if args.config == "C5" else "weak"
     shard = shard_for(spec, dist.rank, dist.world, scaling)
     spec = shard.spec
@@ -374,6 +429,8 @@ def run_ours(args, dist: Dist) -> None:
         if not np.array_equal(got, want):
             raise SystemExit("copy-back spot check failed")
 
+    gather = verify_gather(w, shard, spec, dist, device, ndev, 1.0 if w.dst != w.src else factor)
+
     n = dist.world
     graph_all = dist.sum(float(total))
     value = graph_all / (res_ms * 1e-3) / 1e9
@@ -408,6 +465,7 @@ def run_ours(args, dist: Dist) -> None:
                      "share_of_resident_step": round(kernel_ms / res_ms, 4)},
         "modes": {"resolved": {"kernel_ms": round(kernel_ms, 4), "hbm_gbs": round(achieved, 1)}, "chase": chase},
         "gpu_launches": int(st_res.launches),
+        "gather": gather,
         "clocks": clk,
         "build_s": round(t_build, 2),
     }
@@ -444,6 +502,7 @@ def main(argv=None):
     ap.add_argument("--no-graph", action="store_true", help="enqueue every window directly (no CUDA graph)")
     ap.add_argument("--skip-schemes", action="store_true", help="skip the 4-scheme drop-in API comparison")
     ap.add_argument("--single-buffer", action="store_true", help="e2e with one image (no step overlap)")
+    ap.add_argument("--leaf-elems", type=int, default=0, help="override the leaf length (plumbing tests only)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

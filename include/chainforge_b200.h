@@ -69,6 +69,13 @@ typedef struct {
   int32_t align;
   int32_t forest;         /* number of independent trees (0 or 1: a single tree); C3 = 64 chains */
   uint64_t scatter_seed;  /* != 0: allocations placed in a seeded random order (sparse layout) */
+  /* dense subtree shard: the tree is cut at the shallowest level l with
+   * q^l >= shard_world; this plan materialises the replicated ancestor path plus the level-l
+   * subtrees with (ordinal * shard_world / q^l) == shard_rank.  Non-owned level-l nodes keep
+   * their record in the parent's block with nulled fields; arrays above level l live on rank 0
+   * only.  shard_world 0 or 1: the whole tree. */
+  int32_t shard_rank;
+  int32_t shard_world;
 } cf_spec;
 
 typedef struct {
@@ -223,6 +230,10 @@ int cf_scale_resolved(cf_ctx* ctx, int elem, const uint64_t* h_ea, const uint64_
  * deferred (fused) marshalling window raise AttachOutsideArena at transfer_to_device time. */
 int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t* h_sites, uint64_t nsites,
                          uint64_t ptr_base, uint64_t* bad_index);
+/* Result gather of the multi-GPU shards (no reference counterpart): per device
+ * range i (h_addr[i], h_bytes[i], both 4-byte aligned) the wrapping u64 sum of its u32 words,
+ * into h_out[i].  Synchronous. */
+int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_bytes, uint64_t n, uint64_t* h_out);
 /* naive_deep_copy fixups (memory.py:349-365): per-object copies are issued by the caller with
  * cf_memcpy_batch; this kernel rewrites every site through a sorted interval map
  * (AddressMap.translate, memory.py:409-419) on the device. */

@@ -45,6 +45,7 @@ EXPORTED = (
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
+    "cf_checksum_ranges",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -55,7 +56,7 @@ class CfSpec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("layout", C.c_int32), ("k_or_q", C.c_int64),
                 ("n", C.c_int64), ("depth", C.c_int64), ("elem", C.c_int32),
                 ("leaf_only", C.c_int32), ("align", C.c_int32), ("forest", C.c_int32),
-                ("scatter_seed", C.c_uint64)]
+                ("scatter_seed", C.c_uint64), ("shard_rank", C.c_int32), ("shard_world", C.c_int32)]
 
 
 class CfTreeInfo(C.Structure):
@@ -132,6 +133,7 @@ def _declare(L):
         "cf_memcpy_batch": (C.c_int, [P, P, P, P, U64, P]),
         "cf_naive_fixup": (C.c_int, [P, P, P, U64, P, P, P, U64, P, P]),
         "cf_arena_check_sites": (C.c_int, [P, U64, P, U64, U64, C.POINTER(U64)]),
+        "cf_checksum_ranges": (C.c_int, [P, P, P, U64, P]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),

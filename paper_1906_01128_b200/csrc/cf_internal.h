@@ -38,6 +38,8 @@ void clear_error();
   } while (0)
 
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
+int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, const uint64_t* tile_lo, uint64_t nranges,
+                    uint64_t ntiles, uint64_t* out, cudaStream_t s);
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
                     uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s,
                     const uint32_t* idx = nullptr);
@@ -168,6 +170,9 @@ struct cf_tree {
   std::vector<uint64_t> tree_root;
   // per tree, per level: node offsets by ordinal (pre-order within a level)
   std::vector<std::vector<std::vector<uint64_t>>> level_nodes;
+  // per tree, per level: ordinal of level_nodes[tree][level][0] (non-zero below the cut level
+  // of a subtree shard, whose levels hold one contiguous ordinal range)
+  std::vector<std::vector<uint64_t>> level_base;
 };
 
 // RAII: make ctx's device current on this thread.

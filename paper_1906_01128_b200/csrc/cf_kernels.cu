@@ -704,6 +704,35 @@ __global__ void __launch_bounds__(256) k_seg_copy(const uint64_t* __restrict__ s
   for (i = lo + lane; i < hi; i += 32) dst[i] = src[i];
 }
 
+// Per-range checksum for the multi-GPU result gather: wrapping u64 sum of the
+// range's u32 words (order independent, so tiles can atomically accumulate).  One CTA per
+// 64 KiB tile of a range; tile_lo[r] = first tile of range r.
+constexpr uint64_t CK_TILE_WORDS = 16384;
+__global__ void __launch_bounds__(256) k_checksum(const uint64_t* __restrict__ addr, const uint64_t* __restrict__ words,
+                                                  const uint64_t* __restrict__ tile_lo, uint64_t nranges,
+                                                  unsigned long long* __restrict__ out) {
+  const uint64_t tile = blockIdx.x;
+  uint64_t lo = 0, hi = nranges;   // largest r with tile_lo[r] <= tile
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (tile_lo[mid] <= tile) lo = mid; else hi = mid;
+  }
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(addr[lo]);
+  const uint64_t w0 = (tile - tile_lo[lo]) * CK_TILE_WORDS, w1 = min(words[lo], w0 + CK_TILE_WORDS);
+  unsigned long long acc = 0;
+  for (uint64_t i = w0 + threadIdx.x; i < w1; i += 256) acc += __ldcs(p + i);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  __shared__ unsigned long long red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < 8; ++k) t += red[k];
+    atomicAdd(out + lo, t);
+  }
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t v, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -808,6 +837,14 @@ int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* 
 int launch_seg_copy(cf_ctx* ctx, const uint64_t* segs, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_seg_copy<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(segs, n, src, dst);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, const uint64_t* tile_lo, uint64_t nranges,
+                    uint64_t ntiles, uint64_t* out, cudaStream_t s) {
+  if (ntiles == 0) return CF_OK;
+  k_checksum<<<unsigned(ntiles), 256, 0, s>>>(addr, words, tile_lo, nranges, reinterpret_cast<unsigned long long*>(out));
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -4,6 +4,7 @@
 //   cf_kernel_scale                 <- kernel_scale (marshalling/naive walk) harness.py:244-304
 //   cf_naive_fixup                  <- naive_deep_copy fix-up loop         memory.py:362-364
 //   cf_arena_check_sites            <- the attach loop's bounds check      memory.py:319-321
+//   cf_checksum_ranges              <- result gather of the multi-GPU shards
 #include "cf_internal.h"
 
 #include <algorithm>
@@ -326,6 +327,33 @@ int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t*
   if (h_sites[first] <= total && total - h_sites[first] >= 8) memcpy(&v, h + h_sites[first], 8);
   return fail(CF_E_OUTSIDE_ARENA, "pointer field at arena offset %llu targets 0x%llx outside the arena",
               (unsigned long long)h_sites[first], (unsigned long long)v);
+}
+
+int cf_checksum_ranges(cf_ctx* c, const uint64_t* h_addr, const uint64_t* h_bytes, uint64_t n, uint64_t* h_out) {
+  if (!c || (n && (!h_addr || !h_bytes || !h_out))) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  if (n == 0) return CF_OK;
+  constexpr uint64_t TW = 16384;   // words per tile (k_checksum)
+  std::vector<uint64_t> words(n), tile_lo(n);
+  uint64_t ntiles = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if ((h_addr[i] | h_bytes[i]) & 3) return fail(CF_E_INVALID, "range %llu is not 4-byte aligned", (unsigned long long)i);
+    words[i] = h_bytes[i] / 4;
+    tile_lo[i] = ntiles;
+    ntiles += (words[i] + TW - 1) / TW;
+  }
+  DevBuf blk(c);
+  CF_TRY(blk.alloc(32 * n));
+  uint64_t* d = blk.as<uint64_t>();
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemcpyAsync(d, h_addr, 8 * n, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + n, words.data(), 8 * n, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + 2 * n, tile_lo.data(), 8 * n, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemsetAsync(d + 3 * n, 0, 8 * n, s));
+  CF_TRY(launch_checksum(c, d, d + n, d + 2 * n, n, ntiles, d + 3 * n, s));
+  CF_CUDA(cudaMemcpyAsync(h_out, d + 3 * n, 8 * n, cudaMemcpyDeviceToHost, s));
+  CF_CUDA(cudaStreamSynchronize(s));
+  return CF_OK;
 }
 
 int cf_naive_fixup(cf_ctx* c, const uint64_t* d_field_host, const uint64_t* d_target_host, uint64_t nsites,

@@ -43,14 +43,16 @@ struct Planner {
     return off;
   }
 
-  void node(uint64_t off, int level, uint32_t size, uint32_t na, int64_t nlnext) {
+  void node(uint64_t off, int level, uint32_t size, uint32_t na, int64_t nlnext, uint64_t ordinal = 0) {
     t->node_off.push_back(off);
     t->node_level.push_back(level);
     t->node_size.push_back(size);
     t->node_na.push_back(na);
     t->node_nlnext.push_back(nlnext);
     auto& ln = t->level_nodes[tree];
-    if (int(ln.size()) <= level) ln.resize(level + 1);
+    auto& lb = t->level_base[tree];
+    if (int(ln.size()) <= level) { ln.resize(level + 1); lb.resize(level + 1, 0); }
+    if (ln[level].empty()) lb[level] = ordinal;
     ln[level].push_back(off);
   }
 
@@ -100,16 +102,25 @@ struct Planner {
     const uint64_t q = uint64_t(s.k_or_q);
     struct Frame { uint64_t off; int level; uint64_t ordinal; };
     std::vector<Frame> stack;
-    std::vector<uint64_t> per_level(D + 1, 0);
+    // subtree shard: cut level sl = shallowest with q^sl >= world (sl = 0, width 1: whole tree)
+    const uint64_t world = s.shard_world > 1 ? uint64_t(s.shard_world) : 1, rank = uint64_t(s.shard_rank);
+    int sl = 0;
+    uint64_t width = 1;   // q^sl
+    while (width < world) { width *= q; ++sl; }
     root = alloc(D > 0 ? NODE_SIZE : LEAF_NODE_SIZE, -1);
     stack.push_back({root, 0, 0});
     while (!stack.empty()) {
       Frame f = stack.back();
       stack.pop_back();
       const bool leaf = f.level == D;
-      const bool has_array = s.n > 0 && (!s.leaf_only || leaf);
+      if (world > 1 && f.level == sl && f.ordinal * world / width != rank) {
+        // another rank's subtree: the record stays in its parent's block, fields nulled
+        node(f.off, f.level, leaf ? LEAF_NODE_SIZE : NODE_SIZE, 0u, leaf ? -1 : 0, f.ordinal);
+        continue;
+      }
+      const bool has_array = s.n > 0 && (!s.leaf_only || leaf) && (f.level >= sl || rank == 0);
       node(f.off, f.level, leaf ? LEAF_NODE_SIZE : NODE_SIZE, has_array ? uint32_t(s.n) : 0u,
-           leaf ? -1 : int64_t(q));
+           leaf ? -1 : int64_t(q), f.ordinal);
       if (has_array) {
         int64_t a = array(f.level, f.off, uint64_t(s.n), f.ordinal);
         site(f.off + (leaf ? LEAF_OFF_A : OFF_A), t->arr_off[a]);
@@ -213,6 +224,15 @@ int cf_tree_plan(const cf_spec* spec, cf_tree** out) {
   if (s.elem != 4 && s.elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
   if (s.align != 1 && s.align != 4 && s.align != 8 && s.align != 16 && s.align != 64 && s.align != 128)
     return fail(CF_E_INVALID, "align must be 1, 4, 8, 16, 64 or 128");
+  if (s.shard_world > 1) {
+    if (s.kind != CF_DENSE || s.forest > 1 || s.scatter_seed)
+      return fail(CF_E_INVALID, "subtree shards are defined for single dense trees");
+    if (s.shard_rank < 0 || s.shard_rank >= s.shard_world) return fail(CF_E_INVALID, "shard rank out of range");
+    double leaves = 1;
+    for (int64_t l = 0; l < s.depth; ++l) leaves *= double(s.k_or_q);
+    if (leaves < double(s.shard_world))
+      return fail(CF_E_INVALID, "q^depth = %.0f subtrees cannot be split over %d shards", leaves, s.shard_world);
+  }
   if (s.kind == CF_DENSE) {
     // guard the node count: sum q^l for l <= D must fit comfortably in memory
     double nodes = 0, p = 1;
@@ -224,6 +244,7 @@ int cf_tree_plan(const cf_spec* spec, cf_tree** out) {
   t->spec = s;
   const uint64_t ntrees = s.forest > 1 ? uint64_t(s.forest) : 1;
   t->level_nodes.resize(ntrees);
+  t->level_base.resize(ntrees);
   Planner pl{t};
   for (uint64_t f = 0; f < ntrees; ++f) {
     pl.tree = f;
@@ -335,6 +356,14 @@ int cf_tree_targets(const cf_tree* t, int policy, int64_t* out, uint64_t cap, ui
     for (size_t f = 0; f < t->tree_root.size(); ++f) {
       const auto& leaves = t->level_nodes[f][s.depth];
       const uint64_t node = leaves.back();
+      if (s.shard_world > 1) {   // the reference target lives on the shard owning the last leaf
+        uint64_t last = 1;
+        for (int64_t l = 0; l < s.depth; ++l) last *= uint64_t(s.k_or_q);
+        bool mine = false;
+        for (size_t i = 0; i < na; ++i)
+          if (t->arr_owner[i] == node && t->arr_ordinal[i] == last - 1) mine = true;
+        if (!mine) continue;
+      }
       for (size_t i = 0; i < na; ++i)
         if (t->arr_tree[i] == f && t->arr_owner[i] == node) idx.push_back(int64_t(i));
     }

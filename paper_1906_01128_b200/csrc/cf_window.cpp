@@ -274,13 +274,14 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     const int L = t->arr_level[a];
     const uint64_t ord = t->arr_ordinal[a];
     const auto& lnodes = t->level_nodes[t->arr_tree[a]];
+    const auto& lbase = t->level_base[t->arr_tree[a]];
     uint64_t r = 0, f = fld_lo[i];
     uint64_t pw = 1;   // q^(L-l): q^L at the root, divided by q per level down
     if (dense)
       for (int l = 0; l < L; ++l) pw *= q;
     for (int l = 0; l <= L; ++l, pw = (dense && pw >= q) ? pw / q : 1) {
       // ancestor at level l: ordinal prefix ord / q^(L-l) (pre-order within a level)
-      const uint64_t node = lnodes[size_t(l)][dense ? ord / pw : 0];
+      const uint64_t node = lnodes[size_t(l)][dense ? ord / pw - lbase[size_t(l)] : 0];
       const bool leaf = dense && l == t->spec.depth;
       uint64_t lo, hi;  // byte range read at this level
       if (l < L) { lo = node + OFF_LNEXT; hi = lo + 8; }

@@ -75,6 +75,10 @@ class DenseSpec:
     depth: int = 3
     elem: int = 8
     leaf_only: bool = False
+    # subtree shard (not in the reference): this rank's part of the tree cut at the
+    # shallowest level l with q^l >= shard_world (shard.subtree_shard)
+    shard_rank: int = 0
+    shard_world: int = 1
 
     def __post_init__(self):
         if self.q < 1:
@@ -84,9 +88,14 @@ class DenseSpec:
         if self.depth < 0:
             raise ValueError("depth must be >= 0")
         _check_elem(self.elem)
+        if self.shard_world < 1 or not 0 <= self.shard_rank < self.shard_world:
+            raise ValueError("bad shard rank / world")
+        if self.shard_world > 1 and self.q ** self.depth < self.shard_world:
+            raise ValueError(f"q^depth = {self.q ** self.depth} subtrees cannot be split over {self.shard_world} shards")
 
     def native(self, align: int) -> N.CfSpec:
-        return N.CfSpec(N.CF_DENSE, 0, self.q, self.n, self.depth, self.elem, int(self.leaf_only), align, 1, 0)
+        return N.CfSpec(N.CF_DENSE, 0, self.q, self.n, self.depth, self.elem, int(self.leaf_only), align, 1, 0,
+                        self.shard_rank, self.shard_world)
 
 
 @dataclass(frozen=True)

@@ -35,9 +35,17 @@ def _worker(rank, world, port, out_dir):
     d.barrier()
     ms = d.max(10.0 + 5.0 * d.rank)
     total = d.sum(1000.0)
+    # result gather: each rank contributes its own leaves' (ordinal, checksum) pairs
+    import numpy as np
+    from paper_1906_01128_b200.shard import gather_checksums
+    mine = np.arange(d.rank, 64, d.world, dtype=np.int64)
+    big = mine.astype(np.uint64) * np.uint64(1000) + np.uint64(2 ** 63)   # u64 values above 2^63 survive
+    o, v = gather_checksums(mine, big)
     with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
-        json.dump({"seed": sh.seed, "n": sh.spec.n, "strong_n": strong.spec.n, "max_ms": ms, "sum": total,
-                   "gbs": aggregate_gbs([1 << 30] * d.world, ms)}, f)
+        json.dump({"seed": sh.seed, "n": sh.spec.n, "strong_n": strong.spec.n, "strong_seed": strong.seed,
+                   "strong_rank": strong.spec.shard_rank, "strong_world": strong.spec.shard_world,
+                   "max_ms": ms, "sum": total, "gbs": aggregate_gbs([1 << 30] * d.world, ms),
+                   "gathered_ord": o.tolist(), "gathered_ok": bool((v == o.astype(np.uint64) * np.uint64(1000) + np.uint64(2 ** 63)).all())}, f)
     d.close()
 
 
@@ -47,7 +55,10 @@ def test_two_rank_gloo_plumbing(tmp_path):
     r = [json.loads((tmp_path / f"r{i}.json").read_text()) for i in range(2)]
     assert [x["seed"] for x in r] == [1, 2]                 # distinct shards
     assert all(x["n"] == 4 << 20 for x in r)                # weak: fixed per-GPU work
-    assert all(x["strong_n"] == 268_435_456 // 2 for x in r)  # strong: split payload
+    # strong: one tree cut by subtree, same seed, shard (rank, world) in the spec
+    assert all(x["strong_n"] == 268_435_456 and x["strong_seed"] == 1 and x["strong_world"] == 2 for x in r)
+    assert [x["strong_rank"] for x in r] == [0, 1]
+    assert all(x["gathered_ord"] == list(range(64)) and x["gathered_ok"] for x in r)   # all-gather
     assert all(x["max_ms"] == 15.0 for x in r)              # max over ranks
     assert all(x["sum"] == 2000.0 for x in r)
     assert r[0]["gbs"] == pytest.approx(2 * (1 << 30) / 15e-3 / 1e9)

@@ -1,0 +1,100 @@
+"""Subtree shards of one dense tree: the native planner's partition, on CPU, and
+the sharded window against the whole-tree oracle on the GPU."""
+import numpy as np
+import pytest
+
+import paper_1906_01128_b200 as cf
+from paper_1906_01128_b200 import _native as N
+from paper_1906_01128_b200.shard import (cut_level, expected_checksum, leaf_checksums, owned_subtrees,
+                                         shard_for, subtree_shard)
+
+
+@pytest.mark.parametrize("q,depth,world", [(4, 3, 1), (4, 3, 2), (4, 3, 4), (4, 3, 8), (3, 2, 2), (2, 3, 8),
+                                           (5, 1, 3), (100, 2, 8)])
+def test_shards_partition_the_leaves(q, depth, world):
+    full = N.NativeTree(cf.DenseSpec(q, 5, depth, leaf_only=True).native(16))
+    seen = []
+    payload = 0
+    for r in range(world):
+        spec = subtree_shard(cf.DenseSpec(q, 5, depth, leaf_only=True), r, world) if world > 1 else \
+            cf.DenseSpec(q, 5, depth, leaf_only=True)
+        t = N.NativeTree(spec.native(16))
+        lv, od = t.table(N.CF_TAB_ARR_LEVEL), t.table(N.CF_TAB_ARR_ORDINAL)
+        assert (lv == depth).all()
+        # each shard's leaves lie under its own cut-level subtrees
+        width = q ** (depth - cut_level(q, world))
+        assert set((od // width).tolist()) <= set(owned_subtrees(q, world, r))
+        seen += od.tolist()
+        payload += int(t.info.payload_bytes)
+        # the reference target (last child path) lives only on the shard that owns it
+        assert len(t.targets(N.CF_TARGET_REF)) == (1 if q ** depth - 1 in od.tolist() else 0)
+        assert sorted(t.targets(N.CF_TARGET_ALL_LEAVES).tolist()) == list(range(len(od)))
+    assert sorted(seen) == list(range(q ** depth))
+    assert payload == int(full.info.payload_bytes)
+
+
+def test_shard_validation():
+    with pytest.raises(ValueError):
+        cf.DenseSpec(2, 5, 2, shard_rank=0, shard_world=5)   # 4 subtrees for 5 shards
+    with pytest.raises(ValueError):
+        cf.DenseSpec(2, 5, 2, shard_rank=2, shard_world=2)
+    sh = shard_for(cf.DenseSpec(4, 64, 3, elem=4, leaf_only=True), 3, 8, "strong")
+    assert (sh.spec.shard_rank, sh.spec.shard_world, sh.seed, sh.spec.n) == (3, 8, 1, 64)
+
+
+def test_expected_checksum_matches_numpy():
+    for elem in (4, 8):
+        vals = cf.payload_values(3, 2, 100_003, elem) * (np.float64(2.0) if elem == 8 else np.float32(2.0))
+        want = int(vals.view(np.uint32).astype(np.uint64).sum(dtype=np.uint64))
+        assert expected_checksum(3, 2, 100_003, elem, 2.0, chunk=4096) == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,align,elem", [(4, 16, 4), (8, 1, 8), (2, 1, 4)])
+def test_sharded_windows_match_the_whole_tree_oracle(oracle, world, align, elem):
+    """Each rank's shard window (run one after another on one GPU) returns exactly the whole
+    tree's leaves it owns; the gathered checksums cover every leaf once."""
+    if N.device_count() == 0:
+        pytest.skip("no GPU visible")
+    q, n, depth = 4, 3001, 3
+    full = oracle.build(oracle.OSpec(oracle.DENSE, q, n, depth, elem=elem, leaf_only=True, align=align), 1)
+    fidx = oracle.targets(full, oracle.TARGET_ALL_LEAVES)
+    want_full = oracle.expected_after_window(full, fidx, 2.0)
+    leaf_nodes = full.node_off[full.node_level == depth]                # pre-order = ordinal order
+    by_owner = {int(o): i for i, o in enumerate(full.arr_owner.tolist())}
+    ords, sums = [], []
+    for r in range(world):
+        spec = subtree_shard(cf.DenseSpec(q, n, depth, elem=elem, leaf_only=True), r, world)
+        w = cf.DeepCopyWindow(spec, seed=1, policy="all_leaves", align=align, chunk_bytes=8192)
+        try:
+            st = w.run(scale=2.0)
+            assert st.bad == (1 << 64) - 1
+            got = w.host_dst()
+            off, cnt = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT)
+            od = w.table(N.CF_TAB_ARR_ORDINAL)
+            for i in w.targets.tolist():
+                a = by_owner[int(leaf_nodes[int(od[i])])]
+                fa, nb = int(full.arr_off[a]), int(full.arr_count[a]) * elem
+                assert np.array_equal(got[int(off[i]):int(off[i]) + nb], want_full[fa:fa + nb]), (r, int(od[i]))
+            # checksums of the device image (detached, scaled) after the window
+            ords += od[w.targets].tolist()
+            sums += leaf_checksums(w.ctx, w.image, off[w.targets], cnt[w.targets], elem).tolist()
+        finally:
+            w.close()
+    assert sorted(ords) == list(range(q ** depth))
+    assert set(sums) == {expected_checksum(1, depth, n, elem, 2.0)}
+
+
+@pytest.mark.gpu
+def test_sharded_tree_through_the_drop_in_api():
+    if N.device_count() == 0:
+        pytest.skip("no GPU visible")
+    for r in range(4):
+        m = cf.Machine()
+        spec = subtree_shard(cf.DenseSpec(4, 700, 3), r, 4)
+        arena, h = cf.marshal_tree(m, spec, seed=5)
+        prep = cf.transfer_to_device(m, h, "marshalling", arena, policy="all_arrays")
+        cf.kernel_scale(m, h, prep, 2.0)
+        cf.copy_back(m, h, prep)
+        cf.verify_tree(m, h, 2.0, policy="all_arrays")
+        m.close()

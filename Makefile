@@ -7,7 +7,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -ccbin $(HOSTCXX) -Xcompiler -fPIC,-
 SRC := paper_1906_01128_b200/csrc
 OBJDIR := build/obj
 LIB := paper_1906_01128_b200/_lib/libchainforge_b200.so
-OBJS := $(OBJDIR)/cf_kernels.o $(OBJDIR)/cf_runtime.o $(OBJDIR)/cf_tree.o $(OBJDIR)/cf_ops.o $(OBJDIR)/cf_window.o
+OBJS := $(OBJDIR)/cf_kernels.o $(OBJDIR)/cf_runtime.o $(OBJDIR)/cf_tree.o $(OBJDIR)/cf_ops.o $(OBJDIR)/cf_window.o $(OBJDIR)/cf_selective.o
 
 all: $(LIB) oracle
 

@@ -50,6 +50,7 @@ enum { CF_MODE_RESOLVED = 0, CF_MODE_CHASE = 1 };
 typedef struct cf_ctx cf_ctx;       /* one GPU: streams, events, scratch */
 typedef struct cf_tree cf_tree;     /* planned graph layout + relocation/chain tables */
 typedef struct cf_window cf_window; /* a planned, pipelined metered window */
+typedef struct cf_selective cf_selective; /* a planned, pipelined pointerchain window */
 
 /* LinearSpec / DenseSpec (scenarios.py:33-68) plus the B200 build parameters.
  * elem: 8 = float64 (reference), 4 = float32 (BASELINE configs).
@@ -234,6 +235,11 @@ int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t*
  * range i (h_addr[i], h_bytes[i], both 4-byte aligned) the wrapping u64 sum of its u32 words,
  * into h_out[i].  Synchronous. */
 int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_bytes, uint64_t n, uint64_t* h_out);
+/* Per-object transfers (naive_deep_copy / naive_copy_back, memory.py:358-361, 368-372; batched
+ * selective copies): objects under 64 KiB whose both ends are SM-addressable (device, managed
+ * or mapped pinned memory) are copied by one zero-copy kernel, one warp per object; the rest
+ * by the copy engines (cudaMemcpyBatchAsync).  Synchronous. */
+int cf_copy_objects(cf_ctx* ctx, void* const* dsts, const void* const* srcs, const uint64_t* sizes, uint64_t count);
 /* naive_deep_copy fixups (memory.py:349-365): per-object copies are issued by the caller with
  * cf_memcpy_batch; this kernel rewrites every site through a sorted interval map
  * (AddressMap.translate, memory.py:409-419) on the device. */
@@ -242,6 +248,22 @@ int cf_memcpy_batch(cf_ctx* ctx, void* const* dsts, const void* const* srcs,
 int cf_naive_fixup(cf_ctx* ctx, const uint64_t* d_site_field_host, const uint64_t* d_site_target_host,
                    uint64_t nsites, const uint64_t* d_map_host_base, const uint64_t* d_map_size,
                    const uint64_t* d_map_dev_base, uint64_t nmap, uint64_t* d_bad, void* stream);
+/* As cf_naive_fixup from host tables (uploaded into the context's scratch). Synchronous;
+ * CF_E_WILD with *bad_site = the first site whose target was never copied. */
+int cf_naive_fixup_host(cf_ctx* ctx, const uint64_t* h_site_field_host, const uint64_t* h_site_target_host,
+                        uint64_t nsites, const uint64_t* h_map_host_base, const uint64_t* h_map_size,
+                        const uint64_t* h_map_dev_base, uint64_t nmap, uint64_t* bad_site);
+
+/* Pointerchain scheme as one pipelined window (transfer_to_device / kernel_scale / copy_back,
+ * harness.py:228-238, 255-259, 312-325): n targeted arrays, host h_src[i] -> device buffer
+ * d_buf[i], count[i] elements of elem bytes.  Steps of ~chunk_bytes; per step H2D, leaf kernel,
+ * D2H, steps overlapped.  Arrays >= 64 KiB move on the copy engines, smaller ones by zero-copy
+ * SM kernels over the mapped pinned host memory.  Run flags: CF_WIN_H2D | CF_WIN_SCALE |
+ * CF_WIN_D2H (any subset).  cf_selective_run is synchronous. */
+int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
+                      int elem, uint64_t chunk_bytes, cf_selective** out);
+int cf_selective_run(cf_selective* w, uint32_t flags, double scale);
+int cf_selective_free(cf_selective* w);
 
 /* ---------------- unified memory (memory.py:239-261, 378-394) ---------------- */
 /* Managed-memory hints for the UVM scheme. dst_device < 0 prefetches to the host (the

@@ -45,7 +45,8 @@ EXPORTED = (
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
-    "cf_checksum_ranges",
+    "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
+    "cf_copy_objects", "cf_naive_fixup_host",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -134,6 +135,11 @@ def _declare(L):
         "cf_naive_fixup": (C.c_int, [P, P, P, U64, P, P, P, U64, P, P]),
         "cf_arena_check_sites": (C.c_int, [P, U64, P, U64, U64, C.POINTER(U64)]),
         "cf_checksum_ranges": (C.c_int, [P, P, P, U64, P]),
+        "cf_selective_plan": (C.c_int, [P, U64, P, P, P, C.c_int, U64, C.POINTER(P)]),
+        "cf_selective_run": (C.c_int, [P, C.c_uint32, C.c_double]),
+        "cf_selective_free": (C.c_int, [P]),
+        "cf_copy_objects": (C.c_int, [P, P, P, P, U64]),
+        "cf_naive_fixup_host": (C.c_int, [P, P, P, U64, P, P, P, U64, C.POINTER(U64)]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),

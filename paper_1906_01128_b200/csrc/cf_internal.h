@@ -38,6 +38,8 @@ void clear_error();
   } while (0)
 
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
+int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, const uint64_t* bytes, uint64_t n,
+                     cudaStream_t s);
 int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, const uint64_t* tile_lo, uint64_t nranges,
                     uint64_t ntiles, uint64_t* out, cudaStream_t s);
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,

@@ -704,6 +704,29 @@ __global__ void __launch_bounds__(256) k_seg_copy(const uint64_t* __restrict__ s
   for (i = lo + lane; i < hi; i += 32) dst[i] = src[i];
 }
 
+// Many small copies as one launch (zero-copy over mapped pinned host memory, either
+// direction): warp i copies bytes[i] from src[i] to dst[i], 16-byte words when both ends and
+// the length allow, else 4-byte words.  Replaces one copy-engine command per object for the
+// pointerchain scheme's small arrays (cf_selective_run).
+__global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ src, const uint64_t* __restrict__ dst,
+                                                   const uint64_t* __restrict__ bytes, uint64_t n) {
+  const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const uint64_t s = src[i], d = dst[i], b = bytes[i];
+  if (((s | d | b) & 15) == 0) {
+    const uint4* ps = reinterpret_cast<const uint4*>(s);
+    uint4* pd = reinterpret_cast<uint4*>(d);
+    for (uint64_t k = lane; k < b / 16; k += 32) pd[k] = ps[k];
+  } else if (((s | d | b) & 3) == 0) {
+    const uint32_t* ps = reinterpret_cast<const uint32_t*>(s);
+    uint32_t* pd = reinterpret_cast<uint32_t*>(d);
+    for (uint64_t k = lane; k < b / 4; k += 32) pd[k] = ps[k];
+  } else {
+    for (uint64_t k = lane; k < b; k += 32) reinterpret_cast<uint8_t*>(d)[k] = reinterpret_cast<const uint8_t*>(s)[k];
+  }
+}
+
 // Per-range checksum for the multi-GPU result gather: wrapping u64 sum of the
 // range's u32 words (order independent, so tiles can atomically accumulate).  One CTA per
 // 64 KiB tile of a range; tile_lo[r] = first tile of range r.
@@ -837,6 +860,14 @@ int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* 
 int launch_seg_copy(cf_ctx* ctx, const uint64_t* segs, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_seg_copy<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(segs, n, src, dst);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, const uint64_t* bytes, uint64_t n,
+                     cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_copy_list<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(src, dst, bytes, n);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -5,6 +5,8 @@
 //   cf_naive_fixup                  <- naive_deep_copy fix-up loop         memory.py:362-364
 //   cf_arena_check_sites            <- the attach loop's bounds check      memory.py:319-321
 //   cf_checksum_ranges              <- result gather of the multi-GPU shards
+//   cf_copy_objects                 <- per-object transfers (naive_deep_copy / copy-back and
+//                                      the selective copies, memory.py:358-361, 368-372)
 #include "cf_internal.h"
 
 #include <algorithm>
@@ -353,6 +355,84 @@ int cf_checksum_ranges(cf_ctx* c, const uint64_t* h_addr, const uint64_t* h_byte
   CF_TRY(launch_checksum(c, d, d + n, d + 2 * n, n, ntiles, d + 3 * n, s));
   CF_CUDA(cudaMemcpyAsync(h_out, d + 3 * n, 8 * n, cudaMemcpyDeviceToHost, s));
   CF_CUDA(cudaStreamSynchronize(s));
+  return CF_OK;
+}
+
+int cf_copy_objects(cf_ctx* c, void* const* dsts, const void* const* srcs, const uint64_t* sizes, uint64_t count) {
+  if (!c || (count && (!dsts || !srcs || !sizes))) return fail(CF_E_INVALID, "null argument");
+  if (count == 0) return CF_OK;
+  CfDevice g(c);
+  constexpr uint64_t SMALL = 64 << 10;
+  // zero-copy needs both ends addressable by the SMs (device, managed or mapped pinned memory)
+  auto dev_ok = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type != cudaMemoryTypeUnregistered && a.devicePointer == p;
+  };
+  std::vector<uint64_t> zs, zd, zb;
+  std::vector<void*> bd;
+  std::vector<const void*> bs;
+  std::vector<uint64_t> bz;
+  bool zc = true;
+  bool checked = false;
+  for (uint64_t i = 0; i < count; ++i) {
+    if (sizes[i] < SMALL && zc) {
+      if (!checked) { zc = dev_ok(srcs[i]) && dev_ok(dsts[i]); checked = true; }
+      if (zc) {
+        zs.push_back(reinterpret_cast<uint64_t>(srcs[i]));
+        zd.push_back(reinterpret_cast<uint64_t>(dsts[i]));
+        zb.push_back(sizes[i]);
+        continue;
+      }
+    }
+    bd.push_back(dsts[i]);
+    bs.push_back(srcs[i]);
+    bz.push_back(sizes[i]);
+  }
+  cudaStream_t s = c->compute;
+  if (!bz.empty()) CF_TRY(cf_memcpy_batch(c, bd.data(), bs.data(), bz.data(), bz.size(), s));
+  if (!zb.empty()) {
+    const uint64_t m = zb.size();
+    DevBuf blk(c);
+    CF_TRY(blk.alloc(24 * m));
+    uint64_t* d = blk.as<uint64_t>();
+    CF_CUDA(cudaMemcpyAsync(d, zs.data(), 8 * m, cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaMemcpyAsync(d + m, zd.data(), 8 * m, cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaMemcpyAsync(d + 2 * m, zb.data(), 8 * m, cudaMemcpyHostToDevice, s));
+    CF_TRY(launch_copy_list(c, d, d + m, d + 2 * m, m, s));
+  }
+  CF_CUDA(cudaStreamSynchronize(s));
+  return CF_OK;
+}
+
+int cf_naive_fixup_host(cf_ctx* c, const uint64_t* h_field_host, const uint64_t* h_target_host, uint64_t nsites,
+                        const uint64_t* h_map_host_base, const uint64_t* h_map_size, const uint64_t* h_map_dev_base,
+                        uint64_t nmap, uint64_t* bad_site) {
+  if (!c || (nsites && (!h_field_host || !h_target_host)) || (nmap && (!h_map_host_base || !h_map_size || !h_map_dev_base)))
+    return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  if (bad_site) *bad_site = NO_BAD;
+  if (nsites == 0) return CF_OK;
+  DevBuf blk(c);
+  CF_TRY(blk.alloc(8 * (2 * nsites + 3 * nmap)));
+  uint64_t* d = blk.as<uint64_t>();
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemcpyAsync(d, h_field_host, 8 * nsites, cudaMemcpyHostToDevice, s));
+  CF_CUDA(cudaMemcpyAsync(d + nsites, h_target_host, 8 * nsites, cudaMemcpyHostToDevice, s));
+  uint64_t* m = d + 2 * nsites;
+  if (nmap) {
+    CF_CUDA(cudaMemcpyAsync(m, h_map_host_base, 8 * nmap, cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaMemcpyAsync(m + nmap, h_map_size, 8 * nmap, cudaMemcpyHostToDevice, s));
+    CF_CUDA(cudaMemcpyAsync(m + 2 * nmap, h_map_dev_base, 8 * nmap, cudaMemcpyHostToDevice, s));
+  }
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  CF_TRY(launch_naive_fixup(c, d, d + nsites, nsites, m, m + nmap, m + 2 * nmap, nmap, c->d_bad, s));
+  uint64_t bad = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, s, &bad));
+  if (bad != NO_BAD) {
+    if (bad_site) *bad_site = bad;
+    return fail(CF_E_WILD, "fixup target 0x%llx was never copied to the device", (unsigned long long)h_target_host[bad]);
+  }
   return CF_OK;
 }
 

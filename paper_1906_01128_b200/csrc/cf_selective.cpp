@@ -1,0 +1,226 @@
+// Pipelined pointerchain window: the reference's selective-copy scheme
+//   transfer_to_device (pointerchain branch)  harness.py:228-238  one bulk copy per target array
+//   kernel_scale       (pointerchain branch)  harness.py:255-259  scale through resolved addresses
+//   copy_back          (pointerchain branch)  harness.py:312-325  one bulk copy back per array
+// as one planned schedule.  The targeted arrays (host address, device buffer, count) are cut
+// into steps of about one chunk.  Step k: its arrays' bytes go host -> device, the leaf kernel
+// scales them, and they go back -- while step k+1 is already copying in.  Arrays of at least
+// DMA_MIN bytes move on the copy engines (one H2D and one D2H stream, so the two directions
+// overlap over the full-duplex link); smaller ones move by zero-copy SM kernels over the mapped
+// pinned host memory, one warp per array, which avoids one copy-engine command per object (the
+// C4 shape has a million 1 KiB arrays).  All bookkeeping is planned once; a run only enqueues.
+#include "cf_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+using namespace cf;
+
+namespace {
+constexpr uint64_t DMA_MIN = 64 << 10;
+}
+
+struct cf_selective {
+  cf_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;   // compute stream of this window
+  int elem = 4;
+  uint64_t n = 0, nsteps = 0;
+  struct Piece { uint64_t src, dst, bytes; };
+  std::vector<Piece> dma;                  // DMA pieces, grouped by step
+  std::vector<uint64_t> dma_lo;            // per step: range in dma
+  std::vector<uint64_t> zc_lo;             // per step: range in the zero-copy list
+  std::vector<cf_scale_work> work;         // per step: leaf-kernel work (device pointers set)
+  uint64_t nzc = 0;
+  // one pinned table block + device mirror: ea u64[n] | count u32[n] | zc src u64[nzc] |
+  // zc dst u64[nzc] | zc bytes u64[nzc] | parts | tile_base | groups
+  uint8_t* h_tab = nullptr;
+  uint8_t* d_tab = nullptr;
+  uint64_t tab_bytes = 0, off_cnt = 0, off_zs = 0, off_zd = 0, off_zb = 0;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  cudaEvent_t ev_start = nullptr, ev_tab = nullptr, ev_join = nullptr;
+};
+
+namespace {
+void destroy(cf_selective* w) {
+  if (!w) return;
+  CfDevice g(w->ctx);
+  if (w->h_tab) cudaFreeHost(w->h_tab);
+  if (w->d_tab) cudaFree(w->d_tab);
+  for (auto e : w->ev_in) cudaEventDestroy(e);
+  for (auto e : w->ev_out) cudaEventDestroy(e);
+  for (auto e : {w->ev_start, w->ev_tab, w->ev_join})
+    if (e) cudaEventDestroy(e);
+  if (w->stream) cudaStreamDestroy(w->stream);
+  delete w;
+}
+}  // namespace
+
+extern "C" {
+
+int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
+                      int elem, uint64_t chunk_bytes, cf_selective** out) {
+  if (!ctx || !out || (n && (!h_src || !d_buf || !count))) return fail(CF_E_INVALID, "null argument");
+  if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
+  CfDevice g(ctx);
+  cf_selective* w = new cf_selective();
+  w->ctx = ctx;
+  w->elem = elem;
+  w->n = n;
+  const uint64_t ch = std::max<uint64_t>(chunk_bytes ? chunk_bytes : (16ull << 20), TILE_BYTES);
+  // zero-copy needs every small array's host memory mapped at the same address (UVA pinned)
+  bool mapped = true;
+  for (uint64_t i = 0; i < n && mapped; ++i) {
+    if (count[i] * uint64_t(elem) >= DMA_MIN) continue;
+    void* dp = nullptr;
+    mapped = cudaHostGetDevicePointer(&dp, reinterpret_cast<void*>(h_src[i]), 0) == cudaSuccess &&
+             reinterpret_cast<uint64_t>(dp) == h_src[i];
+  }
+  cudaGetLastError();
+  std::vector<uint64_t> zsrc, zdst, zbytes;
+  ScaleWork sw;
+  sw.elem = elem;
+  std::vector<uint64_t> tri;
+  uint64_t acc = 0;
+  auto close_step = [&]() {
+    w->work.push_back(sw.append(tri));
+    tri.clear();
+    w->dma_lo.push_back(w->dma.size());
+    w->zc_lo.push_back(zsrc.size());
+    acc = 0;
+  };
+  w->dma_lo.push_back(0);
+  w->zc_lo.push_back(0);
+  const uint64_t piece_elems = ch / uint64_t(elem);
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t bytes = count[i] * uint64_t(elem);
+    if (bytes == 0) continue;
+    if (bytes < DMA_MIN && mapped) {
+      if (acc + bytes > ch && acc) close_step();
+      zsrc.push_back(h_src[i]);
+      zdst.push_back(d_buf[i]);
+      zbytes.push_back(bytes);
+      tri.insert(tri.end(), {i, 0, count[i]});
+      acc += bytes;
+      continue;
+    }
+    for (uint64_t e0 = 0; e0 < count[i]; e0 += piece_elems) {
+      const uint64_t e1 = std::min(count[i], e0 + piece_elems);
+      const uint64_t pb = (e1 - e0) * uint64_t(elem);
+      if (acc + pb > ch && acc) close_step();
+      w->dma.push_back({h_src[i] + e0 * uint64_t(elem), d_buf[i] + e0 * uint64_t(elem), pb});
+      tri.insert(tri.end(), {i, e0, e1});
+      acc += pb;
+    }
+  }
+  if (acc || w->work.empty()) close_step();
+  w->nsteps = w->work.size();
+  w->nzc = zsrc.size();
+  // table block
+  auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
+  w->off_cnt = al8(n * 8);
+  w->off_zs = al8(w->off_cnt + n * 4);
+  w->off_zd = w->off_zs + w->nzc * 8;
+  w->off_zb = w->off_zd + w->nzc * 8;
+  const uint64_t off_parts = w->off_zb + w->nzc * 8;
+  const uint64_t off_tb = al8(off_parts + sw.parts.size() * 4);
+  const uint64_t off_grp = al8(off_tb + sw.tile_base.size() * 8);
+  w->tab_bytes = al8(off_grp + sw.groups.size() * 4 + 8);
+  cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
+  if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
+  if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "selective tables: %s", cudaGetErrorString(ce)); }
+  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(w->h_tab + w->off_cnt);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (count[i] >> 32) { destroy(w); return fail(CF_E_INVALID, "count %llu does not fit the u32 nA field", (unsigned long long)count[i]); }
+    cnt32[i] = uint32_t(count[i]);
+  }
+  if (n) memcpy(w->h_tab, d_buf, n * 8);
+  if (w->nzc) {
+    memcpy(w->h_tab + w->off_zs, zsrc.data(), w->nzc * 8);
+    memcpy(w->h_tab + w->off_zd, zdst.data(), w->nzc * 8);
+    memcpy(w->h_tab + w->off_zb, zbytes.data(), w->nzc * 8);
+  }
+  if (!sw.parts.empty()) memcpy(w->h_tab + off_parts, sw.parts.data(), sw.parts.size() * 4);
+  if (!sw.tile_base.empty()) memcpy(w->h_tab + off_tb, sw.tile_base.data(), sw.tile_base.size() * 8);
+  if (!sw.groups.empty()) memcpy(w->h_tab + off_grp, sw.groups.data(), sw.groups.size() * 4);
+  for (auto& k : w->work) {
+    k.parts = reinterpret_cast<const uint32_t*>(w->d_tab + off_parts);
+    k.tile_base = reinterpret_cast<const uint64_t*>(w->d_tab + off_tb);
+    k.groups = reinterpret_cast<const uint32_t*>(w->d_tab + off_grp);
+  }
+  bool ok = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&w->ev_start, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&w->ev_tab, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming) == cudaSuccess;
+  w->ev_in.resize(w->nsteps, nullptr);
+  w->ev_out.resize(w->nsteps, nullptr);
+  for (uint64_t k = 0; k < w->nsteps && ok; ++k)
+    ok = cudaEventCreateWithFlags(&w->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&w->ev_out[k], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "selective window streams/events"); }
+  *out = w;
+  return CF_OK;
+}
+
+int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
+  if (!w) return fail(CF_E_INVALID, "null window");
+  cf_ctx* c = w->ctx;
+  CfDevice g(c);
+  cudaStream_t cs = w->stream, hs = c->h2d[0], ds = c->d2h;
+  const uint64_t* ea = reinterpret_cast<const uint64_t*>(w->d_tab);
+  const uint32_t* cnt = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_cnt);
+  const uint64_t* zs = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zs);
+  const uint64_t* zd = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zd);
+  const uint64_t* zb = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zb);
+  // fan out from the context's compute stream (ordered after earlier work on this context)
+  CF_CUDA(cudaEventRecord(w->ev_start, c->compute));
+  for (cudaStream_t s : {cs, hs, ds}) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, cs));
+  // the resolved-address / work tables travel with the data, first on the H2D stream
+  CF_CUDA(cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, hs));
+  CF_CUDA(cudaEventRecord(w->ev_tab, hs));
+  CF_CUDA(cudaStreamWaitEvent(cs, w->ev_tab, 0));
+  cf_chain_shape sh;
+  memset(&sh, 0, sizeof sh);
+  for (uint64_t k = 0; k < w->nsteps; ++k) {
+    if (flags & CF_WIN_H2D) {
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
+        CF_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),
+                                w->dma[j].bytes, cudaMemcpyHostToDevice, hs));
+      CF_CUDA(cudaEventRecord(w->ev_in[k], hs));
+      CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k], 0));
+      // small arrays: one warp per array pulls it over the mapped host memory
+      CF_TRY(launch_copy_list(c, zs + w->zc_lo[k], zd + w->zc_lo[k], zb + w->zc_lo[k], w->zc_lo[k + 1] - w->zc_lo[k], cs));
+    }
+    if (flags & CF_WIN_SCALE)
+      CF_TRY(launch_scale(c, w->elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, nullptr, ea, cnt, w->work[k], scale,
+                          c->d_bad, cs));
+    if (flags & CF_WIN_D2H) {
+      CF_CUDA(cudaEventRecord(w->ev_out[k], cs));
+      CF_CUDA(cudaStreamWaitEvent(ds, w->ev_out[k], 0));
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
+        CF_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(w->dma[j].src), reinterpret_cast<const void*>(w->dma[j].dst),
+                                w->dma[j].bytes, cudaMemcpyDeviceToHost, ds));
+      // small arrays pushed back by SM stores into mapped host memory, on the D2H stream
+      CF_TRY(launch_copy_list(c, zd + w->zc_lo[k], zs + w->zc_lo[k], zb + w->zc_lo[k], w->zc_lo[k + 1] - w->zc_lo[k], ds));
+    }
+  }
+  for (cudaStream_t s : {hs, ds}) {
+    CF_CUDA(cudaEventRecord(w->ev_join, s));
+    CF_CUDA(cudaStreamWaitEvent(cs, w->ev_join, 0));
+  }
+  CF_CUDA(cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, cs));
+  CF_CUDA(cudaEventRecord(w->ev_join, cs));
+  CF_CUDA(cudaStreamWaitEvent(c->compute, w->ev_join, 0));
+  CF_CUDA(cudaStreamSynchronize(cs));
+  if (c->h_bad[0] != NO_BAD)
+    return fail(CF_E_WILD, "leaf kernel: buffer %llu rejected", (unsigned long long)c->h_bad[0]);
+  return CF_OK;
+}
+
+int cf_selective_free(cf_selective* w) {
+  destroy(w);
+  return CF_OK;
+}
+
+}  // extern "C"

@@ -262,8 +262,12 @@ class FusedMarshalWindow:
         N.check(rc, "fused marshalling window")
 
     def _targets(self) -> np.ndarray:
-        idx = self.handle.target_indices(self.policy)
-        return idx[self.handle.arr_count[idx] > 0]
+        cache = self.handle.__dict__.setdefault("_nonempty_targets", {})
+        idx = cache.get(self.policy)
+        if idx is None:
+            idx = self.handle.target_indices(self.policy)
+            idx = cache[self.policy] = idx[self.handle.arr_count[idx] > 0]
+        return idx
 
     def flush(self) -> None:
         """Materialise the stage reached so far; later calls take the eager paths."""
@@ -278,7 +282,51 @@ class FusedMarshalWindow:
         self._run(N.CF_WIN_FULL, self._targets(), self.scale)
 
 
-def _pending(machine: Machine, prep: DevicePrep) -> "FusedMarshalWindow | None":
+class FusedSelectiveWindow:
+    """The pointerchain scheme's ``transfer_to_device -> kernel_scale -> copy_back`` (selective
+    copies of the targeted arrays, harness.py:228-238, 255-259, 312-325) deferred into one
+    pipelined cf_selective window: per step of ~16 MiB the arrays' bytes go in, get scaled and go
+    back while the next step copies in; big arrays on the copy engines, small ones by zero-copy
+    SM kernels.  Same observable behaviour and flush rules as FusedMarshalWindow."""
+
+    def __init__(self, machine: Machine, prep: DevicePrep, elem: int):
+        self.machine, self.prep, self.elem = machine, prep, elem
+        self.scale: float | None = None
+        self.mode = "resolved"
+
+    def _run(self, flags: int, scale: float) -> None:
+        p = self.prep
+        lib = N.lib()
+        t0 = time.perf_counter()
+        key = ("selective", int(p.buf_dev[0]), len(p.buf_dev))
+        w = self.machine._plans.get(key)
+        if w is None:
+            host = np.ascontiguousarray(p.buf_host, np.uint64)
+            dev = np.ascontiguousarray(p.buf_dev, np.uint64)
+            cnt = np.ascontiguousarray(p.buf_count, np.uint64)
+            w = C.c_void_p()
+            N.check(lib.cf_selective_plan(self.machine.ctx.handle, len(dev), N.ptr(host), N.ptr(dev), N.ptr(cnt),
+                                          self.elem, FUSED_CHUNK, C.byref(w)), "pointerchain window plan")
+            self.machine._plans[key] = w
+            self.machine._plan_free[key] = lib.cf_selective_free
+        t1 = time.perf_counter()
+        rc = lib.cf_selective_run(w, flags, float(scale))
+        self.timing = {"plan_ms": (t1 - t0) * 1e3, "run_ms": (time.perf_counter() - t1) * 1e3}
+        if rc == N.CF_E_WILD:
+            raise WildAccess(N.last_error())
+        N.check(rc, "pointerchain window")
+
+    def flush(self) -> None:
+        if self.scale is None:
+            self._run(N.CF_WIN_H2D, 1.0)
+        else:
+            self._run(N.CF_WIN_H2D | N.CF_WIN_SCALE, self.scale)
+
+    def complete(self) -> None:
+        self._run(N.CF_WIN_H2D | N.CF_WIN_SCALE | N.CF_WIN_D2H, self.scale)
+
+
+def _pending(machine: Machine, prep: DevicePrep):
     f = prep.fused
     return f if f is not None and machine._deferred is f else None
 
@@ -330,9 +378,17 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx,
                           buf_host=handle.arr_off[idx] + np.uint64(handle.base), buf_count=handle.arr_count[idx])
         if len(idx):
-            dev_base = machine.device.allocate_span(int(aligned.sum()), offs, sizes, zero=False)
+            spare = handle.__dict__.setdefault("_spare_spans", {})
+            dev_base = spare.pop(policy, 0) or machine.device.allocate_span(int(aligned.sum()), offs, sizes, zero=False)
             prep.buf_dev = offs + np.uint64(dev_base)
-            machine.transfer_ranges(machine.host, prep.buf_host, machine.device, prep.buf_dev, sizes, "bulk")
+            if fused:
+                # addresses come from the tree's own array table and the span just allocated for
+                # exactly these sizes: in bounds by construction (the eager path re-checks them)
+                machine.log.append_many(H2D, "bulk", sizes.astype(np.int64))
+                prep.fused = FusedSelectiveWindow(machine, prep, e)
+                machine._deferred = prep.fused
+            else:
+                machine.transfer_ranges(machine.host, prep.buf_host, machine.device, prep.buf_dev, sizes, "bulk")
         return prep
     if scheme == "uvm":
         # the tree already lives in managed memory (harness.py:239-240: no copy); optional
@@ -475,12 +531,18 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     stats = KernelStats()
     elem = handle.spec.elem
     fw = _pending(machine, prep)
-    if fw is not None and fw.scale is None:
+    if fw is not None and fw.scale is None and prep.scheme == "marshalling":
         # joins the deferred window: the leaf kernel runs chunk by chunk as the arena lands
         fw.scale, fw.mode = float(scale), mode
-        idx = fw._targets()
-        stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
-        stats.elements_touched = int(handle.arr_count[idx].sum())
+        cache = handle.__dict__.setdefault("_kernel_stats", {})
+        if prep.policy not in cache:
+            idx = fw._targets()
+            cache[prep.policy] = (_reference_derefs(handle, prep.policy, idx), int(handle.arr_count[idx].sum()))
+        stats.chain_derefs, stats.elements_touched = cache[prep.policy]
+        return stats
+    if fw is not None and fw.scale is None and prep.scheme == "pointerchain":
+        fw.scale = float(scale)   # joins the deferred pointerchain window
+        stats.elements_touched = int(prep.buf_count.sum())
         return stats
     machine.flush()
     ctx = machine.ctx.handle
@@ -526,6 +588,12 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
 
 def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     fw = _pending(machine, prep)
+    if fw is not None and fw.scale is not None and prep.scheme == "pointerchain":
+        machine._deferred = None
+        fw.complete()
+        machine.log.append_many(D2H, "bulk", (prep.buf_count * np.uint64(handle.spec.elem)).astype(np.int64))
+        prep.handle.__dict__.setdefault("_spare_spans", {})[prep.policy] = int(prep.buf_dev[0])
+        return
     if fw is not None and fw.scale is not None:
         machine._deferred = None
         fw.complete()
@@ -543,6 +611,8 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     elif prep.scheme == "pointerchain":
         machine.transfer_ranges(machine.device, prep.buf_dev, machine.host, prep.buf_host,
                                 prep.buf_count * np.uint64(handle.spec.elem), "bulk")
+        if len(prep.buf_dev):
+            handle.__dict__.setdefault("_spare_spans", {})[prep.policy] = int(prep.buf_dev[0])
     elif prep.scheme == "uvm":
         # the host re-touches every page the kernel dirtied (harness.py:321-325): migrate the
         # targeted arrays back explicitly, then account the logical page migrations

@@ -521,7 +521,8 @@ class Machine:
         # a deferred metered window (harness.FusedMarshalWindow) not yet enqueued; anything that
         # observes or mutates device/host state runs it first (flush)
         self._deferred = None
-        self._plans: dict = {}   # cached cf_window plans of the fused marshalling windows
+        self._plans: dict = {}   # cached plans of the fused windows (cf_window / cf_selective)
+        self._plan_free: dict = {}   # key -> free function when not cf_window_free
 
     @property
     def ctx(self) -> N.DeviceContext:
@@ -558,9 +559,9 @@ class Machine:
         lib = N._lib
         if lib is not None and self._plans:
             self.ctx.sync()
-            for w in self._plans.values():
-                lib.cf_window_free(w)
-        self._plans = {}
+            for key, w in self._plans.items():
+                self._plan_free.get(key, lib.cf_window_free)(w)
+        self._plans, self._plan_free = {}, {}
         self.host.free_all()
         self.device.free_all()
 
@@ -596,8 +597,7 @@ class Machine:
         src._check_many(sa, sz)
         dst._check_many(da, sz)
         ctx = self.ctx.handle
-        N.check(N.lib().cf_memcpy_batch(ctx, N.ptr(da), N.ptr(sa), N.ptr(sz), sa.size, None), "transfer_ranges")
-        N.check(N.lib().cf_ctx_sync(ctx))
+        N.check(N.lib().cf_copy_objects(ctx, N.ptr(da), N.ptr(sa), N.ptr(sz), sa.size), "transfer_ranges")
         self.log.append_many(H2D if dst.kind == "device" else D2H, op_kind, sz.astype(np.int64))
 
     # -- marshalling (memory.py:307-345) ----------------------------------------------------
@@ -648,12 +648,13 @@ class Machine:
         aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
         span = int(aligned.sum())
         dev_off = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64)
-        dev_base = self.device.allocate_span(span, dev_off, sizes, zero=False)
+        # the span of this tree's previous (copied-back) naive window is reused: a fresh
+        # 1 GiB-class allocation per window costs more than the copies
+        dev_base = tree.__dict__.pop("_spare_naive_span", 0) or self.device.allocate_span(span, dev_off, sizes, zero=False)
         dev = dev_off + np.uint64(dev_base)
         host = allocs[:, 0].astype(np.uint64)
         ctx = self.ctx.handle
-        N.check(N.lib().cf_memcpy_batch(ctx, N.ptr(dev), N.ptr(host), N.ptr(sizes), m, None),
-                "naive per-object copies")
+        N.check(N.lib().cf_copy_objects(ctx, N.ptr(dev), N.ptr(host), N.ptr(sizes), m), "naive per-object copies")
         amap = AddressMap.from_arrays(host, sizes, dev)
         fields, targets = tree.site_field_target_arrays()
         self._device_fixup(amap, fields, targets)
@@ -663,26 +664,17 @@ class Machine:
         return amap.translate(tree.root_addr), amap
 
     def _device_fixup(self, amap: "AddressMap", fields: np.ndarray, targets: np.ndarray) -> None:
-        hb, sz, db = amap.arrays()
-        ctx = self.ctx.handle
-        n = len(fields)
-        if n == 0:
+        hb, sz, db = (np.ascontiguousarray(x, np.uint64) for x in amap.arrays())
+        fields = np.ascontiguousarray(fields, np.uint64)
+        targets = np.ascontiguousarray(targets, np.uint64)
+        if len(fields) == 0:
             return
-        blob = np.concatenate([fields, targets, hb, sz, db, np.array([N.NO_BAD], np.uint64)]).astype(np.uint64)
-        dptr = C.c_void_p()
-        N.check(N.lib().cf_dev_alloc(ctx, blob.nbytes, C.byref(dptr)))
-        try:
-            N.check(N.lib().cf_memcpy(ctx, dptr.value, N.ptr(blob), blob.nbytes))
-            base = dptr.value
-            k = len(hb)
-            N.check(N.lib().cf_naive_fixup(ctx, base, base + 8 * n, n, base + 16 * n, base + 16 * n + 8 * k,
-                                           base + 16 * n + 16 * k, k, base + 16 * n + 24 * k, None))
-            bad = np.zeros(1, np.uint64)
-            N.check(N.lib().cf_memcpy(ctx, N.ptr(bad), base + 16 * n + 24 * k, 8))
-        finally:
-            N.lib().cf_dev_free(ctx, dptr.value)
-        if int(bad[0]) != N.NO_BAD:
-            raise WildAccess(f"fixup target 0x{int(targets[int(bad[0])]):x} was never copied to the device")
+        bad = N.U64(0)
+        rc = N.lib().cf_naive_fixup_host(self.ctx.handle, N.ptr(fields), N.ptr(targets), len(fields), N.ptr(hb),
+                                         N.ptr(sz), N.ptr(db), len(hb), C.byref(bad))
+        if rc == N.CF_E_WILD:
+            raise WildAccess(f"fixup target 0x{int(targets[bad.value]):x} was never copied to the device")
+        N.check(rc, "naive fixup")
 
     def naive_copy_back(self, tree, amap: "AddressMap") -> None:
         """Per-object copy back (one batched submission) plus host-side pointer restore."""
@@ -691,11 +683,12 @@ class Machine:
         host = allocs[:, 0].astype(np.uint64)
         sizes = allocs[:, 1].astype(np.uint64)
         dev = amap.translate_many(host)
-        N.check(N.lib().cf_memcpy_batch(self.ctx.handle, N.ptr(host), N.ptr(dev), N.ptr(sizes),
-                                        len(host), None), "naive copy back")
-        N.check(N.lib().cf_ctx_sync(self.ctx.handle))
+        N.check(N.lib().cf_copy_objects(self.ctx.handle, N.ptr(host), N.ptr(dev), N.ptr(sizes), len(host)),
+                "naive copy back")
         fields, targets = tree.site_field_target_arrays()
         _poke_words(fields, targets)
+        if getattr(self, "_naive_span", None) and int(dev[0]) == self._naive_span[0]:
+            tree.__dict__["_spare_naive_span"] = self._naive_span[0]
         self.log.append_many(D2H, "per_object", sizes.astype(np.int64))
         self.log.append_many(D2H, "detach", np.full(len(fields), 8, np.int64))
 

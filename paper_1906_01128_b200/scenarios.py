@@ -220,7 +220,13 @@ class TreeHandle:
         return [a for a in self.arrays if a.level == level]
 
     def target_indices(self, policy: str = "ref") -> np.ndarray:
-        return self.plan.targets(TARGET_POLICIES[policy])
+        """Array indices the kernel targets (cached per policy: the tree shape is immutable)."""
+        cache = self.__dict__.setdefault("_targets", {})
+        t = cache.get(policy)
+        if t is None:
+            t = cache[policy] = self.plan.targets(TARGET_POLICIES[policy])
+            t.setflags(write=False)
+        return t
 
     def chain_shape(self) -> N.CfChainShape:
         return self.plan.chain_shape()

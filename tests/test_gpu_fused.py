@@ -175,3 +175,48 @@ def test_execute_case_fused_and_eager_agree(cf):
         assert a.gpu_launches > 0
         ma.close()
         mb.close()
+
+
+def _pc_window(cf, spec, fused, seed=3, scale=2.0, policy="ref", align=None):
+    m = cf.Machine()
+    h = cf.build_tree(m, spec, seed=seed, align=align)
+    mark = m.log.mark()
+    prep = cf.transfer_to_device(m, h, "pointerchain", policy=policy, fused=fused)
+    st = cf.kernel_scale(m, h, prep, scale)
+    cf.copy_back(m, h, prep)
+    arrays = [m.host.read_bytes(a.addr, a.count * spec.elem) for a in h.arrays]
+    log = [(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)]
+    cf.verify_tree(m, h, scale, policy)
+    m.close()
+    return arrays, log, st.elements_touched
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+def test_fused_pointerchain_equals_eager(cf, elem):
+    """Selective copies pipelined (DMA for big arrays, zero-copy SM copies for small ones)."""
+    rng = random.Random(5 + elem)
+    specs = [cf.DenseSpec(100, 256, 2, elem=elem), cf.DenseSpec(3, 20001, 2, elem=elem),
+             cf.LinearSpec(5, 1000, "LLinit_LLused", elem=elem), cf.DenseSpec(4, 1 << 16, 3, elem=elem, leaf_only=True)]
+    for spec in specs + [cf.DenseSpec(rng.randint(1, 6), rng.randint(0, 40000), rng.randint(0, 3), elem=elem)
+                         for _ in range(6)]:
+        for policy in ("ref", "all_arrays"):
+            for align in (None, 1):
+                a, la, sa = _pc_window(cf, spec, True, policy=policy, align=align)
+                b, lb, sb = _pc_window(cf, spec, False, policy=policy, align=align)
+                assert a == b and la == lb and sa == sb, (spec, policy, align)
+
+
+def test_fused_pointerchain_flush_and_repeat(cf):
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.DenseSpec(10, 300, 2), seed=2)
+    for r in range(3):   # repeated windows reuse the device span and the plan
+        prep = cf.transfer_to_device(m, h, "pointerchain", policy="all_leaves")
+        cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5)
+        cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    prep = cf.transfer_to_device(m, h, "pointerchain", policy="all_leaves")
+    d0 = int(prep.buf_dev[0])
+    assert m.device.read_f64(d0) == m.host.read_f64(int(prep.buf_host[0]))   # flushed H2D
+    cf.kernel_scale(m, h, prep, 0.5)
+    cf.copy_back(m, h, prep)
+    m.close()

@@ -240,6 +240,9 @@ int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_by
  * or mapped pinned memory) are copied by one zero-copy kernel, one warp per object; the rest
  * by the copy engines (cudaMemcpyBatchAsync).  Synchronous. */
 int cf_copy_objects(cf_ctx* ctx, void* const* dsts, const void* const* srcs, const uint64_t* sizes, uint64_t count);
+/* Diagnostics: the first leaf-kernel address fault caught by the bounds check (flag, target,
+ * address, count, image, image bytes, level, ordinal); reset != 0 clears it. */
+int cf_debug_info(cf_ctx* ctx, uint64_t* out8, int reset);
 /* naive_deep_copy fixups (memory.py:349-365): per-object copies are issued by the caller with
  * cf_memcpy_batch; this kernel rewrites every site through a sorted interval map
  * (AddressMap.translate, memory.py:409-419) on the device. */

@@ -46,7 +46,7 @@ EXPORTED = (
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
-    "cf_copy_objects", "cf_naive_fixup_host",
+    "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -139,6 +139,7 @@ def _declare(L):
         "cf_selective_run": (C.c_int, [P, C.c_uint32, C.c_double]),
         "cf_selective_free": (C.c_int, [P]),
         "cf_copy_objects": (C.c_int, [P, P, P, P, U64]),
+        "cf_debug_info": (C.c_int, [P, P, C.c_int]),
         "cf_naive_fixup_host": (C.c_int, [P, P, P, U64, P, P, P, U64, C.POINTER(U64)]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),

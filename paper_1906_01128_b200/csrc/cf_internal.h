@@ -38,6 +38,7 @@ void clear_error();
   } while (0)
 
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
+int debug_info(uint64_t* out, int reset);
 int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, const uint64_t* bytes, uint64_t n,
                      cudaStream_t s);
 int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, const uint64_t* tile_lo, uint64_t nranges,

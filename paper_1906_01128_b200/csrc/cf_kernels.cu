@@ -262,6 +262,10 @@ template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
 template <> __device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
 template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
 
+// First leaf-kernel address fault seen (flag, target, address, count, image, bytes, level,
+// ordinal) -- read by cf_debug_info for diagnosis.
+__device__ uint64_t g_dbg[8];
+
 struct ScaleArgs {
   const uint8_t* image;
   cf_chain_shape sh;
@@ -287,7 +291,21 @@ __device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uin
     arr = reinterpret_cast<uint8_t*>(a.ea[t]);
     cnt = a.count[t];
   }
-  return arr != nullptr;
+  if (arr == nullptr) return false;
+  // never stream through an address outside the image (a corrupted chain reports, not faults)
+  if (a.image && (arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes)) {
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(&g_dbg[0]), 0ull, 1ull) == 0ull) {
+      g_dbg[1] = t;
+      g_dbg[2] = reinterpret_cast<uint64_t>(arr);
+      g_dbg[3] = cnt;
+      g_dbg[4] = reinterpret_cast<uint64_t>(a.image);
+      g_dbg[5] = a.sh.image_bytes;
+      g_dbg[6] = a.level ? uint64_t(a.level[t]) : ~0ull;
+      g_dbg[7] = a.ordinal ? uint64_t(a.ordinal[t]) : ~0ull;
+    }
+    return false;
+  }
+  return true;
 }
 
 // Re-derive the array address through the chain (CHASE: one walk per 16-byte access).
@@ -877,6 +895,15 @@ int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, co
   if (ntiles == 0) return CF_OK;
   k_checksum<<<unsigned(ntiles), 256, 0, s>>>(addr, words, tile_lo, nranges, reinterpret_cast<unsigned long long*>(out));
   CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int debug_info(uint64_t* out, int reset) {
+  CF_CUDA(cudaMemcpyFromSymbol(out, g_dbg, sizeof(uint64_t) * 8));
+  if (reset) {
+    static const uint64_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CF_CUDA(cudaMemcpyToSymbol(g_dbg, z, sizeof z));
+  }
   return CF_OK;
 }
 

@@ -405,6 +405,12 @@ int cf_copy_objects(cf_ctx* c, void* const* dsts, const void* const* srcs, const
   return CF_OK;
 }
 
+int cf_debug_info(cf_ctx* c, uint64_t* out8, int reset) {
+  if (!c || !out8) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  return debug_info(out8, reset);
+}
+
 int cf_naive_fixup_host(cf_ctx* c, const uint64_t* h_field_host, const uint64_t* h_target_host, uint64_t nsites,
                         const uint64_t* h_map_host_base, const uint64_t* h_map_size, const uint64_t* h_map_dev_base,
                         uint64_t nmap, uint64_t* bad_site) {

@@ -67,7 +67,11 @@ struct cf_window {
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
   bool has_roots = false;
-  bool aligned8 = false;   // every pointer field 8-byte aligned (align >= 8): attach || resolve safe
+  // every pointer field 8-byte aligned: a field read while the attach rewrites it is then one
+  // single-copy-atomic 64-bit access, so attach || resolve in one launch is safe.  Not implied
+  // by an aligned arena: 12-byte dense leaf records put every other leaf's A field at 4 mod 8
+  // (2 x u32 accesses, which a concurrent attach can tear).
+  bool aligned8 = false;
   // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
   struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
   std::vector<Graph> graphs;
@@ -437,7 +441,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
-  w->aligned8 = t->spec.align >= 8;
+  w->aligned8 = std::all_of(sites, sites + nsites, [](uint64_t o) { return (o & 7) == 0; });
   w->off_sites = 0;
   w->off_det = al8(w->off_sites + nsites * 8);
   w->off_level = al8(w->off_det + nsites * 4);

@@ -82,3 +82,37 @@ def test_compute_sanitizer_memcheck(cf, tmp_path):
     assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
     assert "sanitized ok" in out.stdout
     assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr
+
+
+def test_many_small_chains_repeated_windows_stay_exact(cf):
+    """1M chains with 12-byte leaf records (A fields at 4 mod 8 even in the aligned arena): many
+    back-to-back resident and full windows (fused detach, graph replay) must never tear a
+    pointer field.  Scales alternate 2.0 / 0.5, so after an even number of windows the image and
+    the copy-back equal the source arena byte for byte."""
+    from paper_1906_01128_b200 import _native as N
+    w = cf.DeepCopyWindow(cf.DenseSpec(100, 16, 3, elem=4), seed=3, policy="all_leaves", align=16)
+    try:
+        src = w.host_src().copy()
+        w.upload_raw()
+        for flags in (N.CF_WIN_RESIDENT, N.CF_WIN_RESIDENT | N.CF_WIN_GRAPH):
+            for _ in range(20):
+                st = w.run_n(10, flags=flags)
+                assert st.bad == (1 << 64) - 1
+        assert np.array_equal(w.image_bytes(), src)
+        for _ in range(5):
+            st = w.run_n(4, flags=N.CF_WIN_FULL | N.CF_WIN_GRAPH)
+            assert st.bad == (1 << 64) - 1
+        st = w.run(scale=2.0)
+        assert st.bad == (1 << 64) - 1
+        got = w.host_dst()
+        arr = w.table(N.CF_TAB_ARR_OFF)
+        lv = w.table(N.CF_TAB_ARR_LEVEL)
+        mask = np.ones(len(src), bool)
+        for i in w.targets.tolist():
+            mask[int(arr[i]):int(arr[i]) + 64] = False
+        assert np.array_equal(got[mask], src[mask])      # pointers restored, untargeted unchanged
+        i = int(w.targets[-1])
+        want = (cf.payload_values(3, int(lv[i]), 16, 4) * np.float32(2.0)).astype(np.float32)
+        assert np.array_equal(got[int(arr[i]):int(arr[i]) + 64].view(np.float32), want)
+    finally:
+        w.close()

@@ -304,17 +304,25 @@ def verify_gather(w, shard, spec, dist: Dist, device: int, ndev: int, src_factor
     # weak: (rank, position) -- every rank owns a whole tree; strong: the global leaf ordinal
     keys = (np.arange(len(tg), dtype=np.int64) + np.int64(dist.rank) * (1 << 32)) if shard.scaling == "weak" \
         else od[tg].astype(np.int64)
-    pg, dev, backend = None, None, "local"
+    pg, dev, backend, err = None, None, "local", None
     if dist.world > 1:
         import torch
         import torch.distributed as tdist
         backend = "gloo"
         if ndev >= dist.world:   # one GPU per rank: the gather runs over NCCL (NVLink / NVSwitch)
-            torch.cuda.set_device(device)
-            pg, dev, backend = tdist.new_group(backend="nccl"), torch.device("cuda", device), "nccl"
-    o, v = gather_checksums(keys, sums, pg, dev)
+            try:
+                torch.cuda.set_device(device)
+                pg, dev, backend = tdist.new_group(backend="nccl"), torch.device("cuda", device), "nccl"
+                o, v = gather_checksums(keys, sums, pg, dev)
+            except Exception as exc:   # keep the bench line; fall back to the gloo group
+                err = f"{type(exc).__name__}: {exc}"[:200]
+                pg, dev, backend = None, None, "gloo"
+    if backend != "nccl":
+        o, v = gather_checksums(keys, sums, pg, dev)
     out = {"backend": backend, "leaves": int(len(o)), "what": "per-leaf u32-word checksums after a "
            "verification window (scale 2.0), gathered to all ranks"}
+    if err:
+        out["nccl_error"] = err
     if dist.rank == 0:
         f = 2.0 * src_factor
         ok = True

@@ -156,14 +156,20 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "B200_PROFILING.md fallback"}
 
 
-def ncu_traffic(config: str):
+def ncu_record(config: str) -> dict:
+    """k_scale's `ncu --set full` numbers for this config (profiles/ncu_traffic.json), if captured."""
     p = REPO / "profiles" / "ncu_traffic.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        e = d.get(config, {}).get("k_scale")
-        if e:
-            return e.get("dram_bytes_per_launch")
-    return None
+        return json.loads(p.read_text()).get(config, {}).get("k_scale") or {}
+    return {}
+
+
+def ncu_traffic(config: str):
+    return ncu_record(config).get("dram_bytes_per_launch")
+
+
+# nominal B200 HBM3e bandwidth (vendor figure), reported beside the measured-copy roofline
+NOMINAL_HBM_GBS = 8000.0
 
 
 # ------------------------------------------------------------------------------ CPU legs
@@ -469,6 +475,8 @@ def run_ours(args, dist: Dist) -> None:
         "roofline": {"bound": "hbm", "kernel": "k_scale<float,resolved>", "achieved": round(achieved, 1),
                      "peak": peaks["hbm_gbs"], "peak_source": peaks["source"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(args.config),
+                     "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
+                     "ncu_dram_pct_of_peak": ncu_record(args.config).get("dram_pct_of_ncu_peak"),
                      "algorithmic_bytes_per_launch": kernel_traffic, "kernel_ms": round(kernel_ms, 4),
                      "share_of_resident_step": round(kernel_ms / res_ms, 4)},
         "modes": {"resolved": {"kernel_ms": round(kernel_ms, 4), "hbm_gbs": round(achieved, 1)}, "chase": chase},

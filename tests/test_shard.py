@@ -98,3 +98,28 @@ def test_sharded_tree_through_the_drop_in_api():
         cf.copy_back(m, h, prep)
         cf.verify_tree(m, h, 2.0, policy="all_arrays")
         m.close()
+
+
+@pytest.mark.gpu
+def test_gather_over_nccl_single_rank(tmp_path):
+    """The result gather's NCCL path (CUDA tensors) on a one-rank group: the only multi-GPU
+    collective of the benchmark, exercised on the one GPU a gpurun box has."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_1906_01128_b200.shard import gather_checksums
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU visible")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        o = np.array([5, 1, 3], np.int64)
+        v = np.array([2 ** 64 - 1, 7, 2 ** 63], np.uint64)
+        go, gv = gather_checksums(o, v, None, torch.device("cuda", 0))
+        assert go.tolist() == [1, 3, 5] and gv.tolist() == [7, 2 ** 63, 2 ** 64 - 1]
+    finally:
+        dist.destroy_process_group()

@@ -55,11 +55,13 @@ def main():
                          f"{d.get('dram_pct_peak', 0):.1f} | {d.get('sm_pct', 0):.1f} | {d.get('occupancy_pct', 0):.1f} |")
             if d["kernel"].startswith("k_scale"):
                 traffic.setdefault("k_scale", int(d.get("dram_read", 0) + d.get("dram_write", 0)))
+                traffic.setdefault("dram_pct", round(float(d.get("dram_pct_peak", 0)), 1))
     Path(a.out).write_text("\n".join(lines) + "\n")
     tj = Path("profiles/ncu_traffic.json")
     data = json.loads(tj.read_text()) if tj.exists() else {}
     if traffic:
         data.setdefault(a.config, {})["k_scale"] = {"dram_bytes_per_launch": traffic["k_scale"],
+                                                    "dram_pct_of_ncu_peak": traffic["dram_pct"],
                                                     "source": str(Path(a.out).name)}
         tj.write_text(json.dumps(data, indent=1) + "\n")
     print("\n".join(lines))

@@ -16,6 +16,7 @@ from .memory import (AddressMap, Arena, Machine, MemorySpace, TransferEntry, Tra
 from .scenarios import (ArrayRef, DenseSpec, ForestSpec, LinearSpec, TreeHandle, build_dense_tree,
                         build_linear_tree, build_tree, dense_data_size, linear_data_size,
                         marshal_tree, payload_values, targeted_arrays, tree_total_bytes)
+from .report import MissingBaseline, ResultRow, normalize, rows_from_csv, rows_to_csv
 from .engine import DeepCopyWindow
 
 __version__ = "0.1.0"

@@ -13,41 +13,17 @@ from __future__ import annotations
 
 import argparse
 import sys
-from dataclasses import fields
 from pathlib import Path
 
 from .harness import SCHEMES, CostModel, RunMetrics, execute_case, run_case, sweep
+from .report import CSV_HEADER, MissingBaseline, ResultRow, normalize, rows_from_csv  # noqa: F401
+from .report import rows_to_csv as _rows_to_csv
 from .scenarios import LAYOUTS, DenseSpec, LinearSpec
 
-CSV_HEADER = ("scenario,scheme,layout,k_or_q,n,bytes_h2d,bytes_d2h,transfer_ops,attach_ops,page_faults,"
-              "instr_estimate,sim_kernel_us,sim_wall_us,iterations,verified,normalized_wall,normalized_kernel")
-MEASURED = ("wall_us", "mode", "gpu_launches")
 
-
-def _fmt(v) -> str:
-    if v is None:
-        return ""
-    if isinstance(v, bool):
-        return "true" if v else "false"
-    if isinstance(v, float):
-        return repr(v)
-    return str(v)
-
-
-def rows_to_csv(rows: list[RunMetrics], measured: bool = False) -> str:
-    """Reference CSV rows, normalised against the UVM cell of the same (scenario, layout, k_or_q, n)."""
-    base = {(r.scenario, r.layout, r.k_or_q, r.n): r for r in rows if r.scheme == "uvm"}
-    cols = [f.name for f in fields(RunMetrics) if f.name not in MEASURED]
-    lines = [CSV_HEADER + ("," + ",".join(MEASURED) if measured else "")]
-    for r in rows:
-        b = base.get((r.scenario, r.layout, r.k_or_q, r.n))
-        nw = r.sim_wall_us / b.sim_wall_us if b else None
-        nk = r.sim_kernel_us / b.sim_kernel_us if b and b.sim_kernel_us else None
-        vals = [_fmt(getattr(r, c)) for c in cols] + [_fmt(nw), _fmt(nk)]
-        if measured:
-            vals += [_fmt(getattr(r, c)) for c in MEASURED]
-        lines.append(",".join(vals))
-    return "\n".join(lines) + "\n"
+def rows_to_csv(metrics: list[RunMetrics], measured: bool = False) -> str:
+    """Reference CSV rows (report.py:117-122), UVM-normalised where the cell has a UVM row."""
+    return _rows_to_csv(normalize([ResultRow.from_metrics(m) for m in metrics], strict=False), measured)
 
 
 def _spec(scenario: str, k_or_q: int, n: int, layout: str, depth: int, elem: int):
@@ -95,12 +71,16 @@ def _parser() -> argparse.ArgumentParser:
     w.add_argument("--min-iters", type=int, default=3)
     w.add_argument("--elem", type=int, choices=(4, 8), default=8)
     w.add_argument("--measured", action="store_true")
+    r = sub.add_parser("report", help="re-emit (and optionally UVM-normalise) a results CSV")
+    r.add_argument("infile")
+    r.add_argument("--normalize", action="store_true")
+    r.add_argument("--out")
     return p
 
 
 def main(argv=None) -> int:
     args = _parser().parse_args(argv)
-    cm = CostModel.from_file(args.config) if args.config else CostModel()
+    cm = CostModel.from_file(args.config) if getattr(args, "config", None) else CostModel()
     if args.command == "simulate":
         k_or_q = args.k if args.scenario == "linear" else args.q
         if k_or_q is None:
@@ -113,6 +93,20 @@ def main(argv=None) -> int:
             _, machine = execute_case(spec, args.scheme, cm, seed=args.seed, mode=args.mode, policy=args.policy)
             Path(args.dump_log).write_text(machine.log.dump() + "\n")
             machine.close()
+        return 0
+    if args.command == "report":   # cli.py _cmd_report, CSV format (tables are presentation)
+        rows = rows_from_csv(Path(args.infile).read_text())
+        if args.normalize:
+            try:
+                rows = normalize(rows, strict=True)
+            except MissingBaseline as exc:
+                print(f"error: {exc}", file=sys.stderr)
+                return 1
+        text = _rows_to_csv(rows, measured=bool(rows and rows[0].extra))
+        if args.out:
+            Path(args.out).write_text(text)
+        else:
+            sys.stdout.write(text)
         return 0
     rows = sweep(_parse_grid(args.grid, args.elem), cm, seed=args.seed, min_iters=args.min_iters)
     Path(args.out).write_text(rows_to_csv(rows, args.measured))

@@ -68,6 +68,34 @@ def test_fused_equals_eager_random_specs(cf, elem):
         assert _norm(cf, a, spec, ba, 3, align) == _norm(cf, b, spec, bb, 3, align), (spec, policy, mode, align)
 
 
+def test_fused_scattered_forest_in_place(cf):
+    """Scattered forests (C3 shape, small): node pages hoisted and moved by zero-copy kernels,
+    copy-back in place into the source arena -- fused == eager byte for byte."""
+    for elem in (4, 8):
+        spec = cf.ForestSpec(cf.LinearSpec(4, 40000, "LLinit_LLused", elem=elem), 24, scatter_seed=7)
+        outs = []
+        for fused in (True, False):
+            m = cf.Machine()
+            arena, h = cf.marshal_tree(m, spec, seed=2, align=16)
+            prep = cf.transfer_to_device(m, h, "marshalling", arena, policy="all_leaves", fused=fused)
+            cf.kernel_scale(m, h, prep, 2.0)
+            cf.copy_back(m, h, prep)
+            cf.verify_tree(m, h, 2.0, "all_leaves")
+            raw = m.host.read_bytes(arena.buffer_host_addr, arena.total_bytes)
+            outs.append(_norm_sites(raw, h, arena.buffer_host_addr))
+            m.close()
+        assert outs[0] == outs[1]
+
+
+def _norm_sites(raw, h, base):
+    import numpy as np
+    a = np.frombuffer(raw, np.uint8).copy()
+    for f in h.site_off.tolist():
+        v = int.from_bytes(a[f:f + 8].tobytes(), "little") - base
+        a[f:f + 8] = np.frombuffer(v.to_bytes(8, "little"), np.uint8)
+    return a.tobytes()
+
+
 def test_fused_window_multi_chunk_matches_oracle(cf, oracle):
     """An arena spanning many 16 MiB chunks (C2 shape, small) through the drop-in calls."""
     spec = cf.DenseSpec(4, 1 << 20, 3, elem=4, leaf_only=True)

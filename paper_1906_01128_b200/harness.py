@@ -437,15 +437,18 @@ def _pages_of_spans(starts: np.ndarray, counts: np.ndarray, e: int, page: int) -
 
 
 def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int):
-    """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394),
-    as sorted numpy arrays.  Used for the logical page-fault counters; the data itself migrates
-    under the CUDA driver.  Chains are walked level by level for all targets at once."""
+    """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394):
+    the sorted distinct pages of the chain fields it reads, and the inclusive page ranges of the
+    arrays it scales (read, then written).  Used for the logical page-fault counters; the data
+    itself migrates under the CUDA driver.  Chains are walked level by level for all targets at
+    once; array pages stay ranges (a 1 GiB tree is 262,144 pages)."""
     spec = handle.spec
     base, e = handle.base, spec.elem
     forest = isinstance(spec, ForestSpec)
     tree = spec.tree if forest else spec
     linear = isinstance(tree, LinearSpec)
     view = N.host_view(base, handle.total_bytes)
+    arr = None
 
     def rd(offs: np.ndarray) -> np.ndarray:   # 8-byte pointer fields -> arena offsets
         ix = offs.astype(np.int64)[:, None] + np.arange(8, dtype=np.int64)[None, :]
@@ -472,8 +475,10 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
         q = 1 if linear else tree.q
         for lv in range(1, int(L.max()) + 1 if L.size else 1):
             act = L >= lv
-            fields.append(node[act] + OFF_LNEXT)
-            blk = rd(node[act] + OFF_LNEXT)
+            # many chains share their upper nodes: read each distinct Lnext field once
+            un, inv = np.unique(node[act], return_inverse=True)
+            fields.append(un + OFF_LNEXT)
+            blk = rd(un + OFF_LNEXT)[inv]
             if linear:
                 node[act] = blk
             else:
@@ -483,20 +488,25 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
         leaf = (~np.asarray(linear)) & (L == depth) if not linear else np.zeros(L.shape, bool)
         fields.append(node + np.where(leaf, LEAF_OFF_A, OFF_A))
         t_nodes = node
-    # terminal nodes with an array also read their count
+        arr, has = np.asarray(sel, np.int64), np.ones(len(sel), bool)   # each walk ends at its array's owner
+    if arr is None:
+        # terminal nodes with an array (the fixed reference paths above): find it by owner
+        t_nodes = np.asarray(t_nodes, np.int64)
+        owner_sorted = np.argsort(handle.arr_owner, kind="stable")
+        pos = np.searchsorted(handle.arr_owner[owner_sorted], t_nodes.astype(np.uint64))
+        pos = np.minimum(pos, max(len(owner_sorted) - 1, 0))
+        has = (len(owner_sorted) > 0) & (handle.arr_owner[owner_sorted][pos] == t_nodes.astype(np.uint64)) \
+            if len(owner_sorted) else np.zeros(t_nodes.shape, bool)
+        arr = owner_sorted[pos][has] if len(owner_sorted) else np.zeros(0, np.int64)
     t_nodes = np.asarray(t_nodes, np.int64)
-    owner_sorted = np.argsort(handle.arr_owner, kind="stable")
-    pos = np.searchsorted(handle.arr_owner[owner_sorted], t_nodes.astype(np.uint64))
-    pos = np.minimum(pos, max(len(owner_sorted) - 1, 0))
-    has = (len(owner_sorted) > 0) & (handle.arr_owner[owner_sorted][pos] == t_nodes.astype(np.uint64)) \
-        if len(owner_sorted) else np.zeros(t_nodes.shape, bool)
-    arr = owner_sorted[pos][has] if len(owner_sorted) else np.zeros(0, np.int64)
     cnt = handle.arr_count[arr].astype(np.int64)
+    # the walk also reads the count of every terminal node that owns a non-empty array
     fields.append(t_nodes[has][cnt > 0] + OFF_NA)
-    dirty = _pages_of_spans(handle.arr_off[arr].astype(np.int64) + base, cnt, e, page)
+    keep = cnt > 0
+    starts = handle.arr_off[arr].astype(np.int64)[keep] + base
+    dirty = (starts // page, (starts + e * (cnt[keep] - 1)) // page)   # page ranges, inclusive
     f = np.concatenate([np.asarray(x, np.int64) for x in fields]) if fields else np.zeros(0, np.int64)
-    touched = np.union1d((f + base) // page, dirty)
-    return touched, dirty
+    return np.unique((f + base) // page), dirty
 
 
 def _merged_ranges(handle: TreeHandle, idx: np.ndarray, gap: int) -> list:
@@ -559,10 +569,13 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     idx = idx[handle.arr_count[idx] > 0]
     stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
     if prep.scheme == "uvm":
-        touched, dirty = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
-        machine.uvm_touch_pages(touched, "read", "device")
-        if dirty.size:
-            machine.uvm_touch_pages(dirty, "write", "device")
+        fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
+        # every page read once (fields, then array pages -- a page met twice migrates once), then
+        # the array pages written (dirty)
+        machine.uvm_touch_pages(fields, "read", "device")
+        if dlo.size:
+            machine.uvm_touch_ranges(dlo, dhi, "read", "device")
+            machine.uvm_touch_ranges(dlo, dhi, "write", "device")
     if len(idx) == 0:
         return stats
     sh = handle.chain_shape()
@@ -620,8 +633,7 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
         for lo, hi in _merged_ranges(handle, handle.target_indices(prep.policy), machine.uvm.page_size):
             N.check(N.lib().cf_uvm_prefetch(ctx, handle.base + lo, hi - lo, -1, None))
         machine.ctx.sync()
-        dirty = machine.uvm.dirty_pages()
-        machine.uvm_touch_pages(dirty, "read", "host")
+        machine.uvm_touch_mask(machine.uvm._dirty.copy(), "read", "host")
 
 
 def verify_tree(machine: Machine, handle: TreeHandle, scale: float, policy: str = "ref") -> None:

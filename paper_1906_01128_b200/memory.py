@@ -702,6 +702,27 @@ class Machine:
             raise WildAccess(f"unified access at 0x{addr:x} hits no registered page")
         return self._touch(np.array([i]), access, actor)
 
+    def uvm_touch_ranges(self, lo_pages, hi_pages, access: str, actor: str) -> int:
+        """Touch every page of the inclusive page ranges [lo, hi] (each page once)."""
+        if self.uvm is None:
+            raise SimMemoryError("uvm_touch outside UVM mode")
+        u = self.uvm
+        lo = np.asarray(lo_pages, np.int64)
+        hi = np.asarray(hi_pages, np.int64)
+        a = np.searchsorted(u._pages, lo, side="left")
+        b = np.searchsorted(u._pages, hi, side="right")
+        if ((b - a) != (hi - lo + 1)).any():   # some page of a range was never registered
+            raise WildAccess("unified access hits no registered page")
+        n = u._pages.size + 1   # coverage mask by a difference array
+        d = np.bincount(a, minlength=n) - np.bincount(b, minlength=n)
+        return self.uvm_touch_mask(np.cumsum(d[:-1]) > 0, access, actor)
+
+    def uvm_touch_mask(self, mask: np.ndarray, access: str, actor: str) -> int:
+        """Touch the registered pages selected by a boolean mask over the page table."""
+        if self.uvm is None:
+            raise SimMemoryError("uvm_touch outside UVM mode")
+        return self._touch(np.nonzero(mask)[0], access, actor)
+
     def uvm_touch_pages(self, pages, access: str, actor: str) -> int:
         """Vectorised uvm_touch over a set of page numbers (one touch per page)."""
         if self.uvm is None:

@@ -408,8 +408,10 @@ def run_ours(args, dist: Dist) -> None:
     scaling = "strong" if args.config == "C5" else "weak"
     shard = shard_for(spec, dist.rank, dist.world, scaling)
     spec = shard.spec
+    # pinned arenas next to this GPU's host link (multi-socket boxes)
+    numa_node = Nn.gpu_numa_node(device) if ndev else -1
     t_build = time.perf_counter()
-    w = DeepCopyWindow(spec, seed=shard.seed, policy=policy, mode="resolved", align=16,
+    w = DeepCopyWindow(spec, seed=shard.seed, policy=policy, mode="resolved", align=16, numa_node=numa_node,
                        chunk_bytes=args.chunk_mb << 20, device=device,
                        separate_output=spec.n * spec.elem * 64 <= (16 << 30))
     t_build = time.perf_counter() - t_build
@@ -533,6 +535,7 @@ def run_ours(args, dist: Dist) -> None:
                      "share_of_resident_step": round(kernel_ms / res_ms, 4)},
         "modes": {"resolved": {"kernel_ms": round(kernel_ms, 4), "hbm_gbs": round(achieved, 1)}, "chase": chase},
         "gpu_launches": int(st_res.launches),
+        "numa": {"gpu_node": numa_node, "host_arenas": "allocated on the GPU's node" if numa_node >= 0 else "OS placement"},
         "gather": gather,
         "clocks": clk,
         "build_s": round(t_build, 2),

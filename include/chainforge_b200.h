@@ -123,6 +123,12 @@ int cf_abi_version(void);
 const char* cf_last_error(void);
 int cf_device_count(int* count);
 /* nstreams: H2D copy streams (>= 1); a compute and a D2H stream are added. */
+/* NUMA placement of host arenas (no libnuma in the image): the node of the GPU's
+ * PCI device (-1 if unknown), and binding the calling thread's CPUs + preferred memory to a node
+ * so pinned arenas it allocates are local to that GPU's host link; node < 0 restores the default
+ * memory policy (the caller restores its CPU mask). */
+int cf_device_numa_node(int device, int* node);
+int cf_bind_numa_node(int node);
 int cf_ctx_create(int device, int nstreams, cf_ctx** out);
 int cf_ctx_destroy(cf_ctx* ctx);
 int cf_ctx_sync(cf_ctx* ctx);

@@ -6,6 +6,7 @@ The library is built in-tree (``make`` or ``__graft_entry__.build()``) into
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from pathlib import Path
@@ -46,7 +47,7 @@ EXPORTED = (
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
-    "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info",
+    "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -140,6 +141,8 @@ def _declare(L):
         "cf_selective_free": (C.c_int, [P]),
         "cf_copy_objects": (C.c_int, [P, P, P, P, U64]),
         "cf_debug_info": (C.c_int, [P, P, C.c_int]),
+        "cf_device_numa_node": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
+        "cf_bind_numa_node": (C.c_int, [C.c_int]),
         "cf_naive_fixup_host": (C.c_int, [P, P, P, U64, P, P, P, U64, C.POINTER(U64)]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
@@ -193,6 +196,31 @@ def check(rc: int, what: str = "") -> None:
     if rc == CF_E_NODEVICE:
         raise NativeUnavailable(msg)
     raise RuntimeError(f"CUDA failure ({rc}): {msg}")
+
+
+def gpu_numa_node(device: int) -> int:
+    """NUMA node of the GPU's PCI device (-1: unknown / single node)."""
+    node = C.c_int(-1)
+    if lib().cf_device_numa_node(device, C.byref(node)) != CF_OK:
+        return -1
+    return node.value
+
+
+@contextlib.contextmanager
+def numa_bound(node: int | None):
+    """Within the block, this thread runs on ``node``'s CPUs and prefers its memory, so pinned
+    host memory allocated here is local to that GPU's host link.  Restores the CPU mask and the
+    default policy afterwards (OpenMP pools created later are not confined to the node)."""
+    if node is None or node < 0:
+        yield
+        return
+    saved = os.sched_getaffinity(0)
+    check(lib().cf_bind_numa_node(node), "cf_bind_numa_node")
+    try:
+        yield
+    finally:
+        lib().cf_bind_numa_node(-1)
+        os.sched_setaffinity(0, saved)
 
 
 def device_count() -> int:

@@ -3,7 +3,15 @@
 // real pinned host memory, HBM and CUDA streams.
 #include "cf_internal.h"
 
+#include <sched.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <fstream>
+#include <sstream>
+#include <string>
 
 #include <cstdarg>
 #include <cstdio>
@@ -44,6 +52,57 @@ int cf_device_count(int* count) {
     return CF_OK;
   }
   *count = n;
+  return CF_OK;
+}
+
+int cf_device_numa_node(int device, int* node) {
+  if (!node) return fail(CF_E_INVALID, "null node");
+  *node = -1;
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CF_E_NODEVICE, "no PCI bus id for device %d", device);
+  }
+  std::string id(bus);
+  for (auto& ch : id) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+  // sysfs uses a 4-hex-digit domain; the runtime may print 8
+  if (id.size() > 12 && id.find(':') == 8) id = id.substr(4);
+  std::ifstream f("/sys/bus/pci/devices/" + id + "/numa_node");
+  int n = -1;
+  if (f >> n) *node = n;
+  return CF_OK;
+}
+
+int cf_bind_numa_node(int node) {
+  // Pin the calling thread to the node's CPUs and prefer its memory, so pinned arenas allocated
+  // and first-touched by this thread sit next to the GPU's host link (no libnuma in the image:
+  // sysfs cpulist + raw set_mempolicy).
+  if (node < 0) {   // back to the default memory policy (the caller restores its CPU mask)
+    syscall(SYS_set_mempolicy, 0 /* MPOL_DEFAULT */, nullptr, 0);
+    return CF_OK;
+  }
+  std::ifstream f("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist");
+  std::string list;
+  if (!(f >> list)) return fail(CF_E_INVALID, "no cpulist for NUMA node %d", node);
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  std::stringstream ss(list);
+  std::string part;
+  int ncpu = 0;
+  while (std::getline(ss, part, ',')) {
+    const size_t dash = part.find('-');
+    const int lo = std::stoi(part.substr(0, dash));
+    const int hi = dash == std::string::npos ? lo : std::stoi(part.substr(dash + 1));
+    for (int c = lo; c <= hi && c < CPU_SETSIZE; ++c, ++ncpu) CPU_SET(c, &set);
+  }
+  if (ncpu == 0) return fail(CF_E_INVALID, "empty cpulist for NUMA node %d", node);
+  if (sched_setaffinity(0, sizeof set, &set) != 0) return fail(CF_E_INVALID, "sched_setaffinity failed");
+  unsigned long mask[16] = {0};
+  if (node < int(sizeof mask * 8)) {
+    mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+    constexpr int MPOL_PREFERRED_ = 1;
+    syscall(SYS_set_mempolicy, MPOL_PREFERRED_, mask, sizeof mask * 8);   // best effort
+  }
   return CF_OK;
 }
 

@@ -24,8 +24,9 @@ from .scenarios import TARGET_POLICIES
 class DeepCopyWindow:
     def __init__(self, spec, seed: int = 1, policy: str = "all_leaves", mode: str = "resolved",
                  align: int = 16, chunk_bytes: int = 16 << 20, device: int = 0,
-                 separate_output: bool = True, scale: float = 2.0, nstreams: int = 1):
+                 separate_output: bool = True, scale: float = 2.0, nstreams: int = 1, numa_node: int | None = None):
         self.ctx = N.DeviceContext.get(device, nstreams)
+        self.numa_node = numa_node   # pinned buffers allocated on this NUMA node (None: as the OS places them)
         self.spec = spec
         self.seed = seed
         self.plan = N.NativeTree(spec.native(align))
@@ -33,13 +34,15 @@ class DeepCopyWindow:
         lib = N.lib()
         self._owned: list = []
         src = C.c_void_p()
-        N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(src)), "pinned arena")
+        with N.numa_bound(numa_node):
+            N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(src)), "pinned arena")
         self._owned.append(("host", src.value, self.total))
         self.src = src.value
         self.plan.build(self.src, self.src, seed)
         if separate_output:
             dst = C.c_void_p()
-            N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(dst)), "pinned copy-back buffer")
+            with N.numa_bound(numa_node):
+                N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(dst)), "pinned copy-back buffer")
             self._owned.append(("host", dst.value, self.total))
             self.dst = dst.value
         else:
@@ -62,7 +65,8 @@ class DeepCopyWindow:
         t._owned, t._windows = [], {}
         lib = N.lib()
         dst, img = C.c_void_p(), C.c_void_p()
-        N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(dst)), "pinned copy-back buffer")
+        with N.numa_bound(self.numa_node):
+            N.check(lib.cf_host_alloc(self.total, N.CF_MEM_PINNED, C.byref(dst)), "pinned copy-back buffer")
         t._owned.append(("host", dst.value, self.total))
         N.check(lib.cf_dev_alloc(self.ctx.handle, self.total, C.byref(img)), "device image")
         t._owned.append(("dev", img.value, self.total))

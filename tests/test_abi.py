@@ -130,3 +130,20 @@ def test_sass_chase_mode_keeps_per_access_chain_loads():
         assert rows[(t, "resolved")][3] == 0
         assert rows[(t, "chase")][3] > 0
         assert rows[(t, "resolved")][1] > 0 and rows[(t, "resolved")][2] > 0
+
+
+def test_numa_binding_is_scoped():
+    """numa_bound(node) confines the thread to the node's CPUs only inside the block (pinned arenas
+    are allocated there); the CPU mask is restored afterwards."""
+    import os
+    from pathlib import Path
+    from paper_1906_01128_b200 import _native as N
+    if not Path("/sys/devices/system/node/node0/cpulist").exists():
+        pytest.skip("no NUMA sysfs")
+    before = os.sched_getaffinity(0)
+    with N.numa_bound(0):
+        inside = os.sched_getaffinity(0)
+    assert inside <= before or inside
+    assert os.sched_getaffinity(0) == before
+    with N.numa_bound(-1):
+        assert os.sched_getaffinity(0) == before

@@ -22,7 +22,7 @@ def cf():
     return cf
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C4"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
 def test_full_size_window_matches_oracle(cf, oracle, cfg):
     """The BASELINE config at full size (1 GiB): e2e window copy-back and resident image equal
     the oracle's expected arena byte for byte (relocated pointers restored, leaves x2)."""
@@ -33,10 +33,14 @@ def test_full_size_window_matches_oracle(cf, oracle, cfg):
     try:
         st = w.run(scale=2.0)
         assert st.bad == (1 << 64) - 1
-        ospec = oracle.OSpec(oracle.DENSE, spec.q, spec.n, spec.depth, elem=spec.elem, leaf_only=spec.leaf_only,
-                             align=16)
+        if isinstance(spec, cf.LinearSpec):
+            ospec = oracle.OSpec(oracle.LINEAR, spec.k, spec.n, 0, spec.layout, elem=spec.elem, align=16)
+        else:
+            ospec = oracle.OSpec(oracle.DENSE, spec.q, spec.n, spec.depth, elem=spec.elem, leaf_only=spec.leaf_only,
+                                 align=16)
         ot = oracle.build(ospec, 1, ptr_base=w.src)
-        idx = oracle.targets(ot, oracle.TARGET_ALL_LEAVES)
+        idx = oracle.targets(ot, {"all_leaves": oracle.TARGET_ALL_LEAVES,
+                                  "all_arrays": oracle.TARGET_ALL_ARRAYS}[policy])
         want = oracle.expected_after_window(ot, idx, 2.0)[:w.total]
         assert np.array_equal(w.host_dst(), want)
         assert np.array_equal(w.host_src(), ot.buf[:w.total])   # source untouched
@@ -44,6 +48,34 @@ def test_full_size_window_matches_oracle(cf, oracle, cfg):
         st = w.run_resident(scale=2.0, graph=True)
         assert st.bad == (1 << 64) - 1
         assert np.array_equal(w.image_bytes(), want)
+    finally:
+        w.close()
+
+
+def test_full_size_scattered_forest_c3(cf):
+    """C3 at full size (64 scattered chains, 1 GiB of leaves; the oracle has no scattered forests):
+    after the e2e window every targeted leaf equals payload_values x 2 and every other byte --
+    nodes with their restored pointers, untargeted space -- equals the source arena."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    from paper_1906_01128_b200 import _native as N
+    spec, policy, _ = bench.make_spec("C3")
+    w = cf.DeepCopyWindow(spec, seed=1, policy=policy, align=16)
+    try:
+        st = w.run(scale=2.0)
+        assert st.bad == (1 << 64) - 1
+        src, got = w.host_src(), w.host_dst()
+        off, cnt, lvl = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT), w.table(N.CF_TAB_ARR_LEVEL)
+        mask = np.ones(w.total, bool)
+        want_leaf = None
+        for i in w.targets.tolist():
+            a, nb = int(off[i]), int(cnt[i]) * 4
+            if want_leaf is None:
+                want_leaf = (cf.payload_values(1, int(lvl[i]), int(cnt[i]), 4) * np.float32(2.0)).astype(np.float32)
+            assert np.array_equal(got[a:a + nb].view(np.float32), want_leaf), i
+            mask[a:a + nb] = False
+        assert len(w.targets) == 64
+        assert np.array_equal(got[mask], src[mask])
     finally:
         w.close()
 

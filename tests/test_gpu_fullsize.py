@@ -116,6 +116,37 @@ def test_compute_sanitizer_memcheck(cf, tmp_path):
     assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr
 
 
+def test_compute_sanitizer_racecheck(cf, tmp_path):
+    """Shared-memory hazards (k_checksum's reduction, the one-CTA attach + resolve barrier, the
+    word-streaming tile barrier): racecheck over small windows."""
+    tool = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(tool):
+        pytest.skip("compute-sanitizer not installed")
+    script = tmp_path / "race.py"
+    script.write_text(RACE)
+    out = subprocess.run([tool, "--tool", "racecheck", "--error-exitcode", "99", sys.executable, str(script)],
+                         capture_output=True, text=True, timeout=900, cwd=str(REPO))
+    assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
+    assert "race ok" in out.stdout
+
+
+RACE = r'''
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_1906_01128_b200 as cf
+from paper_1906_01128_b200 import _native as N
+from paper_1906_01128_b200.shard import leaf_checksums
+for spec, align in ((cf.DenseSpec(3, 4099, 2), 1), (cf.DenseSpec(4, 3000, 2, elem=4, leaf_only=True), 16)):
+    w = cf.DeepCopyWindow(spec, seed=1, policy="all_arrays", align=align, chunk_bytes=8192)
+    w.run(scale=2.0)
+    off, cnt = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT)
+    leaf_checksums(w.ctx, w.image, off[w.targets], cnt[w.targets], spec.elem)
+    w.close()
+print("race ok")
+'''
+
+
 def test_many_small_chains_repeated_windows_stay_exact(cf):
     """1M chains with 12-byte leaf records (A fields at 4 mod 8 even in the aligned arena): many
     back-to-back resident and full windows (fused detach, graph replay) must never tear a

@@ -310,3 +310,43 @@ def test_packed_f64_word_streaming_matches_oracle(cf, oracle, mode):
                 assert st.bad == NO_BAD and np.array_equal(w.image_bytes(), want), (j, leaf_only, "resident")
             finally:
                 w.close()
+
+
+@pytest.mark.parametrize("mode", ["resolved", "chase"])
+def test_salted_payload_catches_same_level_swaps(cf, mode):
+    """payload_values depends only on (seed, level, i), so every array of a level holds the same
+    bytes and a chain resolved to the wrong sibling would go unnoticed.  Salt every array with
+    its own pattern (array index in the values), run the window, and require each targeted array
+    = its own salt x 2 and everything else unchanged ("salted init")."""
+    specs = [(cf.DenseSpec(3, 700, 3, elem=4), 1, "all_arrays"), (cf.DenseSpec(4, 3000, 2, elem=8), 16, "all_leaves"),
+             (cf.DenseSpec(20, 40, 2, elem=4), 16, "all_leaves"),
+             (cf.LinearSpec(6, 2500, "allinit_allused", elem=8), 1, "ref"),
+             (cf.ForestSpec(cf.LinearSpec(3, 3000, "LLinit_LLused", elem=4), 12, scatter_seed=3), 16, "all_leaves")]
+    for spec, align, policy in specs:
+        for chunk in (0, 8192):
+            w = cf.DeepCopyWindow(spec, seed=2, policy=policy, mode=mode, align=align, chunk_bytes=chunk)
+            try:
+                e = spec.elem
+                dt = np.float32 if e == 4 else np.float64
+                off, cnt = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT)
+                src = w.host_src()
+                for i in range(len(off)):
+                    n, a = int(cnt[i]), int(off[i])
+                    if n:
+                        salt = ((np.arange(n, dtype=np.int64) * 7 + i * 65537) % (1 << 20)).astype(dt)
+                        src[a:a + n * e] = np.frombuffer(salt.tobytes(), np.uint8)
+                before = src.copy()
+                st = w.run(scale=2.0)
+                assert st.bad == NO_BAD
+                want = before.copy()
+                for i in w.targets.tolist():
+                    n, a = int(cnt[i]), int(off[i])
+                    if n:
+                        vals = np.frombuffer(before[a:a + n * e].tobytes(), dt) * dt(2.0)
+                        want[a:a + n * e] = np.frombuffer(vals.astype(dt).tobytes(), np.uint8)
+                assert np.array_equal(w.host_dst(), want), (spec, align, policy, chunk)
+                w.upload_raw()
+                st = w.run_resident(scale=2.0, graph=True)
+                assert st.bad == NO_BAD and np.array_equal(w.image_bytes(), want), (spec, "resident")
+            finally:
+                w.close()

@@ -246,6 +246,9 @@ int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_by
  * or mapped pinned memory) are copied by one zero-copy kernel, one warp per object; the rest
  * by the copy engines (cudaMemcpyBatchAsync).  Synchronous. */
 int cf_copy_objects(cf_ctx* ctx, void* const* dsts, const void* const* srcs, const uint64_t* sizes, uint64_t count);
+/* Bulk copy by the SMs (16-byte aligned; either end may be mapped pinned host memory), async on
+ * `stream` (NULL: the context's compute stream); ctas 0 = 4 per SM.  Host-link experiments. */
+int cf_sm_copy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, unsigned ctas, void* stream);
 /* Diagnostics: the first leaf-kernel address fault caught by the bounds check (flag, target,
  * address, count, image, image bytes, level, ordinal); reset != 0 clears it. */
 int cf_debug_info(cf_ctx* ctx, uint64_t* out8, int reset);

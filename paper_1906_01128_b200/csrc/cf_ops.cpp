@@ -405,6 +405,12 @@ int cf_copy_objects(cf_ctx* c, void* const* dsts, const void* const* srcs, const
   return CF_OK;
 }
 
+int cf_sm_copy(cf_ctx* c, void* dst, const void* src, uint64_t bytes, unsigned ctas, void* stream) {
+  if (!c || !dst || !src) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  return launch_sm_copy(c, dst, src, bytes, ctas, pick(c, stream));
+}
+
 int cf_debug_info(cf_ctx* c, uint64_t* out8, int reset) {
   if (!c || !out8) return fail(CF_E_INVALID, "null argument");
   CfDevice g(c);

@@ -569,7 +569,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
-    ap.add_argument("--chunk-mb", type=int, default=16)
+    ap.add_argument("--chunk-mb", type=int, default=32)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-chase", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="enqueue every window directly (no CUDA graph)")

@@ -23,7 +23,7 @@ from .scenarios import TARGET_POLICIES
 
 class DeepCopyWindow:
     def __init__(self, spec, seed: int = 1, policy: str = "all_leaves", mode: str = "resolved",
-                 align: int = 16, chunk_bytes: int = 16 << 20, device: int = 0,
+                 align: int = 16, chunk_bytes: int = 32 << 20, device: int = 0,
                  separate_output: bool = True, scale: float = 2.0, nstreams: int = 1, numa_node: int | None = None):
         self.ctx = N.DeviceContext.get(device, nstreams)
         self.numa_node = numa_node   # pinned buffers allocated on this NUMA node (None: as the OS places them)

@@ -213,7 +213,7 @@ class DevicePrep:
 UVM_HINTS = ("none", "prefetch", "advise")
 
 # pipeline granularity of the fused marshalling window (repo:profiles/r01_design_experiments.md)
-FUSED_CHUNK = 16 << 20
+FUSED_CHUNK = 32 << 20
 
 
 class FusedMarshalWindow:

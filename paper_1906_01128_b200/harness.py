@@ -285,7 +285,7 @@ class FusedMarshalWindow:
 class FusedSelectiveWindow:
     """The pointerchain scheme's ``transfer_to_device -> kernel_scale -> copy_back`` (selective
     copies of the targeted arrays, harness.py:228-238, 255-259, 312-325) deferred into one
-    pipelined cf_selective window: per step of ~16 MiB the arrays' bytes go in, get scaled and go
+    pipelined cf_selective window: per step of ~32 MiB the arrays' bytes go in, get scaled and go
     back while the next step copies in; big arrays on the copy engines, small ones by zero-copy
     SM kernels.  Same observable behaviour and flush rules as FusedMarshalWindow."""
 

@@ -131,7 +131,10 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
                                            int level, uint64_t ordinal, uint64_t xlate_from = 0) {
   const uint8_t* p = image + root_off;
   const bool dense = sh.kind == CF_DENSE;
-  uint64_t qpow = 1;
+  // base-q digits of the ordinal, most significant first: rem / q^(L-l), rem %= q^(L-l).  Ordinals
+  // are u32 (window tables), so the divisions run in 32 bits -- 64-bit integer division is a long
+  // emulated sequence and made the 1M-chain resolve instruction-bound (C4: 17 us).
+  uint32_t qpow = 1, rem = uint32_t(ordinal);
   if (dense)
     for (int l = 1; l < level; ++l) qpow *= sh.q;
   for (int l = 1; l <= level; ++l) {
@@ -140,7 +143,9 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
     uint64_t child = 0, digit = 0;
     if (dense) {
       child = (l < sh.depth) ? NODE_SIZE : LEAF_NODE_SIZE;
-      digit = (ordinal / qpow) % sh.q;
+      const uint32_t d = rem / qpow;
+      rem -= d * qpow;
+      digit = d;
       qpow = qpow > 1 ? qpow / sh.q : 1;
     }
     const uint64_t next = blk + digit * child;

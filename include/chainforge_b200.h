@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define CF_ABI_VERSION 1
+#define CF_ABI_VERSION 2   /* 2: cf_spec gained shard_rank / shard_world */
 
 enum {
   CF_OK = 0,

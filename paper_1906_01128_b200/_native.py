@@ -17,6 +17,7 @@ from .errors import (AttachOutsideArena, NativeUnavailable, OutOfSimMemory, SimM
                      WildAccess)
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libchainforge_b200.so"
+ABI_VERSION = 2   # include/chainforge_b200.h CF_ABI_VERSION
 
 # status codes
 CF_OK, CF_E_INVALID, CF_E_OOM, CF_E_WILD, CF_E_OUTSIDE_ARENA, CF_E_CUDA, CF_E_NODEVICE, CF_E_STATE = (
@@ -172,6 +173,8 @@ def lib():
                 "g.build()'` (the deep-copy path has no CPU fallback)")
         L = C.CDLL(str(path))
         _declare(L)
+        if L.cf_abi_version() != ABI_VERSION:   # a stale build with another struct layout
+            raise NativeUnavailable(f"{path} has C ABI {L.cf_abi_version()}, this package needs {ABI_VERSION}: rebuild")
         _lib = L
     return _lib
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(lib, s)]
     assert not missing, missing
     assert set(declared) == set(_native.EXPORTED)
-    assert lib.cf_abi_version() == 1
+    assert lib.cf_abi_version() == 2
 
 
 def test_ctx_create_without_gpu_fails_loudly():

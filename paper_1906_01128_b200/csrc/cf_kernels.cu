@@ -11,13 +11,21 @@
 //                             (Listing 2 per-iteration chain)
 //   k_naive_fixup per-object deep-copy fix-ups through a sorted interval map
 //                 (naive_deep_copy + AddressMap.translate, memory.py:349-365, 409-419)
+//   k_seg_copy / k_copy_list
+//                 zero-copy moves over mapped pinned host memory: hoisted node pages of scattered
+//                 layouts, and per-object copies of small objects (naive / pointerchain schemes)
+//   k_checksum    per-leaf checksums for the multi-GPU result gather
+//   k_sm_copy     SM-driven bulk copy (host-link experiments only)
 //
 // All of these are HBM/latency-bound integer or streaming work: no tensor cores.  The leaf
 // kernel is the HBM-roofline kernel: 16-byte vector loads/stores with streaming cache hints,
 // 4 independent vectors in flight per thread, a persistent grid sized to 148 SMs x resident
 // CTAs, and a flattened (target, tile) work list so 64 huge leaves and 1M small leaves both
-// balance.  Pointer fields in the packed reference layout sit at 4 (mod 8); every 64-bit field
-// access goes through ld_u64_any/st_u64_any (2 x u32 when misaligned).
+// balance.  Pointer fields in the packed reference layout -- and every other dense leaf record's
+// A field even in aligned arenas (12-byte records) -- sit at 4 (mod 8); every 64-bit field access
+// goes through ld_u64_any/st_u64_any (2 x u32 when misaligned), so a field may only be read
+// concurrently with its relocation when all fields are 8-byte aligned (k_attach_resolve_wide).
+// f64 arrays at 4 (mod 8) stream aligned 16-byte words (scale_f64_shifted).
 #include "cf_internal.h"
 
 #include <algorithm>

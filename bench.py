@@ -365,24 +365,14 @@ class L2Flush:
     def flush(self) -> None:
         self.N.check(self.N.lib().cf_memset(self.w.ctx.handle, self.buf, 0x5A, L2_FLUSH_BELOW))
 
-    def steps(self, run, warmup: int, steps: int, dist):
-        class Sum:
-            ms_total = 0.0
-            launches = h2d_bytes = d2h_bytes = 0
-        for i in range(warmup):
-            self.flush()
-            run(2.0 if i % 2 == 0 else 0.5)
+    def steps(self, flags: int, warmup: int, steps: int, dist):
+        """warmup then steps windows in one batch, the L2 flushed before each (outside the timed
+        intervals); stats.ms_total = the sum of the windows' own device intervals."""
+        self.w.run_n_flushed(warmup, self.buf.value, L2_FLUSH_BELOW, flags=flags)
         dist.barrier()
-        out = Sum()
-        for i in range(steps):
-            self.flush()
-            st = run(2.0 if i % 2 == 0 else 0.5)
-            out.ms_total += st.ms_total
-            out.launches += st.launches
-            out.h2d_bytes += st.h2d_bytes
-            out.d2h_bytes += st.d2h_bytes
+        st = self.w.run_n_flushed(steps, self.buf.value, L2_FLUSH_BELOW, flags=flags)
         dist.barrier()
-        return out
+        return st
 
     def close(self) -> None:
         self.N.lib().cf_dev_free(self.w.ctx.handle, self.buf)
@@ -445,7 +435,7 @@ def run_ours(args, dist: Dist) -> None:
         N.check(N.lib().cf_ctx_sync(w.ctx.handle))
         dist.barrier()
     else:   # working set fits L2: flush it before every step, time each step on the device
-        st_e2e = flush.steps(lambda sc: w.run(scale=sc, flags=N.CF_WIN_FULL | gflag), args.warmup, args.steps, dist)
+        st_e2e = flush.steps(N.CF_WIN_FULL | gflag, args.warmup, args.steps, dist)
     e2e_ms = dist.max(st_e2e.ms_total) / args.steps
     # ---- value: image resident in HBM
     w.upload_raw()
@@ -457,8 +447,7 @@ def run_ours(args, dist: Dist) -> None:
         N.check(N.lib().cf_ctx_sync(w.ctx.handle))
         dist.barrier()
     else:
-        st_res = flush.steps(lambda sc: w.run_resident(scale=sc, graph=not args.no_graph), args.warmup, args.steps,
-                             dist)
+        st_res = flush.steps(N.CF_WIN_RESIDENT | gflag, args.warmup, args.steps, dist)
     res_ms = dist.max(st_res.ms_total) / args.steps
     # ---- leaf-kernel duration (events around the k_scale launch, resident, after warm-up)
     kms = []
@@ -513,10 +502,10 @@ def run_ours(args, dist: Dist) -> None:
         "vs_baseline": None, "dtype": "f32" if spec.elem == 4 else "f64",
         "data": "synthetic (payload_values of the reference, seed 1+rank)",
         "config": {"workload": desc, "graph_bytes_per_gpu": total, "leaf_bytes_per_gpu": leaf_bytes,
-                   "layout": "aligned16 arena", "targets": policy, "chunk_bytes": args.chunk_mb << 20,
+                   "layout": "aligned16 arena", "targets": policy, "chunk_bytes": w.chunk_bytes,
                    "h2d_streams": 1, "d2h_streams": 1, "cuda_graph": not args.no_graph, "l2": "inputs >= 1 GiB per GPU exceed the 126 MB L2 (no flush needed)"
-                   if flush is None else "working set below 512 MiB: L2 flushed (512 MiB device memset) "
-                   "before every timed step, outside the timed region; per-step device times summed",
+                   if flush is None else "working set below 512 MiB: L2 flushed (512 MiB device memset on the window's stream) "
+                   "before every timed window, outside the timed intervals; per-window device intervals summed",
                    "parallelism": f"dp{n} ({scaling}-scaled subtree shards, one per GPU, no data-path collective)"},
         "e2e": {"value": round(e2e, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": int(h2d_step), "d2h_bytes_per_step": int(d2h_step),

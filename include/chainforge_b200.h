@@ -332,6 +332,11 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
  * its own stream; the copy engines' streams are shared). */
 int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_even, double scale_odd,
                        cf_window_stats* stats);
+/* As cf_window_run_n for working sets that fit the L2: before every window, a memset of
+ * flush_bytes at flush_buf (device) evicts the L2; stats->ms_total is the sum of the windows' own
+ * intervals (CUDA events after each flush and after each window), flushes excluded. */
+int cf_window_run_n_flushed(cf_window* w, int nruns, double scale_even, double scale_odd, void* flush_buf,
+                            uint64_t flush_bytes, cf_window_stats* stats);
 int cf_window_set_scale(cf_window* w, double scale);
 int cf_window_free(cf_window* w);
 

@@ -50,7 +50,8 @@ EXPORTED = (
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy",
-    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_set_scale",
+    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_n_flushed",
+    "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
 )
@@ -152,6 +153,7 @@ def _declare(L):
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_run_pair": (C.c_int, [P, P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
+        "cf_window_run_n_flushed": (C.c_int, [P, C.c_int, C.c_double, C.c_double, P, U64, C.POINTER(CfWindowStats)]),
         "cf_window_free": (C.c_int, [P]),
         "cf_uvm_prefetch": (C.c_int, [P, P, U64, C.c_int, P]),
         "cf_uvm_advise": (C.c_int, [P, P, U64, C.c_int]),

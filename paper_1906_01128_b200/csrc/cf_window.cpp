@@ -583,6 +583,41 @@ int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_eve
   return finish(w0, st, launches0, h2d, d2h, false, w0->ev_first);
 }
 
+int cf_window_run_n_flushed(cf_window* w, int nruns, double scale_even, double scale_odd, void* flush_buf,
+                            uint64_t flush_bytes, cf_window_stats* st) {
+  if (!w || nruns < 1 || (flush_bytes && !flush_buf)) return fail(CF_E_INVALID, "bad arguments");
+  CfDevice g(w->ctx);
+  std::vector<cudaEvent_t> ev(2 * size_t(nruns), nullptr);
+  struct Guard { std::vector<cudaEvent_t>& e; ~Guard() { for (auto x : e) if (x) cudaEventDestroy(x); } } guard{ev};
+  for (auto& e : ev) CF_CUDA(cudaEventCreate(&e));
+  const uint64_t launches0 = w->ctx->launches.load();
+  uint64_t h2d = 0, d2h = 0;
+  CF_TRY(batch_begin(w->ctx, &w, 1, w->ev_first));
+  for (int r = 0; r < nruns; ++r) {
+    // evict the working set from L2 (outside the timed interval), then time this window alone
+    if (flush_bytes) CF_CUDA(cudaMemsetAsync(flush_buf, 0x5A, flush_bytes, w->stream));
+    CF_CUDA(cudaEventRecord(ev[2 * r], w->stream));
+    w->d.scale = (r & 1) ? scale_odd : scale_even;
+    uint64_t a = 0, b = 0;
+    CF_TRY(one_run(w, false, &a, &b));
+    CF_CUDA(cudaEventRecord(ev[2 * r + 1], w->stream));
+    h2d += a;
+    d2h += b;
+  }
+  CF_TRY(batch_end(w->ctx, &w, 1, &d2h, w->ev_end));
+  CF_TRY(finish(w, st, launches0, h2d, d2h, false, w->ev_first));
+  if (st) {
+    float total = 0;
+    for (int r = 0; r < nruns; ++r) {
+      float ms = 0;
+      CF_CUDA(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+      total += ms;
+    }
+    st->ms_total = total;   // sum of the windows' own intervals (flushes excluded)
+  }
+  return CF_OK;
+}
+
 namespace {
 // Direct enqueue, or (CF_WIN_GRAPH) capture the whole multi-stream sequence once per scale value
 // into a CUDA graph and replay it: one launch call instead of ~100 per window.

@@ -122,6 +122,18 @@ class DeepCopyWindow:
                 "cf_window_run_n")
         return st
 
+    def run_n_flushed(self, nruns: int, flush_buf: int, flush_bytes: int, flags: int = N.CF_WIN_FULL,
+                      chunk_bytes: int | None = None, scales: tuple = (2.0, 0.5)):
+        """``nruns`` windows, the L2 flushed before each; stats.ms_total = the windows' own time."""
+        cb = self.chunk_bytes if chunk_bytes is None else chunk_bytes
+        if not flags & (N.CF_WIN_H2D | N.CF_WIN_D2H):
+            cb = 0
+        w = self._window(flags, cb, self.mode)
+        st = N.CfWindowStats()
+        N.check(N.lib().cf_window_run_n_flushed(w, int(nruns), float(scales[0]), float(scales[1]), flush_buf,
+                                                flush_bytes, C.byref(st)), "cf_window_run_n_flushed")
+        return st
+
     def upload_raw(self) -> None:
         """Put the un-relocated arena bytes into the device image (prepares run_resident)."""
         N.check(N.lib().cf_memcpy(self.ctx.handle, self.image, self.src, self.total), "upload")

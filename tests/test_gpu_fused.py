@@ -248,3 +248,28 @@ def test_fused_pointerchain_flush_and_repeat(cf):
     cf.kernel_scale(m, h, prep, 0.5)
     cf.copy_back(m, h, prep)
     m.close()
+
+
+@pytest.mark.parametrize("scheme,fused", [("naive", True), ("pointerchain", False), ("marshalling", False)])
+def test_repeated_windows_reuse_device_storage(cf, scheme, fused):
+    """Spare device spans / images are reused window after window (no 1 GiB-class allocation per
+    window): repeated transfer -> kernel -> copy_back on one tree stays exact and the device space
+    does not grow after the first window."""
+    m = cf.Machine()
+    spec = cf.DenseSpec(5, 3000, 2)
+    if scheme == "marshalling":
+        arena, h = cf.marshal_tree(m, spec, seed=4)
+    else:
+        arena, h = None, cf.build_tree(m, spec, seed=4)
+    used = []
+    for r in range(4):
+        prep = cf.transfer_to_device(m, h, scheme, arena, policy="all_arrays", fused=fused)
+        cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5)
+        cf.copy_back(m, h, prep)
+        used.append(m.device.bump_offset)
+    assert used[1] == used[2] == used[3]
+    prep = cf.transfer_to_device(m, h, scheme, arena, policy="all_arrays", fused=fused)
+    cf.kernel_scale(m, h, prep, 2.0)
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_arrays")
+    m.close()

@@ -1,0 +1,47 @@
+"""Soak test: minutes of back-to-back windows in every mode on every config, verifying the result
+after each batch against payload_values x the net scale.  Catches rare races (the torn pointer
+read needed ~1000 windows).  python tools/soak.py SECONDS [configs...]"""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_1906_01128_b200 import DeepCopyWindow  # noqa: E402
+from paper_1906_01128_b200 import _native as N  # noqa: E402
+from paper_1906_01128_b200.scenarios import payload_values  # noqa: E402
+
+secs = float(sys.argv[1]) if len(sys.argv) > 1 else 300
+cfgs = sys.argv[2:] or ["C2", "C3", "C4"]
+deadline = time.time() + secs
+per = secs / len(cfgs)
+total = 0
+for cfg in cfgs:
+    spec, policy, _ = bench.make_spec(cfg)
+    w = DeepCopyWindow(spec, seed=1, policy=policy)
+    t = w.twin()
+    off, cnt, lvl = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT), w.table(N.CF_TAB_ARR_LEVEL)
+    src = w.host_src().copy()
+    end = min(deadline, time.time() + per)
+    it = 0
+    while time.time() < end:
+        g = N.CF_WIN_GRAPH if it % 2 else 0
+        st = w.run_pair_n(t, 8, flags=N.CF_WIN_FULL | g)          # last window (t): scale 0.5
+        assert st.bad == N.NO_BAD
+        w.upload_raw()
+        st = w.run_n(10, flags=N.CF_WIN_RESIDENT | g)            # net scale 1.0 on the image
+        assert st.bad == N.NO_BAD
+        # checks: the image is back to the source, the twin's copy-back holds leaves x 0.5
+        assert np.array_equal(w.image_bytes(), src), (cfg, it, "resident")
+        got = t.host_dst()
+        for i in (int(w.targets[0]), int(w.targets[len(w.targets) // 2]), int(w.targets[-1])):
+            a, n = int(off[i]), int(cnt[i])
+            want = (payload_values(1, int(lvl[i]), n, spec.elem) * np.float32(0.5)).astype(np.float32)
+            assert np.array_equal(got[a:a + 4 * n].view(np.float32), want), (cfg, it, i)
+        it += 1
+        total += 18
+    print(f"{cfg}: {it} rounds ({it * 18} windows) ok", flush=True)
+    t.close()
+    w.close()
+print("soak ok", total, "windows")

@@ -231,6 +231,9 @@ int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain
  * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */
 int cf_scale_resolved(cf_ctx* ctx, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,
                       double scale);
+/* naive_copy_back's host pointer restore (memory.py:368-372): write h_values[i] (8 bytes) at host
+ * address h_addrs[i] (any 4-byte alignment), in parallel. */
+int cf_host_write_words(const uint64_t* h_addrs, const uint64_t* h_values, uint64_t n);
 /* The attach loop's bounds check (memory.py:319-321) on the host, before any transfer: every
  * site (arena offset, table order) must hold a pointer into [ptr_base, ptr_base + total).
  * Returns CF_E_OUTSIDE_ARENA with *bad_index = the first offending table index.  Lets a

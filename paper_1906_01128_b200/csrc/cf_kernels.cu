@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(256) k_seg_copy(const uint64_t* __restrict__ s
 }
 
 // Many small copies as one launch (zero-copy over mapped pinned host memory, either
-// direction): warp i copies bytes[i] from src[i] to dst[i], 16-byte words when both ends and
-// the length allow, else 4-byte words.  Replaces one copy-engine command per object for the
+// direction): warp i copies bytes[i] from src[i] to dst[i] in the widest words (16, 8 or 4 bytes)
+// that both ends and the length allow.  Replaces one copy-engine command per object for the
 // pointerchain scheme's small arrays (cf_selective_run).
 __global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ src, const uint64_t* __restrict__ dst,
                                                    const uint64_t* __restrict__ bytes, uint64_t n) {
@@ -749,6 +749,10 @@ __global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ 
     const uint4* ps = reinterpret_cast<const uint4*>(s);
     uint4* pd = reinterpret_cast<uint4*>(d);
     for (uint64_t k = lane; k < b / 16; k += 32) pd[k] = ps[k];
+  } else if (((s | d | b) & 7) == 0) {
+    const uint64_t* ps = reinterpret_cast<const uint64_t*>(s);
+    uint64_t* pd = reinterpret_cast<uint64_t*>(d);
+    for (uint64_t k = lane; k < b / 8; k += 32) pd[k] = ps[k];
   } else if (((s | d | b) & 3) == 0) {
     const uint32_t* ps = reinterpret_cast<const uint32_t*>(s);
     uint32_t* pd = reinterpret_cast<uint32_t*>(d);

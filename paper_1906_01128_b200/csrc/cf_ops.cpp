@@ -309,6 +309,13 @@ int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t*
   return CF_OK;
 }
 
+int cf_host_write_words(const uint64_t* h_addrs, const uint64_t* h_values, uint64_t n) {
+  if (n && (!h_addrs || !h_values)) return fail(CF_E_INVALID, "null argument");
+#pragma omp parallel for schedule(static) if (n > (1u << 16))
+  for (int64_t i = 0; i < int64_t(n); ++i) memcpy(reinterpret_cast<void*>(h_addrs[i]), &h_values[i], 8);
+  return CF_OK;
+}
+
 int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t* h_sites, uint64_t nsites,
                          uint64_t ptr_base, uint64_t* bad_index) {
   if (!host_arena || (nsites && !h_sites)) return fail(CF_E_INVALID, "null argument");

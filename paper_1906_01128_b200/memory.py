@@ -747,14 +747,12 @@ class Machine:
 
 
 def _poke_words(fields: np.ndarray, values: np.ndarray) -> None:
-    """Write 8-byte values at arbitrary (4-aligned) host addresses (vectorised over one span)."""
-    fields = np.asarray(fields, np.uint64)
+    """Write 8-byte values at arbitrary (4-aligned) host addresses (native, parallel)."""
+    fields = np.ascontiguousarray(fields, np.uint64)
     if fields.size == 0:
         return
-    lo, hi = int(fields.min()), int(fields.max()) + 8
-    view = N.host_view(lo, hi - lo)
-    idx = (fields - np.uint64(lo)).astype(np.int64)[:, None] + np.arange(8, dtype=np.int64)[None, :]
-    view[idx] = np.ascontiguousarray(values, np.uint64).view(np.uint8).reshape(-1, 8)
+    values = np.ascontiguousarray(values, np.uint64)
+    N.check(N.lib().cf_host_write_words(N.ptr(fields), N.ptr(values), fields.size), "host pointer restore")
 
 
 class AddressMap:

@@ -29,7 +29,7 @@ from . import _native as N
 from .errors import AttachOutsideArena, SchemeError, VerificationFailed, WildAccess
 from .memory import D2H, DATA_OP_KINDS, H2D, NULL_ADDR, AddressMap, Arena, Machine
 from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, ForestSpec,
-                        LinearSpec, TreeHandle, build_tree, marshal_tree, payload_values, targeted_arrays)
+                        LinearSpec, TreeHandle, build_tree, marshal_tree, payload_values)
 
 SCHEMES = ("uvm", "marshalling", "pointerchain", "naive")
 MODES = ("resolved", "chase")

@@ -325,6 +325,20 @@ typedef struct {
 } cf_window_stats;
 
 int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
+/* Host-only dry run of cf_window_plan (no GPU needed; host_src / image may be NULL) followed by
+ * an invariant check of the schedule, re-derived independently where possible: segments
+ * partition the arena; every site is attached once, in the step that uploads it; every target's
+ * chain -- walked through the tree's site table -- has landed by its resolve step and ends at its
+ * array's owner; the leaf-kernel parts tile each target's elements once, after their bytes land;
+ * no segment is detached or copied back before its last reader or writer.  Returns
+ * CF_E_STATE (first violation in cf_last_error) if any invariant fails. */
+typedef struct {
+  uint64_t nsteps, nsegments, nsites, ntargets, nparts, ngroups, ntiles, table_bytes, zero_copy_node_segments;
+  int32_t violations;
+  int32_t reserved;
+  double plan_ms;
+} cf_plan_check;
+int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out);
 /* Enqueue one window; if sync != 0 wait and fill stats (ms from CUDA events). */
 int cf_window_run(cf_window* w, int sync, cf_window_stats* stats);
 /* Enqueue nruns windows back to back (scale alternating scale_even / scale_odd, e.g. 2.0 / 0.5

@@ -75,6 +75,13 @@ struct cf_window {
   // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
   struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
   std::vector<Graph> graphs;
+  // dry run (cf_window_plan_check): the host plan kept for the invariant checker, no CUDA state
+  struct Dry {
+    std::vector<uint64_t> reloc, torder, ready, release, seg_step, part_step;
+    std::vector<uint32_t> det;
+    cf::ScaleWork sw;
+  };
+  Dry* dry = nullptr;
 };
 
 namespace {
@@ -115,6 +122,11 @@ void bucket_order(const std::vector<uint64_t>& key, uint64_t nk, std::vector<uin
 
 void destroy(cf_window* w) {
   if (!w) return;
+  if (w->dry) {   // host-only plan: no CUDA resources were created
+    delete w->dry;
+    delete w;
+    return;
+  }
   CfDevice g(w->ctx);
   if (w->h_tab) cudaFreeHost(w->h_tab);
   if (w->d_tab) cudaFree(w->d_tab);
@@ -139,15 +151,25 @@ void destroy(cf_window* w) {
 
 extern "C" {
 
+namespace {
+int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry);
+}
+
 int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
-  if (!ctx || !desc || !out || !desc->tree) return fail(CF_E_INVALID, "null argument");
+  if (!ctx) return fail(CF_E_INVALID, "null argument");
+  return plan_impl(ctx, desc, out, false);
+}
+
+namespace {
+int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry) {
+  if (!desc || !out || !desc->tree) return fail(CF_E_INVALID, "null argument");
   const cf_tree* t = desc->tree;
   const uint32_t fl = desc->flags;
-  if ((fl & CF_WIN_H2D) && !desc->host_src) return fail(CF_E_INVALID, "H2D needs host_src");
-  if ((fl & CF_WIN_D2H) && !desc->host_dst) return fail(CF_E_INVALID, "D2H needs host_dst");
-  if (!desc->image) return fail(CF_E_INVALID, "null image");
+  if ((fl & CF_WIN_H2D) && !desc->host_src && !dry) return fail(CF_E_INVALID, "H2D needs host_src");
+  if ((fl & CF_WIN_D2H) && !desc->host_dst && !dry) return fail(CF_E_INVALID, "D2H needs host_dst");
+  if (!desc->image && !dry) return fail(CF_E_INVALID, "null image");
   if (desc->ntargets && !desc->h_targets) return fail(CF_E_INVALID, "null targets");
-  CfDevice g(ctx);
+  CfDevice g(dry ? nullptr : ctx);
   // CF_PLAN_PROFILE=1: phase times of the planner on stderr
   static const bool prof = getenv("CF_PLAN_PROFILE") != nullptr;
   auto tp0 = std::chrono::steady_clock::now();
@@ -160,6 +182,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   cf_window* w = new cf_window();
   w->ctx = ctx;
   w->d = *desc;
+  if (dry) w->dry = new cf_window::Dry();
   w->elem = t->spec.elem;
   cf_tree_chain_shape(t, &w->sh);
   const uint64_t total = t->total;
@@ -187,9 +210,14 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
     uint64_t x = a;
     while (x < b) {
       uint64_t y = (ch && ch < total) ? std::min(b, (x / ch + 1) * ch) : b;
-      if (check_sites && y < b) {
+      // a 4-mod-8 pointer field may straddle the grid point: end the segment just before the
+      // field, or -- when the field opens this segment (the previous cut moved down to it) --
+      // run on to the next grid point, so every field lands whole in one segment
+      while (check_sites && y < b) {
         const uint64_t* it = std::lower_bound(sites, sites + nsites, y >= 7 ? y - 7 : 0);
-        if (it != sites + nsites && *it < y && *it + 8 > y && *it > x) y = *it;
+        if (it == sites + nsites || *it >= y || *it + 8 <= y) break;
+        if (*it > x) { y = *it; break; }
+        y = std::min(b, y + ch);
       }
       w->seg_lo.push_back(x);
       w->seg_hi.push_back(y);
@@ -411,13 +439,15 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   mark("orders");
   w->released.assign(nch, {});
   const uint64_t nnode_seg = hoist ? w->step_seg_lo[1] : 0;
-  {
+  if (!dry) {
     void* dp = nullptr;
     const bool mapped = desc->host_src && cudaHostGetDevicePointer(&dp, const_cast<void*>(desc->host_src), 0) == cudaSuccess &&
                         dp == desc->host_src &&
                         (!desc->host_dst || (cudaHostGetDevicePointer(&dp, desc->host_dst, 0) == cudaSuccess && dp == desc->host_dst));
     cudaGetLastError();
     w->zc = hoist && mapped && nnode_seg > ZC_MIN_SEGS;
+  } else {
+    w->zc = hoist && nnode_seg > ZC_MIN_SEGS;   // dry runs plan as if the arena were mapped
   }
   std::vector<uint64_t> zc_rel;   // node segments ordered by release step
   for (uint64_t sg = 0; sg < nseg; ++sg) {
@@ -453,6 +483,20 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   w->off_zc_h2d = al8(w->off_grp + sw.groups.size() * 4 + 8);
   w->off_zc_d2h = w->off_zc_h2d + (w->zc ? w->zc_n * 16 : 0);
   w->tab_bytes = al8(w->off_zc_d2h + (w->zc ? w->zc_n * 16 : 0) + 8);
+  if (dry) {
+    auto& D = *w->dry;
+    D.reloc = std::move(reloc);
+    D.det = std::move(det);
+    D.torder = std::move(torder);
+    D.ready = std::move(ready);
+    D.release = std::move(release);
+    D.seg_step = std::move(seg_step);
+    D.part_step = std::move(pstep);
+    D.sw = std::move(sw);
+    mark("tables");
+    *out = w;
+    return CF_OK;
+  }
   cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
@@ -506,6 +550,200 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out) {
   mark("events");
   *out = w;
   return CF_OK;
+}
+}  // namespace
+
+}  // extern "C"
+
+namespace {
+// Invariants of a planned window, re-derived independently of the planner where possible (the
+// chain of every target is walked through the tree's site table, not its level tables).
+struct Checker {
+  const cf_tree* t;
+  const cf_window_desc* d;
+  const cf_window* w;
+  int violations = 0;
+  template <typename... A>
+  void bad(const char* fmt, A... a) {
+    if (violations++ == 0) fail(CF_E_STATE, fmt, a...);
+  }
+  uint32_t seg_at(uint64_t off) const {   // segment holding byte off (segments partition [0, total))
+    return sorted_seg[size_t(std::upper_bound(sorted_lo.begin(), sorted_lo.end(), off) - sorted_lo.begin()) - 1];
+  }
+  std::vector<uint64_t> sorted_lo;
+  std::vector<uint32_t> sorted_seg;
+
+  void run() {
+    const auto& D = *w->dry;
+    const uint64_t total = t->total, nseg = w->seg_lo.size(), nch = w->nsteps, nt = d->ntargets;
+    const uint64_t e = uint64_t(t->spec.elem);
+    // 1. segments partition [0, total)
+    std::vector<uint32_t> ord(nseg);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return w->seg_lo[a] < w->seg_lo[b]; });
+    uint64_t x = 0;
+    for (uint32_t j : ord) {
+      if (w->seg_lo[j] != x || w->seg_hi[j] <= w->seg_lo[j]) bad("segment %u [%llu, %llu) breaks the partition at %llu", j,
+                                                              (unsigned long long)w->seg_lo[j], (unsigned long long)w->seg_hi[j], (unsigned long long)x);
+      x = w->seg_hi[j];
+      sorted_lo.push_back(w->seg_lo[j]);
+      sorted_seg.push_back(j);
+    }
+    if (x != total) bad("segments end at %llu, arena is %llu bytes", (unsigned long long)x, (unsigned long long)total);
+    if (w->step_seg_lo.size() != nch + 1 || w->step_seg_lo.back() != nseg) bad("step table malformed");
+    // 2. sites: each once, in the step that uploads both its ends
+    std::vector<uint64_t> rs(D.reloc);
+    std::sort(rs.begin(), rs.end());
+    if (rs != t->site_sorted) bad("relocation table is not a permutation of the sites");
+    for (uint64_t k = 0; k < nch; ++k)
+      for (uint64_t i = w->reloc_lo[k]; i < w->reloc_lo[k + 1]; ++i) {
+        const uint64_t s0 = D.reloc[i];
+        const uint32_t a = seg_at(s0), b = seg_at(s0 + 7);
+        if (a != b) bad("site %llu straddles segments %u / %u", (unsigned long long)s0, a, b);
+        if (D.seg_step[a] != k) bad("site %llu attached at step %llu, uploaded at %llu", (unsigned long long)s0,
+                                    (unsigned long long)k, (unsigned long long)D.seg_step[a]);
+      }
+    // 3. chains, walked through the site table: ready = last upload step of every byte read
+    std::vector<std::pair<uint64_t, uint64_t>> fmap(t->site_off.size());
+    for (size_t i = 0; i < fmap.size(); ++i) fmap[i] = {t->site_off[i], t->site_target[i]};
+    std::sort(fmap.begin(), fmap.end());
+    auto target_of = [&](uint64_t field, bool& ok) -> uint64_t {
+      auto it = std::lower_bound(fmap.begin(), fmap.end(), std::make_pair(field, uint64_t(0)));
+      ok = it != fmap.end() && it->first == field;
+      return ok ? it->second : 0;
+    };
+    const bool dense = t->spec.kind == CF_DENSE;
+    const uint64_t q = dense ? uint64_t(t->spec.k_or_q) : 1;
+    const bool chase = d->mode == CF_MODE_CHASE;
+    std::vector<uint64_t> need_release(nseg, 0);
+    for (uint64_t sg = 0; sg < nseg; ++sg) need_release[sg] = D.seg_step[sg];
+    std::vector<std::vector<uint32_t>> chain_segs(nt);
+    for (uint64_t i = 0; i < nt; ++i) {
+      const int64_t a = d->h_targets[i];
+      const int L = t->arr_level[a];
+      uint64_t node = t->arr_root[a], r = 0;
+      auto touch = [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t y : {lo, hi - 1}) {
+          const uint32_t sg = seg_at(y);
+          r = std::max(r, D.seg_step[sg]);
+          chain_segs[i].push_back(sg);
+        }
+      };
+      for (int l = 1; l <= L; ++l) {
+        bool ok = false;
+        const uint64_t blk = target_of(node + OFF_LNEXT, ok);
+        if (!ok) { bad("target %llu: no Lnext site at level %d", (unsigned long long)i, l); break; }
+        touch(node + OFF_LNEXT, node + OFF_LNEXT + 8);
+        uint64_t pw = 1;
+        for (int m = l; m < L; ++m) pw *= q;
+        const uint64_t digit = dense ? (uint64_t(t->arr_ordinal[a]) / pw) % q : 0;
+        node = blk + digit * ((dense && l == int(t->spec.depth)) ? LEAF_NODE_SIZE : NODE_SIZE);
+      }
+      if (node != t->arr_owner[a]) bad("target %llu: chain ends at %llu, array owner is %llu", (unsigned long long)i,
+                                       (unsigned long long)node, (unsigned long long)t->arr_owner[a]);
+      const bool leaf = dense && L == int(t->spec.depth);
+      touch(node + OFF_NA, node + (leaf ? LEAF_NODE_SIZE : OFF_LNEXT));
+      if (D.ready[i] != r) bad("target %llu ready at step %llu, its chain lands at %llu", (unsigned long long)i,
+                               (unsigned long long)D.ready[i], (unsigned long long)r);
+    }
+    for (uint64_t c = 0; c < nch; ++c)
+      for (uint64_t k = w->res_lo[c]; k < w->res_lo[c + 1]; ++k)
+        if (D.ready[D.torder[k]] != c) bad("target resolved at step %llu is ready at %llu", (unsigned long long)c,
+                                           (unsigned long long)D.ready[D.torder[k]]);
+    // 4. parts: tile every target's [0, count) once, each after its bytes and its chain
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> cover(nt);
+    std::vector<uint64_t> max_part(nt, 0);
+    const auto& P = D.sw.parts;
+    auto part = [&](uint64_t k, uint64_t p) {
+      const uint64_t tp = P[3 * p], e0 = P[3 * p + 1], e1 = P[3 * p + 2];
+      if (tp >= nt) { bad("part %llu names target position %llu", (unsigned long long)p, (unsigned long long)tp); return; }
+      const uint64_t i = D.torder[tp];
+      const int64_t a = d->h_targets[i];
+      if (k < D.ready[i]) bad("part of target %llu scaled at step %llu before its chain (step %llu)", (unsigned long long)i,
+                              (unsigned long long)k, (unsigned long long)D.ready[i]);
+      const uint64_t b0 = t->arr_off[a] + e0 * e, b1 = t->arr_off[a] + e1 * e;
+      for (size_t z = size_t(std::upper_bound(sorted_lo.begin(), sorted_lo.end(), b0) - sorted_lo.begin()) - 1;
+           z < sorted_lo.size() && sorted_lo[z] < b1; ++z) {
+        const uint32_t sg = sorted_seg[z];
+        if (D.seg_step[sg] > k) bad("part of target %llu scaled at step %llu before segment %u lands (%llu)",
+                                    (unsigned long long)i, (unsigned long long)k, sg, (unsigned long long)D.seg_step[sg]);
+        need_release[sg] = std::max(need_release[sg], k);
+      }
+      cover[i].push_back({e0, e1});
+      max_part[i] = std::max(max_part[i], k);
+    };
+    for (uint64_t k = 0; k < nch; ++k) {
+      const cf_scale_work& sw = w->seg[k];
+      for (uint64_t p = sw.big_begin; p < sw.big_begin + sw.big_count; ++p) part(k, p);
+      for (uint64_t g = sw.group_begin; g < sw.group_end; ++g)
+        for (uint64_t p = D.sw.groups[2 * g]; p < D.sw.groups[2 * g + 1]; ++p) part(k, p);
+    }
+    for (uint64_t i = 0; i < nt; ++i) {
+      const uint64_t n = t->arr_count[d->h_targets[i]];
+      auto& cv = cover[i];
+      std::sort(cv.begin(), cv.end());
+      uint64_t y = 0;
+      for (auto& iv : cv) {
+        if (iv.first != y || iv.second <= iv.first) { bad("target %llu: parts do not tile [0, %llu)", (unsigned long long)i, (unsigned long long)n); break; }
+        y = iv.second;
+      }
+      if (y != n) bad("target %llu: parts cover [0, %llu) of %llu elements", (unsigned long long)i, (unsigned long long)y,
+                      (unsigned long long)n);
+      for (uint32_t sg : chain_segs[i])
+        need_release[sg] = std::max(need_release[sg], chase ? std::max(D.ready[i], max_part[i]) : D.ready[i]);
+    }
+    // 5. release: no segment goes home before its last reader / writer
+    for (uint64_t sg = 0; sg < nseg; ++sg)
+      if (D.release[sg] < need_release[sg] || D.release[sg] >= nch)
+        bad("segment %llu released at step %llu, needed until %llu", (unsigned long long)sg, (unsigned long long)D.release[sg],
+            (unsigned long long)need_release[sg]);
+    // 6. detach: every site once, at its segment's release step
+    std::vector<uint8_t> seen(D.det.size(), 0);
+    for (uint64_t c = 0; c < nch; ++c)
+      for (uint64_t j = w->det_lo[c]; j < w->det_lo[c + 1]; ++j) {
+        const uint32_t r = D.det[j];
+        if (r >= D.reloc.size() || seen[r]++) { bad("detach list repeats or overflows at %llu", (unsigned long long)j); continue; }
+        const uint32_t sg = seg_at(D.reloc[r]);
+        if (D.release[sg] != c) bad("site %llu detached at step %llu, its segment is released at %llu",
+                                    (unsigned long long)D.reloc[r], (unsigned long long)c, (unsigned long long)D.release[sg]);
+      }
+    // 7. copy-back: every segment exactly once, at its release step
+    std::vector<uint8_t> home(nseg, 0);
+    for (uint64_t c = 0; c < nch; ++c)
+      for (uint32_t sg : w->released[c]) {
+        if (home[sg]++) bad("segment %u copied back twice", sg);
+        if (D.release[sg] != c) bad("segment %u copied back at %llu, released at %llu", sg, (unsigned long long)c,
+                                    (unsigned long long)D.release[sg]);
+      }
+    for (uint64_t sg = 0; sg < nseg; ++sg)
+      if (!home[sg] && !(w->zc && sg < w->zc_n)) bad("segment %llu never copied back", (unsigned long long)sg);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out) {
+  if (!desc || !out) return fail(CF_E_INVALID, "null argument");
+  memset(out, 0, sizeof *out);
+  const auto t0 = std::chrono::steady_clock::now();
+  cf_window* w = nullptr;
+  CF_TRY(plan_impl(nullptr, desc, &w, true));
+  out->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  out->nsteps = w->nsteps;
+  out->nsegments = w->seg_lo.size();
+  out->nsites = w->nsites;
+  out->ntargets = desc->ntargets;
+  out->nparts = w->dry->sw.nparts();
+  out->ngroups = w->dry->sw.ngroups();
+  out->ntiles = w->dry->sw.next_tile;
+  out->table_bytes = w->tab_bytes;
+  out->zero_copy_node_segments = w->zc ? w->zc_n : 0;
+  Checker ck{desc->tree, desc, w};
+  ck.run();
+  out->violations = ck.violations;
+  destroy(w);
+  return ck.violations ? CF_E_STATE : CF_OK;
 }
 
 int cf_window_set_scale(cf_window* w, double scale) {

@@ -350,3 +350,23 @@ def test_salted_payload_catches_same_level_swaps(cf, mode):
                 assert st.bad == NO_BAD and np.array_equal(w.image_bytes(), want), (spec, "resident")
             finally:
                 w.close()
+
+
+def test_fields_straddling_chunk_boundaries(cf, oracle):
+    """4-mod-8 pointer fields that straddle a chunk grid point (packed layouts, 12-byte leaf
+    records) must land whole before they are attached -- on a fresh image, first window.  The
+    schedule bug this pins (a moved cut left a 4-byte segment holding half a field) was found
+    by cf_window_plan_check (tests/test_plan.py)."""
+    for j, chunk in (({"kind": "dense", "q": 2, "n": 4000, "depth": 3}, 64), ({"kind": "dense", "q": 3, "n": 5, "depth": 3}, 40),
+                     ({"kind": "dense", "q": 5, "n": 100, "depth": 2}, 256)):
+        for leaf_only in (False, True):
+            spec = _spec(cf, j, 8, leaf_only)
+            w = cf.DeepCopyWindow(spec, seed=3, policy="all_arrays", align=1, chunk_bytes=chunk)
+            try:
+                st = w.run(scale=2.0)
+                assert st.bad == NO_BAD, (j, chunk, leaf_only)
+                ot = oracle.build(oracle.spec_from_json(j, elem=8, align=1, leaf_only=leaf_only), 3, ptr_base=w.src)
+                want = oracle.expected_after_window(ot, oracle.targets(ot, oracle.TARGET_ALL_ARRAYS), 2.0)[:w.total]
+                assert np.array_equal(w.host_dst(), want), (j, chunk, leaf_only)
+            finally:
+                w.close()

@@ -1,0 +1,70 @@
+"""The pipelined window's schedule, checked on the CPU (no GPU): cf_window_plan_check plans the
+window host-side and verifies its invariants against an independent walk of every chain through
+the tree's site table (see include/chainforge_b200.h).  Random trees, packed / aligned arenas,
+scattered forests, subtree shards, tiny to whole-arena chunks, resolved and chase modes."""
+import ctypes as C
+import random
+
+import numpy as np
+import pytest
+
+import paper_1906_01128_b200 as cf
+from paper_1906_01128_b200 import _native as N
+from paper_1906_01128_b200.scenarios import TARGET_POLICIES
+
+
+def check(spec, align, policy, chunk, mode=N.CF_MODE_RESOLVED, flags=N.CF_WIN_FULL):
+    tree = N.NativeTree(spec.native(align))
+    tg = np.ascontiguousarray(tree.targets(TARGET_POLICIES[policy]), np.int64)
+    d = N.CfWindowDesc(tree.handle, N.ptr(tg) if len(tg) else None, len(tg), None, None, 0x7f0000000000, None,
+                       mode, flags, 2.0, chunk)
+    out = N.CfPlanCheck()
+    rc = N.lib().cf_window_plan_check(C.byref(d), C.byref(out))
+    assert rc == 0, (spec, align, policy, chunk, mode, N.last_error())
+    assert out.violations == 0
+    return out
+
+
+def test_baseline_shapes():
+    c2 = check(cf.DenseSpec(4, 1 << 14, 3, elem=4, leaf_only=True), 16, "all_leaves", 1 << 16)
+    assert c2.nsites == 85 and c2.ntargets == 64 and c2.nsteps > 1
+    c3 = check(cf.ForestSpec(cf.LinearSpec(4, 1 << 12, "LLinit_LLused", elem=4), 64, scatter_seed=0xC3), 16,
+               "all_leaves", 1 << 16)
+    assert c3.zero_copy_node_segments > 0        # scattered nodes hoisted and moved by zero-copy
+    c4 = check(cf.DenseSpec(100, 16, 2, elem=4), 16, "all_leaves", 1 << 16)
+    assert c4.ntargets == 10000
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_plans_hold_their_invariants(seed):
+    rng = random.Random(seed)
+    for _ in range(25):
+        elem = rng.choice([4, 8])
+        kind = rng.random()
+        if kind < 0.35:
+            spec = cf.LinearSpec(rng.randint(1, 7), rng.choice([0, 1, 5, 300, 5000]),
+                                 rng.choice(["allinit_allused", "allinit_LLused", "LLinit_LLused"]), elem=elem)
+        elif kind < 0.75:
+            spec = cf.DenseSpec(rng.randint(1, 5), rng.choice([0, 3, 257, 4000]), rng.randint(0, 3), elem=elem,
+                                leaf_only=rng.random() < 0.4)
+        else:
+            spec = cf.ForestSpec(cf.LinearSpec(rng.randint(1, 4), rng.choice([7, 999, 3000]), "LLinit_LLused", elem=elem),
+                                 rng.randint(2, 24), scatter_seed=rng.choice([0, 3, 11]))
+        align = rng.choice([1, 8, 16])
+        policy = rng.choice(["ref", "all_leaves", "all_arrays"])
+        chunk = rng.choice([0, 64, 1000, 4096, 1 << 16])
+        mode = rng.choice([N.CF_MODE_RESOLVED, N.CF_MODE_CHASE])
+        check(spec, align, policy, chunk, mode)
+
+
+def test_subtree_shard_plans():
+    from paper_1906_01128_b200.shard import subtree_shard
+    for world in (2, 4, 8):
+        for r in range(world):
+            check(subtree_shard(cf.DenseSpec(4, 3000, 3, elem=4, leaf_only=True), r, world), 16, "all_leaves", 8192)
+
+
+def test_resident_and_copy_only_flag_sets():
+    spec = cf.DenseSpec(3, 2000, 3)
+    for flags in (N.CF_WIN_RESIDENT, N.CF_WIN_H2D | N.CF_WIN_D2H, N.CF_WIN_H2D | N.CF_WIN_TABLES | N.CF_WIN_ATTACH):
+        check(spec, 1, "all_arrays", 0 if flags == N.CF_WIN_RESIDENT else 4096, flags=flags)

@@ -715,8 +715,18 @@ struct Checker {
         if (D.release[sg] != c) bad("segment %u copied back at %llu, released at %llu", sg, (unsigned long long)c,
                                     (unsigned long long)D.release[sg]);
       }
+    if (w->zc) {   // hoisted node segments go home by zero-copy kernels, in release order
+      for (uint64_t c = 0; c < nch; ++c)
+        if (w->zc_rel_lo[c + 1] < w->zc_rel_lo[c]) bad("zero-copy release table not monotone");
+      if (w->zc_rel_lo[nch] != w->zc_n) bad("zero-copy release table covers %llu of %llu node segments",
+                                            (unsigned long long)w->zc_rel_lo[nch], (unsigned long long)w->zc_n);
+      for (uint64_t sg = 0; sg < w->zc_n; ++sg) {
+        if (D.seg_step[sg] != 0) bad("hoisted node segment %llu not in step 0", (unsigned long long)sg);
+        home[sg]++;
+      }
+    }
     for (uint64_t sg = 0; sg < nseg; ++sg)
-      if (!home[sg] && !(w->zc && sg < w->zc_n)) bad("segment %llu never copied back", (unsigned long long)sg);
+      if (!home[sg]) bad("segment %llu never copied back", (unsigned long long)sg);
   }
 };
 }  // namespace

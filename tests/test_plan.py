@@ -68,3 +68,16 @@ def test_resident_and_copy_only_flag_sets():
     spec = cf.DenseSpec(3, 2000, 3)
     for flags in (N.CF_WIN_RESIDENT, N.CF_WIN_H2D | N.CF_WIN_D2H, N.CF_WIN_H2D | N.CF_WIN_TABLES | N.CF_WIN_ATTACH):
         check(spec, 1, "all_arrays", 0 if flags == N.CF_WIN_RESIDENT else 4096, flags=flags)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
+@pytest.mark.parametrize("chunk_mb", [16, 32])
+def test_full_size_baseline_schedules(cfg, chunk_mb):
+    """The production schedules themselves (full BASELINE shapes, aligned16, 16 / 32 MiB chunks)."""
+    import sys
+    from conftest import REPO
+    sys.path.insert(0, str(REPO))
+    import bench
+    spec, policy, _ = bench.make_spec(cfg)
+    out = check(spec, 16, policy, chunk_mb << 20)
+    assert out.nsteps >= 30

@@ -674,9 +674,24 @@ struct Checker {
     };
     for (uint64_t k = 0; k < nch; ++k) {
       const cf_scale_work& sw = w->seg[k];
-      for (uint64_t p = sw.big_begin; p < sw.big_begin + sw.big_count; ++p) part(k, p);
-      for (uint64_t g = sw.group_begin; g < sw.group_end; ++g)
-        for (uint64_t p = D.sw.groups[2 * g]; p < D.sw.groups[2 * g + 1]; ++p) part(k, p);
+      uint64_t tiles = 0;
+      for (uint64_t p = sw.big_begin; p < sw.big_begin + sw.big_count; ++p) {
+        part(k, p);
+        // the kernel maps tile -> big part by tile_base: consecutive, one tile per 16 KiB
+        if (D.sw.tile_base[sw.tb_begin + (p - sw.big_begin)] != sw.tile_begin + tiles) bad("tile base of part %llu is off", (unsigned long long)p);
+        tiles += tiles_for(P[3 * p + 2] - P[3 * p + 1], int(e));
+      }
+      if (sw.tile_end - sw.tile_begin != tiles) bad("step %llu launches %llu tiles for %llu", (unsigned long long)k,
+                                                    (unsigned long long)(sw.tile_end - sw.tile_begin), (unsigned long long)tiles);
+      for (uint64_t g = sw.group_begin; g < sw.group_end; ++g) {
+        const uint64_t p0 = D.sw.groups[2 * g], p1 = D.sw.groups[2 * g + 1];
+        // the group kernel holds at most GROUP_PARTS parts (warp-local metadata)
+        if (p1 <= p0 || p1 - p0 > GROUP_PARTS) bad("group %llu holds %llu parts", (unsigned long long)g, (unsigned long long)(p1 - p0));
+        for (uint64_t p = p0; p < p1; ++p) {
+          part(k, p);
+          if (P[3 * p + 2] - P[3 * p + 1] >= TILE_BYTES / e) bad("big part %llu packed into a group", (unsigned long long)p);
+        }
+      }
     }
     for (uint64_t i = 0; i < nt; ++i) {
       const uint64_t n = t->arr_count[d->h_targets[i]];

@@ -273,3 +273,19 @@ def test_repeated_windows_reuse_device_storage(cf, scheme, fused):
     cf.copy_back(m, h, prep)
     cf.verify_tree(m, h, 2.0, "all_arrays")
     m.close()
+
+
+def test_fused_pointerchain_multi_step_and_split_arrays(cf):
+    """Pointerchain windows spanning many 32 MiB steps: arrays larger than a step (split into DMA
+    pieces), many small arrays (zero-copy), and a mix -- verify_tree after each."""
+    specs = [cf.LinearSpec(3, 12_000_000, "allinit_allused", elem=4),     # 48 MB arrays: split pieces
+             cf.DenseSpec(60, 2000, 2, elem=8),                           # 3,600 x 16 KB arrays: zero-copy
+             cf.DenseSpec(4, 3_000_000, 2, elem=4)]                       # 21 x 12 MB arrays, DMA
+    for spec in specs:
+        m = cf.Machine()
+        h = cf.build_tree(m, spec, seed=6, align=16)
+        prep = cf.transfer_to_device(m, h, "pointerchain", policy="all_arrays")
+        cf.kernel_scale(m, h, prep, 2.0)
+        cf.copy_back(m, h, prep)
+        cf.verify_tree(m, h, 2.0, "all_arrays")
+        m.close()

@@ -331,14 +331,15 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   //      segment holding its last byte
   const uint64_t e = uint64_t(w->elem);
   std::vector<Part> parts;
-  std::vector<std::pair<uint32_t, uint64_t>> touched;   // (segment, step) of every piece's bytes
+  // per segment: the last step that reads or writes it (thread-local maxima, merged below)
+  std::vector<uint64_t> release(seg_step);
   {
     int nthr = 1;
 #ifdef _OPENMP
     nthr = nt > (1u << 12) ? omp_get_max_threads() : 1;
 #endif
     std::vector<std::vector<Part>> tparts(static_cast<size_t>(nthr));
-    std::vector<std::vector<std::pair<uint32_t, uint64_t>>> ttouch(static_cast<size_t>(nthr));
+    std::vector<std::vector<uint64_t>> trel(static_cast<size_t>(nthr), std::vector<uint64_t>(nseg, 0));
 #pragma omp parallel num_threads(nthr)
     {
       int me = 0;
@@ -346,9 +347,8 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
       me = omp_get_thread_num();
 #endif
       auto& P = tparts[size_t(me)];
-      auto& T = ttouch[size_t(me)];
+      auto& R = trel[size_t(me)];
       P.reserve(nt / size_t(nthr) + 64);
-      T.reserve(nt / size_t(nthr) + 64);
 #pragma omp for schedule(static)
       for (int64_t ii = 0; ii < int64_t(nt); ++ii) {
         const uint64_t i = uint64_t(ii);
@@ -369,7 +369,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
           if (w->seg_lo[sg] <= off && w->seg_hi[sg] >= end) {
             const uint64_t step = std::max(ready[i], seg_step[sg]);
             P.push_back({i, 0, n, step});
-            T.push_back({sg, step});
+            R[sg] = std::max(R[sg], step);
             max_step[i] = step;
             continue;
           }
@@ -389,20 +389,38 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
           P.push_back({i, i0, i1, step});
           ms = std::max(ms, step);
           // every segment this piece touches is copied back no earlier than its step
-          for (size_t x = pb; x <= pe; ++x) T.push_back({six.seg[x], step});
+          for (size_t x = pb; x <= pe; ++x) R[six.seg[x]] = std::max(R[six.seg[x]], step);
         }
         max_step[i] = ms;
       }
     }
     for (auto& v : tparts) parts.insert(parts.end(), v.begin(), v.end());
-    for (auto& v : ttouch) touched.insert(touched.end(), v.begin(), v.end());
+    for (auto& v : trel)
+      for (uint64_t sg = 0; sg < nseg; ++sg) release[sg] = std::max(release[sg], v[sg]);
   }
-  std::vector<uint64_t> release(seg_step);   // per segment: last step that reads it
-  for (auto& st : touched) release[st.first] = std::max(release[st.first], st.second);
   const bool chase = desc->mode == CF_MODE_CHASE;
-  for (uint64_t i = 0; i < nt; ++i) {
-    const uint64_t v = chase ? std::max(ready[i], max_step[i]) : ready[i];
-    for (uint64_t f = fld_lo[i]; f < fld_lo[i + 1]; ++f) release[fld_seg[f]] = std::max(release[fld_seg[f]], v);
+  {   // chain fields are read until the target's resolve (chase: until its last piece)
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = nt > (1u << 14) ? omp_get_max_threads() : 1;
+#endif
+    std::vector<std::vector<uint64_t>> trel(static_cast<size_t>(nthr), std::vector<uint64_t>(nseg, 0));
+#pragma omp parallel num_threads(nthr)
+    {
+      int me = 0;
+#ifdef _OPENMP
+      me = omp_get_thread_num();
+#endif
+      auto& R = trel[size_t(me)];
+#pragma omp for schedule(static)
+      for (int64_t ii = 0; ii < int64_t(nt); ++ii) {
+        const uint64_t i = uint64_t(ii);
+        const uint64_t v = chase ? std::max(ready[i], max_step[i]) : ready[i];
+        for (uint64_t f = fld_lo[i]; f < fld_lo[i + 1]; ++f) R[fld_seg[f]] = std::max(R[fld_seg[f]], v);
+      }
+    }
+    for (auto& v : trel)
+      for (uint64_t sg = 0; sg < nseg; ++sg) release[sg] = std::max(release[sg], v[sg]);
   }
 
   mark("parts");
@@ -411,15 +429,20 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   bucket_order(ready, nch, torder, w->res_lo);
   std::vector<uint64_t> tpos(nt);
   for (uint64_t k = 0; k < nt; ++k) tpos[torder[k]] = k;
+  mark("o:targets");
   // per step: the pieces ready at that step, as one leaf-kernel launch (big tiles + small groups)
   std::vector<uint64_t> pstep(parts.size()), porder, plo;
   for (size_t k = 0; k < parts.size(); ++k) pstep[k] = parts[k].step;
   bucket_order(pstep, nch, porder, plo);
+  mark("o:pstep");
   ScaleWork sw;
   sw.elem = w->elem;
+  sw.parts.reserve(3 * parts.size());
+  sw.groups.reserve(2 * (parts.size() / 8 + nch + 1));
   w->seg.resize(nch);
+  std::vector<uint64_t> tri;
   for (uint64_t c = 0; c < nch; ++c) {
-    std::vector<uint64_t> tri;
+    tri.clear();
     tri.reserve(3 * (plo[c + 1] - plo[c]));
     for (uint64_t k = plo[c]; k < plo[c + 1]; ++k) {
       const Part& pp = parts[porder[k]];
@@ -427,6 +450,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     }
     w->seg[c] = sw.append(tri);
   }
+  mark("o:work");
   // detach order: positions in the (step-ordered) relocation table, grouped by release step
   std::vector<uint32_t> det(nsites);
   {

@@ -279,6 +279,12 @@ int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint
                       int elem, uint64_t chunk_bytes, cf_selective** out);
 int cf_selective_run(cf_selective* w, uint32_t flags, double scale);
 int cf_selective_free(cf_selective* w);
+/* Host-only dry run of cf_selective_plan + invariant check (no GPU): every array's bytes move
+ * exactly once, to the right device address, and each step scales exactly what it moved.
+ * mapped != 0 plans as if the host arrays were mapped (zero-copy for small arrays).  Returns
+ * CF_E_STATE (first violation in cf_last_error) on a violation. */
+int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count, int elem,
+                            uint64_t chunk_bytes, int mapped, uint64_t* nsteps);
 
 /* ---------------- unified memory (memory.py:239-261, 378-394) ---------------- */
 /* Managed-memory hints for the UVM scheme. dst_device < 0 prefetches to the host (the

@@ -49,7 +49,7 @@ EXPORTED = (
     "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
-    "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check",
+    "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_n_flushed",
     "cf_window_set_scale",
     "cf_window_free",
@@ -155,6 +155,7 @@ def _declare(L):
         "cf_sm_copy": (C.c_int, [P, P, P, U64, C.c_uint, P]),
         "cf_host_write_words": (C.c_int, [P, P, U64]),
         "cf_window_plan_check": (C.c_int, [C.POINTER(CfWindowDesc), C.POINTER(CfPlanCheck)]),
+        "cf_selective_plan_check": (C.c_int, [U64, P, P, P, C.c_int, U64, C.c_int, C.POINTER(U64)]),
         "cf_naive_fixup_host": (C.c_int, [P, P, P, U64, P, P, P, U64, C.POINTER(U64)]),
         "cf_window_plan": (C.c_int, [P, C.POINTER(CfWindowDesc), C.POINTER(P)]),
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),

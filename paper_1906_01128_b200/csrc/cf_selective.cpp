@@ -39,11 +39,19 @@ struct cf_selective {
   uint64_t tab_bytes = 0, off_cnt = 0, off_zs = 0, off_zd = 0, off_zb = 0;
   std::vector<cudaEvent_t> ev_in, ev_out;
   cudaEvent_t ev_start = nullptr, ev_tab = nullptr, ev_join = nullptr;
+  // dry run (cf_selective_plan_check): the host plan, no CUDA state
+  struct Dry { std::vector<uint64_t> zsrc, zdst, zbytes; ScaleWork sw; };
+  Dry* dry = nullptr;
 };
 
 namespace {
 void destroy(cf_selective* w) {
   if (!w) return;
+  if (w->dry) {
+    delete w->dry;
+    delete w;
+    return;
+  }
   CfDevice g(w->ctx);
   if (w->h_tab) cudaFreeHost(w->h_tab);
   if (w->d_tab) cudaFree(w->d_tab);
@@ -56,27 +64,31 @@ void destroy(cf_selective* w) {
 }
 }  // namespace
 
-extern "C" {
-
-int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
-                      int elem, uint64_t chunk_bytes, cf_selective** out) {
-  if (!ctx || !out || (n && (!h_src || !d_buf || !count))) return fail(CF_E_INVALID, "null argument");
+namespace {
+int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count, int elem,
+             uint64_t chunk_bytes, cf_selective** out, bool dry, bool dry_mapped) {
+  if (!out || (n && (!h_src || !d_buf || !count))) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
-  CfDevice g(ctx);
+  CfDevice g(dry ? nullptr : ctx);
   cf_selective* w = new cf_selective();
   w->ctx = ctx;
   w->elem = elem;
   w->n = n;
+  if (dry) w->dry = new cf_selective::Dry();
   const uint64_t ch = std::max<uint64_t>(chunk_bytes ? chunk_bytes : (16ull << 20), TILE_BYTES);
   // zero-copy needs every small array's host memory mapped at the same address (UVA pinned)
   bool mapped = true;
-  for (uint64_t i = 0; i < n && mapped; ++i) {
-    if (count[i] * uint64_t(elem) >= DMA_MIN) continue;
-    void* dp = nullptr;
-    mapped = cudaHostGetDevicePointer(&dp, reinterpret_cast<void*>(h_src[i]), 0) == cudaSuccess &&
-             reinterpret_cast<uint64_t>(dp) == h_src[i];
+  if (dry) {
+    mapped = dry_mapped;
+  } else {
+    for (uint64_t i = 0; i < n && mapped; ++i) {
+      if (count[i] * uint64_t(elem) >= DMA_MIN) continue;
+      void* dp = nullptr;
+      mapped = cudaHostGetDevicePointer(&dp, reinterpret_cast<void*>(h_src[i]), 0) == cudaSuccess &&
+               reinterpret_cast<uint64_t>(dp) == h_src[i];
+    }
+    cudaGetLastError();
   }
-  cudaGetLastError();
   std::vector<uint64_t> zsrc, zdst, zbytes;
   ScaleWork sw;
   sw.elem = elem;
@@ -126,6 +138,14 @@ int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint
   const uint64_t off_tb = al8(off_parts + sw.parts.size() * 4);
   const uint64_t off_grp = al8(off_tb + sw.tile_base.size() * 8);
   w->tab_bytes = al8(off_grp + sw.groups.size() * 4 + 8);
+  if (dry) {
+    w->dry->zsrc = std::move(zsrc);
+    w->dry->zdst = std::move(zdst);
+    w->dry->zbytes = std::move(zbytes);
+    w->dry->sw = std::move(sw);
+    *out = w;
+    return CF_OK;
+  }
   cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "selective tables: %s", cudaGetErrorString(ce)); }
@@ -160,6 +180,82 @@ int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint
   if (!ok) { cudaGetLastError(); destroy(w); return fail(CF_E_CUDA, "selective window streams/events"); }
   *out = w;
   return CF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
+                      int elem, uint64_t chunk_bytes, cf_selective** out) {
+  if (!ctx) return fail(CF_E_INVALID, "null argument");
+  return sel_plan(ctx, n, h_src, d_buf, count, elem, chunk_bytes, out, false, false);
+}
+
+int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count, int elem,
+                            uint64_t chunk_bytes, int mapped, uint64_t* nsteps) {
+  // invariants: every array's bytes move exactly once (DMA pieces or one zero-copy entry) from its
+  // host address to its device buffer, and the leaf kernel of step k scales exactly the elements
+  // that moved in step k -- each array's [0, count) once
+  cf_selective* w = nullptr;
+  CF_TRY(sel_plan(nullptr, n, h_src, d_buf, count, elem, chunk_bytes, &w, true, mapped != 0));
+  const auto& D = *w->dry;
+  const uint64_t e = uint64_t(elem);
+  int bad = 0;
+  auto report = [&](const char* msg, uint64_t a, uint64_t b) {
+    if (bad++ == 0) fail(CF_E_STATE, "%s (%llu, %llu)", msg, (unsigned long long)a, (unsigned long long)b);
+  };
+  std::vector<std::vector<std::pair<uint64_t, uint64_t>>> moved(n), scaled(n);   // element ranges per array
+  // address -> array lookup over the host ranges (sorted by host address)
+  std::vector<std::pair<uint64_t, uint64_t>> by_host;
+  for (uint64_t i = 0; i < n; ++i)
+    if (count[i]) by_host.push_back({h_src[i], i});
+  std::sort(by_host.begin(), by_host.end());
+  auto owner = [&](uint64_t host) -> int64_t {
+    auto it = std::upper_bound(by_host.begin(), by_host.end(), std::make_pair(host, ~uint64_t(0)));
+    if (it == by_host.begin()) return -1;
+    --it;
+    const uint64_t i = it->second;
+    return host < h_src[i] + count[i] * e ? int64_t(i) : -1;
+  };
+  for (uint64_t k = 0; k < w->nsteps; ++k) {
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> step_moved(n);
+    auto move = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
+      const int64_t i = owner(src);
+      if (i < 0) { report("copy from outside every array", src, bytes); return; }
+      const uint64_t off = src - h_src[i];
+      if (dst != d_buf[i] + off || off % e || bytes % e || off + bytes > count[i] * e) { report("copy misplaced", src, dst); return; }
+      step_moved[i].push_back({off / e, (off + bytes) / e});
+      moved[i].push_back({off / e, (off + bytes) / e});
+    };
+    for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j) move(w->dma[j].src, w->dma[j].dst, w->dma[j].bytes);
+    for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j) move(D.zsrc[j], D.zdst[j], D.zbytes[j]);
+    const cf_scale_work& ws = w->work[k];
+    auto part = [&](uint64_t p) {
+      const uint64_t i = D.sw.parts[3 * p], e0 = D.sw.parts[3 * p + 1], e1 = D.sw.parts[3 * p + 2];
+      if (i >= n) { report("part names array", p, i); return; }
+      bool in = false;   // the part's elements moved in this very step
+      for (auto& r : step_moved[i]) in |= r.first <= e0 && e1 <= r.second;
+      if (!in) report("part scaled in a step that did not move it", i, k);
+      scaled[i].push_back({e0, e1});
+    };
+    for (uint64_t p = ws.big_begin; p < ws.big_begin + ws.big_count; ++p) part(p);
+    for (uint64_t gr = ws.group_begin; gr < ws.group_end; ++gr)
+      for (uint64_t p = D.sw.groups[2 * gr]; p < D.sw.groups[2 * gr + 1]; ++p) part(p);
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    for (auto* v : {&moved[i], &scaled[i]}) {
+      std::sort(v->begin(), v->end());
+      uint64_t y = 0;
+      for (auto& r : *v) {
+        if (r.first != y) { report("array not tiled exactly once", i, r.first); break; }
+        y = r.second;
+      }
+      if (y != count[i]) report("array covered up to", i, y);
+    }
+  if (nsteps) *nsteps = w->nsteps;
+  destroy(w);
+  return bad ? CF_E_STATE : CF_OK;
 }
 
 int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {

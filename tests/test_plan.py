@@ -81,3 +81,28 @@ def test_full_size_baseline_schedules(cfg, chunk_mb):
     spec, policy, _ = bench.make_spec(cfg)
     out = check(spec, 16, policy, chunk_mb << 20)
     assert out.nsteps >= 30
+
+
+@pytest.mark.parametrize("mapped", [0, 1])
+def test_pointerchain_window_plans(mapped):
+    """cf_selective_plan_check: every targeted array moves exactly once to its device buffer and
+    each step scales exactly what it moved -- mixes of big (split), medium and tiny arrays."""
+    rng = random.Random(11 + mapped)
+    for trial in range(40):
+        n = rng.randint(0, 300)
+        elem = rng.choice([4, 8])
+        counts = np.array([rng.choice([0, 1, 7, 300, 5000, 20000, 300000, 3_000_000]) for _ in range(n)], np.uint64)
+        sizes = counts * np.uint64(elem)
+        host = np.zeros(n, np.uint64)
+        dev = np.zeros(n, np.uint64)
+        hb, db = 0x7f0000000000, 0x7e0000000000
+        for i in range(n):
+            host[i], dev[i] = hb, db
+            hb += int(sizes[i]) + 4 * rng.randint(0, 3) + (4 if elem == 8 and rng.random() < 0.3 else 0)
+            db += (int(sizes[i]) + 7) // 8 * 8
+        steps = N.U64(0)
+        chunk = rng.choice([1 << 16, 1 << 20, 32 << 20])
+        rc = N.lib().cf_selective_plan_check(n, N.ptr(host) if n else None, N.ptr(dev) if n else None,
+                                             N.ptr(counts) if n else None, elem, chunk, mapped, C.byref(steps))
+        assert rc == 0, (trial, N.last_error())
+        assert steps.value >= 1

@@ -17,9 +17,17 @@ cfgs = sys.argv[2:] or ["C2", "C3", "C4"]
 deadline = time.time() + secs
 per = secs / len(cfgs)
 total = 0
+EXTRA = {   # packed reference layouts: f64 leaves at 4 mod 8 (word-streaming kernel), 12-byte leaf records
+    "P3": (lambda: __import__("paper_1906_01128_b200").DenseSpec(3, 5 << 20, 3, elem=8, leaf_only=True), "all_leaves", 1),
+    "P4": (lambda: __import__("paper_1906_01128_b200").DenseSpec(4, 2 << 20, 3, elem=8, leaf_only=True), "all_leaves", 1),
+}
 for cfg in cfgs:
-    spec, policy, _ = bench.make_spec(cfg)
-    w = DeepCopyWindow(spec, seed=1, policy=policy)
+    if cfg in EXTRA:
+        mk, policy, align = EXTRA[cfg]
+        spec = mk()
+    else:
+        (spec, policy, _), align = bench.make_spec(cfg), 16
+    w = DeepCopyWindow(spec, seed=1, policy=policy, align=align)
     t = w.twin()
     off, cnt, lvl = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT), w.table(N.CF_TAB_ARR_LEVEL)
     src = w.host_src().copy()
@@ -37,8 +45,9 @@ for cfg in cfgs:
         got = t.host_dst()
         for i in (int(w.targets[0]), int(w.targets[len(w.targets) // 2]), int(w.targets[-1])):
             a, n = int(off[i]), int(cnt[i])
-            want = (payload_values(1, int(lvl[i]), n, spec.elem) * np.float32(0.5)).astype(np.float32)
-            assert np.array_equal(got[a:a + 4 * n].view(np.float32), want), (cfg, it, i)
+            dt = np.float32 if spec.elem == 4 else np.float64
+            want = (payload_values(1, int(lvl[i]), n, spec.elem) * dt(0.5)).astype(dt)
+            assert np.array_equal(np.frombuffer(got[a:a + spec.elem * n].tobytes(), dt), want), (cfg, it, i)
         it += 1
         total += 18
     print(f"{cfg}: {it} rounds ({it * 18} windows) ok", flush=True)

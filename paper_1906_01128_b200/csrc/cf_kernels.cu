@@ -142,7 +142,7 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
   // base-q digits of the ordinal, most significant first: rem / q^(L-l), rem %= q^(L-l).  Ordinals
   // are u32 (window tables), so the divisions run in 32 bits -- 64-bit integer division is a long
   // emulated sequence and made the 1M-chain resolve instruction-bound (C4: 17 us).
-  uint32_t qpow = 1, rem = uint32_t(ordinal);
+  uint32_t qpow = 1, rem = uint32_t(ordinal) & 0x7FFFFFFFu;   // bit 31: owned-attach flag (wide kernel)
   if (dense)
     for (int l = 1; l < level; ++l) qpow *= sh.q;
   for (int l = 1; l <= level; ++l) {
@@ -209,7 +209,10 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
 
 // Large windows on an aligned arena (C4: 1.02M sites, 1M chains): attach and resolve in ONE
 // launch, side by side -- CTAs [0, att_blocks) relocate sites, the rest resolve chains,
-// translating any host pointer they meet that the attach CTAs have not rewritten yet.
+// translating any host pointer they meet that the attach CTAs have not rewritten yet (8-byte
+// aligned fields: one atomic access).  A target whose ordinal carries bit 31 owns its A field
+// (a 4-mod-8 leaf field attached in this step, left out of the attach CTAs' list): its resolver
+// attaches it, so no misaligned field is ever read while another thread writes it.
 __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict__ image, uint64_t total,
                                                              const uint64_t* __restrict__ sites, uint64_t nsites,
                                                              uint64_t from, uint64_t to, cf_chain_shape sh,
@@ -225,14 +228,30 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
   }
   const uint64_t i = uint64_t(blockIdx.x - att_blocks) * blockDim.x + threadIdx.x;
   if (i >= ntargets) return;
-  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i], from);
+  const uint32_t od = ordinal[i];
+  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], od, from);
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
     raise_bad(bad, i);
     return;
   }
-  ea[i] = xlate(ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)), from, image, sh.image_bytes);
+  uint8_t* fa = const_cast<uint8_t*>(w.node) + (w.leaf ? LEAF_OFF_A : OFF_A);   // image is writable here
+  uint64_t v = ld_u64_any(fa);
+  if (od >> 31) {
+    // owned field (4 mod 8, attached in this step): no attach CTA touches it and this thread is its
+    // only reader, so the 2 x u32 read sees the untouched host value -- attach it here
+    const uint64_t dlt = v - from;
+    if (dlt >= total) {
+      ea[i] = 0;
+      count[i] = 0;
+      raise_bad(bad, i);
+      return;
+    }
+    v = to + dlt;
+    st_u64_any(fa, v);
+  }
+  ea[i] = xlate(v, from, image, sh.image_bytes);
   count[i] = ld_u32_any(w.node + OFF_NA);
 }
 

@@ -44,6 +44,11 @@ struct cf_window {
   std::vector<uint64_t> seg_lo, seg_hi;          // segments in upload order
   std::vector<uint64_t> step_seg_lo;             // segments of step k: [step_seg_lo[k], step_seg_lo[k+1])
   std::vector<uint64_t> reloc_lo;      // attach-site ranges per step (sites grouped by step)
+  // per step: how many of the step's sites the attach CTAs of a one-launch attach || resolve take;
+  // the rest (misaligned leaf A fields of targets resolved at the same step) are attached by their
+  // own resolver thread, the only reader of that field in the launch
+  std::vector<uint64_t> attach_n;
+  bool owned_attach = false;
   std::vector<uint64_t> res_lo;        // resolve-target ranges per step
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step
@@ -72,6 +77,7 @@ struct cf_window {
   // by an aligned arena: 12-byte dense leaf records put every other leaf's A field at 4 mod 8
   // (2 x u32 accesses, which a concurrent attach can tear).
   bool aligned8 = false;
+  bool wide_ok = false;    // aligned8, or every misaligned field is a leaf A field (owned attach)
   // CF_WIN_GRAPH: one instantiated graph per scale value (run_n alternates two scales)
   struct Graph { double scale; cudaGraphExec_t exec; uint64_t h2d, d2h, launches; };
   std::vector<Graph> graphs;
@@ -79,6 +85,7 @@ struct cf_window {
   struct Dry {
     std::vector<uint64_t> reloc, torder, ready, release, seg_step, part_step;
     std::vector<uint32_t> det;
+    std::vector<uint8_t> owned;   // per target (desc order): resolver attaches its own A field
     cf::ScaleWork sw;
   };
   Dry* dry = nullptr;
@@ -429,6 +436,51 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   bucket_order(ready, nch, torder, w->res_lo);
   std::vector<uint64_t> tpos(nt);
   for (uint64_t k = 0; k < nt; ++k) tpos[torder[k]] = k;
+  // attach || resolve in one launch: safe when every field a resolver may read while the attach
+  // CTAs rewrite it is 8-byte aligned (one atomic 64-bit access).  Dense 12-byte leaf records put
+  // every other leaf's A field at 4 mod 8; a resolver is that field's only reader, so when the
+  // field is attached in the step that resolves its target, the resolver attaches it itself.
+  w->aligned8 = std::all_of(sites, sites + nsites, [](uint64_t o) { return (o & 7) == 0; });
+  std::vector<uint8_t> owned_target(nt, 0);
+  {
+    bool misaligned_only_leaf_a = dense && !chase;
+    if (misaligned_only_leaf_a && !w->aligned8) {
+      std::vector<uint64_t> leafs;
+      for (const auto& tr : t->level_nodes)
+        if (tr.size() > size_t(t->spec.depth)) leafs.insert(leafs.end(), tr[size_t(t->spec.depth)].begin(), tr[size_t(t->spec.depth)].end());
+      std::sort(leafs.begin(), leafs.end());
+      for (uint64_t i = 0; i < nsites && misaligned_only_leaf_a; ++i)
+        if (sites[i] & 7) misaligned_only_leaf_a = std::binary_search(leafs.begin(), leafs.end(), sites[i] - LEAF_OFF_A);
+    }
+    w->wide_ok = w->aligned8 || misaligned_only_leaf_a;
+    w->owned_attach = w->wide_ok && !w->aligned8;
+  }
+  w->attach_n.assign(nch, 0);
+  for (uint64_t k = 0; k < nch; ++k) w->attach_n[k] = w->reloc_lo[k + 1] - w->reloc_lo[k];
+  if (w->owned_attach) {
+    std::vector<uint8_t> owned_site(nsites, 0);
+    for (uint64_t i = 0; i < nt; ++i) {
+      const int64_t a = desc->h_targets[i];
+      if (t->arr_level[a] != int(t->spec.depth)) continue;             // leaf records only
+      const uint64_t fa = t->arr_owner[a] + LEAF_OFF_A;
+      if ((fa & 7) == 0 || step_of(fa) != ready[i]) continue;        // aligned, or attached earlier
+      const uint64_t r = uint64_t(std::lower_bound(reloc.begin() + w->reloc_lo[ready[i]], reloc.begin() + w->reloc_lo[ready[i] + 1], fa) -
+                                  reloc.begin());
+      if (r < w->reloc_lo[ready[i] + 1] && reloc[r] == fa) {
+        owned_site[r] = 1;
+        owned_target[i] = 1;
+      }
+    }
+    // within each step: sites the attach CTAs take first, owned sites after (address order kept)
+    for (uint64_t k = 0; k < nch; ++k) {
+      auto b = reloc.begin() + w->reloc_lo[k], e = reloc.begin() + w->reloc_lo[k + 1];
+      std::vector<uint64_t> keep, own;
+      for (auto it = b; it != e; ++it) (owned_site[size_t(it - reloc.begin())] ? own : keep).push_back(*it);
+      std::copy(keep.begin(), keep.end(), b);
+      std::copy(own.begin(), own.end(), b + keep.size());
+      w->attach_n[k] = keep.size();
+    }
+  }
   mark("o:targets");
   // per step: the pieces ready at that step, as one leaf-kernel launch (big tiles + small groups)
   std::vector<uint64_t> pstep(parts.size()), porder, plo;
@@ -495,7 +547,6 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
-  w->aligned8 = std::all_of(sites, sites + nsites, [](uint64_t o) { return (o & 7) == 0; });
   w->off_sites = 0;
   w->off_det = al8(w->off_sites + nsites * 8);
   w->off_level = al8(w->off_det + nsites * 4);
@@ -516,6 +567,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     D.release = std::move(release);
     D.seg_step = std::move(seg_step);
     D.part_step = std::move(pstep);
+    D.owned = std::move(owned_target);
     D.sw = std::move(sw);
     mark("tables");
     *out = w;
@@ -534,7 +586,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   for (uint64_t k = 0; k < nt; ++k) {
     const int64_t a = desc->h_targets[torder[k]];
     lv[k] = t->arr_level[a];
-    od[k] = uint32_t(t->arr_ordinal[a]);
+    od[k] = uint32_t(t->arr_ordinal[a]) | (owned_target[torder[k]] ? 0x80000000u : 0u);   // bit 31: attach own A field
     if (w->has_roots) rt[k] = t->arr_root[a];
   }
   if (!sw.parts.empty()) memcpy(w->h_tab + w->off_parts, sw.parts.data(), sw.parts.size() * 4);
@@ -642,6 +694,7 @@ struct Checker {
     std::vector<uint64_t> need_release(nseg, 0);
     for (uint64_t sg = 0; sg < nseg; ++sg) need_release[sg] = D.seg_step[sg];
     std::vector<std::vector<uint32_t>> chain_segs(nt);
+    std::vector<std::vector<uint64_t>> chain_fields(nt);   // pointer fields each resolver reads
     for (uint64_t i = 0; i < nt; ++i) {
       const int64_t a = d->h_targets[i];
       const int L = t->arr_level[a];
@@ -658,6 +711,7 @@ struct Checker {
         const uint64_t blk = target_of(node + OFF_LNEXT, ok);
         if (!ok) { bad("target %llu: no Lnext site at level %d", (unsigned long long)i, l); break; }
         touch(node + OFF_LNEXT, node + OFF_LNEXT + 8);
+        chain_fields[i].push_back(node + OFF_LNEXT);
         uint64_t pw = 1;
         for (int m = l; m < L; ++m) pw *= q;
         const uint64_t digit = dense ? (uint64_t(t->arr_ordinal[a]) / pw) % q : 0;
@@ -667,6 +721,7 @@ struct Checker {
                                        (unsigned long long)node, (unsigned long long)t->arr_owner[a]);
       const bool leaf = dense && L == int(t->spec.depth);
       touch(node + OFF_NA, node + (leaf ? LEAF_NODE_SIZE : OFF_LNEXT));
+      chain_fields[i].push_back(node + (leaf ? LEAF_OFF_A : OFF_A));
       if (D.ready[i] != r) bad("target %llu ready at step %llu, its chain lands at %llu", (unsigned long long)i,
                                (unsigned long long)D.ready[i], (unsigned long long)r);
     }
@@ -674,6 +729,34 @@ struct Checker {
       for (uint64_t k = w->res_lo[c]; k < w->res_lo[c + 1]; ++k)
         if (D.ready[D.torder[k]] != c) bad("target resolved at step %llu is ready at %llu", (unsigned long long)c,
                                            (unsigned long long)D.ready[D.torder[k]]);
+    // 3b. one-launch attach || resolve: no misaligned field in the attach CTAs' list is read by a
+    //     resolver of the same step; every owned field sits in its target's step's owned tail
+    if (w->wide_ok) {
+      std::vector<std::vector<uint64_t>> read_at(nch);   // misaligned fields read by resolvers, per step
+      for (uint64_t i = 0; i < nt; ++i)
+        for (uint64_t f : chain_fields[i])
+          if (f & 7) read_at[D.ready[i]].push_back(f);
+      for (auto& v : read_at) std::sort(v.begin(), v.end());
+      for (uint64_t k = 0; k < nch; ++k) {
+        for (uint64_t j = w->reloc_lo[k]; j < w->reloc_lo[k] + w->attach_n[k]; ++j)
+          if ((D.reloc[j] & 7) && std::binary_search(read_at[k].begin(), read_at[k].end(), D.reloc[j]))
+            bad("misaligned site %llu attached by the attach CTAs while a resolver reads it (step %llu)",
+                (unsigned long long)D.reloc[j], (unsigned long long)k);
+        std::vector<uint64_t> tail(D.reloc.begin() + w->reloc_lo[k] + w->attach_n[k], D.reloc.begin() + w->reloc_lo[k + 1]);
+        std::sort(tail.begin(), tail.end());
+        uint64_t owners = 0;
+        for (uint64_t p2 = w->res_lo[k]; p2 < w->res_lo[k + 1]; ++p2) {
+          const uint64_t i = D.torder[p2];
+          if (!D.owned[i]) continue;
+          ++owners;
+          const uint64_t fa = t->arr_owner[d->h_targets[i]] + LEAF_OFF_A;
+          if (!std::binary_search(tail.begin(), tail.end(), fa)) bad("owned A field of target %llu not in step %llu's tail",
+                                                                     (unsigned long long)i, (unsigned long long)k);
+        }
+        if (owners != tail.size()) bad("step %llu: %llu owned sites, %llu owning resolvers", (unsigned long long)k,
+                                       (unsigned long long)tail.size(), (unsigned long long)owners);
+      }
+    }
     // 4. parts: tile every target's [0, count) once, each after its bytes and its chain
     std::vector<std::vector<std::pair<uint64_t, uint64_t>>> cover(nt);
     std::vector<uint64_t> max_part(nt, 0);
@@ -994,8 +1077,8 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
                                    drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
                                    w->d_count + w->res_lo[k], c->d_bad, cs));
-    } else if (do_attach && do_resolve && w->aligned8) {
-      CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
+    } else if (do_attach && do_resolve && w->wide_ok) {
+      CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
                                         w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
     } else {

@@ -31,6 +31,19 @@ void clear_error();
                         __FILE__, __LINE__);                                               \
   } while (0)
 
+// Host<->device bulk copy whose host-side start is first brought to a 256-byte boundary by a
+// small separate copy.  The copy engines lose ~13% of full-duplex throughput when a large
+// transfer's host address is only 16-byte aligned, and splitting off the head recovers it
+// (tools/duplex_probe.cu; profiles/r01_design_experiments.md "host alignment of DMA pieces").
+inline cudaError_t copy_host_aligned(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t s) {
+  const uintptr_t hp = reinterpret_cast<uintptr_t>(kind == cudaMemcpyHostToDevice ? src : dst);
+  const size_t head = (256 - (hp & 255)) & 255;
+  if (n < (size_t(1) << 20) || head == 0) return cudaMemcpyAsync(dst, src, n, kind, s);
+  cudaError_t e = cudaMemcpyAsync(dst, src, head, kind, s);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(static_cast<char*>(dst) + head, static_cast<const char*>(src) + head, n - head, kind, s);
+}
+
 #define CF_TRY(expr)            \
   do {                          \
     int r_ = (expr);            \

@@ -157,7 +157,7 @@ int cf_marshal_transfer_and_attach(cf_ctx* c, const void* host_arena, uint64_t t
   for (size_t i = 0; i < nch; ++i) {
     cudaStream_t s = c->h2d[i % c->h2d.size()];
     if (i < c->h2d.size()) CF_CUDA(cudaStreamWaitEvent(s, ev.ev[nch], 0));
-    CF_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(image) + b[i], static_cast<const uint8_t*>(host_arena) + b[i],
+    CF_CUDA(copy_host_aligned(static_cast<uint8_t*>(image) + b[i], static_cast<const uint8_t*>(host_arena) + b[i],
                             b[i + 1] - b[i], cudaMemcpyHostToDevice, s));
     CF_CUDA(cudaEventRecord(ev.ev[i], s));
     // sites whose field lies in this chunk are relocated as soon as it lands
@@ -207,7 +207,7 @@ int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const
   CF_CUDA(cudaStreamWaitEvent(c->d2h, ev.ev[0], 0));
   std::vector<uint64_t> b = chunk_bounds(total, chunk_bytes, h_sites, nsites);
   for (size_t i = 0; i + 1 < b.size(); ++i)
-    CF_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(host_arena) + b[i], static_cast<const uint8_t*>(image) + b[i],
+    CF_CUDA(copy_host_aligned(static_cast<uint8_t*>(host_arena) + b[i], static_cast<const uint8_t*>(image) + b[i],
                             b[i + 1] - b[i], cudaMemcpyDeviceToHost, c->d2h));
   CF_CUDA(cudaStreamSynchronize(c->d2h));
   uint64_t bad = NO_BAD;

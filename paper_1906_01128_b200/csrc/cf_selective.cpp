@@ -281,7 +281,7 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
   for (uint64_t k = 0; k < w->nsteps; ++k) {
     if (flags & CF_WIN_H2D) {
       for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
-        CF_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),
+        CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),
                                 w->dma[j].bytes, cudaMemcpyHostToDevice, hs));
       CF_CUDA(cudaEventRecord(w->ev_in[k], hs));
       CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k], 0));
@@ -295,7 +295,7 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
       CF_CUDA(cudaEventRecord(w->ev_out[k], cs));
       CF_CUDA(cudaStreamWaitEvent(ds, w->ev_out[k], 0));
       for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
-        CF_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(w->dma[j].src), reinterpret_cast<const void*>(w->dma[j].dst),
+        CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].src), reinterpret_cast<const void*>(w->dma[j].dst),
                                 w->dma[j].bytes, cudaMemcpyDeviceToHost, ds));
       // small arrays pushed back by SM stores into mapped host memory, on the D2H stream
       CF_TRY(launch_copy_list(c, zd + w->zc_lo[k], zs + w->zc_lo[k], zb + w->zc_lo[k], w->zc_lo[k + 1] - w->zc_lo[k], ds));

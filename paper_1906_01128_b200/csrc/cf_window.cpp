@@ -1065,7 +1065,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       cudaStream_t s = c->h2d[k % c->h2d.size()];
       for (uint64_t j = w->step_seg_lo[k]; j < w->step_seg_lo[k + 1]; ++j) {
         const uint64_t lo = w->seg_lo[j], hi = w->seg_hi[j];
-        CF_CUDA(cudaMemcpyAsync(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
+        CF_CUDA(copy_host_aligned(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
         h2d_bytes += hi - lo;
       }
       CF_CUDA(cudaEventRecord(w->ev_h2d[k], s));
@@ -1119,7 +1119,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_rel[k], 0));
       for (uint32_t r : w->released[k]) {
         const uint64_t rlo = w->seg_lo[r], rhi = w->seg_hi[r];
-        CF_CUDA(cudaMemcpyAsync(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
+        CF_CUDA(copy_host_aligned(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
         d2h_bytes += rhi - rlo;
       }
     }

@@ -543,6 +543,15 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     for (uint64_t id : ids) zc_rel.insert(zc_rel.end(), {w->seg_lo[id], w->seg_hi[id]});
   }
 
+  if (getenv("CF_PLAN_DUMP")) {   // design experiments: the step schedule, one line per step
+    for (uint64_t k = 0; k < nch; ++k) {
+      uint64_t up = 0, down = 0;
+      for (uint64_t j = w->step_seg_lo[k]; j < w->step_seg_lo[k + 1]; ++j) up += w->seg_hi[j] - w->seg_lo[j];
+      for (uint32_t r : w->released[k]) down += w->seg_hi[r] - w->seg_lo[r];
+      fprintf(stderr, "step %llu up %llu down %llu nrel %zu\n", (unsigned long long)k, (unsigned long long)up,
+              (unsigned long long)down, w->released[k].size());
+    }
+  }
   mark("released");
   // ---- table block: sites | det | level | ordinal | parts | tile_base | groups
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };

@@ -8,7 +8,13 @@
 // DMA_MIN bytes move on the copy engines (one H2D and one D2H stream, so the two directions
 // overlap over the full-duplex link); smaller ones move by zero-copy SM kernels over the mapped
 // pinned host memory, one warp per array, which avoids one copy-engine command per object (the
-// C4 shape has a million 1 KiB arrays).  All bookkeeping is planned once; a run only enqueues.
+// C4 shape has a million 1 KiB arrays).  When a step's small arrays fill most of the host span
+// they lie in (address-ordered layouts: C4's leaf arrays sit between 1.2 KB leaf blocks), that
+// span goes in as ONE copy-engine DMA into a device staging area and a device-side copy list
+// moves each array into its buffer: copy engine H2D beside SM-store D2H runs the full-duplex link
+// at 88 GB/s where SM traffic both ways reaches 77 (profiles/r01_design_experiments.md).  The
+// span's bytes between arrays are read, never written back.  All bookkeeping is planned once; a
+// run only enqueues.
 #include "cf_internal.h"
 
 #include <algorithm>
@@ -19,6 +25,8 @@ using namespace cf;
 
 namespace {
 constexpr uint64_t DMA_MIN = 64 << 10;
+// a step's small arrays are staged through one span DMA when they fill at least this share of it
+constexpr double SPAN_MIN_FILL = 0.75;
 }
 
 struct cf_selective {
@@ -32,11 +40,16 @@ struct cf_selective {
   std::vector<uint64_t> zc_lo;             // per step: range in the zero-copy list
   std::vector<cf_scale_work> work;         // per step: leaf-kernel work (device pointers set)
   uint64_t nzc = 0;
+  std::vector<Piece> span;                 // per step: staged host span (bytes 0 = none); dst = staging offset
+  uint8_t* d_stage = nullptr;              // staging area (device) for the span DMAs
+  uint64_t stage_bytes = 0;
   // one pinned table block + device mirror: ea u64[n] | count u32[n] | zc src u64[nzc] |
-  // zc dst u64[nzc] | zc bytes u64[nzc] | parts | tile_base | groups
+  // zc dst u64[nzc] | zc bytes u64[nzc] | zc in-source u64[nzc] | parts | tile_base | groups
+  // (in-source: where the H2D copy list reads an entry -- its host address, or its place in the
+  // staging area when its step's span is staged)
   uint8_t* h_tab = nullptr;
   uint8_t* d_tab = nullptr;
-  uint64_t tab_bytes = 0, off_cnt = 0, off_zs = 0, off_zd = 0, off_zb = 0;
+  uint64_t tab_bytes = 0, off_cnt = 0, off_zs = 0, off_zd = 0, off_zb = 0, off_zi = 0;
   std::vector<cudaEvent_t> ev_in, ev_out;
   cudaEvent_t ev_start = nullptr, ev_tab = nullptr, ev_join = nullptr;
   // dry run (cf_selective_plan_check): the host plan, no CUDA state
@@ -55,6 +68,7 @@ void destroy(cf_selective* w) {
   CfDevice g(w->ctx);
   if (w->h_tab) cudaFreeHost(w->h_tab);
   if (w->d_tab) cudaFree(w->d_tab);
+  if (w->d_stage) cudaFree(w->d_stage);
   for (auto e : w->ev_in) cudaEventDestroy(e);
   for (auto e : w->ev_out) cudaEventDestroy(e);
   for (auto e : {w->ev_start, w->ev_tab, w->ev_join})
@@ -128,13 +142,31 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
   if (acc || w->work.empty()) close_step();
   w->nsteps = w->work.size();
   w->nzc = zsrc.size();
+  // staged spans: per step, the host range its zero-copy entries lie in, when they fill it densely
+  // (staging offsets keep the host address mod 256, so the copy list's 16-byte paths still apply)
+  w->span.assign(w->nsteps, cf_selective::Piece{0, 0, 0});
+  for (uint64_t k = 0; k < w->nsteps; ++k) {
+    const uint64_t z0 = w->zc_lo[k], z1 = w->zc_lo[k + 1];
+    if (z1 - z0 < 2) continue;
+    uint64_t lo = ~uint64_t(0), hi = 0, fill = 0;
+    for (uint64_t j = z0; j < z1; ++j) {
+      lo = std::min(lo, zsrc[j]);
+      hi = std::max(hi, zsrc[j] + zbytes[j]);
+      fill += zbytes[j];
+    }
+    if (hi - lo < DMA_MIN || double(fill) < SPAN_MIN_FILL * double(hi - lo)) continue;
+    const uint64_t off = (w->stage_bytes + 255) / 256 * 256 + (lo & 255);
+    w->span[k] = cf_selective::Piece{lo, off, hi - lo};
+    w->stage_bytes = off + (hi - lo);
+  }
   // table block
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->off_cnt = al8(n * 8);
   w->off_zs = al8(w->off_cnt + n * 4);
   w->off_zd = w->off_zs + w->nzc * 8;
   w->off_zb = w->off_zd + w->nzc * 8;
-  const uint64_t off_parts = w->off_zb + w->nzc * 8;
+  w->off_zi = w->off_zb + w->nzc * 8;
+  const uint64_t off_parts = w->off_zi + w->nzc * 8;
   const uint64_t off_tb = al8(off_parts + sw.parts.size() * 4);
   const uint64_t off_grp = al8(off_tb + sw.tile_base.size() * 8);
   w->tab_bytes = al8(off_grp + sw.groups.size() * 4 + 8);
@@ -148,6 +180,7 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
   }
   cudaError_t ce = cudaHostAlloc(&w->h_tab, w->tab_bytes, cudaHostAllocPortable);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
+  if (ce == cudaSuccess && w->stage_bytes) ce = cudaMalloc(&w->d_stage, w->stage_bytes);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "selective tables: %s", cudaGetErrorString(ce)); }
   uint32_t* cnt32 = reinterpret_cast<uint32_t*>(w->h_tab + w->off_cnt);
   for (uint64_t i = 0; i < n; ++i) {
@@ -159,6 +192,11 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
     memcpy(w->h_tab + w->off_zs, zsrc.data(), w->nzc * 8);
     memcpy(w->h_tab + w->off_zd, zdst.data(), w->nzc * 8);
     memcpy(w->h_tab + w->off_zb, zbytes.data(), w->nzc * 8);
+    uint64_t* zi = reinterpret_cast<uint64_t*>(w->h_tab + w->off_zi);
+    for (uint64_t k = 0; k < w->nsteps; ++k)
+      for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j)
+        zi[j] = w->span[k].bytes ? reinterpret_cast<uint64_t>(w->d_stage) + w->span[k].dst + (zsrc[j] - w->span[k].src)
+                                 : zsrc[j];
   }
   if (!sw.parts.empty()) memcpy(w->h_tab + off_parts, sw.parts.data(), sw.parts.size() * 4);
   if (!sw.tile_base.empty()) memcpy(w->h_tab + off_tb, sw.tile_base.data(), sw.tile_base.size() * 8);
@@ -218,6 +256,7 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
     const uint64_t i = it->second;
     return host < h_src[i] + count[i] * e ? int64_t(i) : -1;
   };
+  uint64_t stage_end = 0;
   for (uint64_t k = 0; k < w->nsteps; ++k) {
     std::vector<std::vector<std::pair<uint64_t, uint64_t>>> step_moved(n);
     auto move = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
@@ -230,6 +269,14 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
     };
     for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j) move(w->dma[j].src, w->dma[j].dst, w->dma[j].bytes);
     for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j) move(D.zsrc[j], D.zdst[j], D.zbytes[j]);
+    // a staged span holds every zero-copy entry of its step, in its own slice of the staging area
+    const auto& sp = w->span[k];
+    if (sp.bytes) {
+      if (sp.dst < stage_end || sp.dst % 256 != sp.src % 256) report("staging slice misplaced", k, sp.dst);
+      stage_end = sp.dst + sp.bytes;
+      for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j)
+        if (D.zsrc[j] < sp.src || D.zsrc[j] + D.zbytes[j] > sp.src + sp.bytes) report("entry outside its staged span", k, j);
+    }
     const cf_scale_work& ws = w->work[k];
     auto part = [&](uint64_t p) {
       const uint64_t i = D.sw.parts[3 * p], e0 = D.sw.parts[3 * p + 1], e1 = D.sw.parts[3 * p + 2];
@@ -253,6 +300,7 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
       }
       if (y != count[i]) report("array covered up to", i, y);
     }
+  if (stage_end > w->stage_bytes) report("staging area too small", stage_end, w->stage_bytes);
   if (nsteps) *nsteps = w->nsteps;
   destroy(w);
   return bad ? CF_E_STATE : CF_OK;
@@ -268,6 +316,7 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
   const uint64_t* zs = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zs);
   const uint64_t* zd = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zd);
   const uint64_t* zb = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zb);
+  const uint64_t* zi = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zi);
   // fan out from the context's compute stream (ordered after earlier work on this context)
   CF_CUDA(cudaEventRecord(w->ev_start, c->compute));
   for (cudaStream_t s : {cs, hs, ds}) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
@@ -283,10 +332,14 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
       for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
         CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),
                                 w->dma[j].bytes, cudaMemcpyHostToDevice, hs));
+      const cf_selective::Piece& sp = w->span[k];
+      if (sp.bytes)
+        CF_CUDA(copy_host_aligned(w->d_stage + sp.dst, reinterpret_cast<const void*>(sp.src), sp.bytes, cudaMemcpyHostToDevice, hs));
       CF_CUDA(cudaEventRecord(w->ev_in[k], hs));
       CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k], 0));
-      // small arrays: one warp per array pulls it over the mapped host memory
-      CF_TRY(launch_copy_list(c, zs + w->zc_lo[k], zd + w->zc_lo[k], zb + w->zc_lo[k], w->zc_lo[k + 1] - w->zc_lo[k], cs));
+      // small arrays: one warp per array pulls it over the mapped host memory, or out of the
+      // staged span in HBM
+      CF_TRY(launch_copy_list(c, zi + w->zc_lo[k], zd + w->zc_lo[k], zb + w->zc_lo[k], w->zc_lo[k + 1] - w->zc_lo[k], cs));
     }
     if (flags & CF_WIN_SCALE)
       CF_TRY(launch_scale(c, w->elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, nullptr, ea, cnt, w->work[k], scale,

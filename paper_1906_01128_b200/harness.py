@@ -369,22 +369,34 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
     if scheme == "pointerchain":
         # host-side chain resolution, then one selective bulk copy per targeted array
         # (harness.py:228-238), submitted together as one batched copy into one device span
-        idx = handle.target_indices(policy)
-        idx = idx[handle.arr_count[idx] > 0]
+        # the selection and its span layout depend only on the (immutable) tree shape and the
+        # policy: computed once per tree (C4: 1M targets, 16 ms of numpy per window otherwise)
         e = handle.spec.elem
-        sizes = handle.arr_count[idx] * np.uint64(e)
-        aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
-        offs = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64) if len(idx) else aligned
-        prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx,
-                          buf_host=handle.arr_off[idx] + np.uint64(handle.base), buf_count=handle.arr_count[idx])
+        cache = handle.__dict__.setdefault("_selective_layout", {})
+        lay = cache.get(policy)
+        if lay is None:
+            idx = handle.target_indices(policy)
+            idx = idx[handle.arr_count[idx] > 0]
+            sizes = handle.arr_count[idx] * np.uint64(e)
+            aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
+            offs = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64) if len(idx) else aligned
+            lay = cache[policy] = (idx, sizes, sizes.astype(np.int64), offs, int(aligned.sum()),
+                                   np.ascontiguousarray(handle.arr_off[idx] + np.uint64(handle.base)),
+                                   np.ascontiguousarray(handle.arr_count[idx]), {})
+        idx, sizes, sizes_i64, offs, span, buf_host, buf_count, by_base = lay
+        prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx, buf_host=buf_host, buf_count=buf_count)
         if len(idx):
             spare = handle.__dict__.setdefault("_spare_spans", {})
-            dev_base = spare.pop(policy, 0) or machine.device.allocate_span(int(aligned.sum()), offs, sizes, zero=False)
-            prep.buf_dev = offs + np.uint64(dev_base)
+            dev_base = spare.pop(policy, 0) or machine.device.allocate_span(span, offs, sizes, zero=False)
+            prep.buf_dev = by_base.get(dev_base)
+            if prep.buf_dev is None:
+                if len(by_base) >= 4:
+                    by_base.clear()
+                prep.buf_dev = by_base[dev_base] = offs + np.uint64(dev_base)
             if fused:
                 # addresses come from the tree's own array table and the span just allocated for
                 # exactly these sizes: in bounds by construction (the eager path re-checks them)
-                machine.log.append_many(H2D, "bulk", sizes.astype(np.int64))
+                machine.log.append_many(H2D, "bulk", sizes_i64)
                 prep.fused = FusedSelectiveWindow(machine, prep, e)
                 machine._deferred = prep.fused
             else:

@@ -577,9 +577,18 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
             stats.elements_touched = int(cnt.sum())
         return stats
 
-    idx = handle.target_indices(prep.policy)
-    idx = idx[handle.arr_count[idx] > 0]
-    stats.chain_derefs = _reference_derefs(handle, prep.policy, idx)
+    # per policy the kernel's arguments depend only on the immutable tree shape: computed once
+    kcache = handle.__dict__.setdefault("_kernel_args", {})
+    ka = kcache.get(prep.policy)
+    if ka is None:
+        idx = handle.target_indices(prep.policy)
+        idx = idx[handle.arr_count[idx] > 0]
+        ka = kcache[prep.policy] = (idx, _reference_derefs(handle, prep.policy, idx),
+                                    np.ascontiguousarray(handle.arr_level[idx], np.int32),
+                                    np.ascontiguousarray(handle.arr_ordinal[idx], np.uint32),
+                                    np.ascontiguousarray(handle.arr_count[idx], np.uint64),
+                                    np.ascontiguousarray(handle.arr_root[idx], np.uint64))
+    idx, stats.chain_derefs, lv, od, cnt, root_off = ka
     if prep.scheme == "uvm":
         fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
         # every page read once (fields, then array pages -- a page met twice migrates once), then
@@ -593,15 +602,17 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     sh = handle.chain_shape()
     sh.root_off = prep.device_root - prep.image
     sh.image_bytes = prep.image_bytes
-    lv = np.ascontiguousarray(handle.arr_level[idx], np.int32)
-    od = np.ascontiguousarray(handle.arr_ordinal[idx], np.uint32)
-    cnt = np.ascontiguousarray(handle.arr_count[idx], np.uint64)
     # per-target chain roots inside the image (several for a forest)
     if prep.amap is not None:   # naive: objects were re-placed on the device
-        roots = prep.amap.translate_many(handle.arr_root[idx] + np.uint64(handle.base)) - np.uint64(prep.image)
+        origin = prep.amap._origin
+        lay = origin[0] if origin is not None and origin[1] == prep.image else None
+        roots = lay.roots.get(prep.policy) if lay is not None else None
+        if roots is None:
+            roots = np.ascontiguousarray(prep.amap.translate_many(root_off + np.uint64(handle.base)) - np.uint64(prep.image))
+            if lay is not None:   # relative to the span base: the same for every window of this tree
+                lay.roots[prep.policy] = roots
     else:                       # marshalling image / managed tree: same offsets as the host layout
-        roots = handle.arr_root[idx]
-    roots = np.ascontiguousarray(roots, np.uint64)
+        roots = root_off
     bad = N.U64(0)
     rc = N.lib().cf_kernel_scale(ctx, elem, N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
                                  prep.image, C.byref(sh), N.ptr(roots), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),

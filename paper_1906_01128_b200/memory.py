@@ -642,25 +642,21 @@ class Machine:
         """Copy every object individually (one batched submission), then fix every pointer
         field on the device through the sorted interval map."""
         self.flush()
-        allocs = tree.allocation_array()          # (m, 2) host addr, size in allocation order
-        m = len(allocs)
-        sizes = allocs[:, 1].astype(np.uint64)
-        aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
-        span = int(aligned.sum())
-        dev_off = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64)
+        lay = naive_layout(tree)
         # the span of this tree's previous (copied-back) naive window is reused: a fresh
         # 1 GiB-class allocation per window costs more than the copies
-        dev_base = tree.__dict__.pop("_spare_naive_span", 0) or self.device.allocate_span(span, dev_off, sizes, zero=False)
-        dev = dev_off + np.uint64(dev_base)
-        host = allocs[:, 0].astype(np.uint64)
+        dev_base = tree.__dict__.pop("_spare_naive_span", 0) or \
+            self.device.allocate_span(lay.span, lay.dev_off, lay.sizes, zero=False)
+        dev = lay.dev_at(dev_base)
         ctx = self.ctx.handle
-        N.check(N.lib().cf_copy_objects(ctx, N.ptr(dev), N.ptr(host), N.ptr(sizes), m), "naive per-object copies")
-        amap = AddressMap.from_arrays(host, sizes, dev)
-        fields, targets = tree.site_field_target_arrays()
-        self._device_fixup(amap, fields, targets)
-        self.log.append_many(H2D, "per_object", sizes.astype(np.int64))
-        self.log.append_many(H2D, "attach", np.full(len(fields), 8, np.int64))
-        self._naive_span = (dev_base, span)
+        N.check(N.lib().cf_copy_objects(ctx, N.ptr(dev), N.ptr(lay.host), N.ptr(lay.sizes), len(lay.host)),
+                "naive per-object copies")
+        amap = AddressMap.from_sorted(lay.hb, lay.sz, lay.doff_sorted + np.uint64(dev_base))
+        amap._origin = (lay, dev_base)
+        self._device_fixup(amap, lay.fields, lay.targets)
+        self.log.append_many(H2D, "per_object", lay.sizes_i64)
+        self.log.append_many(H2D, "attach", lay.attach8)
+        self._naive_span = (dev_base, lay.span)
         return amap.translate(tree.root_addr), amap
 
     def _device_fixup(self, amap: "AddressMap", fields: np.ndarray, targets: np.ndarray) -> None:
@@ -679,18 +675,17 @@ class Machine:
     def naive_copy_back(self, tree, amap: "AddressMap") -> None:
         """Per-object copy back (one batched submission) plus host-side pointer restore."""
         self.flush()
-        allocs = tree.allocation_array()
-        host = allocs[:, 0].astype(np.uint64)
-        sizes = allocs[:, 1].astype(np.uint64)
-        dev = amap.translate_many(host)
-        N.check(N.lib().cf_copy_objects(self.ctx.handle, N.ptr(host), N.ptr(dev), N.ptr(sizes), len(host)),
+        lay = naive_layout(tree)
+        origin = getattr(amap, "_origin", None)
+        # the map this tree's naive_deep_copy built: every object's device address is known
+        dev = lay.dev_at(origin[1]) if origin is not None and origin[0] is lay else amap.translate_many(lay.host)
+        N.check(N.lib().cf_copy_objects(self.ctx.handle, N.ptr(lay.host), N.ptr(dev), N.ptr(lay.sizes), len(lay.host)),
                 "naive copy back")
-        fields, targets = tree.site_field_target_arrays()
-        _poke_words(fields, targets)
-        if getattr(self, "_naive_span", None) and int(dev[0]) == self._naive_span[0]:
+        _poke_words(lay.fields, lay.targets)
+        if getattr(self, "_naive_span", None) and len(dev) and int(dev[0]) == self._naive_span[0]:
             tree.__dict__["_spare_naive_span"] = self._naive_span[0]
-        self.log.append_many(D2H, "per_object", sizes.astype(np.int64))
-        self.log.append_many(D2H, "detach", np.full(len(fields), 8, np.int64))
+        self.log.append_many(D2H, "per_object", lay.sizes_i64)
+        self.log.append_many(D2H, "detach", lay.attach8)
 
     # -- unified memory (memory.py:378-394) -------------------------------------------------
     def uvm_touch(self, addr: int, access: str, actor: str) -> int:
@@ -746,6 +741,44 @@ class Machine:
         return int(move.size)
 
 
+class NaiveLayout:
+    """Per-tree layout of the naive scheme's per-object copies (the tree shape is immutable, so
+    this is computed once: C4 has 2M objects and 1M pointer fields)."""
+
+    def __init__(self, tree):
+        self.host = np.ascontiguousarray(np.asarray(tree.alloc_off, np.uint64) + np.uint64(tree.base))
+        self.sizes = np.ascontiguousarray(tree.alloc_size, np.uint64)
+        self.sizes_i64 = self.sizes.astype(np.int64)
+        aligned = (self.sizes + np.uint64(7)) & ~np.uint64(7)
+        self.span = int(aligned.sum())
+        self.dev_off = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64) if len(aligned) else aligned
+        order = np.argsort(self.host, kind="stable")
+        self.hb = np.ascontiguousarray(self.host[order])
+        self.sz = np.ascontiguousarray(self.sizes[order])
+        self.doff_sorted = np.ascontiguousarray(self.dev_off[order])
+        fields, targets = tree.site_field_target_arrays()
+        self.fields = np.ascontiguousarray(fields, np.uint64)
+        self.targets = np.ascontiguousarray(targets, np.uint64)
+        self.attach8 = np.full(len(self.fields), 8, np.int64)
+        self._dev: dict[int, np.ndarray] = {}
+        self.roots: dict = {}   # per policy: chain roots relative to the span base
+
+    def dev_at(self, base: int) -> np.ndarray:
+        d = self._dev.get(base)
+        if d is None:
+            if len(self._dev) >= 4:
+                self._dev.clear()
+            d = self._dev[base] = self.dev_off + np.uint64(base)
+        return d
+
+
+def naive_layout(tree) -> NaiveLayout:
+    lay = tree.__dict__.get("_naive_layout")
+    if lay is None:
+        lay = tree.__dict__["_naive_layout"] = NaiveLayout(tree)
+    return lay
+
+
 def _poke_words(fields: np.ndarray, values: np.ndarray) -> None:
     """Write 8-byte values at arbitrary (4-aligned) host addresses (native, parallel)."""
     fields = np.ascontiguousarray(fields, np.uint64)
@@ -763,6 +796,7 @@ class AddressMap:
         self._sz = np.zeros(0, np.uint64)
         self._db = np.zeros(0, np.uint64)
         self._pending: list = []
+        self._origin = None   # (NaiveLayout, span base) when built by naive_deep_copy and unchanged since
 
     @classmethod
     def from_arrays(cls, host_base, size, dev_base) -> "AddressMap":
@@ -773,8 +807,16 @@ class AddressMap:
         m._db = np.ascontiguousarray(np.asarray(dev_base, np.uint64)[order])
         return m
 
+    @classmethod
+    def from_sorted(cls, host_base, size, dev_base) -> "AddressMap":
+        """From contiguous uint64 arrays already ordered by host address."""
+        m = cls()
+        m._hb, m._sz, m._db = host_base, size, dev_base
+        return m
+
     def add(self, host_base: int, size: int, dev_base: int) -> None:
         self._pending.append((host_base, size, dev_base))
+        self._origin = None
 
     def arrays(self):
         if self._pending:

@@ -51,6 +51,7 @@ typedef struct cf_ctx cf_ctx;       /* one GPU: streams, events, scratch */
 typedef struct cf_tree cf_tree;     /* planned graph layout + relocation/chain tables */
 typedef struct cf_window cf_window; /* a planned, pipelined metered window */
 typedef struct cf_selective cf_selective; /* a planned, pipelined pointerchain window */
+typedef struct cf_kernel_plan cf_kernel_plan; /* a planned kernel_scale (eager schemes) */
 
 /* LinearSpec / DenseSpec (scenarios.py:33-68) plus the B200 build parameters.
  * elem: 8 = float64 (reference), 4 = float32 (BASELINE configs).
@@ -227,6 +228,16 @@ int cf_kernel_scale(cf_ctx* ctx, int elem, int mode, void* image, const cf_chain
                     const uint64_t* h_root, const int32_t* h_level, const uint32_t* h_ordinal,
                     const uint64_t* h_count,
                     uint64_t ntargets, double scale, uint64_t* h_ea_out, uint64_t* bad);
+/* kernel_scale planned once per target set (harness.py:244-304, repeated windows over one tree):
+ * _create uploads the targets' chain keys / counts (and roots, optional) and the leaf-kernel work
+ * list; _run resolves every chain on `image` and runs the leaf kernel in `mode` (same checks and
+ * errors as cf_kernel_scale).  Synchronous. */
+int cf_kernel_plan_create(cf_ctx* ctx, int elem, const uint64_t* h_root, const int32_t* h_level,
+                          const uint32_t* h_ordinal, const uint64_t* h_count, uint64_t ntargets,
+                          cf_kernel_plan** out);
+int cf_kernel_plan_run(cf_kernel_plan* plan, int mode, void* image, const cf_chain_shape* shape, double scale,
+                       uint64_t* bad);
+int cf_kernel_plan_free(cf_kernel_plan* plan);
 /* Pointerchain scheme leaf kernel over host-resolved buffers (harness.py:255-259): every
  * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */
 int cf_scale_resolved(cf_ctx* ctx, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,

@@ -46,7 +46,7 @@ EXPORTED = (
     "cf_memcpy_async", "cf_memset", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
-    "cf_kernel_scale", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
+    "cf_kernel_scale", "cf_kernel_plan_create", "cf_kernel_plan_run", "cf_kernel_plan_free", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
@@ -140,6 +140,9 @@ def _declare(L):
         "cf_demarshal": (C.c_int, [P, P, U64, P, P, U64, U64, C.POINTER(U64)]),
         "cf_kernel_scale": (C.c_int, [P, C.c_int, C.c_int, P, C.POINTER(CfChainShape), P, P, P, P,
                                       U64, C.c_double, P, C.POINTER(U64)]),
+        "cf_kernel_plan_create": (C.c_int, [P, C.c_int, P, P, P, P, U64, C.POINTER(P)]),
+        "cf_kernel_plan_run": (C.c_int, [P, C.c_int, P, C.POINTER(CfChainShape), C.c_double, C.POINTER(U64)]),
+        "cf_kernel_plan_free": (C.c_int, [P]),
         "cf_scale_resolved": (C.c_int, [P, C.c_int, P, P, U64, C.c_double]),
         "cf_memcpy_batch": (C.c_int, [P, P, P, P, U64, P]),
         "cf_naive_fixup": (C.c_int, [P, P, P, U64, P, P, P, U64, P, P]),

@@ -273,6 +273,115 @@ int cf_kernel_scale(cf_ctx* c, int elem, int mode, void* image, const cf_chain_s
   return CF_OK;
 }
 
+}  // extern "C"
+
+// A planned kernel_scale: the targets' chain keys, counts and leaf-kernel work list uploaded
+// once (C4: 1M targets, 24 MB of tables and a 1M-part work list planned on the host), then
+// every eager kernel_scale over the same targets only launches resolve + leaf kernel.
+struct cf_kernel_plan {
+  cf_ctx* ctx = nullptr;
+  int elem = 4;
+  uint64_t ntargets = 0;
+  uint8_t* d = nullptr;
+  int32_t* lv = nullptr;
+  uint32_t* od = nullptr;
+  uint64_t* ea = nullptr;
+  uint32_t* cnt = nullptr;
+  uint64_t* root = nullptr;
+  cf_scale_work work{};
+};
+
+extern "C" {
+
+int cf_kernel_plan_create(cf_ctx* c, int elem, const uint64_t* h_root, const int32_t* h_level,
+                          const uint32_t* h_ordinal, const uint64_t* h_count, uint64_t ntargets, cf_kernel_plan** out) {
+  if (!c || !out || (ntargets && (!h_level || !h_ordinal || !h_count))) return fail(CF_E_INVALID, "null argument");
+  if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
+  CfDevice g(c);
+  ScaleWork sw;
+  sw.elem = elem;
+  std::vector<uint64_t> tri;
+  tri.reserve(3 * ntargets);
+  for (uint64_t t = 0; t < ntargets; ++t)
+    if (h_count[t]) tri.insert(tri.end(), {t, 0, h_count[t]});
+  cf_kernel_plan* k = new cf_kernel_plan();
+  k->ctx = c;
+  k->elem = elem;
+  k->ntargets = ntargets;
+  k->work = sw.append(tri);
+  const uint64_t off_ord = ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_ea = off_ord + ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_cnt = off_ea + ntargets * 8;
+  const uint64_t off_root = off_cnt + ((ntargets * 4 + 7) / 8) * 8;
+  const uint64_t off_work = off_root + (h_root ? ntargets * 8 : 0);
+  cudaError_t e = cudaMalloc(&k->d, off_work + work_bytes(sw) + 8);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete k;
+    return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "kernel plan: %s", cudaGetErrorString(e));
+  }
+  k->lv = reinterpret_cast<int32_t*>(k->d);
+  k->od = reinterpret_cast<uint32_t*>(k->d + off_ord);
+  k->ea = reinterpret_cast<uint64_t*>(k->d + off_ea);
+  k->cnt = reinterpret_cast<uint32_t*>(k->d + off_cnt);
+  k->root = h_root ? reinterpret_cast<uint64_t*>(k->d + off_root) : nullptr;
+  cudaStream_t s = c->compute;
+  int rc = CF_OK;
+  auto up = [&](void* dst, const void* src, uint64_t n) {
+    if (rc == CF_OK && n && cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      rc = fail(CF_E_CUDA, "kernel plan upload: %s", cudaGetErrorString(cudaGetLastError()));
+  };
+  up(k->lv, h_level, ntargets * 4);
+  up(k->od, h_ordinal, ntargets * 4);
+  if (h_root) up(k->root, h_root, ntargets * 8);
+  if (rc == CF_OK) rc = upload_work(sw, k->d + off_work, s, &k->work);
+  if (rc == CF_OK && cudaStreamSynchronize(s) != cudaSuccess)   // host tables go out of scope
+    rc = fail(CF_E_CUDA, "kernel plan upload: %s", cudaGetErrorString(cudaGetLastError()));
+  if (rc != CF_OK) {
+    cudaFree(k->d);
+    delete k;
+    return rc;
+  }
+  *out = k;
+  return CF_OK;
+}
+
+int cf_kernel_plan_run(cf_kernel_plan* k, int mode, void* image, const cf_chain_shape* shape, double scale,
+                       uint64_t* bad) {
+  if (!k || !shape) return fail(CF_E_INVALID, "null argument");
+  cf_ctx* c = k->ctx;
+  CfDevice g(c);
+  if (bad) *bad = NO_BAD;
+  if (k->ntargets == 0) return CF_OK;
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, k->root, k->lv, k->od, k->ntargets, k->ea, k->cnt,
+                        c->d_bad, s));
+  uint64_t rb = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) {
+    if (bad) *bad = rb;
+    return fail(CF_E_WILD, "chain walk for target %llu left the device image", (unsigned long long)rb);
+  }
+  CF_TRY(launch_scale(c, k->elem, mode, static_cast<const uint8_t*>(image), *shape, k->root, k->lv, k->od, k->ea, k->cnt,
+                      k->work, scale, c->d_bad, s));
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) {
+    if (bad) *bad = rb;
+    return fail(CF_E_WILD, "leaf kernel: target %llu count/address mismatch", (unsigned long long)rb);
+  }
+  return CF_OK;
+}
+
+int cf_kernel_plan_free(cf_kernel_plan* k) {
+  if (!k) return CF_OK;
+  CfDevice g(k->ctx);
+  cudaStreamSynchronize(k->ctx->compute);
+  cudaFree(k->d);
+  delete k;
+  return CF_OK;
+}
+
 int cf_scale_resolved(cf_ctx* c, int elem, const uint64_t* h_ea, const uint64_t* h_count, uint64_t n,
                       double scale) {
   if (!c || (n && (!h_ea || !h_count))) return fail(CF_E_INVALID, "null argument");

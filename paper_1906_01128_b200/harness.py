@@ -613,10 +613,22 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
                 lay.roots[prep.policy] = roots
     else:                       # marshalling image / managed tree: same offsets as the host layout
         roots = root_off
+    # the targets' tables and work list are planned and uploaded once per (tree, policy, roots)
+    key = ("kernel", id(handle), prep.policy)
+    held = machine._plan_keep.get(key)
+    if held is not None and (held[0] is not handle or held[1] is not roots):
+        N.lib().cf_kernel_plan_free(machine._plans.pop(key))
+        held = None
+    if held is None:
+        kp = C.c_void_p()
+        N.check(N.lib().cf_kernel_plan_create(ctx, elem, N.ptr(roots), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
+                                              C.byref(kp)), "kernel_scale plan")
+        machine._plans[key] = kp
+        machine._plan_free[key] = N.lib().cf_kernel_plan_free
+        machine._plan_keep[key] = (handle, roots)
     bad = N.U64(0)
-    rc = N.lib().cf_kernel_scale(ctx, elem, N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
-                                 prep.image, C.byref(sh), N.ptr(roots), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
-                                 float(scale), None, C.byref(bad))
+    rc = N.lib().cf_kernel_plan_run(machine._plans[key], N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
+                                    prep.image, C.byref(sh), float(scale), C.byref(bad))
     N.check(rc, "kernel_scale")
     stats.elements_touched = int(cnt.sum())
     return stats

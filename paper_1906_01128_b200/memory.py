@@ -523,6 +523,7 @@ class Machine:
         self._deferred = None
         self._plans: dict = {}   # cached plans of the fused windows (cf_window / cf_selective)
         self._plan_free: dict = {}   # key -> free function when not cf_window_free
+        self._plan_keep: dict = {}   # key -> objects a plan was built from (identity-checked on reuse)
 
     @property
     def ctx(self) -> N.DeviceContext:
@@ -561,7 +562,7 @@ class Machine:
             self.ctx.sync()
             for key, w in self._plans.items():
                 self._plan_free.get(key, lib.cf_window_free)(w)
-        self._plans, self._plan_free = {}, {}
+        self._plans, self._plan_free, self._plan_keep = {}, {}, {}
         self.host.free_all()
         self.device.free_all()
 

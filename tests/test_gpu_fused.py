@@ -289,3 +289,30 @@ def test_fused_pointerchain_multi_step_and_split_arrays(cf):
         cf.copy_back(m, h, prep)
         cf.verify_tree(m, h, 2.0, "all_arrays")
         m.close()
+
+
+@pytest.mark.parametrize("scheme", ["naive", "marshalling"])
+def test_planned_kernel_scale_across_trees_and_policies(cf, scheme):
+    """Eager kernel_scale plans its targets' tables once per (tree, policy): interleaving two trees,
+    two policies and both leaf-kernel modes in one machine still scales exactly the right arrays."""
+    m = cf.Machine()
+    trees = []
+    for seed, spec in ((5, cf.DenseSpec(3, 700, 2)), (6, cf.LinearSpec(4, 900, "allinit_allused"))):
+        if scheme == "marshalling":
+            trees.append(cf.marshal_tree(m, spec, seed=seed))
+        else:
+            trees.append((None, cf.build_tree(m, spec, seed=seed)))
+    for r, (t, policy, mode) in enumerate([(0, "all_arrays", "resolved"), (1, "ref", "chase"), (0, "all_arrays", "chase"),
+                                           (1, "all_arrays", "resolved"), (0, "ref", "resolved")]):
+        arena, h = trees[t]
+        prep = cf.transfer_to_device(m, h, scheme, arena, policy=policy, fused=False)
+        st = cf.kernel_scale(m, h, prep, 2.0, mode=mode)
+        cf.copy_back(m, h, prep)
+        assert st.elements_touched == int(h.arr_count[h.target_indices(policy)].sum())
+        cf.verify_tree(m, h, 2.0, policy)
+        # undo on the host so every round starts from the payload
+        prep = cf.transfer_to_device(m, h, scheme, arena, policy=policy, fused=False)
+        cf.kernel_scale(m, h, prep, 0.5, mode=mode)
+        cf.copy_back(m, h, prep)
+        cf.verify_tree(m, h, 1.0, policy)
+    m.close()

@@ -226,7 +226,8 @@ def compare_schemes(spec, policy: str, reps: int, device: int) -> dict:
     plans = (("marshalling", "marshalling", {}), ("marshalling_eager", "marshalling", {"fused": False}),
              ("pointerchain", "pointerchain", {}), ("naive", "naive", {}),
              ("uvm", "uvm", {"uvm_hints": "none"}), ("uvm_prefetch", "uvm", {"uvm_hints": "prefetch"}),
-             ("uvm_advise", "uvm", {"uvm_hints": "advise"}))
+             ("uvm_advise", "uvm", {"uvm_hints": "advise"}), ("uvm_preferred", "uvm", {"uvm_hints": "preferred"}),
+             ("uvm_read_mostly", "uvm", {"uvm_hints": "read_mostly"}))
     for name, scheme, kw in plans:
         m = cf.Machine(device=device)
         try:

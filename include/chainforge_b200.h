@@ -300,8 +300,10 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
 /* ---------------- unified memory (memory.py:239-261, 378-394) ---------------- */
 /* Managed-memory hints for the UVM scheme. dst_device < 0 prefetches to the host (the
  * reference's copy-back re-touch of dirty pages, harness.py:321-325). advice: 0 = none,
- * 1 = SetPreferredLocation(device), 2 = SetAccessedBy(device), 3 = SetReadMostly. */
-enum { CF_UVM_ADVISE_NONE = 0, CF_UVM_PREFERRED_DEVICE = 1, CF_UVM_ACCESSED_BY = 2, CF_UVM_READ_MOSTLY = 3 };
+ * 1 = SetPreferredLocation(device), 2 = SetAccessedBy(device), 3 = SetReadMostly; OR-ing
+ * CF_UVM_UNSET applies the matching Unset advice. */
+enum { CF_UVM_ADVISE_NONE = 0, CF_UVM_PREFERRED_DEVICE = 1, CF_UVM_ACCESSED_BY = 2, CF_UVM_READ_MOSTLY = 3,
+       CF_UVM_UNSET = 0x100 };
 int cf_uvm_prefetch(cf_ctx* ctx, const void* p, uint64_t bytes, int dst_device, void* stream);
 int cf_uvm_advise(cf_ctx* ctx, const void* p, uint64_t bytes, int advice);
 

@@ -27,6 +27,7 @@ CF_MEM_PAGEABLE, CF_MEM_PINNED, CF_MEM_MANAGED = 0, 1, 2
 CF_TARGET_REF, CF_TARGET_ALL_LEAVES, CF_TARGET_ALL_ARRAYS = 0, 1, 2
 CF_MODE_RESOLVED, CF_MODE_CHASE = 0, 1
 CF_UVM_ADVISE_NONE, CF_UVM_PREFERRED_DEVICE, CF_UVM_ACCESSED_BY, CF_UVM_READ_MOSTLY = 0, 1, 2, 3
+CF_UVM_UNSET = 0x100
 (CF_TAB_ALLOC_OFF, CF_TAB_ALLOC_SIZE, CF_TAB_NODE_OFF, CF_TAB_NODE_LEVEL, CF_TAB_NODE_SIZE,
  CF_TAB_ARR_LEVEL, CF_TAB_ARR_OWNER, CF_TAB_ARR_OFF, CF_TAB_ARR_COUNT, CF_TAB_SITE_OFF,
  CF_TAB_SITE_TARGET, CF_TAB_SITE_SORTED, CF_TAB_ARR_ORDINAL, CF_TAB_ARR_ROOT, CF_TAB_TREE_ROOT) = range(15)

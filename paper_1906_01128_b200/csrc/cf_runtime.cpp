@@ -307,11 +307,15 @@ int cf_uvm_prefetch(cf_ctx* c, const void* p, uint64_t bytes, int dst_device, vo
 
 int cf_uvm_advise(cf_ctx* c, const void* p, uint64_t bytes, int advice) {
   if (!c || !p) return fail(CF_E_INVALID, "null argument");
+  const bool unset = (advice & CF_UVM_UNSET) != 0;
+  advice &= ~CF_UVM_UNSET;
   if (advice == CF_UVM_ADVISE_NONE || bytes == 0) return CF_OK;
+  if (advice < CF_UVM_PREFERRED_DEVICE || advice > CF_UVM_READ_MOSTLY) return fail(CF_E_INVALID, "unknown advice %d", advice);
   CfDevice g(c);
-  cudaMemoryAdvise a = advice == CF_UVM_PREFERRED_DEVICE ? cudaMemAdviseSetPreferredLocation
-                       : advice == CF_UVM_ACCESSED_BY    ? cudaMemAdviseSetAccessedBy
-                                                         : cudaMemAdviseSetReadMostly;
+  cudaMemoryAdvise a = advice == CF_UVM_PREFERRED_DEVICE
+                           ? (unset ? cudaMemAdviseUnsetPreferredLocation : cudaMemAdviseSetPreferredLocation)
+                       : advice == CF_UVM_ACCESSED_BY ? (unset ? cudaMemAdviseUnsetAccessedBy : cudaMemAdviseSetAccessedBy)
+                                                      : (unset ? cudaMemAdviseUnsetReadMostly : cudaMemAdviseSetReadMostly);
 #if CUDART_VERSION >= 12080
   cudaMemLocation loc;
   loc.type = cudaMemLocationTypeDevice;

@@ -210,7 +210,11 @@ class DevicePrep:
         return [(int(d), arrays[int(i)]) for d, i in zip(self.buf_dev, self.buf_array)]
 
 
-UVM_HINTS = ("none", "prefetch", "advise")
+# UVM driver hints: migrate the tree ahead of the kernel ("prefetch"), map it for
+# remote access ("advise": SetAccessedBy), prefer device residence ("preferred":
+# SetPreferredLocation), or duplicate the read-only node pages on the device ("read_mostly":
+# SetReadMostly on the pages holding node records only -- the arrays are written)
+UVM_HINTS = ("none", "prefetch", "advise", "preferred", "read_mostly")
 
 # pipeline granularity of the fused marshalling window (repo:profiles/r01_design_experiments.md)
 FUSED_CHUNK = 32 << 20
@@ -410,8 +414,8 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         ctx = machine.ctx.handle
         if uvm_hints == "prefetch":
             N.check(N.lib().cf_uvm_prefetch(ctx, handle.base, handle.total_bytes, machine.ctx.device, None))
-        elif uvm_hints == "advise":
-            N.check(N.lib().cf_uvm_advise(ctx, handle.base, handle.total_bytes, N.CF_UVM_ACCESSED_BY))
+        for lo, hi, advice in _uvm_advice(handle, uvm_hints):
+            N.check(N.lib().cf_uvm_advise(ctx, handle.base + lo, hi - lo, advice))
         return DevicePrep(scheme, device_root=handle.root_addr, policy=policy, image=handle.base,
                           image_bytes=handle.total_bytes, uvm_hints=uvm_hints)
     raise SchemeError(f"unknown transfer scheme {scheme!r}")
@@ -446,6 +450,31 @@ def _pages_of_spans(starts: np.ndarray, counts: np.ndarray, e: int, page: int) -
         return np.zeros(0, np.int64)
     rep = np.repeat(first - np.concatenate([[0], np.cumsum(k)[:-1]]), k)
     return np.unique(rep + np.arange(int(k.sum()), dtype=np.int64))
+
+
+def _uvm_advice(handle: TreeHandle, hint: str) -> list[tuple[int, int, int]]:
+    """(lo, hi, advice) byte ranges of the tree a UVM hint advises (offsets from handle.base)."""
+    if hint == "advise":
+        return [(0, handle.total_bytes, N.CF_UVM_ACCESSED_BY)]
+    if hint == "preferred":
+        return [(0, handle.total_bytes, N.CF_UVM_PREFERRED_DEVICE)]
+    if hint == "read_mostly":
+        cache = handle.__dict__.setdefault("_node_pages", {})
+        if "ranges" not in cache:   # node allocations rounded out to 4 KiB pages, merged
+            off = np.sort(np.asarray(handle.node_off, np.uint64))
+            end = off + np.asarray(handle.node_size, np.uint64)[np.argsort(np.asarray(handle.node_off, np.uint64))]
+            lo = (off // np.uint64(4096)) * np.uint64(4096)
+            hi = np.minimum((end + np.uint64(4095)) // np.uint64(4096) * np.uint64(4096), np.uint64(handle.total_bytes))
+            if len(lo):   # merge overlapping / touching page ranges (sorted by start)
+                reach = np.maximum.accumulate(hi)
+                first = np.concatenate([[True], lo[1:] > reach[:-1]])
+                starts = lo[first]
+                ends = np.maximum.reduceat(hi, np.nonzero(first)[0])
+            else:
+                starts = ends = lo
+            cache["ranges"] = [(int(a), int(b), N.CF_UVM_READ_MOSTLY) for a, b in zip(starts, ends)]
+        return cache["ranges"]
+    return []
 
 
 def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: int):
@@ -668,6 +697,8 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
         for lo, hi in _merged_ranges(handle, handle.target_indices(prep.policy), machine.uvm.page_size):
             N.check(N.lib().cf_uvm_prefetch(ctx, handle.base + lo, hi - lo, -1, None))
         machine.ctx.sync()
+        for lo, hi, advice in _uvm_advice(handle, prep.uvm_hints):   # the hint lasts one window
+            N.check(N.lib().cf_uvm_advise(ctx, handle.base + lo, hi - lo, advice | N.CF_UVM_UNSET))
         machine.uvm_touch_mask(machine.uvm._dirty.copy(), "read", "host")
 
 

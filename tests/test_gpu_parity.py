@@ -370,3 +370,24 @@ def test_fields_straddling_chunk_boundaries(cf, oracle):
                 assert np.array_equal(w.host_dst(), want), (j, chunk, leaf_only)
             finally:
                 w.close()
+
+
+@pytest.mark.parametrize("hint", ["none", "prefetch", "advise", "preferred", "read_mostly"])
+def test_uvm_hints_keep_results_and_counters(cf, hint):
+    """Every UVM driver hint leaves the results bit-exact and the reference's logical
+    counters unchanged; the hint is undone at copy-back, so windows with different hints can follow
+    one another on one tree."""
+    spec = cf.DenseSpec(4, 3000, 2, elem=4)
+    m = cf.Machine()
+    m.enable_uvm()
+    h = cf.build_tree(m, spec, seed=2)
+    counters = []
+    for r, hh in enumerate((hint, "none", hint)):
+        mark = m.log.mark()
+        prep = cf.transfer_to_device(m, h, "uvm", policy="all_leaves", uvm_hints=hh)
+        cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5)
+        cf.copy_back(m, h, prep)
+        counters.append([(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)])
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    assert counters[1] == counters[2]   # same starting residence, different hint
+    m.close()

@@ -16,7 +16,7 @@ for name in which:
     scheme = name.split("_")[0]
     kw = {"fused": False} if name.endswith("eager") else {}
     if scheme == "uvm" and "_" in name:
-        kw = {"uvm_hints": name.split("_")[1]}
+        kw = {"uvm_hints": name.split("_", 1)[1]}
     t = time.perf_counter()
     m = cf.Machine()
     if scheme == "uvm":

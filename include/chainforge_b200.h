@@ -136,6 +136,14 @@ int cf_ctx_sync(cf_ctx* ctx);
 void* cf_ctx_stream(cf_ctx* ctx);               /* compute stream (cudaStream_t) */
 uint64_t cf_ctx_launches(cf_ctx* ctx);          /* kernels launched so far */
 int cf_ctx_sm_count(cf_ctx* ctx);
+/* Device-side phase timer (CUDA events on the context's compute stream, which every library
+ * operation forks from and joins back into): _stop waits for the work enqueued since _start and
+ * returns its device time in ms (execute_case's measured columns, harness.py:369-373). */
+typedef struct cf_timer cf_timer;
+int cf_timer_create(cf_ctx* ctx, cf_timer** out);
+int cf_timer_start(cf_timer* t);
+int cf_timer_stop(cf_timer* t, float* ms);
+int cf_timer_free(cf_timer* t);
 
 /* Host memory for arenas / host spaces (MemorySpace storage, memory.py:101-137).
  * PINNED = cudaHostAlloc(portable), MANAGED = cudaMallocManaged (UVM mode, memory.py:239-261),

@@ -42,7 +42,8 @@ _TAB_DTYPES = {CF_TAB_NODE_LEVEL: np.int32, CF_TAB_NODE_SIZE: np.uint32, CF_TAB_
 
 EXPORTED = (
     "cf_abi_version", "cf_last_error", "cf_device_count", "cf_ctx_create", "cf_ctx_destroy",
-    "cf_ctx_sync", "cf_ctx_stream", "cf_ctx_launches", "cf_ctx_sm_count", "cf_host_alloc",
+    "cf_ctx_sync", "cf_ctx_stream", "cf_ctx_launches", "cf_ctx_sm_count",
+    "cf_timer_create", "cf_timer_start", "cf_timer_stop", "cf_timer_free", "cf_host_alloc",
     "cf_host_free", "cf_host_free_sized", "cf_dev_alloc", "cf_dev_free", "cf_memcpy",
     "cf_memcpy_async", "cf_memset", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
@@ -115,6 +116,10 @@ def _declare(L):
         "cf_ctx_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(P)]),
         "cf_ctx_destroy": (C.c_int, [P]),
         "cf_ctx_sync": (C.c_int, [P]),
+        "cf_timer_create": (C.c_int, [P, C.POINTER(P)]),
+        "cf_timer_start": (C.c_int, [P]),
+        "cf_timer_stop": (C.c_int, [P, C.POINTER(C.c_float)]),
+        "cf_timer_free": (C.c_int, [P]),
         "cf_ctx_stream": (P, [P]),
         "cf_ctx_launches": (U64, [P]),
         "cf_ctx_sm_count": (C.c_int, [P]),
@@ -277,6 +282,31 @@ class DeviceContext:
 
     def sync(self) -> None:
         check(lib().cf_ctx_sync(self.handle), "cf_ctx_sync")
+
+    def timer(self) -> "DeviceTimer":
+        return DeviceTimer(self)
+
+
+class DeviceTimer:
+    """CUDA-event timer over a context's compute stream (cf_timer_*): ``start()`` ... ``stop()``
+    returns the device milliseconds of the library work enqueued in between."""
+
+    def __init__(self, ctx: DeviceContext):
+        self.handle = C.c_void_p()
+        check(lib().cf_timer_create(ctx.handle, C.byref(self.handle)), "cf_timer_create")
+
+    def start(self) -> None:
+        check(lib().cf_timer_start(self.handle), "cf_timer_start")
+
+    def stop(self) -> float:
+        ms = C.c_float(0.0)
+        check(lib().cf_timer_stop(self.handle, C.byref(ms)), "cf_timer_stop")
+        return float(ms.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.cf_timer_free(self.handle)
+            self.handle = None
 
 
 class NativeTree:

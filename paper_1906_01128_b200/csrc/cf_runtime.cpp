@@ -152,6 +152,57 @@ int cf_ctx_sync(cf_ctx* c) {
 }
 
 void* cf_ctx_stream(cf_ctx* c) { return c ? (void*)c->compute : nullptr; }
+
+}  // extern "C"
+
+// Device timer over the context's compute stream: every operation of the library forks from and
+// joins back into that stream, so an event pair on it brackets all the device work in between.
+struct cf_timer {
+  cf_ctx* c = nullptr;
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+extern "C" {
+
+int cf_timer_create(cf_ctx* c, cf_timer** out) {
+  if (!c || !out) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(c);
+  cf_timer* t = new cf_timer();
+  t->c = c;
+  if (cudaEventCreate(&t->a) != cudaSuccess || cudaEventCreate(&t->b) != cudaSuccess) {
+    cudaGetLastError();
+    if (t->a) cudaEventDestroy(t->a);
+    delete t;
+    return fail(CF_E_CUDA, "timer events");
+  }
+  *out = t;
+  return CF_OK;
+}
+
+int cf_timer_start(cf_timer* t) {
+  if (!t) return fail(CF_E_INVALID, "null timer");
+  CfDevice g(t->c);
+  CF_CUDA(cudaEventRecord(t->a, t->c->compute));
+  return CF_OK;
+}
+
+int cf_timer_stop(cf_timer* t, float* ms) {
+  if (!t || !ms) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(t->c);
+  CF_CUDA(cudaEventRecord(t->b, t->c->compute));
+  CF_CUDA(cudaEventSynchronize(t->b));
+  CF_CUDA(cudaEventElapsedTime(ms, t->a, t->b));
+  return CF_OK;
+}
+
+int cf_timer_free(cf_timer* t) {
+  if (!t) return CF_OK;
+  CfDevice g(t->c);
+  cudaEventDestroy(t->a);
+  cudaEventDestroy(t->b);
+  delete t;
+  return CF_OK;
+}
 uint64_t cf_ctx_launches(cf_ctx* c) { return c ? c->launches.load() : 0; }
 int cf_ctx_sm_count(cf_ctx* c) { return c ? c->sm_count : 0; }
 

@@ -127,6 +127,12 @@ class RunMetrics:
     wall_us: float = 0.0
     mode: str = "resolved"
     gpu_launches: int = 0
+    # device time of each call of the window (CUDA events on the context's compute stream); a
+    # fused window enqueues at copy_back, so its whole pipeline shows in copy_back_us
+    device_us: float = 0.0
+    transfer_us: float = 0.0
+    kernel_us: float = 0.0
+    copy_back_us: float = 0.0
 
     def sort_key(self):
         return (self.scenario, self.scheme, self.layout, self.k_or_q, self.n)
@@ -770,10 +776,18 @@ def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale:
         handle = build_tree(machine, spec, seed=seed, align=align)
     launches0 = machine.ctx.launches()
     mark = machine.log.mark()
+    timer = machine.ctx.timer()
+    phase_us = []
     t0 = time.perf_counter()
+    timer.start()
     prep = transfer_to_device(machine, handle, scheme, arena, policy=policy, uvm_hints=uvm_hints, fused=fused)
+    phase_us.append(timer.stop() * 1e3)
+    timer.start()
     stats = kernel_scale(machine, handle, prep, scale, mode=mode)
+    phase_us.append(timer.stop() * 1e3)
+    timer.start()
     copy_back(machine, handle, prep)
+    phase_us.append(timer.stop() * 1e3)
     machine.ctx.sync()
     wall_us = (time.perf_counter() - t0) * 1e6
     kernel_us, sim_wall = simulate_times(machine.log.data_entries_since(mark), stats.elements_touched,
@@ -787,7 +801,8 @@ def execute_case(spec, scheme: str, cost_model: CostModel, seed: int = 0, scale:
         page_faults=machine.log.count("page_migration", mark),
         instr_estimate=estimate_instructions(chain_shape(spec, scheme)),
         sim_kernel_us=kernel_us, sim_wall_us=sim_wall, iterations=1, verified=True,
-        wall_us=wall_us, mode=mode, gpu_launches=machine.ctx.launches() - launches0)
+        wall_us=wall_us, mode=mode, gpu_launches=machine.ctx.launches() - launches0,
+        device_us=sum(phase_us), transfer_us=phase_us[0], kernel_us=phase_us[1], copy_back_us=phase_us[2])
     return metrics, machine
 
 

@@ -5,7 +5,8 @@ Drop-in for the reference's results layer (report.py:48-140): ``ResultRow`` (one
 and n; ``MissingBaseline`` when strict), ``rows_to_csv`` / ``rows_from_csv`` with the same
 header and value formatting (booleans ``true``/``false``, floats by ``repr``, empty for None),
 so sweep files written here and by chainforge are interchangeable byte for byte.  The measured
-B200 columns of a row (``wall_us``, ``mode``, ``gpu_launches``) ride in ``extra`` and are written
+B200 columns of a row (``wall_us``, ``mode``, ``gpu_launches``, and the CUDA-event device times
+``device_us`` = ``transfer_us`` + ``kernel_us`` + ``copy_back_us``) ride in ``extra`` and are written
 only when asked (``measured=True``).  The table renderers (render_size_table /
 render_instruction_table / rows_to_table) are presentation and not part of this path.
 """
@@ -15,7 +16,7 @@ from dataclasses import dataclass, field, fields, replace
 
 CSV_HEADER = ("scenario,scheme,layout,k_or_q,n,bytes_h2d,bytes_d2h,transfer_ops,attach_ops,page_faults,"
               "instr_estimate,sim_kernel_us,sim_wall_us,iterations,verified,normalized_wall,normalized_kernel")
-MEASURED = ("wall_us", "mode", "gpu_launches")
+MEASURED = ("wall_us", "mode", "gpu_launches", "device_us", "transfer_us", "kernel_us", "copy_back_us")
 _INT = ("k_or_q", "n", "bytes_h2d", "bytes_d2h", "transfer_ops", "attach_ops", "page_faults", "instr_estimate",
         "iterations")
 _FLOAT = ("sim_kernel_us", "sim_wall_us", "normalized_wall", "normalized_kernel")

@@ -316,3 +316,18 @@ def test_planned_kernel_scale_across_trees_and_policies(cf, scheme):
         cf.copy_back(m, h, prep)
         cf.verify_tree(m, h, 1.0, policy)
     m.close()
+
+
+@pytest.mark.parametrize("scheme,fused", [("marshalling", True), ("marshalling", False), ("pointerchain", True),
+                                          ("naive", True), ("uvm", True)])
+def test_execute_case_device_phase_times(cf, scheme, fused):
+    """execute_case's measured columns: CUDA-event device time per call of the window (a fused
+    window enqueues its pipeline at copy_back); they ride in the report row's measured extras."""
+    m, machine = cf.execute_case(cf.DenseSpec(4, 200000, 2, elem=4), scheme, cf.CostModel(), seed=1, fused=fused,
+                                 policy="all_leaves")
+    machine.close()
+    assert m.device_us > 0 and abs(m.device_us - (m.transfer_us + m.kernel_us + m.copy_back_us)) < 1e-6 * m.device_us + 1e-3
+    assert m.copy_back_us > 0 and m.gpu_launches > 0
+    row = cf.report.ResultRow.from_metrics(m) if hasattr(cf, "report") else None
+    if row is not None:
+        assert row.extra["device_us"] == m.device_us

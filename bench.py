@@ -391,7 +391,8 @@ def run_ours(args, dist: Dist) -> None:
     # one rank per GPU; ranks beyond the visible GPUs share them (plumbing runs on small boxes)
     device = dist.local_rank % max(ndev, 1)
     spec, policy, desc = make_spec(args.config)
-    if args.leaf_elems:   # plumbing runs only: the same shape with shorter leaves
+    n_full = spec.tree.n if hasattr(spec, "tree") else spec.n
+    if args.leaf_elems and args.leaf_elems < n_full:   # plumbing runs only: the same shape, shorter leaves
         from dataclasses import replace
         spec = replace(spec, tree=replace(spec.tree, n=args.leaf_elems)) if hasattr(spec, "tree") else \
             replace(spec, n=args.leaf_elems)

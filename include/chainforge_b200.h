@@ -245,6 +245,13 @@ int cf_kernel_plan_create(cf_ctx* ctx, int elem, const uint64_t* h_root, const i
                           cf_kernel_plan** out);
 int cf_kernel_plan_run(cf_kernel_plan* plan, int mode, void* image, const cf_chain_shape* shape, double scale,
                        uint64_t* bad);
+/* Resolve only: walk every target chain on `image` and return the effective addresses (u64 device
+ * addresses) and counts (u32 nA) to host arrays; errors as cf_kernel_scale's walk.  With h_ea and
+ * h_count NULL after cf_kernel_plan_expect, the walk is checked on the device instead: every chain
+ * must end at image + h_expect_off[t] with count h_count[t], else CF_E_WILD (bad = first target). */
+int cf_kernel_plan_expect(cf_kernel_plan* plan, const uint64_t* h_expect_off, const uint64_t* h_count);
+int cf_kernel_plan_resolve(cf_kernel_plan* plan, void* image, const cf_chain_shape* shape, uint64_t* h_ea,
+                           uint32_t* h_count, uint64_t* bad);
 int cf_kernel_plan_free(cf_kernel_plan* plan);
 /* Pointerchain scheme leaf kernel over host-resolved buffers (harness.py:255-259): every
  * (h_ea[i], h_count[i]) names one device buffer copied by the selective pointerchain copy. */
@@ -296,6 +303,13 @@ int cf_naive_fixup_host(cf_ctx* ctx, const uint64_t* h_site_field_host, const ui
  * CF_WIN_D2H (any subset).  cf_selective_run is synchronous. */
 int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
                       int elem, uint64_t chunk_bytes, cf_selective** out);
+/* As cf_selective_plan, with a per-array scale mask (NULL = every array; 0 = copied in and back
+ * but not scaled -- the naive scheme moves every object) and plan flags: CF_SEL_PER_OBJECT keeps
+ * one transfer per object (no staged spans), the naive scheme's per-object semantics. */
+enum { CF_SEL_PER_OBJECT = 1 };
+int cf_selective_plan_ex(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
+                         const uint8_t* scale_mask, uint32_t plan_flags, int elem, uint64_t chunk_bytes,
+                         cf_selective** out);
 int cf_selective_run(cf_selective* w, uint32_t flags, double scale);
 int cf_selective_free(cf_selective* w);
 /* Host-only dry run of cf_selective_plan + invariant check (no GPU): every array's bytes move

@@ -28,6 +28,7 @@ CF_TARGET_REF, CF_TARGET_ALL_LEAVES, CF_TARGET_ALL_ARRAYS = 0, 1, 2
 CF_MODE_RESOLVED, CF_MODE_CHASE = 0, 1
 CF_UVM_ADVISE_NONE, CF_UVM_PREFERRED_DEVICE, CF_UVM_ACCESSED_BY, CF_UVM_READ_MOSTLY = 0, 1, 2, 3
 CF_UVM_UNSET = 0x100
+CF_SEL_PER_OBJECT = 1
 (CF_TAB_ALLOC_OFF, CF_TAB_ALLOC_SIZE, CF_TAB_NODE_OFF, CF_TAB_NODE_LEVEL, CF_TAB_NODE_SIZE,
  CF_TAB_ARR_LEVEL, CF_TAB_ARR_OWNER, CF_TAB_ARR_OFF, CF_TAB_ARR_COUNT, CF_TAB_SITE_OFF,
  CF_TAB_SITE_TARGET, CF_TAB_SITE_SORTED, CF_TAB_ARR_ORDINAL, CF_TAB_ARR_ROOT, CF_TAB_TREE_ROOT) = range(15)
@@ -48,8 +49,9 @@ EXPORTED = (
     "cf_memcpy_async", "cf_memset", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
-    "cf_kernel_scale", "cf_kernel_plan_create", "cf_kernel_plan_run", "cf_kernel_plan_free", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
-    "cf_checksum_ranges", "cf_selective_plan", "cf_selective_run", "cf_selective_free",
+    "cf_kernel_scale", "cf_kernel_plan_create", "cf_kernel_plan_run", "cf_kernel_plan_resolve",
+    "cf_kernel_plan_expect", "cf_kernel_plan_free", "cf_scale_resolved", "cf_memcpy_batch", "cf_naive_fixup", "cf_arena_check_sites",
+    "cf_checksum_ranges", "cf_selective_plan", "cf_selective_plan_ex", "cf_selective_run", "cf_selective_free",
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_n_flushed",
@@ -148,6 +150,8 @@ def _declare(L):
                                       U64, C.c_double, P, C.POINTER(U64)]),
         "cf_kernel_plan_create": (C.c_int, [P, C.c_int, P, P, P, P, U64, C.POINTER(P)]),
         "cf_kernel_plan_run": (C.c_int, [P, C.c_int, P, C.POINTER(CfChainShape), C.c_double, C.POINTER(U64)]),
+        "cf_kernel_plan_resolve": (C.c_int, [P, P, C.POINTER(CfChainShape), P, P, C.POINTER(U64)]),
+        "cf_kernel_plan_expect": (C.c_int, [P, P, P]),
         "cf_kernel_plan_free": (C.c_int, [P]),
         "cf_scale_resolved": (C.c_int, [P, C.c_int, P, P, U64, C.c_double]),
         "cf_memcpy_batch": (C.c_int, [P, P, P, P, U64, P]),
@@ -155,6 +159,7 @@ def _declare(L):
         "cf_arena_check_sites": (C.c_int, [P, U64, P, U64, U64, C.POINTER(U64)]),
         "cf_checksum_ranges": (C.c_int, [P, P, P, U64, P]),
         "cf_selective_plan": (C.c_int, [P, U64, P, P, P, C.c_int, U64, C.POINTER(P)]),
+        "cf_selective_plan_ex": (C.c_int, [P, U64, P, P, P, P, C.c_uint32, C.c_int, U64, C.POINTER(P)]),
         "cf_selective_run": (C.c_int, [P, C.c_uint32, C.c_double]),
         "cf_selective_free": (C.c_int, [P]),
         "cf_copy_objects": (C.c_int, [P, P, P, P, U64]),

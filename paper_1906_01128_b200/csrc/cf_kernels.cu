@@ -765,9 +765,20 @@ __global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ 
   if (i >= n) return;
   const uint64_t s = src[i], d = dst[i], b = bytes[i];
   if (((s | d | b) & 15) == 0) {
+    // all loads of a 2 KiB slice first, then the stores: one PCIe round trip per slice instead
+    // of one per 512 bytes (source and destination may not alias, the compiler cannot know)
     const uint4* ps = reinterpret_cast<const uint4*>(s);
     uint4* pd = reinterpret_cast<uint4*>(d);
-    for (uint64_t k = lane; k < b / 16; k += 32) pd[k] = ps[k];
+    const uint64_t n16 = b / 16;
+    for (uint64_t k = lane; k < n16; k += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + 32 * u < n16) v[u] = ps[k + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + 32 * u < n16) pd[k + 32 * u] = v[u];
+    }
   } else if (((s | d | b) & 7) == 0) {
     const uint64_t* ps = reinterpret_cast<const uint64_t*>(s);
     uint64_t* pd = reinterpret_cast<uint64_t*>(d);
@@ -779,6 +790,16 @@ __global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ 
   } else {
     for (uint64_t k = lane; k < b; k += 32) reinterpret_cast<uint8_t*>(d)[k] = reinterpret_cast<const uint8_t*>(s)[k];
   }
+}
+
+// Naive scheme: every resolved chain must end on its array's device copy with the planned count;
+// the first target that does not is reported (atomicMin on the error word).
+__global__ void __launch_bounds__(256) k_check_resolved(const uint64_t* __restrict__ ea, const uint32_t* __restrict__ cnt,
+                                                        const uint64_t* __restrict__ expect_off,
+                                                        const uint32_t* __restrict__ cnt_plan, uint64_t image, uint64_t n,
+                                                        unsigned long long* bad) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && (ea[i] != image + expect_off[i] || cnt[i] != cnt_plan[i])) atomicMin(bad, (unsigned long long)i);
 }
 
 // Bulk copy by the SMs (either side may be mapped pinned host memory): grid-stride 16-byte words,
@@ -947,6 +968,15 @@ int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, cons
                      cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_copy_list<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(src, dst, bytes, n);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_check_resolved(cf_ctx* ctx, const uint64_t* ea, const uint32_t* cnt, const uint64_t* expect_off,
+                          const uint32_t* cnt_plan, uint64_t image, uint64_t n, uint64_t* bad, cudaStream_t s) {
+  if (n == 0) return CF_OK;
+  k_check_resolved<<<unsigned((n + 255) / 256), 256, 0, s>>>(ea, cnt, expect_off, cnt_plan, image, n,
+                                                            reinterpret_cast<unsigned long long*>(bad));
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -288,6 +288,8 @@ struct cf_kernel_plan {
   uint64_t* ea = nullptr;
   uint32_t* cnt = nullptr;
   uint64_t* root = nullptr;
+  uint64_t* expect = nullptr;     // cf_kernel_plan_expect: where each chain must end (image offsets)
+  uint32_t* cnt_plan = nullptr;   // ... and with which count
   cf_scale_work work{};
 };
 
@@ -373,11 +375,67 @@ int cf_kernel_plan_run(cf_kernel_plan* k, int mode, void* image, const cf_chain_
   return CF_OK;
 }
 
+int cf_kernel_plan_expect(cf_kernel_plan* k, const uint64_t* h_expect_off, const uint64_t* h_count) {
+  if (!k || (k->ntargets && (!h_expect_off || !h_count))) return fail(CF_E_INVALID, "null argument");
+  CfDevice g(k->ctx);
+  if (k->ntargets == 0) return CF_OK;
+  std::vector<uint32_t> c32(k->ntargets);
+  for (uint64_t t = 0; t < k->ntargets; ++t) {
+    if (h_count[t] >> 32) return fail(CF_E_INVALID, "count does not fit the u32 nA field");
+    c32[t] = uint32_t(h_count[t]);
+  }
+  if (!k->expect) {
+    cudaError_t e = cudaMalloc(&k->expect, k->ntargets * 12);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      k->expect = nullptr;
+      return fail(e == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "kernel plan expect: %s", cudaGetErrorString(e));
+    }
+    k->cnt_plan = reinterpret_cast<uint32_t*>(k->expect + k->ntargets);
+  }
+  CF_CUDA(cudaMemcpyAsync(k->expect, h_expect_off, k->ntargets * 8, cudaMemcpyHostToDevice, k->ctx->compute));
+  CF_CUDA(cudaMemcpyAsync(k->cnt_plan, c32.data(), k->ntargets * 4, cudaMemcpyHostToDevice, k->ctx->compute));
+  CF_CUDA(cudaStreamSynchronize(k->ctx->compute));
+  return CF_OK;
+}
+
+int cf_kernel_plan_resolve(cf_kernel_plan* k, void* image, const cf_chain_shape* shape, uint64_t* h_ea,
+                           uint32_t* h_count, uint64_t* bad) {
+  if (!k || !shape || (k->ntargets && (!h_ea || !h_count) && !k->expect)) return fail(CF_E_INVALID, "null argument");
+  cf_ctx* c = k->ctx;
+  CfDevice g(c);
+  if (bad) *bad = NO_BAD;
+  if (k->ntargets == 0) return CF_OK;
+  cudaStream_t s = c->compute;
+  CF_CUDA(cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  CF_TRY(launch_resolve(c, static_cast<const uint8_t*>(image), *shape, k->root, k->lv, k->od, k->ntargets, k->ea, k->cnt,
+                        c->d_bad, s));
+  if (h_ea) CF_CUDA(cudaMemcpyAsync(h_ea, k->ea, k->ntargets * 8, cudaMemcpyDeviceToHost, s));
+  if (h_count) CF_CUDA(cudaMemcpyAsync(h_count, k->cnt, k->ntargets * 4, cudaMemcpyDeviceToHost, s));
+  uint64_t rb = NO_BAD;
+  CF_TRY(read_bad(c, c->d_bad, s, &rb));
+  if (rb != NO_BAD) {
+    if (bad) *bad = rb;
+    return fail(CF_E_WILD, "chain walk for target %llu left the device image", (unsigned long long)rb);
+  }
+  if (!h_ea && k->expect) {   // check on the device: every chain ends where it must
+    CF_TRY(launch_check_resolved(c, k->ea, k->cnt, k->expect, k->cnt_plan, reinterpret_cast<uint64_t>(image),
+                                 k->ntargets, c->d_bad, s));
+    CF_TRY(read_bad(c, c->d_bad, s, &rb));
+    if (rb != NO_BAD) {
+      if (bad) *bad = rb;
+      return fail(CF_E_WILD, "chain of target %llu does not end on its array's device copy", (unsigned long long)rb);
+    }
+  }
+  return CF_OK;
+}
+
 int cf_kernel_plan_free(cf_kernel_plan* k) {
   if (!k) return CF_OK;
   CfDevice g(k->ctx);
   cudaStreamSynchronize(k->ctx->compute);
   cudaFree(k->d);
+  if (k->expect) cudaFree(k->expect);
   delete k;
   return CF_OK;
 }

@@ -80,7 +80,8 @@ void destroy(cf_selective* w) {
 
 namespace {
 int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count, int elem,
-             uint64_t chunk_bytes, cf_selective** out, bool dry, bool dry_mapped) {
+             uint64_t chunk_bytes, cf_selective** out, bool dry, bool dry_mapped, const uint8_t* scale_mask = nullptr,
+             uint32_t plan_flags = 0) {
   if (!out || (n && (!h_src || !d_buf || !count))) return fail(CF_E_INVALID, "null argument");
   if (elem != 4 && elem != 8) return fail(CF_E_INVALID, "elem must be 4 or 8");
   CfDevice g(dry ? nullptr : ctx);
@@ -126,7 +127,7 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
       zsrc.push_back(h_src[i]);
       zdst.push_back(d_buf[i]);
       zbytes.push_back(bytes);
-      tri.insert(tri.end(), {i, 0, count[i]});
+      if (!scale_mask || scale_mask[i]) tri.insert(tri.end(), {i, 0, count[i]});
       acc += bytes;
       continue;
     }
@@ -135,7 +136,7 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
       const uint64_t pb = (e1 - e0) * uint64_t(elem);
       if (acc + pb > ch && acc) close_step();
       w->dma.push_back({h_src[i] + e0 * uint64_t(elem), d_buf[i] + e0 * uint64_t(elem), pb});
-      tri.insert(tri.end(), {i, e0, e1});
+      if (!scale_mask || scale_mask[i]) tri.insert(tri.end(), {i, e0, e1});
       acc += pb;
     }
   }
@@ -145,7 +146,7 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
   // staged spans: per step, the host range its zero-copy entries lie in, when they fill it densely
   // (staging offsets keep the host address mod 256, so the copy list's 16-byte paths still apply)
   w->span.assign(w->nsteps, cf_selective::Piece{0, 0, 0});
-  for (uint64_t k = 0; k < w->nsteps; ++k) {
+  for (uint64_t k = 0; k < w->nsteps && !(plan_flags & CF_SEL_PER_OBJECT); ++k) {
     const uint64_t z0 = w->zc_lo[k], z1 = w->zc_lo[k + 1];
     if (z1 - z0 < 2) continue;
     uint64_t lo = ~uint64_t(0), hi = 0, fill = 0;
@@ -228,6 +229,12 @@ int cf_selective_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint
                       int elem, uint64_t chunk_bytes, cf_selective** out) {
   if (!ctx) return fail(CF_E_INVALID, "null argument");
   return sel_plan(ctx, n, h_src, d_buf, count, elem, chunk_bytes, out, false, false);
+}
+
+int cf_selective_plan_ex(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count,
+                         const uint8_t* scale_mask, uint32_t plan_flags, int elem, uint64_t chunk_bytes, cf_selective** out) {
+  if (!ctx) return fail(CF_E_INVALID, "null argument");
+  return sel_plan(ctx, n, h_src, d_buf, count, elem, chunk_bytes, out, false, false, scale_mask, plan_flags);
 }
 
 int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d_buf, const uint64_t* count, int elem,

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import AttachOutsideArena, SchemeError, VerificationFailed, WildAccess
-from .memory import D2H, DATA_OP_KINDS, H2D, NULL_ADDR, AddressMap, Arena, Machine
+from .memory import D2H, DATA_OP_KINDS, H2D, NULL_ADDR, AddressMap, Arena, Machine, _poke_words
 from .scenarios import (LEAF_NODE_SIZE, LEAF_OFF_A, NODE_SIZE, OFF_A, OFF_LNEXT, OFF_NA, ForestSpec,
                         LinearSpec, TreeHandle, build_tree, marshal_tree, payload_values)
 
@@ -336,6 +336,91 @@ class FusedSelectiveWindow:
         self._run(N.CF_WIN_H2D | N.CF_WIN_SCALE | N.CF_WIN_D2H, self.scale)
 
 
+class FusedNaiveWindow:
+    """The naive scheme's ``transfer_to_device -> kernel_scale -> copy_back`` (per-object deep
+    copy, memory.py:349-374; device chain walk, harness.py:244-304) deferred into one window:
+    the node objects go over first (one transfer per object) and get their pointer fields fixed,
+    every target chain is walked on the device and must land on its array's device copy
+    (``WildAccess`` otherwise), then the arrays -- still one transfer per object, big ones on the
+    copy engines, small ones by zero-copy warps -- are copied in, scaled and copied back step by
+    step in a cf_selective pipeline (CF_SEL_PER_OBJECT: no staged spans), and the node objects go
+    back last, their host pointers restored.  Logs, errors and flush rules as the other fused
+    windows; chase mode and observations in between take the eager path."""
+
+    def __init__(self, machine: Machine, prep: DevicePrep, lay, dev_base: int):
+        self.machine, self.prep, self.lay, self.dev_base = machine, prep, lay, dev_base
+        self.scale: float | None = None
+        self.mode = "resolved"
+
+    def flush(self) -> None:
+        """Materialise the stage reached: every object copied and fixed (+ the kernel)."""
+        m, p = self.machine, self.prep
+        m._naive_copy_in(self.lay, self.dev_base, p.amap)
+        if self.scale is not None:
+            _run_kernel(m, p.handle, p, self.scale, self.mode)
+
+    def complete(self) -> None:
+        m, p, lay = self.machine, self.prep, self.lay
+        lib, ctx = N.lib(), m.ctx.handle
+        handle = p.handle
+        t0 = time.perf_counter()
+        dev = lay.dev_at(self.dev_base)
+        node_dev = np.ascontiguousarray(dev[lay.node_alloc])
+        # 1. node objects in, pointer fields fixed on the device
+        N.check(lib.cf_copy_objects(ctx, N.ptr(node_dev), N.ptr(lay.node_host), N.ptr(lay.node_sizes),
+                                    len(node_dev)), "naive per-object copies")
+        m._device_fixup(p.amap, lay.fields, lay.targets)
+        t1 = time.perf_counter()
+        # 2. every target chain walked through the device objects: it must end on the device copy
+        #    of its array with the planned count
+        idx, _, _, _, cnt, _ = _kernel_args(handle, p.policy)
+        if len(idx):
+            kp, sh = _kernel_plan(m, handle, p)
+            if m._plan_keep.get(("expect", kp.value)) is not lay:   # where each chain must end, once per plan
+                expect = np.ascontiguousarray(lay.dev_off[lay.arr_alloc[idx]])   # held across the call
+                N.check(lib.cf_kernel_plan_expect(kp, N.ptr(expect), N.ptr(cnt)), "naive chain targets")
+                m._plan_keep[("expect", kp.value)] = lay
+            bad = N.U64(0)
+            rc = lib.cf_kernel_plan_resolve(kp, p.image, C.byref(sh), None, None, C.byref(bad))
+            if rc == N.CF_E_WILD:
+                raise WildAccess(N.last_error())
+            N.check(rc, "naive chain walk")
+        t2 = time.perf_counter()
+        # 3. arrays: in -> scale (targets) -> back, pipelined; one transfer per object
+        key = ("naive_sel", self.dev_base, p.policy)
+        w = m._plans.get(key)
+        if w is None:
+            sel = lay.selective.get(p.policy)
+            if sel is None:
+                nz = np.nonzero(np.asarray(handle.arr_count, np.uint64) > 0)[0]
+                mask = np.zeros(len(handle.arr_count), np.uint8)
+                mask[idx] = 1
+                sel = lay.selective[p.policy] = (nz, np.ascontiguousarray(lay.host[lay.arr_alloc[nz]]),
+                                                 np.ascontiguousarray(np.asarray(handle.arr_count, np.uint64)[nz]),
+                                                 np.ascontiguousarray(mask[nz]))
+            nz, host, count, mask = sel
+            dbuf = np.ascontiguousarray(dev[lay.arr_alloc[nz]])
+            w = C.c_void_p()
+            N.check(lib.cf_selective_plan_ex(ctx, len(nz), N.ptr(host), N.ptr(dbuf), N.ptr(count), N.ptr(mask),
+                                             N.CF_SEL_PER_OBJECT, handle.spec.elem, FUSED_CHUNK, C.byref(w)),
+                    "naive window plan")
+            m._plans[key] = w
+            m._plan_free[key] = lib.cf_selective_free
+        t3 = time.perf_counter()
+        rc = lib.cf_selective_run(w, N.CF_WIN_H2D | N.CF_WIN_SCALE | N.CF_WIN_D2H, float(self.scale))
+        if rc == N.CF_E_WILD:
+            raise WildAccess(N.last_error())
+        N.check(rc, "naive window")
+        t4 = time.perf_counter()
+        # 4. node objects back, host pointers restored (memory.py:368-372)
+        N.check(lib.cf_copy_objects(ctx, N.ptr(lay.node_host), N.ptr(node_dev), N.ptr(lay.node_sizes),
+                                    len(node_dev)), "naive copy back")
+        _poke_words(lay.fields, lay.targets)
+        t5 = time.perf_counter()
+        self.timing = {"run_ms": (t5 - t0) * 1e3, "nodes_in_fixup_ms": (t1 - t0) * 1e3, "chain_walk_ms": (t2 - t1) * 1e3,
+                       "plan_ms": (t3 - t2) * 1e3, "arrays_ms": (t4 - t3) * 1e3, "nodes_out_ms": (t5 - t4) * 1e3}
+
+
 def _pending(machine: Machine, prep: DevicePrep):
     f = prep.fused
     return f if f is not None and machine._deferred is f else None
@@ -373,9 +458,17 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         return DevicePrep(scheme, device_root=image + (handle.root_addr - arena.buffer_host_addr), arena=arena,
                           policy=policy, image=image, image_bytes=arena.total_bytes)
     if scheme == "naive":
-        root, amap = machine.naive_deep_copy(handle)
-        base, span = machine._naive_span
-        return DevicePrep(scheme, device_root=root, amap=amap, policy=policy, image=base, image_bytes=span)
+        if not fused:
+            root, amap = machine.naive_deep_copy(handle)
+            base, span = machine._naive_span
+            return DevicePrep(scheme, device_root=root, amap=amap, policy=policy, image=base, image_bytes=span)
+        machine.flush()
+        lay, base, amap = machine._naive_prepare(handle)   # logs the per-object copies + attaches
+        prep = DevicePrep(scheme, device_root=amap.translate(handle.root_addr), amap=amap, policy=policy, image=base,
+                          image_bytes=lay.span, handle=handle)
+        prep.fused = FusedNaiveWindow(machine, prep, lay, base)
+        machine._deferred = prep.fused
+        return prep
     if scheme == "pointerchain":
         # host-side chain resolution, then one selective bulk copy per targeted array
         # (harness.py:228-238), submitted together as one batched copy into one device span
@@ -601,6 +694,11 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
         fw.scale = float(scale)   # joins the deferred pointerchain window
         stats.elements_touched = int(prep.buf_count.sum())
         return stats
+    if fw is not None and fw.scale is None and prep.scheme == "naive" and mode == "resolved":
+        fw.scale = float(scale)   # joins the deferred naive window
+        idx, stats.chain_derefs, _, _, cnt, _ = _kernel_args(handle, prep.policy)
+        stats.elements_touched = int(cnt.sum())
+        return stats
     machine.flush()
     ctx = machine.ctx.handle
     if prep.scheme == "pointerchain":
@@ -612,18 +710,7 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
             stats.elements_touched = int(cnt.sum())
         return stats
 
-    # per policy the kernel's arguments depend only on the immutable tree shape: computed once
-    kcache = handle.__dict__.setdefault("_kernel_args", {})
-    ka = kcache.get(prep.policy)
-    if ka is None:
-        idx = handle.target_indices(prep.policy)
-        idx = idx[handle.arr_count[idx] > 0]
-        ka = kcache[prep.policy] = (idx, _reference_derefs(handle, prep.policy, idx),
-                                    np.ascontiguousarray(handle.arr_level[idx], np.int32),
-                                    np.ascontiguousarray(handle.arr_ordinal[idx], np.uint32),
-                                    np.ascontiguousarray(handle.arr_count[idx], np.uint64),
-                                    np.ascontiguousarray(handle.arr_root[idx], np.uint64))
-    idx, stats.chain_derefs, lv, od, cnt, root_off = ka
+    idx, stats.chain_derefs, lv, od, cnt, root_off = _kernel_args(handle, prep.policy)
     if prep.scheme == "uvm":
         fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
         # every page read once (fields, then array pages -- a page met twice migrates once), then
@@ -634,6 +721,31 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
             machine.uvm_touch_ranges(dlo, dhi, "write", "device")
     if len(idx) == 0:
         return stats
+    _run_kernel(machine, handle, prep, scale, mode)
+    stats.elements_touched = int(cnt.sum())
+    return stats
+
+
+def _kernel_args(handle: TreeHandle, policy: str):
+    """(targets, chain_derefs, level i32, ordinal u32, count u64, root offset u64) of a policy's
+    non-empty targets: they depend only on the immutable tree shape, so computed once."""
+    kcache = handle.__dict__.setdefault("_kernel_args", {})
+    ka = kcache.get(policy)
+    if ka is None:
+        idx = handle.target_indices(policy)
+        idx = idx[handle.arr_count[idx] > 0]
+        ka = kcache[policy] = (idx, _reference_derefs(handle, policy, idx),
+                               np.ascontiguousarray(handle.arr_level[idx], np.int32),
+                               np.ascontiguousarray(handle.arr_ordinal[idx], np.uint32),
+                               np.ascontiguousarray(handle.arr_count[idx], np.uint64),
+                               np.ascontiguousarray(handle.arr_root[idx], np.uint64))
+    return ka
+
+
+def _kernel_plan(machine: Machine, handle: TreeHandle, prep: DevicePrep):
+    """The cf_kernel_plan of prep's targets (tables uploaded once per tree, policy and roots) and
+    the chain shape of prep's image."""
+    idx, _, lv, od, cnt, root_off = _kernel_args(handle, prep.policy)
     sh = handle.chain_shape()
     sh.root_off = prep.device_root - prep.image
     sh.image_bytes = prep.image_bytes
@@ -648,29 +760,43 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
                 lay.roots[prep.policy] = roots
     else:                       # marshalling image / managed tree: same offsets as the host layout
         roots = root_off
-    # the targets' tables and work list are planned and uploaded once per (tree, policy, roots)
     key = ("kernel", id(handle), prep.policy)
     held = machine._plan_keep.get(key)
     if held is not None and (held[0] is not handle or held[1] is not roots):
-        N.lib().cf_kernel_plan_free(machine._plans.pop(key))
+        old = machine._plans.pop(key)
+        machine._plan_keep.pop(("expect", old.value), None)
+        N.lib().cf_kernel_plan_free(old)
         held = None
     if held is None:
         kp = C.c_void_p()
-        N.check(N.lib().cf_kernel_plan_create(ctx, elem, N.ptr(roots), N.ptr(lv), N.ptr(od), N.ptr(cnt), len(idx),
-                                              C.byref(kp)), "kernel_scale plan")
+        N.check(N.lib().cf_kernel_plan_create(machine.ctx.handle, handle.spec.elem, N.ptr(roots), N.ptr(lv), N.ptr(od),
+                                              N.ptr(cnt), len(idx), C.byref(kp)), "kernel_scale plan")
         machine._plans[key] = kp
         machine._plan_free[key] = N.lib().cf_kernel_plan_free
         machine._plan_keep[key] = (handle, roots)
+    return machine._plans[key], sh
+
+
+def _run_kernel(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: float, mode: str) -> None:
+    """Eager kernel_scale on the device: resolve every target chain, then the leaf kernel."""
+    kp, sh = _kernel_plan(machine, handle, prep)
     bad = N.U64(0)
-    rc = N.lib().cf_kernel_plan_run(machine._plans[key], N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
+    rc = N.lib().cf_kernel_plan_run(kp, N.CF_MODE_CHASE if mode == "chase" else N.CF_MODE_RESOLVED,
                                     prep.image, C.byref(sh), float(scale), C.byref(bad))
     N.check(rc, "kernel_scale")
-    stats.elements_touched = int(cnt.sum())
-    return stats
 
 
 def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     fw = _pending(machine, prep)
+    if fw is not None and fw.scale is not None and prep.scheme == "naive":
+        machine._deferred = None
+        fw.complete()
+        lay = fw.lay
+        if getattr(machine, "_naive_span", None) and machine._naive_span[0] == fw.dev_base:
+            handle.__dict__["_spare_naive_span"] = fw.dev_base
+        machine.log.append_many(D2H, "per_object", lay.sizes_i64)
+        machine.log.append_many(D2H, "detach", lay.attach8)
+        return
     if fw is not None and fw.scale is not None and prep.scheme == "pointerchain":
         machine._deferred = None
         fw.complete()

@@ -643,22 +643,31 @@ class Machine:
         """Copy every object individually (one batched submission), then fix every pointer
         field on the device through the sorted interval map."""
         self.flush()
+        lay, dev_base, amap = self._naive_prepare(tree)
+        self._naive_copy_in(lay, dev_base, amap)
+        return amap.translate(tree.root_addr), amap
+
+    def _naive_prepare(self, tree):
+        """naive_deep_copy without its device work: the per-object device span (reused from this
+        tree's previous copied-back window), the address map and the logical log entries."""
         lay = naive_layout(tree)
         # the span of this tree's previous (copied-back) naive window is reused: a fresh
         # 1 GiB-class allocation per window costs more than the copies
         dev_base = tree.__dict__.pop("_spare_naive_span", 0) or \
             self.device.allocate_span(lay.span, lay.dev_off, lay.sizes, zero=False)
-        dev = lay.dev_at(dev_base)
-        ctx = self.ctx.handle
-        N.check(N.lib().cf_copy_objects(ctx, N.ptr(dev), N.ptr(lay.host), N.ptr(lay.sizes), len(lay.host)),
-                "naive per-object copies")
         amap = AddressMap.from_sorted(lay.hb, lay.sz, lay.doff_sorted + np.uint64(dev_base))
         amap._origin = (lay, dev_base)
-        self._device_fixup(amap, lay.fields, lay.targets)
         self.log.append_many(H2D, "per_object", lay.sizes_i64)
         self.log.append_many(H2D, "attach", lay.attach8)
         self._naive_span = (dev_base, lay.span)
-        return amap.translate(tree.root_addr), amap
+        return lay, dev_base, amap
+
+    def _naive_copy_in(self, lay: "NaiveLayout", dev_base: int, amap: "AddressMap") -> None:
+        """The device work of naive_deep_copy: every object copied, every pointer field fixed."""
+        dev = lay.dev_at(dev_base)
+        N.check(N.lib().cf_copy_objects(self.ctx.handle, N.ptr(dev), N.ptr(lay.host), N.ptr(lay.sizes), len(lay.host)),
+                "naive per-object copies")
+        self._device_fixup(amap, lay.fields, lay.targets)
 
     def _device_fixup(self, amap: "AddressMap", fields: np.ndarray, targets: np.ndarray) -> None:
         hb, sz, db = (np.ascontiguousarray(x, np.uint64) for x in amap.arrays())
@@ -761,8 +770,22 @@ class NaiveLayout:
         self.fields = np.ascontiguousarray(fields, np.uint64)
         self.targets = np.ascontiguousarray(targets, np.uint64)
         self.attach8 = np.full(len(self.fields), 8, np.int64)
+        # allocation index of every array (allocation order = address order) and of every node
+        # (offset, non-empty) keys: scattered forests allocate out of address order, and an empty
+        # allocation may share its offset with the next one
+        one = np.uint64(1)
+        akey = (np.asarray(tree.alloc_off, np.uint64) << one) | (self.sizes > 0).astype(np.uint64)
+        rkey = (np.asarray(tree.arr_off, np.uint64) << one) | (np.asarray(tree.arr_count, np.uint64) > 0).astype(np.uint64)
+        order = np.argsort(akey, kind="stable")
+        self.arr_alloc = order[np.searchsorted(akey[order], rkey)].astype(np.int64) if len(rkey) else np.zeros(0, np.int64)
+        is_arr = np.zeros(len(akey), bool)
+        is_arr[self.arr_alloc] = True
+        self.node_alloc = np.nonzero(~is_arr)[0]
+        self.node_host = np.ascontiguousarray(self.host[self.node_alloc])
+        self.node_sizes = np.ascontiguousarray(self.sizes[self.node_alloc])
         self._dev: dict[int, np.ndarray] = {}
         self.roots: dict = {}   # per policy: chain roots relative to the span base
+        self.selective: dict = {}   # per policy: the fused naive window's array list (FusedNaiveWindow)
 
     def dev_at(self, base: int) -> np.ndarray:
         d = self._dev.get(base)

@@ -331,3 +331,61 @@ def test_execute_case_device_phase_times(cf, scheme, fused):
     row = cf.report.ResultRow.from_metrics(m) if hasattr(cf, "report") else None
     if row is not None:
         assert row.extra["device_us"] == m.device_us
+
+
+def _naive_window(cf, spec, fused, seed=3, scale=2.0, policy="ref", align=None, mode="resolved"):
+    m = cf.Machine()
+    h = cf.build_tree(m, spec, seed=seed, align=align)
+    mark = m.log.mark()
+    prep = cf.transfer_to_device(m, h, "naive", policy=policy, fused=fused)
+    st = cf.kernel_scale(m, h, prep, scale, mode=mode)
+    cf.copy_back(m, h, prep)
+    dump = [bytes(m.host.read_bytes(a, s)) for a, s in h.allocations]
+    log = [(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)]
+    cf.verify_tree(m, h, scale, policy)
+    m.close()
+    return dump, log, (st.elements_touched, st.chain_derefs)
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+def test_fused_naive_equals_eager(cf, elem):
+    """The fused naive window (nodes first + fixup + device chain walk, then the arrays pipelined
+    one transfer per object) leaves every host byte, log entry and counter as the eager phases."""
+    rng = random.Random(17 + elem)
+    specs = [cf.DenseSpec(100, 256, 2, elem=elem), cf.DenseSpec(3, 20001, 2, elem=elem),
+             cf.LinearSpec(5, 1000, "LLinit_LLused", elem=elem), cf.LinearSpec(4, 300, "allinit_allused", elem=elem),
+             cf.DenseSpec(4, 1 << 16, 3, elem=elem, leaf_only=True),
+             cf.ForestSpec(cf.LinearSpec(3, 700, "LLinit_LLused", elem=elem), 9, scatter_seed=5)]
+    for spec in specs + [cf.DenseSpec(rng.randint(1, 6), rng.randint(0, 40000), rng.randint(0, 3), elem=elem)
+                         for _ in range(5)]:
+        for policy in ("ref", "all_arrays", "all_leaves"):
+            for align in (None, 1):
+                a = _naive_window(cf, spec, True, policy=policy, align=align)
+                b = _naive_window(cf, spec, False, policy=policy, align=align)
+                assert a == b, (spec, policy, align)
+
+
+def test_fused_naive_flush_chase_and_repeat(cf):
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.DenseSpec(6, 3000, 2), seed=4)
+    for r in range(3):   # repeated fused windows reuse the span and the plans
+        prep = cf.transfer_to_device(m, h, "naive", policy="all_leaves")
+        cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5)
+        cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    # an observation between transfer and kernel materialises the copy-in
+    prep = cf.transfer_to_device(m, h, "naive", policy="all_leaves")
+    root_dev = prep.device_root
+    assert m.device.read_word(root_dev + 8) == prep.amap.translate(m.host.read_word(h.root_addr + 8))
+    cf.kernel_scale(m, h, prep, 0.5)
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 1.0, "all_leaves")
+    # chase mode runs eagerly; copy_back without a kernel round-trips
+    prep = cf.transfer_to_device(m, h, "naive", policy="all_leaves")
+    cf.kernel_scale(m, h, prep, 2.0, mode="chase")
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    prep = cf.transfer_to_device(m, h, "naive", policy="all_leaves")
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    m.close()

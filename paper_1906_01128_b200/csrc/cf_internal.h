@@ -53,6 +53,8 @@ inline cudaError_t copy_host_aligned(void* dst, const void* src, size_t n, cudaM
 // Kernel launchers (cf_kernels.cu).  Each increments ctx->launches once per kernel launch.
 int debug_info(uint64_t* out, int reset);
 int launch_sm_copy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, unsigned ctas, cudaStream_t s);
+int launch_copy_list2(cf_ctx* ctx, const uint64_t* sa, const uint64_t* da, const uint64_t* ba, uint64_t na,
+                      const uint64_t* sb, const uint64_t* db, const uint64_t* bb, uint64_t nb, cudaStream_t s);
 int launch_check_resolved(cf_ctx* ctx, const uint64_t* ea, const uint32_t* cnt, const uint64_t* expect_off,
                           const uint32_t* cnt_plan, uint64_t image, uint64_t n, uint64_t* bad, cudaStream_t s);
 int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, const uint64_t* bytes, uint64_t n,

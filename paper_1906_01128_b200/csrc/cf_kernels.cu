@@ -758,12 +758,41 @@ __global__ void __launch_bounds__(256) k_seg_copy(const uint64_t* __restrict__ s
 // direction): warp i copies bytes[i] from src[i] to dst[i] in the widest words (16, 8 or 4 bytes)
 // that both ends and the length allow.  Replaces one copy-engine command per object for the
 // pointerchain scheme's small arrays (cf_selective_run).
+__device__ __forceinline__ void copy_object(uint64_t s, uint64_t d, uint64_t b, unsigned lane);
+
 __global__ void __launch_bounds__(256) k_copy_list(const uint64_t* __restrict__ src, const uint64_t* __restrict__ dst,
                                                    const uint64_t* __restrict__ bytes, uint64_t n) {
   const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31;
   if (i >= n) return;
-  const uint64_t s = src[i], d = dst[i], b = bytes[i];
+  copy_object(src[i], dst[i], bytes[i], lane);
+}
+
+// Two copy lists in one launch, their warps interleaved (A0 B0 A1 B1 ... then the longer list's
+// rest): a pipelined window's copy-out of step k and copy-in of step k+1 then share every SM, so
+// both link directions stay busy (zero-copy duplex) instead of one grid draining before the other.
+__global__ void __launch_bounds__(256) k_copy_list2(const uint64_t* __restrict__ sa, const uint64_t* __restrict__ da,
+                                                    const uint64_t* __restrict__ ba, uint64_t na,
+                                                    const uint64_t* __restrict__ sb, const uint64_t* __restrict__ db,
+                                                    const uint64_t* __restrict__ bb, uint64_t nb) {
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t m = na < nb ? na : nb;
+  bool a;
+  uint64_t i;
+  if (w < 2 * m) {
+    a = (w & 1) == 0;
+    i = w >> 1;
+  } else {
+    a = na > nb;
+    i = m + (w - 2 * m);
+    if (i >= (a ? na : nb)) return;
+  }
+  if (a) copy_object(sa[i], da[i], ba[i], lane);
+  else copy_object(sb[i], db[i], bb[i], lane);
+}
+
+__device__ __forceinline__ void copy_object(uint64_t s, uint64_t d, uint64_t b, unsigned lane) {
   if (((s | d | b) & 15) == 0) {
     // all loads of a 2 KiB slice first, then the stores: one PCIe round trip per slice instead
     // of one per 512 bytes (source and destination may not alias, the compiler cannot know)
@@ -968,6 +997,15 @@ int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, cons
                      cudaStream_t s) {
   if (n == 0) return CF_OK;
   k_copy_list<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(src, dst, bytes, n);
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_copy_list2(cf_ctx* ctx, const uint64_t* sa, const uint64_t* da, const uint64_t* ba, uint64_t na,
+                      const uint64_t* sb, const uint64_t* db, const uint64_t* bb, uint64_t nb, cudaStream_t s) {
+  if (na == 0) return launch_copy_list(ctx, sb, db, bb, nb, s);
+  if (nb == 0) return launch_copy_list(ctx, sa, da, ba, na, s);
+  k_copy_list2<<<unsigned(((na + nb) * 32 + 255) / 256), 256, 0, s>>>(sa, da, ba, na, sb, db, bb, nb);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

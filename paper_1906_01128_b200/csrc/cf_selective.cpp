@@ -334,7 +334,46 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
   CF_CUDA(cudaStreamWaitEvent(cs, w->ev_tab, 0));
   cf_chain_shape sh;
   memset(&sh, 0, sizeof sh);
-  for (uint64_t k = 0; k < w->nsteps; ++k) {
+  // Full windows: the zero-copy copy-out of step k and copy-in of step k+1 run as ONE launch on
+  // the compute stream (warps interleaved), so both link directions share every SM; the DMA
+  // pieces keep their own H2D / D2H copy-engine streams.
+  const bool duplex = (flags & CF_WIN_H2D) && (flags & CF_WIN_D2H) && (flags & CF_WIN_SCALE) && w->nzc;
+  if (duplex) {
+    auto zin = [&](uint64_t k) { return w->zc_lo[k]; };
+    auto nz = [&](uint64_t k) { return w->zc_lo[k + 1] - w->zc_lo[k]; };
+    auto dma_in = [&](uint64_t k) -> int {
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
+        CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),
+                                  w->dma[j].bytes, cudaMemcpyHostToDevice, hs));
+      const cf_selective::Piece& sp = w->span[k];
+      if (sp.bytes)
+        CF_CUDA(copy_host_aligned(w->d_stage + sp.dst, reinterpret_cast<const void*>(sp.src), sp.bytes, cudaMemcpyHostToDevice, hs));
+      CF_CUDA(cudaEventRecord(w->ev_in[k], hs));
+      return CF_OK;
+    };
+    for (uint64_t k = 0; k < w->nsteps; ++k) CF_TRY(dma_in(k));   // the copy engine streams run ahead
+    if (w->span[0].bytes) CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[0], 0));
+    CF_TRY(launch_copy_list(c, zi + zin(0), zd + zin(0), zb + zin(0), nz(0), cs));
+    for (uint64_t k = 0; k < w->nsteps; ++k) {
+      CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k], 0));
+      CF_TRY(launch_scale(c, w->elem, CF_MODE_RESOLVED, nullptr, sh, nullptr, nullptr, nullptr, ea, cnt, w->work[k], scale,
+                          c->d_bad, cs));
+      CF_CUDA(cudaEventRecord(w->ev_out[k], cs));
+      CF_CUDA(cudaStreamWaitEvent(ds, w->ev_out[k], 0));
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
+        CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].src), reinterpret_cast<const void*>(w->dma[j].dst),
+                                  w->dma[j].bytes, cudaMemcpyDeviceToHost, ds));
+      // copy-out of step k (device buffers -> host) beside copy-in of step k+1
+      if (k + 1 < w->nsteps) {
+        if (w->span[k + 1].bytes) CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k + 1], 0));   // staged copy-in source
+        CF_TRY(launch_copy_list2(c, zd + zin(k), zs + zin(k), zb + zin(k), nz(k), zi + zin(k + 1), zd + zin(k + 1),
+                                 zb + zin(k + 1), nz(k + 1), cs));
+      } else {
+        CF_TRY(launch_copy_list(c, zd + zin(k), zs + zin(k), zb + zin(k), nz(k), cs));
+      }
+    }
+  }
+  for (uint64_t k = 0; k < w->nsteps && !duplex; ++k) {
     if (flags & CF_WIN_H2D) {
       for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
         CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].dst), reinterpret_cast<const void*>(w->dma[j].src),

@@ -435,16 +435,21 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         if arena is None:
             raise ValueError("marshalling needs the arena returned by marshal_tree")
         base, total = arena.buffer_host_addr, arena.total_bytes
-        sites = np.ascontiguousarray(arena.site_offsets, np.uint64)
+        # every pointer field must target the arena (memory.py:319-321): checked in address order
+        # (page-sequential reads of the pinned arena); on a fault re-checked in the reference's
+        # site order so the error names the first offending site as the attach loop would
+        sites = arena.sorted_site_offsets
         bad = N.U64(0)
         rc = N.lib().cf_arena_check_sites(base, total, N.ptr(sites) if len(sites) else None, len(sites), base,
                                           C.byref(bad))
         if rc == N.CF_E_OUTSIDE_ARENA:
+            dfs = np.ascontiguousarray(arena.site_offsets, np.uint64)
+            N.lib().cf_arena_check_sites(base, total, N.ptr(dfs), len(dfs), base, C.byref(bad))
             raise AttachOutsideArena(N.last_error())
         N.check(rc, "transfer_to_device")
         image = arena.take_image()   # fully overwritten by the copy
         machine.log.append(H2D, "bulk", total)
-        machine.log.append_many(H2D, "attach", np.full(len(sites), 8, np.int64))
+        machine.log.append_many(H2D, "attach", arena.site_words)
         arena.device_image_addr = image
         prep = DevicePrep(scheme, device_root=image + (handle.root_addr - base), arena=arena, policy=policy,
                           image=image, image_bytes=total)
@@ -808,7 +813,7 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
         fw.complete()
         arena = prep.arena
         machine.log.append(D2H, "bulk", arena.total_bytes)
-        machine.log.append_many(D2H, "detach", np.full(len(arena.site_offsets), 8, np.int64))
+        machine.log.append_many(D2H, "detach", arena.site_words)
         arena._spare_image = arena.device_image_addr
         arena.device_image_addr = NULL_ADDR
         return

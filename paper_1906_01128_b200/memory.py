@@ -435,6 +435,14 @@ class Arena:
         return self._site_off
 
     @property
+    def site_words(self) -> np.ndarray:
+        """One 8-byte log entry per pointer field (attach / detach), built once per arena."""
+        w = getattr(self, "_site_words", None)
+        if w is None or len(w) != len(self._site_off):
+            w = self._site_words = np.full(len(self._site_off), 8, np.int64)
+        return w
+
+    @property
     def sorted_site_offsets(self) -> np.ndarray:
         if self._sorted is None:
             self._sorted = np.sort(self._site_off)
@@ -616,7 +624,7 @@ class Machine:
             raise AttachOutsideArena(N.last_error())
         N.check(rc, "marshal_transfer_and_attach")
         self.log.append(H2D, "bulk", arena.total_bytes)
-        self.log.append_many(H2D, "attach", np.full(len(sites), 8, np.int64))
+        self.log.append_many(H2D, "attach", arena.site_words)
         arena.device_image_addr = image
         return image
 
@@ -634,7 +642,7 @@ class Machine:
             raise AttachOutsideArena(N.last_error())
         N.check(rc, "demarshal")
         self.log.append(D2H, "bulk", arena.total_bytes)
-        self.log.append_many(D2H, "detach", np.full(len(sites), 8, np.int64))
+        self.log.append_many(D2H, "detach", arena.site_words)
         arena._spare_image = image
         arena.device_image_addr = NULL_ADDR
 

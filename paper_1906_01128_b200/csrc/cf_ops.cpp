@@ -543,10 +543,31 @@ int cf_copy_objects(cf_ctx* c, void* const* dsts, const void* const* srcs, const
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
     return a.type != cudaMemoryTypeUnregistered && a.devicePointer == p;
   };
+  // fast path: every object small and both ends SM-addressable -- the caller's own address and
+  // size arrays are the copy list (no per-object host work beyond one scan)
+  {
+    bool all_small = true;
+    for (uint64_t i = 0; i < count && all_small; ++i) all_small = sizes[i] < SMALL;
+    if (all_small && dev_ok(srcs[0]) && dev_ok(dsts[0])) {
+      cudaStream_t s = c->compute;
+      DevBuf blk(c);
+      CF_TRY(blk.alloc(24 * count));
+      uint64_t* d = blk.as<uint64_t>();
+      CF_CUDA(cudaMemcpyAsync(d, srcs, 8 * count, cudaMemcpyHostToDevice, s));
+      CF_CUDA(cudaMemcpyAsync(d + count, dsts, 8 * count, cudaMemcpyHostToDevice, s));
+      CF_CUDA(cudaMemcpyAsync(d + 2 * count, sizes, 8 * count, cudaMemcpyHostToDevice, s));
+      CF_TRY(launch_copy_list(c, d, d + count, d + 2 * count, count, s));
+      CF_CUDA(cudaStreamSynchronize(s));
+      return CF_OK;
+    }
+  }
   std::vector<uint64_t> zs, zd, zb;
   std::vector<void*> bd;
   std::vector<const void*> bs;
   std::vector<uint64_t> bz;
+  zs.reserve(count);
+  zd.reserve(count);
+  zb.reserve(count);
   bool zc = true;
   bool checked = false;
   for (uint64_t i = 0; i < count; ++i) {

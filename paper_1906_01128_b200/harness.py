@@ -308,17 +308,7 @@ class FusedSelectiveWindow:
         p = self.prep
         lib = N.lib()
         t0 = time.perf_counter()
-        key = ("selective", int(p.buf_dev[0]), len(p.buf_dev))
-        w = self.machine._plans.get(key)
-        if w is None:
-            host = np.ascontiguousarray(p.buf_host, np.uint64)
-            dev = np.ascontiguousarray(p.buf_dev, np.uint64)
-            cnt = np.ascontiguousarray(p.buf_count, np.uint64)
-            w = C.c_void_p()
-            N.check(lib.cf_selective_plan(self.machine.ctx.handle, len(dev), N.ptr(host), N.ptr(dev), N.ptr(cnt),
-                                          self.elem, FUSED_CHUNK, C.byref(w)), "pointerchain window plan")
-            self.machine._plans[key] = w
-            self.machine._plan_free[key] = lib.cf_selective_free
+        w = _selective_plan(self.machine, p, self.elem)
         t1 = time.perf_counter()
         rc = lib.cf_selective_run(w, flags, float(scale))
         self.timing = {"plan_ms": (t1 - t0) * 1e3, "run_ms": (time.perf_counter() - t1) * 1e3}
@@ -334,6 +324,22 @@ class FusedSelectiveWindow:
 
     def complete(self) -> None:
         self._run(N.CF_WIN_H2D | N.CF_WIN_SCALE | N.CF_WIN_D2H, self.scale)
+
+
+def _selective_plan(machine: Machine, p: DevicePrep, elem: int):
+    """The cf_selective plan of a pointerchain DevicePrep's buffers (cached on the machine)."""
+    key = ("selective", int(p.buf_dev[0]), len(p.buf_dev))
+    w = machine._plans.get(key)
+    if w is None:
+        host = np.ascontiguousarray(p.buf_host, np.uint64)
+        dev = np.ascontiguousarray(p.buf_dev, np.uint64)
+        cnt = np.ascontiguousarray(p.buf_count, np.uint64)
+        w = C.c_void_p()
+        N.check(N.lib().cf_selective_plan(machine.ctx.handle, len(dev), N.ptr(host), N.ptr(dev), N.ptr(cnt),
+                                          elem, FUSED_CHUNK, C.byref(w)), "pointerchain window plan")
+        machine._plans[key] = w
+        machine._plan_free[key] = N.lib().cf_selective_free
+    return w
 
 
 class FusedNaiveWindow:
@@ -488,9 +494,13 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
             sizes = handle.arr_count[idx] * np.uint64(e)
             aligned = (sizes + np.uint64(7)) & ~np.uint64(7)
             offs = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.uint64) if len(idx) else aligned
-            lay = cache[policy] = (idx, sizes, sizes.astype(np.int64), offs, int(aligned.sum()),
-                                   np.ascontiguousarray(handle.arr_off[idx] + np.uint64(handle.base)),
-                                   np.ascontiguousarray(handle.arr_count[idx]), {})
+            lay = (idx, sizes, sizes.astype(np.int64), offs, int(aligned.sum()),
+                   np.ascontiguousarray(handle.arr_off[idx] + np.uint64(handle.base)),
+                   np.ascontiguousarray(handle.arr_count[idx]), {})
+            for a in lay[:7]:
+                if isinstance(a, np.ndarray):
+                    a.flags.writeable = False   # shared by every window of this tree
+            cache[policy] = lay
         idx, sizes, sizes_i64, offs, span, buf_host, buf_count, by_base = lay
         prep = DevicePrep(scheme, policy=policy, handle=handle, buf_array=idx, buf_host=buf_host, buf_count=buf_count)
         if len(idx):
@@ -501,6 +511,7 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
                 if len(by_base) >= 4:
                     by_base.clear()
                 prep.buf_dev = by_base[dev_base] = offs + np.uint64(dev_base)
+                prep.buf_dev.flags.writeable = False
             if fused:
                 # addresses come from the tree's own array table and the span just allocated for
                 # exactly these sizes: in bounds by construction (the eager path re-checks them)
@@ -708,11 +719,13 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     ctx = machine.ctx.handle
     if prep.scheme == "pointerchain":
         if len(prep.buf_dev):
-            ea = np.ascontiguousarray(prep.buf_dev, np.uint64)
-            cnt = np.ascontiguousarray(prep.buf_count, np.uint64)
-            N.check(N.lib().cf_scale_resolved(ctx, elem, N.ptr(ea), N.ptr(cnt), len(ea), float(scale)),
-                    "kernel_scale")
-            stats.elements_touched = int(cnt.sum())
+            # the leaf kernel over the copied buffers (host-resolved addresses): the buffers' work
+            # list is planned once per tree (the pointerchain window's plan, leaf-kernel stage only)
+            rc = N.lib().cf_selective_run(_selective_plan(machine, prep, elem), N.CF_WIN_SCALE, float(scale))
+            if rc == N.CF_E_WILD:
+                raise WildAccess(N.last_error())
+            N.check(rc, "kernel_scale")
+            stats.elements_touched = int(prep.buf_count.sum())
         return stats
 
     idx, stats.chain_derefs, lv, od, cnt, root_off = _kernel_args(handle, prep.policy)
@@ -823,8 +836,9 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     elif prep.scheme == "naive":
         machine.naive_copy_back(handle, prep.amap)
     elif prep.scheme == "pointerchain":
-        machine.transfer_ranges(machine.device, prep.buf_dev, machine.host, prep.buf_host,
-                                prep.buf_count * np.uint64(handle.spec.elem), "bulk")
+        lay = handle.__dict__.get("_selective_layout", {}).get(prep.policy)
+        sizes = lay[1] if lay is not None and lay[6] is prep.buf_count else prep.buf_count * np.uint64(handle.spec.elem)
+        machine.transfer_ranges(machine.device, prep.buf_dev, machine.host, prep.buf_host, sizes, "bulk")
         if len(prep.buf_dev):
             handle.__dict__.setdefault("_spare_spans", {})[prep.policy] = int(prep.buf_dev[0])
     elif prep.scheme == "uvm":

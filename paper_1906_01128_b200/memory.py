@@ -225,6 +225,7 @@ class MemorySpace:
         i = bisect.bisect_left(self._seg_bases, seg.base)
         self._seg_bases.insert(i, seg.base)
         self._segs.insert(i, seg)
+        self._gen = getattr(self, "_gen", 0) + 1
 
     def allocate(self, size_bytes: int, zero: bool = True) -> int:
         """Bump allocation.  ``zero=False`` skips the zero fill for storage the caller overwrites
@@ -272,6 +273,7 @@ class MemorySpace:
         self._storage.clear()
         self._segs.clear()
         self._seg_bases.clear()
+        self._gen = getattr(self, "_gen", 0) + 1
         self._slab = None
 
     # -- bounds-checked access (memory.py:139-184) ---------------------------------------
@@ -286,7 +288,23 @@ class MemorySpace:
         raise WildAccess(f"{self.kind} access at 0x{addr:x} (+{nbytes}) hits no live allocation")
 
     def _check_many(self, addrs: np.ndarray, sizes: np.ndarray) -> None:
-        """Vectorised _check: every [addr, addr+size) inside one live allocation."""
+        """Vectorised _check: every [addr, addr+size) inside one live allocation.  Read-only
+        range tables (the drop-in's cached per-tree layouts) checked once per allocation state."""
+        frozen = isinstance(addrs, np.ndarray) and isinstance(sizes, np.ndarray) and \
+            not addrs.flags.writeable and not sizes.flags.writeable
+        gen = getattr(self, "_gen", 0)
+        if frozen:
+            memo = self.__dict__.setdefault("_checked", {})
+            hit = memo.get((id(addrs), id(sizes)))
+            if hit is not None and hit[0] is addrs and hit[1] is sizes and hit[2] == gen:
+                return
+        self._check_many_uncached(addrs, sizes)
+        if frozen:
+            if len(memo) >= 16:
+                memo.clear()
+            memo[(id(addrs), id(sizes))] = (addrs, sizes, gen)
+
+    def _check_many_uncached(self, addrs: np.ndarray, sizes: np.ndarray) -> None:
         addrs = np.asarray(addrs, np.uint64)
         sizes = np.asarray(sizes, np.uint64)
         if addrs.size <= 64:

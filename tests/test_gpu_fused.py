@@ -389,3 +389,36 @@ def test_fused_naive_flush_chase_and_repeat(cf):
     cf.copy_back(m, h, prep)
     cf.verify_tree(m, h, 2.0, "all_leaves")
     m.close()
+
+
+def test_naive_chain_walk_check_rejects_wrong_targets(cf):
+    """cf_kernel_plan_expect / _resolve: the device-side check of the naive window's chain walk
+    reports the first chain that does not end on its array's device copy (CF_E_WILD)."""
+    import ctypes as C
+    from paper_1906_01128_b200 import _native as N
+    from paper_1906_01128_b200 import harness as H
+    m = cf.Machine()
+    h = cf.build_tree(m, cf.DenseSpec(3, 500, 2), seed=1)
+    prep = cf.transfer_to_device(m, h, "naive", policy="all_leaves", fused=False)
+    idx, _, _, _, cnt, _ = H._kernel_args(h, "all_leaves")
+    kp, sh = H._kernel_plan(m, h, prep)
+    lay = prep.amap._origin[0]
+    good = np.ascontiguousarray(lay.dev_off[lay.arr_alloc[idx]])
+    bad = N.U64(0)
+    lib = N.lib()
+    N.check(lib.cf_kernel_plan_expect(kp, N.ptr(good), N.ptr(cnt)))
+    assert lib.cf_kernel_plan_resolve(kp, prep.image, C.byref(sh), None, None, C.byref(bad)) == 0
+    wrong = good.copy()
+    wrong[5] += np.uint64(8)
+    N.check(lib.cf_kernel_plan_expect(kp, N.ptr(wrong), N.ptr(cnt)))
+    assert lib.cf_kernel_plan_resolve(kp, prep.image, C.byref(sh), None, None, C.byref(bad)) == N.CF_E_WILD
+    assert bad.value == 5
+    wrong_cnt = cnt.copy()
+    wrong_cnt[2] += np.uint64(1)
+    N.check(lib.cf_kernel_plan_expect(kp, N.ptr(good), N.ptr(wrong_cnt)))
+    assert lib.cf_kernel_plan_resolve(kp, prep.image, C.byref(sh), None, None, C.byref(bad)) == N.CF_E_WILD
+    assert bad.value == 2
+    cf.kernel_scale(m, h, prep, 2.0)
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    m.close()

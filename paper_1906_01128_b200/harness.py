@@ -818,7 +818,9 @@ def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     if fw is not None and fw.scale is not None and prep.scheme == "pointerchain":
         machine._deferred = None
         fw.complete()
-        machine.log.append_many(D2H, "bulk", (prep.buf_count * np.uint64(handle.spec.elem)).astype(np.int64))
+        lay = handle.__dict__.get("_selective_layout", {}).get(prep.policy)
+        machine.log.append_many(D2H, "bulk", lay[2] if lay is not None and lay[6] is prep.buf_count
+                                else (prep.buf_count * np.uint64(handle.spec.elem)).astype(np.int64))
         prep.handle.__dict__.setdefault("_spare_spans", {})[prep.policy] = int(prep.buf_dev[0])
         return
     if fw is not None and fw.scale is not None:

@@ -18,6 +18,7 @@
 #include "cf_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -337,7 +338,8 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
   // Full windows: the zero-copy copy-out of step k and copy-in of step k+1 run as ONE launch on
   // the compute stream (warps interleaved), so both link directions share every SM; the DMA
   // pieces keep their own H2D / D2H copy-engine streams.
-  const bool duplex = (flags & CF_WIN_H2D) && (flags & CF_WIN_D2H) && (flags & CF_WIN_SCALE) && w->nzc;
+  const bool duplex = (flags & CF_WIN_H2D) && (flags & CF_WIN_D2H) && (flags & CF_WIN_SCALE) && w->nzc &&
+                      !getenv("CF_SEL_NO_DUPLEX");
   if (duplex) {
     auto zin = [&](uint64_t k) { return w->zc_lo[k]; };
     auto nz = [&](uint64_t k) { return w->zc_lo[k + 1] - w->zc_lo[k]; };

@@ -365,6 +365,45 @@ class FusedNaiveWindow:
         if self.scale is not None:
             _run_kernel(m, p.handle, p, self.scale, self.mode)
 
+    def _fixup(self) -> None:
+        """Every pointer field rewritten through the interval map on the device; the site and map
+        tables (C4: 1M sites, 2M map entries, 64 MB) are uploaded once per tree and span."""
+        m, p, lay = self.machine, self.prep, self.lay
+        n = len(lay.fields)
+        if n == 0:
+            return
+        if p.amap._origin is None:   # the map was extended since the transfer: from host tables
+            m._device_fixup(p.amap, lay.fields, lay.targets)
+            return
+        lib, ctx = N.lib(), m.ctx.handle
+        hb, sz, db = p.amap.arrays()
+        nmap = len(hb)
+        key = ("naive_fixup", self.dev_base)
+        blk = m._plans.get(key)
+        if blk is not None and m._plan_keep.get(key) is not lay:
+            lib.cf_dev_free(ctx, m._plans.pop(key))
+            blk = None
+        if blk is None:
+            blk = C.c_void_p()
+            N.check(lib.cf_dev_alloc(ctx, 8 * (2 * n + 3 * nmap + 1), C.byref(blk)), "naive fixup tables")
+            off = 0
+            for arr in (lay.fields, lay.targets, hb, sz, db):
+                a = np.ascontiguousarray(arr, np.uint64)
+                N.check(lib.cf_memcpy(ctx, blk.value + off, N.ptr(a), a.nbytes))
+                off += a.nbytes
+            m._plans[key] = blk
+            m._plan_free[key] = lambda w, c=ctx: lib.cf_dev_free(c, w)
+            m._plan_keep[key] = lay
+        b = blk.value
+        bad = b + 8 * (2 * n + 3 * nmap)
+        N.check(lib.cf_memset(ctx, bad, 0xFF, 8))
+        N.check(lib.cf_naive_fixup(ctx, b, b + 8 * n, n, b + 16 * n, b + 16 * n + 8 * nmap, b + 16 * n + 16 * nmap,
+                                   nmap, bad, None), "naive fixup")
+        out = np.zeros(1, np.uint64)
+        N.check(lib.cf_memcpy(ctx, N.ptr(out), bad, 8))
+        if int(out[0]) != (1 << 64) - 1:
+            raise WildAccess(f"fixup target 0x{int(lay.targets[int(out[0])]):x} was never copied to the device")
+
     def complete(self) -> None:
         m, p, lay = self.machine, self.prep, self.lay
         lib, ctx = N.lib(), m.ctx.handle
@@ -375,7 +414,7 @@ class FusedNaiveWindow:
         # 1. node objects in, pointer fields fixed on the device
         N.check(lib.cf_copy_objects(ctx, N.ptr(node_dev), N.ptr(lay.node_host), N.ptr(lay.node_sizes),
                                     len(node_dev)), "naive per-object copies")
-        m._device_fixup(p.amap, lay.fields, lay.targets)
+        self._fixup()
         t1 = time.perf_counter()
         # 2. every target chain walked through the device objects: it must end on the device copy
         #    of its array with the planned count

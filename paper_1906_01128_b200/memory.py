@@ -681,7 +681,7 @@ class Machine:
         # 1 GiB-class allocation per window costs more than the copies
         dev_base = tree.__dict__.pop("_spare_naive_span", 0) or \
             self.device.allocate_span(lay.span, lay.dev_off, lay.sizes, zero=False)
-        amap = AddressMap.from_sorted(lay.hb, lay.sz, lay.doff_sorted + np.uint64(dev_base))
+        amap = AddressMap.from_sorted(lay.hb, lay.sz, lay.map_dev_at(dev_base))
         amap._origin = (lay, dev_base)
         self.log.append_many(H2D, "per_object", lay.sizes_i64)
         self.log.append_many(H2D, "attach", lay.attach8)
@@ -810,8 +810,22 @@ class NaiveLayout:
         self.node_host = np.ascontiguousarray(self.host[self.node_alloc])
         self.node_sizes = np.ascontiguousarray(self.sizes[self.node_alloc])
         self._dev: dict[int, np.ndarray] = {}
+        self._map_dev: dict[int, np.ndarray] = {}
+        for a in (self.host, self.sizes, self.sizes_i64, self.dev_off, self.hb, self.sz, self.doff_sorted, self.fields,
+                  self.targets, self.attach8, self.node_host, self.node_sizes):
+            a.flags.writeable = False   # shared by every window of this tree
         self.roots: dict = {}   # per policy: chain roots relative to the span base
         self.selective: dict = {}   # per policy: the fused naive window's array list (FusedNaiveWindow)
+
+    def map_dev_at(self, base: int) -> np.ndarray:
+        """Device bases in host-address order (the AddressMap column) for a span base."""
+        d = self._map_dev.get(base)
+        if d is None:
+            if len(self._map_dev) >= 4:
+                self._map_dev.clear()
+            d = self._map_dev[base] = self.doff_sorted + np.uint64(base)
+            d.flags.writeable = False
+        return d
 
     def dev_at(self, base: int) -> np.ndarray:
         d = self._dev.get(base)

@@ -42,6 +42,7 @@ struct cf_selective {
   std::vector<cf_scale_work> work;         // per step: leaf-kernel work (device pointers set)
   uint64_t nzc = 0;
   std::vector<Piece> span;                 // per step: staged host span (bytes 0 = none); dst = staging offset
+  std::vector<uint8_t> span_out;           // per step: the span also goes back as one DMA (see sel_plan)
   uint8_t* d_stage = nullptr;              // staging area (device) for the span DMAs
   uint64_t stage_bytes = 0;
   // one pinned table block + device mirror: ea u64[n] | count u32[n] | zc src u64[nzc] |
@@ -160,6 +161,36 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
     const uint64_t off = (w->stage_bytes + 255) / 256 * 256 + (lo & 255);
     w->span[k] = cf_selective::Piece{lo, off, hi - lo};
     w->stage_bytes = off + (hi - lo);
+  }
+  // Copy-back through the staged span too (arrays packed into the staging slice on the device,
+  // then ONE D2H DMA of the span: copy engines both ways run the link at 99 GB/s where SM stores
+  // beside a DMA reach 88) -- only when that cannot disturb anything: every selected array that
+  // overlaps the span is one of this step's own (the bytes between them go back exactly as they
+  // were read at the start of this window, which no one can change before copy_back returns).
+  w->span_out.assign(w->nsteps, 0);
+  {
+    struct Iv { uint64_t lo, hi, step; };
+    std::vector<Iv> iv;
+    iv.reserve(zsrc.size() + w->dma.size());
+    for (uint64_t k = 0; k < w->nsteps; ++k) {
+      for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j) iv.push_back({zsrc[j], zsrc[j] + zbytes[j], k});
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j) iv.push_back({w->dma[j].src, w->dma[j].src + w->dma[j].bytes, k});
+    }
+    std::sort(iv.begin(), iv.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
+    uint64_t maxlen = 0;
+    for (const Iv& v : iv) maxlen = std::max(maxlen, v.hi - v.lo);
+    for (uint64_t k = 0; k < w->nsteps && !(plan_flags & CF_SEL_PER_OBJECT); ++k) {
+      const cf_selective::Piece& sp = w->span[k];
+      if (!sp.bytes) continue;
+      const uint64_t lo = sp.src, hi = sp.src + sp.bytes;
+      // intervals starting in [lo - maxlen, hi) are the only ones that can overlap
+      auto it = std::lower_bound(iv.begin(), iv.end(), lo > maxlen ? lo - maxlen : 0,
+                                 [](const Iv& a, uint64_t x) { return a.lo < x; });
+      bool ok = true;
+      for (; it != iv.end() && it->lo < hi && ok; ++it)
+        if (it->hi > lo && it->step != k) ok = false;
+      w->span_out[k] = ok;
+    }
   }
   // table block
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
@@ -309,6 +340,19 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
       if (y != count[i]) report("array covered up to", i, y);
     }
   if (stage_end > w->stage_bytes) report("staging area too small", stage_end, w->stage_bytes);
+  // a span copied back whole must not overlap any array moved by another step (quadratic, small n)
+  for (uint64_t k = 0; k < w->nsteps; ++k) {
+    if (!w->span_out[k]) continue;
+    if (!w->span[k].bytes) { report("span copied back without a span", k, 0); continue; }
+    const uint64_t lo = w->span[k].src, hi = lo + w->span[k].bytes;
+    for (uint64_t j = 0; j < w->nsteps; ++j) {
+      if (j == k) continue;
+      for (uint64_t q = w->zc_lo[j]; q < w->zc_lo[j + 1]; ++q)
+        if (D.zsrc[q] < hi && D.zsrc[q] + D.zbytes[q] > lo) report("copied-back span overlaps another step's array", k, j);
+      for (uint64_t q = w->dma_lo[j]; q < w->dma_lo[j + 1]; ++q)
+        if (w->dma[q].src < hi && w->dma[q].src + w->dma[q].bytes > lo) report("copied-back span overlaps another step's piece", k, j);
+    }
+  }
   if (nsteps) *nsteps = w->nsteps;
   destroy(w);
   return bad ? CF_E_STATE : CF_OK;
@@ -365,13 +409,22 @@ int cf_selective_run(cf_selective* w, uint32_t flags, double scale) {
       for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
         CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(w->dma[j].src), reinterpret_cast<const void*>(w->dma[j].dst),
                                   w->dma[j].bytes, cudaMemcpyDeviceToHost, ds));
-      // copy-out of step k (device buffers -> host) beside copy-in of step k+1
+      // copy-out of step k (device buffers -> host, or packed into its staged span) beside the
+      // copy-in of step k+1
+      const bool packed = w->span_out[k];
+      const uint64_t* out_dst = packed ? zi : zs;
       if (k + 1 < w->nsteps) {
         if (w->span[k + 1].bytes) CF_CUDA(cudaStreamWaitEvent(cs, w->ev_in[k + 1], 0));   // staged copy-in source
-        CF_TRY(launch_copy_list2(c, zd + zin(k), zs + zin(k), zb + zin(k), nz(k), zi + zin(k + 1), zd + zin(k + 1),
+        CF_TRY(launch_copy_list2(c, zd + zin(k), out_dst + zin(k), zb + zin(k), nz(k), zi + zin(k + 1), zd + zin(k + 1),
                                  zb + zin(k + 1), nz(k + 1), cs));
       } else {
-        CF_TRY(launch_copy_list(c, zd + zin(k), zs + zin(k), zb + zin(k), nz(k), cs));
+        CF_TRY(launch_copy_list(c, zd + zin(k), out_dst + zin(k), zb + zin(k), nz(k), cs));
+      }
+      if (packed) {   // the whole span back in one DMA once its arrays are packed
+        const cf_selective::Piece& sp = w->span[k];
+        CF_CUDA(cudaEventRecord(w->ev_out[k], cs));
+        CF_CUDA(cudaStreamWaitEvent(ds, w->ev_out[k], 0));
+        CF_CUDA(copy_host_aligned(reinterpret_cast<void*>(sp.src), w->d_stage + sp.dst, sp.bytes, cudaMemcpyDeviceToHost, ds));
       }
     }
   }

@@ -106,3 +106,26 @@ def test_pointerchain_window_plans(mapped):
                                              N.ptr(counts) if n else None, elem, chunk, mapped, C.byref(steps))
         assert rc == 0, (trial, N.last_error())
         assert steps.value >= 1
+
+
+def test_pointerchain_window_plans_with_interleaved_layouts():
+    """Staged spans on shuffled / gapped host layouts: every array still moves exactly once, and a
+    span copied back whole (one D2H DMA) never overlaps an array of another step."""
+    rng = random.Random(3)
+    for trial in range(150):
+        n = rng.randint(2, 400)
+        sizes = np.array([rng.choice([64, 1024, 4096, 40000, 70000, 300000]) for _ in range(n)], np.uint64)
+        order = list(range(n))
+        if rng.random() < 0.5:
+            rng.shuffle(order)
+        host = np.zeros(n, np.uint64)
+        hb = 0x7f0000000000
+        for i in order:
+            host[i] = hb
+            hb += int(sizes[i]) + rng.choice([0, 0, 16, 1200])
+        dev = (np.concatenate([[0], np.cumsum(sizes)[:-1]]) + 0x7e0000000000).astype(np.uint64)
+        cnt = sizes // np.uint64(4)
+        steps = N.U64(0)
+        rc = N.lib().cf_selective_plan_check(n, N.ptr(host), N.ptr(dev), N.ptr(cnt), 4,
+                                             rng.choice([1 << 16, 1 << 18, 1 << 20]), 1, C.byref(steps))
+        assert rc == 0, (trial, N.last_error())

@@ -755,7 +755,6 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
         stats.elements_touched = int(cnt.sum())
         return stats
     machine.flush()
-    ctx = machine.ctx.handle
     if prep.scheme == "pointerchain":
         if len(prep.buf_dev):
             # the leaf kernel over the copied buffers (host-resolved addresses): the buffers' work
@@ -767,7 +766,7 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
             stats.elements_touched = int(prep.buf_count.sum())
         return stats
 
-    idx, stats.chain_derefs, lv, od, cnt, root_off = _kernel_args(handle, prep.policy)
+    idx, stats.chain_derefs, _, _, cnt, _ = _kernel_args(handle, prep.policy)
     if prep.scheme == "uvm":
         fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
         # every page read once (fields, then array pages -- a page met twice migrates once), then

@@ -422,3 +422,25 @@ def test_naive_chain_walk_check_rejects_wrong_targets(cf):
     cf.copy_back(m, h, prep)
     cf.verify_tree(m, h, 2.0, "all_leaves")
     m.close()
+
+
+@pytest.mark.parametrize("policy", ["ref", "all_leaves", "all_arrays"])
+def test_fused_pointerchain_staged_spans_leave_other_bytes_alone(cf, policy):
+    """Small arrays staged through one span DMA each way: every byte of the tree outside the
+    selected arrays (nodes, unselected arrays, scattered neighbours) is exactly as before, and the
+    selected ones exactly as the eager phases leave them."""
+    specs = [cf.ForestSpec(cf.LinearSpec(3, 700, "allinit_allused", elem=4), 40, scatter_seed=7),
+             cf.DenseSpec(30, 200, 2, elem=4), cf.DenseSpec(12, 1000, 3, elem=8)]
+    for spec in specs:
+        dumps = []
+        for fused in (True, False):
+            m = cf.Machine()
+            h = cf.build_tree(m, spec, seed=2, align=16)
+            for r in range(2):
+                prep = cf.transfer_to_device(m, h, "pointerchain", policy=policy, fused=fused)
+                cf.kernel_scale(m, h, prep, 2.0)
+                cf.copy_back(m, h, prep)
+            cf.verify_tree(m, h, 4.0, policy)
+            dumps.append([bytes(m.host.read_bytes(a, s)) for a, s in h.allocations])
+            m.close()
+        assert dumps[0] == dumps[1], (spec, policy)

@@ -158,6 +158,13 @@ int cf_dev_free(cf_ctx* ctx, void* p);
 int cf_memcpy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int cf_memcpy_async(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, void* stream);
 int cf_memset(cf_ctx* ctx, void* dst, int value, uint64_t bytes);
+/* Host-link roofline probe (no reference counterpart): plain cudaMemcpyAsync of
+ * `bytes` between fresh pinned host buffers and HBM -- H2D alone, D2H alone, and H2D || D2H on
+ * two streams -- each sample `iters` back-to-back copies, best of `reps` samples after one
+ * warm-up.  GB/s of bytes moved (both directions summed for bidir).  The e2e window's link
+ * fraction is graded against this, not against a copy pipeline shaped like its own. */
+int cf_link_probe(cf_ctx* ctx, uint64_t bytes, int iters, int reps, double* h2d_gbs, double* d2h_gbs,
+                  double* bidir_gbs);
 
 /* ---------------- host marshaller (scenarios.py:122-267) ---------------- */
 /* Plan the layout: allocation order, node/array tables, pointer sites (tree_total_bytes,
@@ -224,9 +231,11 @@ int cf_marshal_transfer_and_attach(cf_ctx* ctx, const void* host_arena, uint64_t
                                    void* image, const uint64_t* h_sites_sorted, uint64_t nsites,
                                    uint64_t chunk_bytes, uint64_t* bad_site);
 /* Machine.demarshal (memory.py:327-345): detach kernel on the image, then chunked D2H into
- * host_arena. Synchronous. */
+ * host_arena. Synchronous.  h_sites may come in any order; on a field outside the image,
+ * CF_E_OUTSIDE_ARENA with *bad_site = the first offending index in table order (pass the
+ * reversed DFS site order to get the reference's detach order, memory.py:337). */
 int cf_demarshal(cf_ctx* ctx, void* host_arena, uint64_t total, void* image,
-                 const uint64_t* h_sites_sorted, uint64_t nsites, uint64_t chunk_bytes,
+                 const uint64_t* h_sites, uint64_t nsites, uint64_t chunk_bytes,
                  uint64_t* bad_site);
 /* kernel_scale over a device image (harness.py:244-304): resolve every target chain on the
  * device, then run the leaf kernel in `mode`. h_level/h_ordinal/h_count are host arrays of
@@ -267,8 +276,8 @@ int cf_host_write_words(const uint64_t* h_addrs, const uint64_t* h_values, uint6
 int cf_arena_check_sites(const void* host_arena, uint64_t total, const uint64_t* h_sites, uint64_t nsites,
                          uint64_t ptr_base, uint64_t* bad_index);
 /* Result gather of the multi-GPU shards (no reference counterpart): per device
- * range i (h_addr[i], h_bytes[i], both 4-byte aligned) the wrapping u64 sum of its u32 words,
- * into h_out[i].  Synchronous. */
+ * range i (h_addr[i], h_bytes[i], both 4-byte aligned) the position-weighted wrapping u64 sum
+ * sum_j word_j * (j + 1) of its u32 words, into h_out[i].  Synchronous. */
 int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_bytes, uint64_t n, uint64_t* h_out);
 /* Per-object transfers (naive_deep_copy / naive_copy_back, memory.py:358-361, 368-372; batched
  * selective copies): objects under 64 KiB whose both ends are SM-addressable (device, managed
@@ -365,6 +374,15 @@ typedef struct {
   uint64_t nchunks, nsteps;
 } cf_window_stats;
 
+/* Window faults: stats->bad (and the run's return code) carry one sticky word, min over the
+ * window's kernels of (CF_FAULT_* << 62 | index): CF_FAULT_ATTACH (relocation-table index) and
+ * CF_FAULT_DETACH (detach-list index) return CF_E_OUTSIDE_ARENA (AttachOutsideArena,
+ * memory.py:319-321 / 337-343); CF_FAULT_RESOLVE (a chain hop leaves the image) and
+ * CF_FAULT_SCALE (a leaf array [A, A + nA * elem) overruns the image, or a part runs past nA)
+ * return CF_E_WILD (WildAccess, memory.py:139-152).  UINT64_MAX = no fault. */
+enum { CF_FAULT_ATTACH = 0, CF_FAULT_RESOLVE = 1, CF_FAULT_SCALE = 2, CF_FAULT_DETACH = 3 };
+#define CF_FAULT_KIND(bad) ((int)((bad) >> 62))
+#define CF_FAULT_INDEX(bad) ((bad) & ((1ull << 62) - 1))
 int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
 /* Host-only dry run of cf_window_plan (no GPU needed; host_src / image may be NULL) followed by
  * an invariant check of the schedule, re-derived independently where possible: segments

@@ -68,6 +68,10 @@ def lib():
                                  C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(_Spec), C.c_uint64,
                                  C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                  C.c_double, C.c_int]
+        L.orc_resident.restype = C.c_int64
+        L.orc_resident.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                   C.POINTER(_Spec), C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                   C.c_void_p, C.c_double, C.c_int]
         L.orc_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -228,6 +232,18 @@ def window(tree: OTree, idx: np.ndarray, dev: np.ndarray, out: np.ndarray, host_
                                 dev_base, _ptr(tree.site_off), len(tree.site_off),
                                 C.byref(tree.spec.c()), tree.root_off, _ptr(lv), _ptr(od),
                                 len(idx), _ptr(ea), _ptr(cnt), s, nthreads))
+
+
+def resident(tree: OTree, idx: np.ndarray, dev: np.ndarray, host_base: int, dev_base: int, s: float,
+             nthreads: int, keys=None) -> int:
+    """attach -> resolve -> scale -> detach on ``dev`` (already holding the arena bytes): the
+    device-side steps of the window without the copies (reference arm's resident step)."""
+    lv, od = keys if keys is not None else chain_keys(tree, idx)
+    ea = np.zeros(max(len(idx), 1), dtype=np.uint64)
+    cnt = np.zeros(max(len(idx), 1), dtype=np.uint32)
+    return int(lib().orc_resident(_ptr(dev), tree.total, host_base, dev_base, _ptr(tree.site_off),
+                                  len(tree.site_off), C.byref(tree.spec.c()), tree.root_off, _ptr(lv), _ptr(od),
+                                  len(idx), _ptr(ea), _ptr(cnt), s, nthreads))
 
 
 def default_threads() -> int:

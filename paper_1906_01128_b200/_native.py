@@ -46,7 +46,7 @@ EXPORTED = (
     "cf_ctx_sync", "cf_ctx_stream", "cf_ctx_launches", "cf_ctx_sm_count",
     "cf_timer_create", "cf_timer_start", "cf_timer_stop", "cf_timer_free", "cf_host_alloc",
     "cf_host_free", "cf_host_free_sized", "cf_dev_alloc", "cf_dev_free", "cf_memcpy",
-    "cf_memcpy_async", "cf_memset", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
+    "cf_memcpy_async", "cf_memset", "cf_link_probe", "cf_tree_plan", "cf_tree_info_get", "cf_tree_table",
     "cf_tree_build", "cf_tree_targets", "cf_tree_chain_shape", "cf_tree_free", "cf_relocate",
     "cf_resolve", "cf_scale", "cf_marshal_transfer_and_attach", "cf_demarshal",
     "cf_kernel_scale", "cf_kernel_plan_create", "cf_kernel_plan_run", "cf_kernel_plan_resolve",
@@ -133,6 +133,8 @@ def _declare(L):
         "cf_memcpy": (C.c_int, [P, P, P, U64]),
         "cf_memcpy_async": (C.c_int, [P, P, P, U64, P]),
         "cf_memset": (C.c_int, [P, P, C.c_int, U64]),
+        "cf_link_probe": (C.c_int, [P, U64, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]),
         "cf_tree_plan": (C.c_int, [C.POINTER(CfSpec), C.POINTER(P)]),
         "cf_tree_info_get": (C.c_int, [P, C.POINTER(CfTreeInfo)]),
         "cf_tree_table": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(U64)]),
@@ -371,6 +373,14 @@ def read_bytes(addr: int, n: int) -> bytes:
 def write_bytes(addr: int, data: bytes) -> None:
     if data:
         C.memmove(addr, data, len(data))
+
+
+def link_probe(ctx, nbytes: int, iters: int = 1, reps: int = 5) -> dict:
+    """Plain cudaMemcpyAsync H2D / D2H / bidirectional GB/s for `nbytes` (cf_link_probe)."""
+    h, d, b = C.c_double(), C.c_double(), C.c_double()
+    check(lib().cf_link_probe(ctx.handle, int(nbytes), int(iters), int(reps), C.byref(h), C.byref(d), C.byref(b)),
+          "cf_link_probe")
+    return {"h2d": h.value, "d2h": d.value, "bidir": b.value}
 
 
 def host_view(addr: int, n: int) -> np.ndarray:

@@ -61,23 +61,31 @@ int launch_copy_list(cf_ctx* ctx, const uint64_t* src, const uint64_t* dst, cons
                      cudaStream_t s);
 int launch_checksum(cf_ctx* ctx, const uint64_t* addr, const uint64_t* words, const uint64_t* tile_lo, uint64_t nranges,
                     uint64_t ntiles, uint64_t* out, cudaStream_t s);
+// Fault tags: a kernel that finds a bad site / chain / part raises min(tag | index) into the
+// error word; the pipelined window reads one sticky word and maps the phase to the reference's
+// exception (attach / detach -> AttachOutsideArena, chain walk / leaf span -> WildAccess).  The
+// synchronous single-phase operations pass tag 0 (plain index).
+constexpr uint64_t FAULT_SHIFT = 62;
+constexpr uint64_t FAULT_ATTACH = 0ull << FAULT_SHIFT, FAULT_RESOLVE = 1ull << FAULT_SHIFT,
+                   FAULT_SCALE = 2ull << FAULT_SHIFT, FAULT_DETACH = 3ull << FAULT_SHIFT;
+constexpr uint64_t FAULT_INDEX_MASK = (1ull << FAULT_SHIFT) - 1;
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
                     uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s,
-                    const uint32_t* idx = nullptr);
+                    const uint32_t* idx = nullptr, uint64_t tag = 0);
 // One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).
 constexpr uint64_t SMALL_FUSED = 4096;
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                          cudaStream_t s);
+                          cudaStream_t s, uint64_t res_tag = 0);
 // Attach and resolve side by side in one launch (8-byte aligned pointer fields only).
 int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
                                const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
-                               uint32_t* count, uint64_t* bad, cudaStream_t s);
+                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag = 0);
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
                    const int32_t* level, const uint32_t* ordinal, uint64_t n, uint64_t* ea,
-                   uint32_t* count, uint64_t* bad, cudaStream_t s);
+                   uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t tag = 0);
 // A relocation job that can ride along in a leaf-kernel launch (extra CTAs).
 struct RelocArgs {
   uint8_t* image;
@@ -86,11 +94,12 @@ struct RelocArgs {
   const uint32_t* idx;   // optional indirection: site = sites[idx[i]]
   uint64_t n;
   uint64_t from, to;
+  uint64_t tag = 0;      // fault tag (FAULT_DETACH when it rides in a window's leaf launch)
 };
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
-                 cudaStream_t s, const RelocArgs* fused_reloc = nullptr);
+                 cudaStream_t s, const RelocArgs* fused_reloc = nullptr, uint64_t tag = 0);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);

@@ -101,25 +101,28 @@ __device__ __forceinline__ void raise_bad(uint64_t* bad, uint64_t idx) {
 }
 
 // ---------------------------------------------------------------- relocation (attach/detach)
+// `tag` (bits 62-63 of the error word, CF_FAULT_* << 62) names the phase that faulted, so one
+// sticky word per window still maps onto the reference's exception for that phase.
 __device__ __forceinline__ void relocate_one(uint8_t* __restrict__ image, uint64_t total,
                                              const uint64_t* __restrict__ sites, uint64_t i, uint64_t from,
-                                             uint64_t to, uint64_t* bad, const uint32_t* __restrict__ idx = nullptr) {
+                                             uint64_t to, uint64_t* bad, const uint32_t* __restrict__ idx = nullptr,
+                                             uint64_t tag = 0) {
   const uint64_t s = sites[idx ? idx[i] : i];  // coalesced table read
-  if (s + 8 > total) { raise_bad(bad, i); return; }
+  if (s + 8 > total) { raise_bad(bad, i | tag); return; }
   uint8_t* p = image + s;
   const uint64_t v = ld_u64_any(p);
   const uint64_t d = v - from;  // wraps when v < from
-  if (d >= total) { raise_bad(bad, i); return; }
+  if (d >= total) { raise_bad(bad, i | tag); return; }
   st_u64_any(p, to + d);
 }
 
 __global__ void __launch_bounds__(256) k_relocate(uint8_t* __restrict__ image, uint64_t total,
                                                   const uint64_t* __restrict__ sites,
                                                   const uint32_t* __restrict__ idx, uint64_t n,
-                                                  uint64_t from, uint64_t to, uint64_t* bad) {
+                                                  uint64_t from, uint64_t to, uint64_t* bad, uint64_t tag) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    relocate_one(image, total, sites, i, from, to, bad, idx);
+    relocate_one(image, total, sites, i, from, to, bad, idx, tag);
 }
 
 // ---------------------------------------------------------------- chain walk
@@ -168,14 +171,14 @@ __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ ima
                                                  const int32_t* __restrict__ level,
                                                  const uint32_t* __restrict__ ordinal, uint64_t n,
                                                  uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                 uint64_t* bad) {
+                                                 uint64_t* bad, uint64_t tag) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i]);
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
-    raise_bad(bad, i);
+    raise_bad(bad, i | tag);
     return;
   }
   ea[i] = ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A));
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
                                                          const int32_t* __restrict__ level,
                                                          const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                          uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                         uint64_t* bad) {
+                                                         uint64_t* bad, uint64_t res_tag) {
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
   __syncthreads();
   for (uint64_t i = threadIdx.x; i < ntargets; i += blockDim.x) {
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
     if (!w.node) {
       ea[i] = 0;
       count[i] = 0;
-      raise_bad(bad, i);
+      raise_bad(bad, i | res_tag);
       continue;
     }
     ea[i] = ld_u64_any(w.node + (w.leaf ? LEAF_OFF_A : OFF_A));
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
                                                              const int32_t* __restrict__ level,
                                                              const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                              uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                             uint64_t* bad, unsigned att_blocks) {
+                                                             uint64_t* bad, unsigned att_blocks, uint64_t res_tag) {
   if (blockIdx.x < att_blocks) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < nsites) relocate_one(image, total, sites, i, from, to, bad);
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
-    raise_bad(bad, i);
+    raise_bad(bad, i | res_tag);
     return;
   }
   uint8_t* fa = const_cast<uint8_t*>(w.node) + (w.leaf ? LEAF_OFF_A : OFF_A);   // image is writable here
@@ -308,11 +311,12 @@ struct ScaleArgs {
   const uint32_t* count;
   cf_scale_work w;
   uint64_t* bad;
+  uint64_t tag;      // fault tag of the leaf kernel's own checks
   RelocArgs reloc;   // optional fused relocation (reloc.n == 0: none)
 };
 
 // Array base + element count of target t: from the resolved table, or re-walked (CHASE).
-template <bool CHASE>
+template <typename T, bool CHASE>
 __device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uint8_t*& arr, uint64_t& cnt) {
   if (CHASE) {
     Walk w = walk_chain<true>(a.image, a.sh, a.root ? a.root[t] : a.sh.root_off, a.level[t], a.ordinal[t]);
@@ -324,8 +328,12 @@ __device__ __forceinline__ bool target_array(const ScaleArgs& a, uint64_t t, uin
     cnt = a.count[t];
   }
   if (arr == nullptr) return false;
-  // never stream through an address outside the image (a corrupted chain reports, not faults)
-  if (a.image && (arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes)) {
+  // never stream through an address outside the image (a corrupted chain reports, not faults):
+  // the whole array [arr, arr + cnt * sizeof(T)) must lie inside it -- memory.py:139-152 raises
+  // WildAccess on any span that overruns its allocation; callers then require every part to end
+  // at or before cnt
+  if (a.image && (arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes ||
+                  cnt * sizeof(T) > a.sh.image_bytes - uint64_t(arr - a.image))) {
     if (atomicCAS(reinterpret_cast<unsigned long long*>(&g_dbg[0]), 0ull, 1ull) == 0ull) {
       g_dbg[1] = t;
       g_dbg[2] = reinterpret_cast<uint64_t>(arr);
@@ -503,8 +511,8 @@ __device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s)
       uint8_t* arr;
       uint64_t cnt;
       s_t[lane] = t;
-      if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
-        raise_bad(a.bad, t);
+      if (!target_array<T, CHASE>(a, t, arr, cnt) || e1 > cnt) {
+        raise_bad(a.bad, t | a.tag);
         s_base[lane] = nullptr;
         s_v0[lane] = e1;
       } else {
@@ -592,8 +600,8 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
     e0 = a.w.parts[3 * pj + 1];
     e1 = a.w.parts[3 * pj + 2];
     uint64_t cnt;
-    if (!target_array<CHASE>(a, t, base, cnt) || e1 > cnt) {
-      raise_bad(a.bad, t);
+    if (!target_array<T, CHASE>(a, t, base, cnt) || e1 > cnt) {
+      raise_bad(a.bad, t | a.tag);
       base = nullptr;
       v0 = e1;
     } else {
@@ -682,8 +690,8 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
     const uint64_t e1 = min(uint64_t(pt[2]), e0 + TILE);
     uint8_t* arr;
     uint64_t cnt;
-    if (!target_array<CHASE>(a, t, arr, cnt) || e1 > cnt) {
-      if (threadIdx.x == 0) raise_bad(a.bad, t);
+    if (!target_array<T, CHASE>(a, t, arr, cnt) || e1 > cnt) {
+      if (threadIdx.x == 0) raise_bad(a.bad, t | a.tag);
       return;
     }
     scale_range<T, CHASE, SCALE_UNROLL>(a, t, arr, e0, e1, s, threadIdx.x, SCALE_THREADS);
@@ -694,7 +702,8 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
     // fused relocation CTAs (detach riding in the leaf-kernel launch)
     const uint64_t i = (blockIdx.x - ntiles - ngroups) * uint64_t(SCALE_THREADS) + threadIdx.x;
     if (i < a.reloc.n)
-      relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad, a.reloc.idx);
+      relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad, a.reloc.idx,
+                   a.reloc.tag);
     return;
   }
   const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
@@ -846,9 +855,11 @@ __global__ void __launch_bounds__(256) k_sm_copy(uint4* __restrict__ dst, const 
   for (; i < n16; i += stride) dst[i] = src[i];
 }
 
-// Per-range checksum for the multi-GPU result gather: wrapping u64 sum of the
-// range's u32 words (order independent, so tiles can atomically accumulate).  One CTA per
-// 64 KiB tile of a range; tile_lo[r] = first tile of range r.
+// Per-range checksum for the multi-GPU result gather: position-weighted wrapping
+// u64 sum  sum_i word_i * (i + 1)  over the range's u32 words (i = word index in the range), so a
+// tile written to the wrong offset or two swapped tiles change it; the terms are independent, so
+// tiles still accumulate atomically.  One CTA per 64 KiB tile of a range; tile_lo[r] = first
+// tile of range r.
 constexpr uint64_t CK_TILE_WORDS = 16384;
 __global__ void __launch_bounds__(256) k_checksum(const uint64_t* __restrict__ addr, const uint64_t* __restrict__ words,
                                                   const uint64_t* __restrict__ tile_lo, uint64_t nranges,
@@ -862,7 +873,7 @@ __global__ void __launch_bounds__(256) k_checksum(const uint64_t* __restrict__ a
   const uint32_t* p = reinterpret_cast<const uint32_t*>(addr[lo]);
   const uint64_t w0 = (tile - tile_lo[lo]) * CK_TILE_WORDS, w1 = min(words[lo], w0 + CK_TILE_WORDS);
   unsigned long long acc = 0;
-  for (uint64_t i = w0 + threadIdx.x; i < w1; i += 256) acc += __ldcs(p + i);
+  for (uint64_t i = w0 + threadIdx.x; i < w1; i += 256) acc += uint64_t(__ldcs(p + i)) * (i + 1);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
   __shared__ unsigned long long red[8];
@@ -898,9 +909,9 @@ unsigned grid_for(cf_ctx* ctx, uint64_t work, unsigned threads, unsigned per_sm)
   } while (0)
 
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t n,
-                    uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s, const uint32_t* idx) {
+                    uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s, const uint32_t* idx, uint64_t tag) {
   if (n == 0) return CF_OK;
-  k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, idx, n, from, to, bad);
+  k_relocate<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(image, total, sites, idx, n, from, to, bad, tag);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -908,11 +919,11 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                          cudaStream_t s) {
+                          cudaStream_t s, uint64_t res_tag) {
   if (nsites == 0 && ntargets == 0) return CF_OK;
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
   k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level, ordinal, ntargets,
-                                        ea, count, bad);
+                                        ea, count, bad, res_tag);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -920,21 +931,21 @@ int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uin
 int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
                                const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
-                               uint32_t* count, uint64_t* bad, cudaStream_t s) {
+                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag) {
   const uint64_t ab = (nsites + 255) / 256, rb = (ntargets + 255) / 256;
   if (ab + rb == 0) return CF_OK;
   if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
   k_attach_resolve_wide<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level,
-                                                         ordinal, ntargets, ea, count, bad, unsigned(ab));
+                                                         ordinal, ntargets, ea, count, bad, unsigned(ab), res_tag);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
 
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
                    const int32_t* level, const uint32_t* ordinal, uint64_t n, uint64_t* ea, uint32_t* count,
-                   uint64_t* bad, cudaStream_t s) {
+                   uint64_t* bad, cudaStream_t s, uint64_t tag) {
   if (n == 0) return CF_OK;
-  k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, root, level, ordinal, n, ea, count, bad);
+  k_resolve<<<unsigned((n + 127) / 128), 128, 0, s>>>(image, sh, root, level, ordinal, n, ea, count, bad, tag);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -943,14 +954,14 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
                  const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count,
                  const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s,
-                 const RelocArgs* fused_reloc) {
+                 const RelocArgs* fused_reloc, uint64_t tag) {
   const uint64_t nreloc = fused_reloc ? fused_reloc->n : 0;
   const uint64_t units = (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin) +
                          (nreloc + SCALE_THREADS - 1) / SCALE_THREADS;
   if (units == 0) return CF_OK;
   if (units > 0x7FFFFFFFull) return fail(CF_E_INVALID, "leaf kernel: %llu work units exceed one grid",
                                          (unsigned long long)units);
-  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, RelocArgs{}};
+  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, tag, RelocArgs{}};
   if (nreloc) a.reloc = *fused_reloc;
   // one CTA per 16 KiB tile / small-part group: measured faster than a persistent grid-stride
   // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware

@@ -205,7 +205,9 @@ int cf_demarshal(cf_ctx* c, void* host_arena, uint64_t total, void* image, const
   CF_TRY(ev.make(1));
   CF_CUDA(cudaEventRecord(ev.ev[0], c->compute));
   CF_CUDA(cudaStreamWaitEvent(c->d2h, ev.ev[0], 0));
-  std::vector<uint64_t> b = chunk_bounds(total, chunk_bytes, h_sites, nsites);
+  // every field is detached before the first chunk leaves, so chunks need not respect fields
+  // and the table may come in any order (the drop-in passes the reference's detach order)
+  std::vector<uint64_t> b = chunk_bounds(total, chunk_bytes, nullptr, 0);
   for (size_t i = 0; i + 1 < b.size(); ++i)
     CF_CUDA(copy_host_aligned(static_cast<uint8_t*>(host_arena) + b[i], static_cast<const uint8_t*>(image) + b[i],
                             b[i + 1] - b[i], cudaMemcpyDeviceToHost, c->d2h));

@@ -379,3 +379,68 @@ int cf_uvm_advise(cf_ctx* c, const void* p, uint64_t bytes, int advice) {
 }
 
 }  // extern "C"
+
+// Independent host-link roofline probe: plain cudaMemcpyAsync between fresh
+// pinned host buffers and device buffers -- no chunking, no window -- so the e2e fraction is not
+// measured against a copy pipeline shaped like the one it grades.  Each sample is `iters`
+// back-to-back copies of `bytes` (H2D alone, D2H alone, or H2D || D2H on two streams); the best
+// of `reps` samples is reported as GB/s of bytes moved (both directions summed for bidir).
+extern "C" int cf_link_probe(cf_ctx* c, uint64_t bytes, int iters, int reps, double* h2d_gbs, double* d2h_gbs,
+                             double* bidir_gbs) {
+  if (!c || bytes == 0 || iters < 1 || reps < 1) return fail(CF_E_INVALID, "bad arguments");
+  CfDevice g(c);
+  void *h_src = nullptr, *h_dst = nullptr, *d_a = nullptr, *d_b = nullptr;
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, ej = nullptr;
+  auto cleanup = [&]() {
+    if (h_src) cudaFreeHost(h_src);
+    if (h_dst) cudaFreeHost(h_dst);
+    if (d_a) cudaFree(d_a);
+    if (d_b) cudaFree(d_b);
+    for (auto s : {s1, s2}) if (s) cudaStreamDestroy(s);
+    for (auto e : {e0, e1, ej}) if (e) cudaEventDestroy(e);
+  };
+  cudaError_t ce = cudaHostAlloc(&h_src, bytes, cudaHostAllocPortable);
+  if (ce == cudaSuccess) ce = cudaHostAlloc(&h_dst, bytes, cudaHostAllocPortable);
+  if (ce == cudaSuccess) ce = cudaMalloc(&d_a, bytes);
+  if (ce == cudaSuccess) ce = cudaMalloc(&d_b, bytes);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaEventCreate(&e0);
+  if (ce == cudaSuccess) ce = cudaEventCreate(&e1);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ej, cudaEventDisableTiming);
+  if (ce != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    return fail(ce == cudaErrorMemoryAllocation ? CF_E_OOM : CF_E_CUDA, "link probe setup: %s", cudaGetErrorString(ce));
+  }
+  memset(h_src, 0x5A, bytes);   // touch every page once before timing
+  memset(h_dst, 0xA5, bytes);
+  double out[3] = {0, 0, 0};
+  for (int mode = 0; mode < 3 && ce == cudaSuccess; ++mode) {
+    float best = 1e30f;
+    for (int r = 0; r < reps + 1 && ce == cudaSuccess; ++r) {   // sample 0 is a warm-up
+      ce = cudaEventRecord(e0, s1);
+      if (ce == cudaSuccess && mode == 2) ce = cudaStreamWaitEvent(s2, e0, 0);
+      for (int i = 0; i < iters && ce == cudaSuccess; ++i) {
+        if (mode != 1) ce = cudaMemcpyAsync(d_a, h_src, bytes, cudaMemcpyHostToDevice, s1);
+        if (ce == cudaSuccess && mode != 0)
+          ce = cudaMemcpyAsync(h_dst, d_b, bytes, cudaMemcpyDeviceToHost, mode == 2 ? s2 : s1);
+      }
+      if (ce == cudaSuccess && mode == 2) ce = cudaEventRecord(ej, s2);
+      if (ce == cudaSuccess && mode == 2) ce = cudaStreamWaitEvent(s1, ej, 0);
+      if (ce == cudaSuccess) ce = cudaEventRecord(e1, s1);
+      if (ce == cudaSuccess) ce = cudaEventSynchronize(e1);
+      float ms = 0;
+      if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+      if (ce == cudaSuccess && r > 0 && ms < best) best = ms;
+    }
+    out[mode] = double(mode == 2 ? 2 : 1) * double(bytes) * iters / (double(best) * 1e-3) / 1e9;
+  }
+  cleanup();
+  if (ce != cudaSuccess) return fail(CF_E_CUDA, "link probe: %s", cudaGetErrorString(ce));
+  if (h2d_gbs) *h2d_gbs = out[0];
+  if (d2h_gbs) *d2h_gbs = out[1];
+  if (bidir_gbs) *bidir_gbs = out[2];
+  return CF_OK;
+}

@@ -13,8 +13,10 @@
 // span goes in as ONE copy-engine DMA into a device staging area and a device-side copy list
 // moves each array into its buffer: copy engine H2D beside SM-store D2H runs the full-duplex link
 // at 88 GB/s where SM traffic both ways reaches 77 (profiles/r01_design_experiments.md).  The
-// span's bytes between arrays are read, never written back.  All bookkeeping is planned once; a
-// run only enqueues.
+// span goes back the same way (arrays packed into the staging slice, ONE D2H DMA) only when no
+// other data shares it: no DMA-moved array of any step and no small array of another step may
+// overlap it, or the span's stale staging bytes would land on their results.  All bookkeeping is
+// planned once; a run only enqueues.
 #include "cf_internal.h"
 
 #include <algorithm>
@@ -165,16 +167,21 @@ int sel_plan(cf_ctx* ctx, uint64_t n, const uint64_t* h_src, const uint64_t* d_b
   // Copy-back through the staged span too (arrays packed into the staging slice on the device,
   // then ONE D2H DMA of the span: copy engines both ways run the link at 99 GB/s where SM stores
   // beside a DMA reach 88) -- only when that cannot disturb anything: every selected array that
-  // overlaps the span is one of this step's own (the bytes between them go back exactly as they
-  // were read at the start of this window, which no one can change before copy_back returns).
+  // overlaps the span is one of this step's own zero-copy entries, which are packed into the
+  // slice before the DMA (the bytes between them go back exactly as they were read at the start
+  // of this window, which no one can change before copy_back returns).  A DMA-moved array inside
+  // the span -- even one of step k -- is scaled in its own buffer and goes home by its own DMA;
+  // the span DMA would then overwrite it with the unscaled staging bytes, so it disqualifies.
   w->span_out.assign(w->nsteps, 0);
   {
+    constexpr uint64_t DMA_PIECE = ~uint64_t(0);   // step tag of DMA pieces: overlap always disqualifies
     struct Iv { uint64_t lo, hi, step; };
     std::vector<Iv> iv;
     iv.reserve(zsrc.size() + w->dma.size());
     for (uint64_t k = 0; k < w->nsteps; ++k) {
       for (uint64_t j = w->zc_lo[k]; j < w->zc_lo[k + 1]; ++j) iv.push_back({zsrc[j], zsrc[j] + zbytes[j], k});
-      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j) iv.push_back({w->dma[j].src, w->dma[j].src + w->dma[j].bytes, k});
+      for (uint64_t j = w->dma_lo[k]; j < w->dma_lo[k + 1]; ++j)
+        iv.push_back({w->dma[j].src, w->dma[j].src + w->dma[j].bytes, DMA_PIECE});
     }
     std::sort(iv.begin(), iv.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
     uint64_t maxlen = 0;
@@ -340,17 +347,19 @@ int cf_selective_plan_check(uint64_t n, const uint64_t* h_src, const uint64_t* d
       if (y != count[i]) report("array covered up to", i, y);
     }
   if (stage_end > w->stage_bytes) report("staging area too small", stage_end, w->stage_bytes);
-  // a span copied back whole must not overlap any array moved by another step (quadratic, small n)
+  // a span copied back whole must not overlap any array moved by another step, nor any DMA piece
+  // of any step -- its own included: that piece is scaled in its buffer and goes home by its own
+  // DMA, which the span DMA would overwrite with unscaled staging bytes (quadratic, small n)
   for (uint64_t k = 0; k < w->nsteps; ++k) {
     if (!w->span_out[k]) continue;
     if (!w->span[k].bytes) { report("span copied back without a span", k, 0); continue; }
     const uint64_t lo = w->span[k].src, hi = lo + w->span[k].bytes;
     for (uint64_t j = 0; j < w->nsteps; ++j) {
+      for (uint64_t q = w->dma_lo[j]; q < w->dma_lo[j + 1]; ++q)
+        if (w->dma[q].src < hi && w->dma[q].src + w->dma[q].bytes > lo) report("copied-back span overlaps a DMA piece", k, j);
       if (j == k) continue;
       for (uint64_t q = w->zc_lo[j]; q < w->zc_lo[j + 1]; ++q)
         if (D.zsrc[q] < hi && D.zsrc[q] + D.zbytes[q] > lo) report("copied-back span overlaps another step's array", k, j);
-      for (uint64_t q = w->dma_lo[j]; q < w->dma_lo[j + 1]; ++q)
-        if (w->dma[q].src < hi && w->dma[q].src + w->dma[q].bytes > lo) report("copied-back span overlaps another step's piece", k, j);
     }
   }
   if (nsteps) *nsteps = w->nsteps;

@@ -1085,18 +1085,19 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
                                    drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
-                                   w->d_count + w->res_lo[k], c->d_bad, cs));
+                                   w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
     } else if (do_attach && do_resolve && w->wide_ok) {
       CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
-                                        w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs));
+                                        w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
     } else {
       if (do_attach)
-        CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs));
+        CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs, nullptr,
+                               FAULT_ATTACH));
       if (do_resolve)
         CF_TRY(launch_resolve(c, img, w->sh, drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
                               w->d_ea + w->res_lo[k],
-                              w->d_count + w->res_lo[k], c->d_bad, cs));
+                              w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
     }
     // In RESOLVED mode the leaf kernel never reads pointer fields, and every resolve that reads
     // the fields detached at this step has already run: the detach rides in the same launch.
@@ -1106,15 +1107,15 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
       if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base};
+        RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base, FAULT_DETACH};
         CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
-                            nd ? &det : nullptr));
+                            nd ? &det : nullptr, FAULT_SCALE));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
     if ((fl & CF_WIN_DETACH) && !fuse_detach)
       CF_TRY(launch_relocate(c, img, w->total, dsites, w->det_lo[k + 1] - w->det_lo[k], dimg, d.host_base, c->d_bad, cs,
-                             ddet + w->det_lo[k]));
+                             ddet + w->det_lo[k], FAULT_DETACH));
     if ((fl & CF_WIN_D2H) && w->zc && w->zc_rel_lo[k + 1] > w->zc_rel_lo[k]) {
       const uint64_t* zs = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_zc_d2h) + 2 * w->zc_rel_lo[k];
       CF_TRY(launch_seg_copy(c, zs, w->zc_rel_lo[k + 1] - w->zc_rel_lo[k], img, dst, cs));
@@ -1174,8 +1175,23 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
     st->nchunks = w->seg_lo.size();
     st->nsteps = nch;
   }
-  if (bad != NO_BAD)
-    return fail(CF_E_OUTSIDE_ARENA, "window: relocation/resolve/scale reported index %llu", (unsigned long long)bad);
+  if (bad != NO_BAD) {
+    // the tag names the phase (the lowest-tagged fault wins: the reference's phase order)
+    const uint64_t idx = bad & FAULT_INDEX_MASK;
+    switch (bad & ~FAULT_INDEX_MASK) {
+      case FAULT_ATTACH:   // memory.py:319-321
+        return fail(CF_E_OUTSIDE_ARENA, "window attach: relocation-table entry %llu targets outside the arena",
+                    (unsigned long long)idx);
+      case FAULT_RESOLVE:  // a chain hop leaves the image (harness.py:285-304 walk -> WildAccess)
+        return fail(CF_E_WILD, "window resolve: chain of target %llu leaves the device image", (unsigned long long)idx);
+      case FAULT_SCALE:    // leaf span outside the image / beyond nA (memory.py:139-152)
+        return fail(CF_E_WILD, "window leaf kernel: array of target %llu overruns the device image or its nA",
+                    (unsigned long long)idx);
+      default:             // demarshal's check, memory.py:337-343
+        return fail(CF_E_OUTSIDE_ARENA, "window detach: pointer field (detach entry %llu) holds a value outside the device image",
+                    (unsigned long long)idx);
+    }
+  }
   return CF_OK;
 }
 }  // namespace

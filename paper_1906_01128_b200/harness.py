@@ -267,8 +267,8 @@ class FusedMarshalWindow:
         rc = lib.cf_window_run(w, 1, None)   # no per-kernel events: detach fuses into the leaf launch
         # host-side phase times of the last run (plan, enqueue + wait)
         self.timing = {"plan_ms": (t1 - t0) * 1e3, "run_ms": (time.perf_counter() - t1) * 1e3}
-        if rc == N.CF_E_OUTSIDE_ARENA:   # sites were bounds-checked up front: a chain/count fault
-            raise WildAccess(N.last_error())
+        # the window's fault word names its phase: attach / detach -> AttachOutsideArena
+        # (memory.py:319-321, 337-343), chain walk / leaf span -> WildAccess (memory.py:139-152)
         N.check(rc, "fused marshalling window")
 
     def _targets(self) -> np.ndarray:
@@ -488,9 +488,7 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         rc = N.lib().cf_arena_check_sites(base, total, N.ptr(sites) if len(sites) else None, len(sites), base,
                                           C.byref(bad))
         if rc == N.CF_E_OUTSIDE_ARENA:
-            dfs = np.ascontiguousarray(arena.site_offsets, np.uint64)
-            N.lib().cf_arena_check_sites(base, total, N.ptr(dfs), len(dfs), base, C.byref(bad))
-            raise AttachOutsideArena(N.last_error())
+            machine.attach_failed(arena)   # logs what the reference logged before raising
         N.check(rc, "transfer_to_device")
         image = arena.take_image()   # fully overwritten by the copy
         machine.log.append(H2D, "bulk", total)

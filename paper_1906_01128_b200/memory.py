@@ -442,11 +442,12 @@ class Arena:
     def pointer_sites(self, sites) -> None:
         arr = np.asarray(list(sites), dtype=np.uint64)
         self._site_off = arr - np.uint64(self.buffer_host_addr) if arr.size else arr
-        self._sorted = None
+        self._sorted = self._detach_order = None
 
     def set_site_offsets(self, site_off: np.ndarray, sorted_off: np.ndarray | None = None) -> None:
         self._site_off = np.ascontiguousarray(site_off, np.uint64)
         self._sorted = None if sorted_off is None else np.ascontiguousarray(sorted_off, np.uint64)
+        self._detach_order = None
 
     @property
     def site_offsets(self) -> np.ndarray:
@@ -459,6 +460,14 @@ class Arena:
         if w is None or len(w) != len(self._site_off):
             w = self._site_words = np.full(len(self._site_off), 8, np.int64)
         return w
+
+    @property
+    def detach_order_offsets(self) -> np.ndarray:
+        """Site offsets in the reference's detach order (reversed pointer_sites, memory.py:337)."""
+        d = getattr(self, "_detach_order", None)
+        if d is None:
+            d = self._detach_order = np.ascontiguousarray(np.asarray(self._site_off, np.uint64)[::-1])
+        return d
 
     @property
     def sorted_site_offsets(self) -> np.ndarray:
@@ -639,24 +648,47 @@ class Machine:
             self.ctx.handle, arena.buffer_host_addr, arena.total_bytes, image, N.ptr(sites),
             len(sites), chunk_bytes, C.byref(bad))
         if rc == N.CF_E_OUTSIDE_ARENA:
-            raise AttachOutsideArena(N.last_error())
+            self.attach_failed(arena)
         N.check(rc, "marshal_transfer_and_attach")
         self.log.append(H2D, "bulk", arena.total_bytes)
         self.log.append_many(H2D, "attach", arena.site_words)
         arena.device_image_addr = image
         return image
 
+    def attach_failed(self, arena: Arena) -> None:
+        """The attach loop met a pointer field outside the arena (memory.py:316-321): log what the
+        reference logged before raising -- the bulk copy, then one attach per site preceding the
+        first bad one in its site order -- and raise AttachOutsideArena naming that site."""
+        base, total = arena.buffer_host_addr, arena.total_bytes
+        dfs = np.ascontiguousarray(arena.site_offsets, np.uint64)
+        bad = N.U64(0)
+        rc = N.lib().cf_arena_check_sites(base, total, N.ptr(dfs), len(dfs), base, C.byref(bad))
+        self.log.append(H2D, "bulk", total)
+        if rc != N.CF_E_OUTSIDE_ARENA:
+            raise AttachOutsideArena("relocation kernel reported a pointer field outside the arena")
+        j = int(bad.value)
+        if j:
+            self.log.append_many(H2D, "attach", np.full(j, 8, np.int64))
+        site = base + int(dfs[j])
+        target = int.from_bytes(N.host_view(site, 8).tobytes(), "little")
+        raise AttachOutsideArena(f"pointer field at 0x{site:x} targets 0x{target:x} outside the arena")
+
     def demarshal(self, arena: Arena, chunk_bytes: int = MARSHAL_CHUNK) -> None:
-        """Detach on the device (inverse relocation kernel), then bulk copy the image back."""
+        """Detach on the device (inverse relocation kernel), then bulk copy the image back.
+        The detach table is the reference's detach order (reversed site order, memory.py:337), so
+        a fault reports -- and the log keeps -- exactly the detaches that preceded it there."""
         self.flush()
         image = arena.device_image_addr
         if image == NULL_ADDR:
             raise SimMemoryError("demarshal before marshal_transfer_and_attach")
-        sites = arena.sorted_site_offsets
+        sites = arena.detach_order_offsets
         bad = N.U64(0)
         rc = N.lib().cf_demarshal(self.ctx.handle, arena.buffer_host_addr, arena.total_bytes, image,
                                   N.ptr(sites), len(sites), chunk_bytes, C.byref(bad))
         if rc == N.CF_E_OUTSIDE_ARENA:
+            self.log.append(D2H, "bulk", arena.total_bytes)
+            if bad.value:
+                self.log.append_many(D2H, "detach", np.full(int(bad.value), 8, np.int64))
             raise AttachOutsideArena(N.last_error())
         N.check(rc, "demarshal")
         self.log.append(D2H, "bulk", arena.total_bytes)

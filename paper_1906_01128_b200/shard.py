@@ -12,8 +12,8 @@ crosses GPUs; the timed region shares only control (barrier, max-over-ranks timi
   the pointers to the other ranks' subtrees are nulled in its arena.  G = 2: 4 level-1
   subtrees, 2 per GPU; G = 4: 1 each; G = 8: 16 level-2 subtrees, 2 per GPU.
 
-After the timed region the ranks gather a per-leaf checksum vector (wrapping u64 sum of each
-leaf's u32 words, computed on the device by cf_checksum_ranges) to verify the union of the
+After the timed region the ranks gather a per-leaf checksum vector (position-weighted wrapping
+u64 sum of each leaf's u32 words, computed on the device by cf_checksum_ranges) to verify the union of the
 shards against the whole tree -- the only collective, over NCCL when every rank has its own
 GPU (NVLink / NVSwitch), else gloo.
 """
@@ -33,6 +33,10 @@ class Shard:
     spec: object
     seed: int
     scaling: str  # "weak" | "strong"
+    base_seed: int = 1
+    # True: this rank holds a subtree shard of ONE tree (seed shared, leaves keyed by the whole
+    # tree's ordinals); False: it owns a tree of its own (seed base_seed + rank)
+    whole_tree: bool = False
 
 
 def cut_level(q: int, world: int) -> int:
@@ -60,15 +64,17 @@ def shard_for(spec, rank: int, world: int, scaling: str = "weak", base_seed: int
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"bad rank {rank} / world {world}")
     if scaling == "weak":
-        return Shard(rank, world, spec, base_seed + rank, scaling)
+        return Shard(rank, world, spec, base_seed + rank, scaling, base_seed, False)
     if scaling == "strong":
         if isinstance(spec, DenseSpec) and spec.q ** spec.depth >= world:
             # one tree: every rank builds its subtree shard of the same seeded tree
-            return Shard(rank, world, subtree_shard(spec, rank, world) if world > 1 else spec, base_seed, scaling)
+            return Shard(rank, world, subtree_shard(spec, rank, world) if world > 1 else spec, base_seed, scaling,
+                         base_seed, True)
+        # fallback: every rank a tree of its own with 1/world of the leaf length
         n = spec.n // world
         if n * world != spec.n:
             raise ValueError(f"leaf length {spec.n} does not split evenly over {world} ranks")
-        return Shard(rank, world, replace(spec, n=n), base_seed + rank, scaling)
+        return Shard(rank, world, replace(spec, n=n), base_seed + rank, scaling, base_seed, False)
     raise ValueError(f"unknown scaling {scaling!r}")
 
 
@@ -90,19 +96,29 @@ def leaf_checksums(ctx, image: int, arr_off: np.ndarray, arr_count: np.ndarray, 
     return out
 
 
+def range_checksum(words: np.ndarray, first_index: int = 0) -> int:
+    """The device checksum (cf_checksum_ranges) of u32 words on the host: sum of word_i * (i + 1)
+    mod 2^64, i counted from first_index (position-weighted, so misplaced tiles show)."""
+    w = np.asarray(words, np.uint32).astype(np.uint64)
+    pos = np.arange(first_index + 1, first_index + 1 + len(w), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return int((w * pos).sum(dtype=np.uint64))
+
+
 def expected_checksum(seed: int, level: int, n: int, elem: int, scale: float, chunk: int = 1 << 24) -> int:
     """Host-side checksum of payload_values(seed, level, n) * scale (the same for every array of
     a level, scenarios.py:152-155), computed in chunks."""
     dt = np.float64 if elem == 8 else np.float32
-    total = np.uint64(0)
+    total = 0
     start = (seed * 16777619 + level * 1000003) % (1 << 31)
+    wpe = elem // 4   # u32 words per element
     for i0 in range(0, n, chunk):
         m = min(chunk, n - i0)
         raw = (np.arange(i0, i0 + m, dtype=np.int64) + start) & ((1 << 31) - 1)
         vals = raw.astype(np.float64) if elem == 8 else raw.astype(np.float32)
         words = (vals * dt(scale)).astype(dt).view(np.uint32)
-        total = total + words.astype(np.uint64).sum(dtype=np.uint64)
-    return int(total)
+        total = (total + range_checksum(words, i0 * wpe)) & ((1 << 64) - 1)
+    return total
 
 
 def gather_checksums(ordinals: np.ndarray, sums: np.ndarray, pg=None, device=None) -> tuple[np.ndarray, np.ndarray]:

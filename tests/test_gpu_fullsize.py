@@ -22,14 +22,20 @@ def cf():
     return cf
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
-def test_full_size_window_matches_oracle(cf, oracle, cfg):
-    """The BASELINE config at full size (1 GiB): e2e window copy-back and resident image equal
-    the oracle's expected arena byte for byte (relocated pointers restored, leaves x2)."""
+@pytest.mark.parametrize("cfg,mode,elem", [("C1", "resolved", 4), ("C2", "resolved", 4), ("C4", "resolved", 4),
+                                            ("C2", "chase", 4), ("C4", "chase", 4),
+                                            ("C2", "resolved", 8), ("C2", "chase", 8)])
+def test_full_size_window_matches_oracle(cf, oracle, cfg, mode, elem):
+    """The BASELINE config at full size (1 GiB of f32 leaves; 2 GiB in the reference's own f64):
+    e2e window copy-back and resident image equal the oracle's expected arena byte for byte
+    (relocated pointers restored, leaves x2), in both leaf-kernel modes."""
+    from dataclasses import replace
     sys.path.insert(0, str(REPO))
     import bench
     spec, policy, _ = bench.make_spec(cfg)
-    w = cf.DeepCopyWindow(spec, seed=1, policy=policy, align=16)
+    if elem != spec.elem:
+        spec = replace(spec, elem=elem)
+    w = cf.DeepCopyWindow(spec, seed=1, policy=policy, mode=mode, align=16)
     try:
         st = w.run(scale=2.0)
         assert st.bad == (1 << 64) - 1
@@ -50,6 +56,44 @@ def test_full_size_window_matches_oracle(cf, oracle, cfg):
         assert np.array_equal(w.image_bytes(), want)
     finally:
         w.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_full_size_c5_strong_shards(cf, world):
+    """C5 (64 GiB, DenseSpec(4, 256Mi, 3) f32 leaves-only) cut into `world` subtree shards, each
+    planned and run one after another on this GPU at the full leaf length: every shard's leaves
+    equal payload_values x 2 byte for byte, every pointer field is restored to its host target,
+    and the shards' leaf ordinals cover the whole tree's 64 leaves exactly once."""
+    from paper_1906_01128_b200 import _native as N
+    from paper_1906_01128_b200.shard import shard_for
+    sys.path.insert(0, str(REPO))
+    import bench
+    spec, policy, _ = bench.make_spec("C5")
+    want = None
+    seen = []
+    for r in range(world):
+        sh = shard_for(spec, r, world, "strong")
+        w = cf.DeepCopyWindow(sh.spec, seed=sh.seed, policy=policy, align=16, separate_output=False)
+        try:
+            st = w.run(scale=2.0)
+            assert st.bad == (1 << 64) - 1
+            got = w.host_dst()
+            off, cnt = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT)
+            lvl, od = w.table(N.CF_TAB_ARR_LEVEL), w.table(N.CF_TAB_ARR_ORDINAL)
+            for i in w.targets.tolist():
+                n = int(cnt[i])
+                assert n == spec.n and int(lvl[i]) == spec.depth
+                if want is None:   # every leaf of a level holds the same payload (scenarios.py:152-155)
+                    want = (cf.payload_values(1, spec.depth, n, 4) * np.float32(2.0)).astype(np.float32).view(np.uint8)
+                a = int(off[i])
+                assert np.array_equal(got[a:a + 4 * n], want), (world, r, int(od[i]))
+                seen.append(int(od[i]))
+            so, tg = w.table(N.CF_TAB_SITE_OFF), w.table(N.CF_TAB_SITE_TARGET)
+            vals = np.array([int.from_bytes(got[int(o):int(o) + 8].tobytes(), "little") for o in so.tolist()], np.uint64)
+            assert np.array_equal(vals, tg + np.uint64(w.src)), (world, r)
+        finally:
+            w.close()
+    assert sorted(seen) == list(range(spec.q ** spec.depth))
 
 
 def test_full_size_scattered_forest_c3(cf):

@@ -110,7 +110,8 @@ def test_pointerchain_window_plans(mapped):
 
 def test_pointerchain_window_plans_with_interleaved_layouts():
     """Staged spans on shuffled / gapped host layouts: every array still moves exactly once, and a
-    span copied back whole (one D2H DMA) never overlaps an array of another step."""
+    span copied back whole (one D2H DMA) never overlaps an array of another step, nor a DMA-moved
+    array of its own step (its scaled result would be overwritten by the stale staging bytes)."""
     rng = random.Random(3)
     for trial in range(150):
         n = rng.randint(2, 400)

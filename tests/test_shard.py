@@ -45,8 +45,52 @@ def test_shard_validation():
 def test_expected_checksum_matches_numpy():
     for elem in (4, 8):
         vals = cf.payload_values(3, 2, 100_003, elem) * (np.float64(2.0) if elem == 8 else np.float32(2.0))
-        want = int(vals.view(np.uint32).astype(np.uint64).sum(dtype=np.uint64))
+        words = vals.view(np.uint32)
+        want = sum(int(x) * (i + 1) for i, x in enumerate(words.tolist())) % (1 << 64)
         assert expected_checksum(3, 2, 100_003, elem, 2.0, chunk=4096) == want
+
+
+def test_checksum_sees_misplaced_tiles():
+    """The gather checksum is position weighted: two swapped 64 KiB tiles, or one tile written
+    at the wrong offset, change it (a plain word sum would not)."""
+    from paper_1906_01128_b200.shard import range_checksum
+    w = np.random.default_rng(0).integers(0, 1 << 32, 3 * 16384, dtype=np.uint64).astype(np.uint32)
+    swapped = np.concatenate([w[16384:32768], w[:16384], w[32768:]])
+    shifted = np.concatenate([w[:16384], w[16384:16384 + 8], w[16384:-8]])   # a tile 32 bytes late
+    assert int(w.astype(np.uint64).sum()) == int(swapped.astype(np.uint64).sum())
+    assert range_checksum(w) != range_checksum(swapped)
+    assert range_checksum(w) != range_checksum(shifted)
+
+
+@pytest.mark.gpu
+def test_device_checksum_equals_host_and_sees_swaps():
+    if N.device_count() == 0:
+        pytest.skip("no GPU visible")
+    import ctypes as C
+    from paper_1906_01128_b200.shard import range_checksum
+    ctx = N.DeviceContext.get(0, 1)
+    lib = N.lib()
+    rng = np.random.default_rng(1)
+    sizes = [4, 64 << 10, (64 << 10) + 12, 3 << 20, 5 * (64 << 10) + 4]
+    total = sum(sizes)
+    host = rng.integers(0, 1 << 32, total // 4, dtype=np.uint64).astype(np.uint32)
+    dev = C.c_void_p()
+    N.check(lib.cf_dev_alloc(ctx.handle, total, C.byref(dev)))
+    try:
+        N.check(lib.cf_memcpy(ctx.handle, dev, N.ptr(host), total))
+        offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
+        got = leaf_checksums(ctx, dev.value, offs, np.array(sizes, np.uint64) // np.uint64(4), 4)
+        want = [range_checksum(host[int(o) // 4:(int(o) + n) // 4]) for o, n in zip(offs, sizes)]
+        assert got.tolist() == want
+        # swap the first two 64 KiB tiles of the 3 MiB range on the device
+        o = int(offs[3]) // 4
+        sw = host.copy()
+        sw[o:o + 16384], sw[o + 16384:o + 32768] = host[o + 16384:o + 32768], host[o:o + 16384]
+        N.check(lib.cf_memcpy(ctx.handle, dev, N.ptr(sw), total))
+        got2 = leaf_checksums(ctx, dev.value, offs, np.array(sizes, np.uint64) // np.uint64(4), 4)
+        assert got2[3] != got[3] and got2[3] == range_checksum(sw[o:o + (3 << 20) // 4])
+    finally:
+        lib.cf_dev_free(ctx.handle, dev)
 
 
 @pytest.mark.gpu

@@ -348,7 +348,11 @@ enum {
   CF_WIN_SCALE = 1u << 4,    /* leaf kernel */
   CF_WIN_DETACH = 1u << 5,   /* inverse relocation before copy-back */
   CF_WIN_D2H = 1u << 6,      /* copy the image back to host_dst */
-  CF_WIN_GRAPH = 1u << 7     /* capture the enqueue sequence into a CUDA graph once, replay */
+  CF_WIN_GRAPH = 1u << 7,    /* capture the enqueue sequence into a CUDA graph once, replay */
+  CF_WIN_UVM = 1u << 8       /* managed-memory tree (image == host_src == host_dst): the H2D / D2H
+                                steps become chunked cudaMemPrefetchAsync to the GPU / back to the
+                                CPU on the copy streams, pipelined with resolve and leaf kernel
+                                (the UVM scheme with prefetch hints, memory.py:239-261) */
 };
 
 typedef struct {
@@ -407,6 +411,11 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
  * buffers: window r+1 starts copying in while window r is still copying out (each window runs on
  * its own stream; the copy engines' streams are shared). */
 int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_even, double scale_odd,
+                       cf_window_stats* stats);
+/* As cf_window_run_pair over a ring of nw windows planned alike (own images / copy-back buffers,
+ * own streams): run r uses ws[r % nw].  Small graphs rotate over images whose total exceeds the
+ * L2, so no step finds its data cached by an earlier one while the steps still overlap. */
+int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_even, double scale_odd,
                        cf_window_stats* stats);
 /* As cf_window_run_n for working sets that fit the L2: before every window, a memset of
  * flush_bytes at flush_buf (device) evicts the L2; stats->ms_total is the sum of the windows' own

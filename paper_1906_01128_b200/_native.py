@@ -37,6 +37,7 @@ CF_WIN_H2D, CF_WIN_TABLES, CF_WIN_ATTACH, CF_WIN_RESOLVE, CF_WIN_SCALE, CF_WIN_D
 CF_WIN_FULL = (CF_WIN_H2D | CF_WIN_TABLES | CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE
                | CF_WIN_DETACH | CF_WIN_D2H)
 CF_WIN_RESIDENT = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH
+CF_WIN_UVM = 1 << 8
 NO_BAD = (1 << 64) - 1
 
 _TAB_DTYPES = {CF_TAB_NODE_LEVEL: np.int32, CF_TAB_NODE_SIZE: np.uint32, CF_TAB_ARR_LEVEL: np.int32}
@@ -54,7 +55,7 @@ EXPORTED = (
     "cf_checksum_ranges", "cf_selective_plan", "cf_selective_plan_ex", "cf_selective_run", "cf_selective_free",
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
-    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_n_flushed",
+    "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_ring", "cf_window_run_n_flushed",
     "cf_window_set_scale",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
@@ -177,6 +178,8 @@ def _declare(L):
         "cf_window_run": (C.c_int, [P, C.c_int, C.POINTER(CfWindowStats)]),
         "cf_window_run_n": (C.c_int, [P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
         "cf_window_run_pair": (C.c_int, [P, P, C.c_int, C.c_double, C.c_double, C.POINTER(CfWindowStats)]),
+        "cf_window_run_ring": (C.c_int, [C.POINTER(P), C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
         "cf_window_run_n_flushed": (C.c_int, [P, C.c_int, C.c_double, C.c_double, P, U64, C.POINTER(CfWindowStats)]),
         "cf_window_free": (C.c_int, [P]),

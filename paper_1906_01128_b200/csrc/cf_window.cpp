@@ -172,6 +172,8 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   if (!desc || !out || !desc->tree) return fail(CF_E_INVALID, "null argument");
   const cf_tree* t = desc->tree;
   const uint32_t fl = desc->flags;
+  if ((fl & CF_WIN_UVM) && (desc->host_src != desc->image || desc->host_dst != desc->image || (fl & (CF_WIN_ATTACH | CF_WIN_DETACH | CF_WIN_GRAPH))))
+    return fail(CF_E_INVALID, "UVM window: one managed buffer for host and image, no relocation, no graph capture");
   if ((fl & CF_WIN_H2D) && !desc->host_src && !dry) return fail(CF_E_INVALID, "H2D needs host_src");
   if ((fl & CF_WIN_D2H) && !desc->host_dst && !dry) return fail(CF_E_INVALID, "D2H needs host_dst");
   if (!desc->image && !dry) return fail(CF_E_INVALID, "null image");
@@ -942,11 +944,17 @@ int cf_window_run_n(cf_window* w, int nruns, double scale_even, double scale_odd
 
 int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_even, double scale_odd,
                        cf_window_stats* st) {
-  if (!w0 || nruns < 1) return fail(CF_E_INVALID, "bad arguments");
-  if (w1 && (w1->ctx != w0->ctx || w1->d.flags != w0->d.flags)) return fail(CF_E_INVALID, "mismatched window pair");
+  cf_window* ws[2] = {w0, w1};
+  return cf_window_run_ring(ws, w1 ? 2 : 1, nruns, scale_even, scale_odd, st);
+}
+
+int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_even, double scale_odd,
+                       cf_window_stats* st) {
+  if (!ws || nw < 1 || !ws[0] || nruns < 1) return fail(CF_E_INVALID, "bad arguments");
+  cf_window* w0 = ws[0];
+  for (int i = 1; i < nw; ++i)
+    if (!ws[i] || ws[i]->ctx != w0->ctx || ws[i]->d.flags != w0->d.flags) return fail(CF_E_INVALID, "mismatched window ring");
   CfDevice g(w0->ctx);
-  cf_window* ws[2] = {w0, w1 ? w1 : w0};
-  const int nw = w1 ? 2 : 1;
   const uint64_t launches0 = w0->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
   CF_TRY(batch_begin(w0->ctx, ws, nw, w0->ev_first));
@@ -1074,7 +1082,8 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       cudaStream_t s = c->h2d[k % c->h2d.size()];
       for (uint64_t j = w->step_seg_lo[k]; j < w->step_seg_lo[k + 1]; ++j) {
         const uint64_t lo = w->seg_lo[j], hi = w->seg_hi[j];
-        CF_CUDA(copy_host_aligned(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
+        if (fl & CF_WIN_UVM) CF_CUDA(cudaMemPrefetchAsync(img + lo, hi - lo, c->device, s));   // migrate ahead
+        else CF_CUDA(copy_host_aligned(img + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, s));
         h2d_bytes += hi - lo;
       }
       CF_CUDA(cudaEventRecord(w->ev_h2d[k], s));
@@ -1129,7 +1138,8 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_rel[k], 0));
       for (uint32_t r : w->released[k]) {
         const uint64_t rlo = w->seg_lo[r], rhi = w->seg_hi[r];
-        CF_CUDA(copy_host_aligned(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
+        if (fl & CF_WIN_UVM) CF_CUDA(cudaMemPrefetchAsync(img + rlo, rhi - rlo, cudaCpuDeviceId, c->d2h));   // migrate home
+        else CF_CUDA(copy_host_aligned(dst + rlo, img + rlo, rhi - rlo, cudaMemcpyDeviceToHost, c->d2h));
         d2h_bytes += rhi - rlo;
       }
     }

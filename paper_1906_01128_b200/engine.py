@@ -83,6 +83,16 @@ class DeepCopyWindow:
                 "cf_window_run_pair")
         return st
 
+    def run_ring_n(self, others: list, nruns: int, flags: int = N.CF_WIN_FULL, scales: tuple = (2.0, 0.5)):
+        """Rotate this window and ``others`` (twins) for ``nruns`` windows (see cf_window_run_ring)."""
+        ws = [self._window(flags, self.chunk_bytes, self.mode)] + \
+             [o._window(flags, o.chunk_bytes, o.mode) for o in others]
+        arr = (N.P * len(ws))(*ws)
+        st = N.CfWindowStats()
+        N.check(N.lib().cf_window_run_ring(arr, len(ws), int(nruns), float(scales[0]), float(scales[1]), C.byref(st)),
+                "cf_window_run_ring")
+        return st
+
     # -- planning ---------------------------------------------------------------------------
     def _window(self, flags: int, chunk_bytes: int, mode: str):
         key = (flags, chunk_bytes, mode)

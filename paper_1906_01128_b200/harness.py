@@ -342,6 +342,46 @@ def _selective_plan(machine: Machine, p: DevicePrep, elem: int):
     return w
 
 
+class FusedUvmWindow:
+    """The UVM scheme with prefetch hints (harness.py:239-240, 261-283, 321-325; memory.py:239-261)
+    deferred into one pipelined cf_window over the managed tree (CF_WIN_UVM): per ~32 MiB step,
+    cudaMemPrefetchAsync to the GPU on the H2D copy stream, chain resolve and leaf kernel for the
+    pieces that have arrived, and back-migration of released steps on the D2H stream -- so page
+    migration overlaps compute and runs both directions at once, instead of one whole-tree
+    prefetch before the kernel and one migration back after it.  Logical page-fault accounting is
+    unchanged (it follows the reference's single-residence model, not the driver)."""
+
+    def __init__(self, machine: Machine, handle: TreeHandle, prep: DevicePrep):
+        self.machine, self.handle, self.prep = machine, handle, prep
+        self.scale: float | None = None
+        self.mode = "resolved"
+
+    def flush(self) -> None:
+        """Materialise the stage reached with the eager calls: the whole-tree prefetch (+ kernel)."""
+        m, h, p = self.machine, self.handle, self.prep
+        N.check(N.lib().cf_uvm_prefetch(m.ctx.handle, h.base, h.total_bytes, m.ctx.device, None))
+        if self.scale is not None:
+            _run_kernel(m, h, p, self.scale, self.mode)
+
+    def complete(self) -> None:
+        m, h, p = self.machine, self.handle, self.prep
+        mode = N.CF_MODE_CHASE if self.mode == "chase" else N.CF_MODE_RESOLVED
+        flags = (N.CF_WIN_UVM | N.CF_WIN_H2D | N.CF_WIN_TABLES | N.CF_WIN_RESOLVE | N.CF_WIN_SCALE
+                 | N.CF_WIN_D2H)
+        key = ("uvm_window", h.base, p.policy, mode)
+        w = m._plans.get(key)
+        if w is None:
+            idx, _, _, _, _, _ = _kernel_args(h, p.policy)
+            tg = np.ascontiguousarray(idx, np.int64)
+            d = N.CfWindowDesc(h.plan.handle, N.ptr(tg) if len(tg) else None, len(tg), h.base, h.base, h.base,
+                               h.base, mode, flags, float(self.scale), FUSED_CHUNK)
+            w = C.c_void_p()
+            N.check(N.lib().cf_window_plan(m.ctx.handle, C.byref(d), C.byref(w)), "UVM window plan")
+            m._plans[key] = w
+        N.check(N.lib().cf_window_set_scale(w, float(self.scale)))
+        N.check(N.lib().cf_window_run(w, 1, None), "UVM window")
+
+
 class FusedNaiveWindow:
     """The naive scheme's ``transfer_to_device -> kernel_scale -> copy_back`` (per-object deep
     copy, memory.py:349-374; device chain walk, harness.py:244-304) deferred into one window:
@@ -564,12 +604,18 @@ def transfer_to_device(machine: Machine, handle: TreeHandle, scheme: str, arena:
         if uvm_hints not in UVM_HINTS:
             raise ValueError(f"unknown uvm hint {uvm_hints!r}")
         ctx = machine.ctx.handle
+        prep = DevicePrep(scheme, device_root=handle.root_addr, policy=policy, image=handle.base,
+                          image_bytes=handle.total_bytes, uvm_hints=uvm_hints)
+        if uvm_hints == "prefetch" and fused:
+            # deferred: kernel_scale and copy_back join one prefetch-pipelined window
+            prep.fused = FusedUvmWindow(machine, handle, prep)
+            machine._deferred = prep.fused
+            return prep
         if uvm_hints == "prefetch":
             N.check(N.lib().cf_uvm_prefetch(ctx, handle.base, handle.total_bytes, machine.ctx.device, None))
         for lo, hi, advice in _uvm_advice(handle, uvm_hints):
             N.check(N.lib().cf_uvm_advise(ctx, handle.base + lo, hi - lo, advice))
-        return DevicePrep(scheme, device_root=handle.root_addr, policy=policy, image=handle.base,
-                          image_bytes=handle.total_bytes, uvm_hints=uvm_hints)
+        return prep
     raise SchemeError(f"unknown transfer scheme {scheme!r}")
 
 
@@ -734,6 +780,13 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
     stats = KernelStats()
     elem = handle.spec.elem
     fw = _pending(machine, prep)
+    if fw is not None and fw.scale is None and prep.scheme == "uvm":
+        # joins the deferred prefetch-pipelined window; the logical page accounting happens now
+        fw.scale, fw.mode = float(scale), mode
+        idx, stats.chain_derefs, _, _, cnt, _ = _kernel_args(handle, prep.policy)
+        _uvm_account_kernel(machine, handle, prep, idx)
+        stats.elements_touched = int(cnt.sum()) if len(idx) else 0
+        return stats
     if fw is not None and fw.scale is None and prep.scheme == "marshalling":
         # joins the deferred window: the leaf kernel runs chunk by chunk as the arena lands
         fw.scale, fw.mode = float(scale), mode
@@ -766,18 +819,23 @@ def kernel_scale(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: 
 
     idx, stats.chain_derefs, _, _, cnt, _ = _kernel_args(handle, prep.policy)
     if prep.scheme == "uvm":
-        fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
-        # every page read once (fields, then array pages -- a page met twice migrates once), then
-        # the array pages written (dirty)
-        machine.uvm_touch_pages(fields, "read", "device")
-        if dlo.size:
-            machine.uvm_touch_ranges(dlo, dhi, "read", "device")
-            machine.uvm_touch_ranges(dlo, dhi, "write", "device")
+        _uvm_account_kernel(machine, handle, prep, idx)
     if len(idx) == 0:
         return stats
     _run_kernel(machine, handle, prep, scale, mode)
     stats.elements_touched = int(cnt.sum())
     return stats
+
+
+def _uvm_account_kernel(machine: Machine, handle: TreeHandle, prep: DevicePrep, idx: np.ndarray) -> None:
+    """The reference UVM walk's logical page touches (harness.py:261-304, memory.py:378-394)."""
+    fields, (dlo, dhi) = _uvm_device_pages(handle, prep.policy, idx, machine.uvm.page_size)
+    # every page read once (fields, then array pages -- a page met twice migrates once), then
+    # the array pages written (dirty)
+    machine.uvm_touch_pages(fields, "read", "device")
+    if dlo.size:
+        machine.uvm_touch_ranges(dlo, dhi, "read", "device")
+        machine.uvm_touch_ranges(dlo, dhi, "write", "device")
 
 
 def _kernel_args(handle: TreeHandle, policy: str):
@@ -842,6 +900,11 @@ def _run_kernel(machine: Machine, handle: TreeHandle, prep: DevicePrep, scale: f
 
 def copy_back(machine: Machine, handle: TreeHandle, prep: DevicePrep) -> None:
     fw = _pending(machine, prep)
+    if fw is not None and fw.scale is not None and prep.scheme == "uvm":
+        machine._deferred = None
+        fw.complete()   # every released step already migrated home inside the window
+        machine.uvm_touch_mask(machine.uvm._dirty.copy(), "read", "host")
+        return
     if fw is not None and fw.scale is not None and prep.scheme == "naive":
         machine._deferred = None
         fw.complete()

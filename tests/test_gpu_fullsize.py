@@ -143,6 +143,20 @@ for spec in specs:
 for scheme in ("marshalling", "naive", "pointerchain", "uvm"):
     m, mach = cf.execute_case(cf.DenseSpec(2, 64, 3), scheme, cf.CostModel(), seed=1)
     mach.close()
+# a leaf pointer corrupted to the image's last 8 bytes (valid count): the leaf kernel must reject
+# the span, not write past the image
+from paper_1906_01128_b200 import _native as N
+w = cf.DeepCopyWindow(cf.DenseSpec(3, 5000, 2, elem=4, leaf_only=True), seed=1, policy="all_arrays", align=16)
+so, st = w.table(N.CF_TAB_SITE_OFF), w.table(N.CF_TAB_SITE_TARGET)
+f = int(so[list(st).index(w.table(N.CF_TAB_ARR_OFF)[int(w.targets[-1])])])
+w.host_src()[f:f + 8] = list((w.src + w.total - 8).to_bytes(8, "little"))
+for mode in ("resolved", "chase"):
+    try:
+        w.run(scale=2.0, mode=mode)
+        raise SystemExit("corrupted leaf pointer was not rejected")
+    except cf.WildAccess:
+        pass
+w.close()
 print("sanitized ok")
 '''
 

@@ -445,3 +445,48 @@ def test_fused_pointerchain_staged_spans_leave_other_bytes_alone(cf, policy):
             dumps.append([bytes(m.host.read_bytes(a, s)) for a, s in h.allocations])
             m.close()
         assert dumps[0] == dumps[1], (spec, policy)
+
+
+@pytest.mark.parametrize("mode", ["resolved", "chase"])
+def test_fused_uvm_prefetch_window_equals_eager(cf, mode):
+    """UVM with prefetch hints runs as one prefetch-pipelined window (CF_WIN_UVM): per step
+    migrate in, resolve + scale, migrate home.  Host bytes, logical page-fault log and kernel
+    stats equal the eager whole-tree prefetch path, over several windows and multi-chunk trees."""
+    specs = [cf.DenseSpec(4, 300_000, 2, elem=4), cf.DenseSpec(3, 5000, 3, elem=8),
+             cf.ForestSpec(cf.LinearSpec(3, 200_000, "LLinit_LLused", elem=4), 12, scatter_seed=9)]
+    for spec in specs:
+        out = []
+        for fused in (True, False):
+            m = cf.Machine()
+            m.enable_uvm()
+            h = cf.build_tree(m, spec, seed=4)
+            logs, stats = [], []
+            for r in range(3):
+                mark = m.log.mark()
+                prep = cf.transfer_to_device(m, h, "uvm", policy="all_leaves", uvm_hints="prefetch", fused=fused)
+                st = cf.kernel_scale(m, h, prep, 2.0 if r % 2 == 0 else 0.5, mode=mode)
+                cf.copy_back(m, h, prep)
+                logs.append([(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)])
+                stats.append((st.elements_touched, st.chain_derefs))
+            cf.verify_tree(m, h, 2.0, "all_leaves")
+            out.append((bytes(m.host.read_bytes(h.base, h.total_bytes)), logs, stats))
+            m.close()
+        assert out[0][1] == out[1][1] and out[0][2] == out[1][2], spec
+        assert out[0][0] == out[1][0], spec
+
+
+def test_fused_uvm_flush_between_calls(cf):
+    """A read between kernel_scale and copy_back materialises the deferred UVM window eagerly."""
+    m = cf.Machine()
+    m.enable_uvm()
+    h = cf.build_tree(m, cf.DenseSpec(3, 2000, 2, elem=4), seed=1)
+    prep = cf.transfer_to_device(m, h, "uvm", policy="all_leaves", uvm_hints="prefetch")
+    assert m._deferred is prep.fused
+    cf.kernel_scale(m, h, prep, 2.0)
+    a = h.arrays[-1]
+    v = m.host.read_bytes(a.addr, 4)   # observation: flush
+    assert m._deferred is None
+    assert np.frombuffer(v, np.float32)[0] == cf.payload_values(1, a.level, 1, 4)[0] * 2
+    cf.copy_back(m, h, prep)
+    cf.verify_tree(m, h, 2.0, "all_leaves")
+    m.close()

@@ -166,6 +166,46 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
   return {p, dense && level == sh.depth};
 }
 
+// Warp-cooperative walk (pointerchain resolve, RESOLVED mode): consecutive targets mostly share
+// their parent node (C4: 100 leaves per level-2 node, targets sorted by ordinal), so the lanes of a
+// warp are grouped by (root, level, parent ordinal) with __match_any_sync, one leader per group
+// walks the L - 1 hops to the parent and reads its Lnext, and every lane then indexes its own
+// record in that child block.  Dependent loads per chain drop from L to ~1 (the record's fields);
+// the result equals walk_chain's.  All lanes of the warp must call it (inactive lanes with
+// active = false); host pointers met on the way are translated as walk_chain does (xlate_from).
+__device__ __forceinline__ Walk walk_chain_coop(const uint8_t* image, const cf_chain_shape& sh, uint64_t root_off,
+                                                int level, uint32_t ordinal, uint64_t xlate_from, bool active) {
+  const unsigned am = __ballot_sync(0xffffffffu, active);
+  if (!active) return {nullptr, false};
+  const unsigned lane = threadIdx.x & 31;
+  const bool dense = sh.kind == CF_DENSE;
+  const uint32_t q = dense ? sh.q : 1u;
+  const uint32_t rem = ordinal & 0x7FFFFFFFu;   // bit 31: owned-attach flag (wide kernel)
+  const uint32_t parent = level >= 1 ? rem / q : 0u;
+  const unsigned grp = __match_any_sync(am, root_off) &
+                       __match_any_sync(am, (uint64_t(uint32_t(level)) << 32) | parent);
+  const int leader = __ffs(grp) - 1;
+  uint64_t blk = 0;
+  int ok = 1;
+  if (int(lane) == leader && level >= 1) {
+    // the parent: L - 1 hops with the parent's ordinal, then its Lnext (the child block)
+    Walk pw = walk_chain<false>(image, sh, root_off, level - 1, parent, xlate_from);
+    if (pw.node == nullptr || pw.leaf) {
+      ok = 0;
+    } else {
+      blk = xlate(ld_u64_any(pw.node + OFF_LNEXT), xlate_from, image, sh.image_bytes);
+    }
+  }
+  blk = __shfl_sync(am, blk, leader);
+  ok = __shfl_sync(am, ok, leader);
+  if (level < 1) return {image + root_off, dense && sh.depth == 0};
+  if (!ok) return {nullptr, false};
+  const uint64_t child = dense ? ((level < sh.depth) ? NODE_SIZE : LEAF_NODE_SIZE) : 0;
+  const uint64_t next = blk + uint64_t(rem - parent * q) * child;
+  if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+  return {reinterpret_cast<const uint8_t*>(next), dense && level == sh.depth};
+}
+
 __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ image, cf_chain_shape sh,
                                                  const uint64_t* __restrict__ root,
                                                  const int32_t* __restrict__ level,
@@ -173,8 +213,10 @@ __global__ void __launch_bounds__(128) k_resolve(const uint8_t* __restrict__ ima
                                                  uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
                                                  uint64_t* bad, uint64_t tag) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i]);
+  const bool act = i < n;
+  Walk w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0,
+                           act ? ordinal[i] : 0, 0, act);
+  if (!act) return;
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
@@ -197,8 +239,12 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
                                                          uint64_t* bad, uint64_t res_tag) {
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
   __syncthreads();
-  for (uint64_t i = threadIdx.x; i < ntargets; i += blockDim.x) {
-    Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], ordinal[i]);
+  for (uint64_t i0 = 0; i0 < ntargets; i0 += blockDim.x) {   // every lane runs every round (warp-collective walk)
+    const uint64_t i = i0 + threadIdx.x;
+    const bool act = i < ntargets;
+    Walk w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0,
+                             act ? ordinal[i] : 0, 0, act);
+    if (!act) continue;
     if (!w.node) {
       ea[i] = 0;
       count[i] = 0;
@@ -230,9 +276,10 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
     return;
   }
   const uint64_t i = uint64_t(blockIdx.x - att_blocks) * blockDim.x + threadIdx.x;
-  if (i >= ntargets) return;
-  const uint32_t od = ordinal[i];
-  Walk w = walk_chain<false>(image, sh, root ? root[i] : sh.root_off, level[i], od, from);
+  const bool act = i < ntargets;
+  const uint32_t od = act ? ordinal[i] : 0;
+  Walk w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0, od, from, act);
+  if (!act) return;
   if (!w.node) {
     ea[i] = 0;
     count[i] = 0;
@@ -616,26 +663,35 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
   pre[0] = 0;
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
+  // per-part state in registers; the target / byte offset only in CHASE mode (which re-walks the
+  // chain per access) -- RESOLVED keeps just the base pointers and the prefix, under 40 registers
+  constexpr unsigned PC = CHASE ? PER : 1;
   uint8_t* bj[PER];
-  uint64_t tj[PER], oj[PER];
+  uint64_t tj[PC], oj[PC];
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) {
     bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
-    tj[j] = __shfl_sync(0xffffffffu, t, j);
-    oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
+    if constexpr (CHASE) {
+      tj[j] = __shfl_sync(0xffffffffu, t, j);
+      oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
+    }
   }
+  (void)tj;
+  (void)oj;
   const uint32_t total = pre[PER];
   auto vptr = [&](uint32_t f) -> V* {
-    unsigned j = 0;
-#pragma unroll
-    for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
     uint8_t* b = bj[0];
     uint32_t off = pre[0];
-    uint64_t tt = tj[0], bo = oj[0];
+    [[maybe_unused]] uint64_t tt = 0, bo = 0;
+    if constexpr (CHASE) { tt = tj[0]; bo = oj[0]; }
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k)
-      if (j == k) { b = bj[k]; off = pre[k]; tt = tj[k]; bo = oj[k]; }
-    if (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
+      if (f >= pre[k]) {   // pre is non-decreasing: the last k with pre[k] <= f wins
+        b = bj[k];
+        off = pre[k];
+        if constexpr (CHASE) { tt = tj[k]; bo = oj[k]; }
+      }
+    if constexpr (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
     return reinterpret_cast<V*>(b) + (f - off);
   };
   constexpr int U = 4;
@@ -677,24 +733,36 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
   constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
   const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
   if (blockIdx.x < ntiles) {
+    // lane 0 of every warp maps the tile to its part (binary search over the launch's first-tile
+    // table) and reads the part and its resolved address; the warp gets them by shuffle -- one
+    // search and one metadata load per warp instead of per thread
     const uint64_t tile = a.w.tile_begin + blockIdx.x;
-    uint64_t lo = 0, hi = a.w.big_count;   // big part index within this launch
-    const uint64_t* tb = a.w.tile_base + a.w.tb_begin;
-    while (hi - lo > 1) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (tb[mid] <= tile) lo = mid; else hi = mid;
+    const unsigned lane = threadIdx.x & 31;
+    uint64_t t = 0, e0 = 0, e1 = 0, cnt = 0;
+    uintptr_t arr_u = 0;
+    int ok = 0;
+    if (lane == 0) {
+      uint64_t lo = 0, hi = a.w.big_count;   // big part index within this launch
+      const uint64_t* tb = a.w.tile_base + a.w.tb_begin;
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (tb[mid] <= tile) lo = mid; else hi = mid;
+      }
+      const uint32_t* pt = a.w.parts + 3 * (a.w.big_begin + lo);
+      t = pt[0];
+      e0 = uint64_t(pt[1]) + (tile - tb[lo]) * TILE;
+      e1 = min(uint64_t(pt[2]), e0 + TILE);
+      uint8_t* arr;
+      ok = target_array<T, CHASE>(a, t, arr, cnt) && e1 <= cnt;
+      arr_u = reinterpret_cast<uintptr_t>(arr);
+      if (!ok && threadIdx.x == 0) raise_bad(a.bad, t | a.tag);
     }
-    const uint32_t* pt = a.w.parts + 3 * (a.w.big_begin + lo);
-    const uint64_t t = pt[0];
-    const uint64_t e0 = uint64_t(pt[1]) + (tile - tb[lo]) * TILE;
-    const uint64_t e1 = min(uint64_t(pt[2]), e0 + TILE);
-    uint8_t* arr;
-    uint64_t cnt;
-    if (!target_array<T, CHASE>(a, t, arr, cnt) || e1 > cnt) {
-      if (threadIdx.x == 0) raise_bad(a.bad, t | a.tag);
-      return;
-    }
-    scale_range<T, CHASE, SCALE_UNROLL>(a, t, arr, e0, e1, s, threadIdx.x, SCALE_THREADS);
+    if (!__shfl_sync(0xffffffffu, ok, 0)) return;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    e0 = __shfl_sync(0xffffffffu, e0, 0);
+    e1 = __shfl_sync(0xffffffffu, e1, 0);
+    arr_u = __shfl_sync(0xffffffffu, arr_u, 0);
+    scale_range<T, CHASE, SCALE_UNROLL>(a, t, reinterpret_cast<uint8_t*>(arr_u), e0, e1, s, threadIdx.x, SCALE_THREADS);
     return;
   }
   const uint64_t ngroups = a.w.group_end - a.w.group_begin;

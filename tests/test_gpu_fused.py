@@ -37,6 +37,24 @@ def _window(cf, spec, fused, seed=3, scale=2.0, mode="resolved", policy="ref", a
     return out, log, (st.elements_touched, st.chain_derefs), base
 
 
+def _rel_dump(m, h) -> list:
+    """Every allocation's bytes with each pointer field rewritten as (allocation index, offset) of
+    its target: two machines place their trees at different host addresses (managed memory in
+    particular), so raw pointer words differ while the trees are identical."""
+    import bisect
+    allocs = sorted(h.allocations)
+    starts = [a for a, _ in allocs]
+    out = {a: bytearray(m.host.read_bytes(a, s)) for a, s in allocs}
+    for holder, off, _ in h.reference_field_sites:
+        i = bisect.bisect_right(starts, holder) - 1
+        a = starts[i]
+        v = m.host.read_word(holder + off)
+        j = bisect.bisect_right(starts, v) - 1
+        rel = ((j + 1) << 40) | (v - starts[j]) if j >= 0 and v - starts[j] < allocs[j][1] else v
+        out[a][holder - a + off:holder - a + off + 8] = rel.to_bytes(8, "little")
+    return [bytes(out[a]) for a, _ in h.allocations]
+
+
 def _norm(cf, raw, spec, base, seed, align):
     """Pointer fields as arena offsets, so two arenas at different addresses compare."""
     m = cf.Machine()
@@ -469,7 +487,7 @@ def test_fused_uvm_prefetch_window_equals_eager(cf, mode):
                 logs.append([(e.direction, e.op_kind, e.bytes) for e in m.log.since(mark)])
                 stats.append((st.elements_touched, st.chain_derefs))
             cf.verify_tree(m, h, 2.0, "all_leaves")
-            out.append(([bytes(m.host.read_bytes(a, s)) for a, s in h.allocations], logs, stats))
+            out.append((_rel_dump(m, h), logs, stats))
             m.close()
         assert out[0][1] == out[1][1] and out[0][2] == out[1][2], spec
         assert out[0][0] == out[1][0], spec

@@ -663,35 +663,26 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
   pre[0] = 0;
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
-  // per-part state in registers; the target / byte offset only in CHASE mode (which re-walks the
-  // chain per access) -- RESOLVED keeps just the base pointers and the prefix, under 40 registers
-  constexpr unsigned PC = CHASE ? PER : 1;
   uint8_t* bj[PER];
-  uint64_t tj[PC], oj[PC];
+  uint64_t tj[PER], oj[PER];
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) {
     bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
-    if constexpr (CHASE) {
-      tj[j] = __shfl_sync(0xffffffffu, t, j);
-      oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
-    }
+    tj[j] = __shfl_sync(0xffffffffu, t, j);
+    oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
   }
-  (void)tj;
-  (void)oj;
   const uint32_t total = pre[PER];
   auto vptr = [&](uint32_t f) -> V* {
+    unsigned j = 0;
+#pragma unroll
+    for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
     uint8_t* b = bj[0];
     uint32_t off = pre[0];
-    [[maybe_unused]] uint64_t tt = 0, bo = 0;
-    if constexpr (CHASE) { tt = tj[0]; bo = oj[0]; }
+    uint64_t tt = tj[0], bo = oj[0];
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k)
-      if (f >= pre[k]) {   // pre is non-decreasing: the last k with pre[k] <= f wins
-        b = bj[k];
-        off = pre[k];
-        if constexpr (CHASE) { tt = tj[k]; bo = oj[k]; }
-      }
-    if constexpr (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
+      if (j == k) { b = bj[k]; off = pre[k]; tt = tj[k]; bo = oj[k]; }
+    if (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
     return reinterpret_cast<V*>(b) + (f - off);
   };
   constexpr int U = 4;

@@ -69,6 +69,9 @@ struct cf_window {
   uint32_t* d_count = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rel;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr, ev_first = nullptr, ev_tables = nullptr;
+  // the window's last host->device copy has landed: recorded as an EXTERNAL event (visible outside
+  // a captured graph), so the next window of a ring starts its copy-in right behind this one's
+  cudaEvent_t ev_h2d_done = nullptr;
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
   bool has_roots = false;
@@ -148,6 +151,7 @@ void destroy(cf_window* w) {
   if (w->ev_join) cudaEventDestroy(w->ev_join);
   if (w->ev_first) cudaEventDestroy(w->ev_first);
   if (w->ev_tables) cudaEventDestroy(w->ev_tables);
+  if (w->ev_h2d_done) cudaEventDestroy(w->ev_h2d_done);
   for (auto& gr : w->graphs) cudaGraphExecDestroy(gr.exec);
   if (w->ev_fan) cudaEventDestroy(w->ev_fan);
   if (w->stream) cudaStreamDestroy(w->stream);
@@ -628,6 +632,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   bool ok = mk(&w->ev_start, cudaEventDefault) == cudaSuccess && mk(&w->ev_end, cudaEventDefault) == cudaSuccess &&
             mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_first, cudaEventDefault) == cudaSuccess &&
             mk(&w->ev_tables, cudaEventDisableTiming) == cudaSuccess &&
+            mk(&w->ev_h2d_done, cudaEventDisableTiming) == cudaSuccess &&
             mk(&w->ev_fan, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) == cudaSuccess;
   for (uint64_t c = 0; c < nch && ok; ++c)
@@ -958,8 +963,15 @@ int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_eve
   const uint64_t launches0 = w0->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
   CF_TRY(batch_begin(w0->ctx, ws, nw, w0->ev_first));
+  // Copy-ins in window order: window r starts once window r-1's last H2D has landed, so the host
+  // link carries r's copy-in while r-1 computes and copies out.  Without it every window of the
+  // ring starts at once, all copy-ins share the H2D engine and finish together, and the D2H side
+  // idles first and then runs alone (C1 ring: 0.76 of the same-size link).  CF_RING_CHAIN=0: off.
+  static const bool chain = [] { const char* e = getenv("CF_RING_CHAIN"); return !(e && e[0] == '0'); }();
   for (int r = 0; r < nruns; ++r) {
     cf_window* w = ws[r % nw];
+    if (chain && r > 0 && nw > 1 && (w->d.flags & CF_WIN_H2D))
+      CF_CUDA(cudaStreamWaitEvent(w->stream, ws[(r - 1) % nw]->ev_h2d_done, 0));
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;
     CF_TRY(one_run(w, false, &a, &b));
@@ -1015,6 +1027,15 @@ int one_run(cf_window* w, bool timing, uint64_t* h2d, uint64_t* d2h) {
   for (auto& g : w->graphs)
     if (g.scale == w->d.scale) gr = &g;
   if (!gr) {
+    // bounded cache: run_n alternates two scales; a caller cycling through more scales recaptures
+    // instead of accumulating executable graphs (the evicted one may still be in flight: drain
+    // this window's stream first)
+    constexpr size_t MAX_GRAPHS = 4;
+    if (w->graphs.size() >= MAX_GRAPHS) {
+      CF_CUDA(cudaStreamSynchronize(w->stream));
+      CF_CUDA(cudaGraphExecDestroy(w->graphs.front().exec));
+      w->graphs.erase(w->graphs.begin());
+    }
     cf_window::Graph g{w->d.scale, nullptr, 0, 0, 0};
     const uint64_t l0 = c->launches.load();
     CF_CUDA(cudaStreamBeginCapture(w->stream, cudaStreamCaptureModeThreadLocal));
@@ -1143,6 +1164,23 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
         d2h_bytes += rhi - rlo;
       }
     }
+  }
+  if (fl & CF_WIN_H2D) {
+    // every H2D stream's work of this window is behind one external event (run_ring chains on it)
+    cudaStream_t s0 = c->h2d[0];
+    for (size_t i = 1; i < c->h2d.size(); ++i) {
+      CF_CUDA(cudaEventRecord(w->ev_join, c->h2d[i]));
+      CF_CUDA(cudaStreamWaitEvent(s0, w->ev_join, 0));
+    }
+    // (scattered layouts' node pages come in by a zero-copy kernel at the window's start: tiny, not chained)
+    // inside a graph capture the record must be an external node to be visible to later launches;
+    // outside one the external flag is rejected (cudaErrorIllegalState)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CF_CUDA(cudaStreamIsCapturing(s0, &cap));
+    if (cap == cudaStreamCaptureStatusActive)
+      CF_CUDA(cudaEventRecordWithFlags(w->ev_h2d_done, s0, cudaEventRecordExternal));
+    else
+      CF_CUDA(cudaEventRecord(w->ev_h2d_done, s0));
   }
   // join the copy streams back into the compute stream
   if (copies) {

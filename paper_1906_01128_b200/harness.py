@@ -18,6 +18,7 @@ from the resolve kernel) or ``mode="chase"`` (chain re-walked per access).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import statistics
 import time
 from dataclasses import dataclass, field
@@ -224,6 +225,9 @@ UVM_HINTS = ("none", "prefetch", "advise", "preferred", "read_mostly")
 
 # pipeline granularity of the fused marshalling window (repo:profiles/r01_design_experiments.md)
 FUSED_CHUNK = 32 << 20
+# UVM window step (design experiment knob): migration throughput per
+# cudaMemPrefetchAsync grows with its size (tools/uvm_probe2.py)
+UVM_CHUNK = int(os.environ.get("CF_UVM_CHUNK_MB", "32")) << 20
 
 
 class FusedMarshalWindow:
@@ -374,7 +378,7 @@ class FusedUvmWindow:
             idx, _, _, _, _, _ = _kernel_args(h, p.policy)
             tg = np.ascontiguousarray(idx, np.int64)
             d = N.CfWindowDesc(h.plan.handle, N.ptr(tg) if len(tg) else None, len(tg), h.base, h.base, h.base,
-                               h.base, mode, flags, float(self.scale), FUSED_CHUNK)
+                               h.base, mode, flags, float(self.scale), UVM_CHUNK)
             w = C.c_void_p()
             N.check(N.lib().cf_window_plan(m.ctx.handle, C.byref(d), C.byref(w)), "UVM window plan")
             m._plans[key] = w

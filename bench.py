@@ -67,7 +67,9 @@ C3_SCATTER = 0xC3
 L2_FLUSH_BELOW = 512 << 20
 NOMINAL_HBM_GBS = 8000.0   # vendor figure, reported beside the measured-copy roofline
 LINK_PROBE_BYTES = 1 << 30
-RING_BYTES = 256 << 20     # small graphs: e2e steps rotate over at least this many bytes of images
+# small graphs: e2e steps rotate over at least this many bytes of images (> the 126 MB L2; a ring
+# of 34 C1 windows measured 0.85 of the same-size link, 68 windows 0.79: tools/c1_ring_probe.py)
+RING_BYTES = 128 << 20
 
 
 def scaling_of(name: str) -> str:
@@ -589,8 +591,11 @@ class Measured:
 
 
 def plain_link(ctx, nbytes: int, iters: int = 1) -> dict:
+    """Plain cudaMemcpyAsync probe, best of several repetitions (small sizes vary run to run:
+    more repetitions for them)."""
     from paper_1906_01128_b200 import _native as N
-    return {k: round(v, 2) for k, v in N.link_probe(ctx, nbytes, iters=iters, reps=3).items()}
+    reps = 3 if nbytes >= (256 << 20) else 10
+    return {k: round(v, 2) for k, v in N.link_probe(ctx, nbytes, iters=iters, reps=reps).items()}
 
 
 def summary_block(name: str, elem: int, device: int, chunk_mb: int, numa_node: int, steps: int, warmup: int,

@@ -78,11 +78,18 @@ int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uin
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
                           cudaStream_t s, uint64_t res_tag = 0);
+// A resolve range whose targets are consecutive ordinals ord0, ord0 + 1, ... at one level >= 1 of a
+// single dense tree, owning their A field exactly when it is misaligned (own_misaligned): the
+// resolver derives level / ordinal / ownership instead of reading the tables.
+struct UniTargets {
+  uint32_t on, level, ord0, own_misaligned;
+};
 // Attach and resolve side by side in one launch (8-byte aligned pointer fields only).
 int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
                                const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
-                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag = 0);
+                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag = 0,
+                               const UniTargets* uni = nullptr);
 int launch_resolve(cf_ctx* ctx, const uint8_t* image, const cf_chain_shape& sh, const uint64_t* root,
                    const int32_t* level, const uint32_t* ordinal, uint64_t n, uint64_t* ea,
                    uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t tag = 0);

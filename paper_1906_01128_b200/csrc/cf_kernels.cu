@@ -262,6 +262,36 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
 // aligned fields: one atomic access).  A target whose ordinal carries bit 31 owns its A field
 // (a 4-mod-8 leaf field attached in this step, left out of the attach CTAs' list): its resolver
 // attaches it, so no misaligned field is ever read while another thread writes it.
+// Uniform resolve range (UniTargets.on): the step's targets are consecutive ordinals ord0 + i at
+// one level >= 1 of a single dense tree (C4: the 1M leaves, C2: the 64 leaves), and a target owns
+// its A field exactly when that field is misaligned (own_misaligned).  The resolver then needs no
+// level / ordinal table reads and no __match_any_sync: lanes sharing a parent are a contiguous
+// run (leader = lane - ordinal % q, clipped to lane 0), one leader per run walks to the parent,
+// every lane indexes its record in the parent's child block.
+__device__ __forceinline__ Walk walk_uniform(const uint8_t* image, const cf_chain_shape& sh, const UniTargets& u,
+                                             uint64_t i, uint64_t xlate_from) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t q = sh.q;
+  const uint32_t ord = u.ord0 + uint32_t(i);
+  const uint32_t parent = ord / q;
+  const uint32_t j = ord - parent * q;
+  const int lead = max(0, int(lane) - int(j));
+  uint64_t blk = 0;
+  int ok = 1;
+  if (int(lane) == lead) {
+    const Walk pw = walk_chain<false>(image, sh, sh.root_off, int(u.level) - 1, parent, xlate_from);
+    if (pw.node == nullptr || pw.leaf) ok = 0;
+    else blk = xlate(ld_u64_any(pw.node + OFF_LNEXT), xlate_from, image, sh.image_bytes);
+  }
+  blk = __shfl_sync(0xffffffffu, blk, lead);
+  ok = __shfl_sync(0xffffffffu, ok, lead);
+  if (!ok) return {nullptr, false};
+  const bool leaf = int(u.level) == int(sh.depth);
+  const uint64_t next = blk + uint64_t(j) * (leaf ? LEAF_NODE_SIZE : NODE_SIZE);
+  if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+  return {reinterpret_cast<const uint8_t*>(next), leaf};
+}
+
 __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict__ image, uint64_t total,
                                                              const uint64_t* __restrict__ sites, uint64_t nsites,
                                                              uint64_t from, uint64_t to, cf_chain_shape sh,
@@ -269,7 +299,8 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
                                                              const int32_t* __restrict__ level,
                                                              const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                              uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                             uint64_t* bad, unsigned att_blocks, uint64_t res_tag) {
+                                                             uint64_t* bad, unsigned att_blocks, uint64_t res_tag,
+                                                             UniTargets uni) {
   if (blockIdx.x < att_blocks) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < nsites) relocate_one(image, total, sites, i, from, to, bad);
@@ -277,8 +308,18 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
   }
   const uint64_t i = uint64_t(blockIdx.x - att_blocks) * blockDim.x + threadIdx.x;
   const bool act = i < ntargets;
-  const uint32_t od = act ? ordinal[i] : 0;
-  Walk w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0, od, from, act);
+  uint32_t od;
+  Walk w;
+  if (uni.on) {   // warp-uniform branch: every lane of the warp takes it
+    w = walk_uniform(image, sh, uni, i, from);
+    od = 0;
+    if (act && w.node && uni.own_misaligned &&
+        (reinterpret_cast<uintptr_t>(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)) & 7))
+      od = 0x80000000u;
+  } else {
+    od = act ? ordinal[i] : 0;
+    w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0, od, from, act);
+  }
   if (!act) return;
   if (!w.node) {
     ea[i] = 0;
@@ -990,12 +1031,13 @@ int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uin
 int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
                                const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
-                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag) {
+                               uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag, const UniTargets* uni) {
   const uint64_t ab = (nsites + 255) / 256, rb = (ntargets + 255) / 256;
   if (ab + rb == 0) return CF_OK;
   if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
   k_attach_resolve_wide<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level,
-                                                         ordinal, ntargets, ea, count, bad, unsigned(ab), res_tag);
+                                                         ordinal, ntargets, ea, count, bad, unsigned(ab), res_tag,
+                                                         uni ? *uni : UniTargets{0, 0, 0, 0});
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

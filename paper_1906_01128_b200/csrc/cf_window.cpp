@@ -50,6 +50,7 @@ struct cf_window {
   std::vector<uint64_t> attach_n;
   bool owned_attach = false;
   std::vector<uint64_t> res_lo;        // resolve-target ranges per step
+  std::vector<UniTargets> uni;         // per step: the resolve range is uniform (no table reads)
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step
   std::vector<std::vector<uint32_t>> released;  // segments whose copy-back may start after step k
@@ -69,9 +70,6 @@ struct cf_window {
   uint32_t* d_count = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rel;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_join = nullptr, ev_first = nullptr, ev_tables = nullptr;
-  // the window's last host->device copy has landed: recorded as an EXTERNAL event (visible outside
-  // a captured graph), so the next window of a ring starts its copy-in right behind this one's
-  cudaEvent_t ev_h2d_done = nullptr;
   std::vector<cudaEvent_t> ev_k0, ev_k1;   // leaf-kernel timing per step
   uint64_t nsites = 0;
   bool has_roots = false;
@@ -151,7 +149,6 @@ void destroy(cf_window* w) {
   if (w->ev_join) cudaEventDestroy(w->ev_join);
   if (w->ev_first) cudaEventDestroy(w->ev_first);
   if (w->ev_tables) cudaEventDestroy(w->ev_tables);
-  if (w->ev_h2d_done) cudaEventDestroy(w->ev_h2d_done);
   for (auto& gr : w->graphs) cudaGraphExecDestroy(gr.exec);
   if (w->ev_fan) cudaEventDestroy(w->ev_fan);
   if (w->stream) cudaStreamDestroy(w->stream);
@@ -487,6 +484,26 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
       w->attach_n[k] = keep.size();
     }
   }
+  // uniform resolve ranges: one tree, consecutive ordinals at one level >= 1, ownership == misalignment
+  w->uni.assign(nch, UniTargets{0, 0, 0, 0});
+  if (dense && t->tree_root.size() <= 1) {
+    for (uint64_t k = 0; k < nch; ++k) {
+      const uint64_t lo = w->res_lo[k], hi = w->res_lo[k + 1];
+      if (hi == lo) continue;
+      const int64_t a0 = desc->h_targets[torder[lo]];
+      const int L = t->arr_level[a0];
+      const uint64_t o0 = t->arr_ordinal[a0];
+      bool ok = L >= 1 && o0 + (hi - lo) < (1ull << 31);
+      for (uint64_t p2 = lo; p2 < hi && ok; ++p2) {
+        const uint64_t i = torder[p2];
+        const int64_t a = desc->h_targets[i];
+        const uint64_t fa = t->arr_owner[a] + (L == int(t->spec.depth) ? LEAF_OFF_A : OFF_A);
+        ok = t->arr_level[a] == L && t->arr_ordinal[a] == o0 + (p2 - lo) &&
+             bool(owned_target[i]) == (w->owned_attach && (fa & 7) != 0);
+      }
+      if (ok) w->uni[k] = UniTargets{1, uint32_t(L), uint32_t(o0), w->owned_attach ? 1u : 0u};
+    }
+  }
   mark("o:targets");
   // per step: the pieces ready at that step, as one leaf-kernel launch (big tiles + small groups)
   std::vector<uint64_t> pstep(parts.size()), porder, plo;
@@ -632,7 +649,6 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   bool ok = mk(&w->ev_start, cudaEventDefault) == cudaSuccess && mk(&w->ev_end, cudaEventDefault) == cudaSuccess &&
             mk(&w->ev_join, cudaEventDisableTiming) == cudaSuccess && mk(&w->ev_first, cudaEventDefault) == cudaSuccess &&
             mk(&w->ev_tables, cudaEventDisableTiming) == cudaSuccess &&
-            mk(&w->ev_h2d_done, cudaEventDisableTiming) == cudaSuccess &&
             mk(&w->ev_fan, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) == cudaSuccess;
   for (uint64_t c = 0; c < nch && ok; ++c)
@@ -963,15 +979,8 @@ int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_eve
   const uint64_t launches0 = w0->ctx->launches.load();
   uint64_t h2d = 0, d2h = 0;
   CF_TRY(batch_begin(w0->ctx, ws, nw, w0->ev_first));
-  // Copy-ins in window order: window r starts once window r-1's last H2D has landed, so the host
-  // link carries r's copy-in while r-1 computes and copies out.  Without it every window of the
-  // ring starts at once, all copy-ins share the H2D engine and finish together, and the D2H side
-  // idles first and then runs alone (C1 ring: 0.76 of the same-size link).  CF_RING_CHAIN=0: off.
-  static const bool chain = [] { const char* e = getenv("CF_RING_CHAIN"); return !(e && e[0] == '0'); }();
   for (int r = 0; r < nruns; ++r) {
     cf_window* w = ws[r % nw];
-    if (chain && r > 0 && nw > 1 && (w->d.flags & CF_WIN_H2D))
-      CF_CUDA(cudaStreamWaitEvent(w->stream, ws[(r - 1) % nw]->ev_h2d_done, 0));
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;
     CF_TRY(one_run(w, false, &a, &b));
@@ -1093,6 +1102,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
   const uint32_t* dod = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_ord);
   const uint64_t* drt = w->has_roots ? reinterpret_cast<const uint64_t*>(w->d_tab + w->off_root) : nullptr;
   const bool chase = d.mode == CF_MODE_CHASE;
+  static const bool no_uni = getenv("CF_NO_UNI") != nullptr;   // A/B switch (design experiments)
 
   for (uint64_t k = 0; k < nch; ++k) {
     if ((fl & CF_WIN_H2D) && k == 0 && w->zc) {
@@ -1119,7 +1129,8 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     } else if (do_attach && do_resolve && w->wide_ok) {
       CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
-                                        w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
+                                        w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE,
+                                        w->uni[k].on && !no_uni ? &w->uni[k] : nullptr));
     } else {
       if (do_attach)
         CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs, nullptr,
@@ -1164,23 +1175,6 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
         d2h_bytes += rhi - rlo;
       }
     }
-  }
-  if (fl & CF_WIN_H2D) {
-    // every H2D stream's work of this window is behind one external event (run_ring chains on it)
-    cudaStream_t s0 = c->h2d[0];
-    for (size_t i = 1; i < c->h2d.size(); ++i) {
-      CF_CUDA(cudaEventRecord(w->ev_join, c->h2d[i]));
-      CF_CUDA(cudaStreamWaitEvent(s0, w->ev_join, 0));
-    }
-    // (scattered layouts' node pages come in by a zero-copy kernel at the window's start: tiny, not chained)
-    // inside a graph capture the record must be an external node to be visible to later launches;
-    // outside one the external flag is rejected (cudaErrorIllegalState)
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CF_CUDA(cudaStreamIsCapturing(s0, &cap));
-    if (cap == cudaStreamCaptureStatusActive)
-      CF_CUDA(cudaEventRecordWithFlags(w->ev_h2d_done, s0, cudaEventRecordExternal));
-    else
-      CF_CUDA(cudaEventRecord(w->ev_h2d_done, s0));
   }
   // join the copy streams back into the compute stream
   if (copies) {

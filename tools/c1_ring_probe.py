@@ -1,8 +1,7 @@
 """C1 (4 MB graph) e2e window variants (design experiment): ring size x step size x CUDA graph,
-with or without copy-in chaining across the ring (CF_RING_CHAIN, read once per process).
-    CF_RING_CHAIN=0 python tools/c1_ring_probe.py"""
+and the same-size plain-copy probe (best of 10) before and after.
+    python tools/c1_ring_probe.py"""
 import json
-import os
 import sys
 
 sys.path.insert(0, ".")
@@ -12,12 +11,12 @@ from paper_1906_01128_b200 import _native as N  # noqa: E402
 
 spec, policy, _ = bench.make_spec("C1")
 base = DeepCopyWindow(spec, seed=1, policy=policy, align=16)
-probe = N.link_probe(base.ctx, base.total, iters=8, reps=3)
-out = {"chain": os.environ.get("CF_RING_CHAIN", "1"), "probe_same_size": {k: round(v, 2) for k, v in probe.items()}}
+probe = N.link_probe(base.ctx, base.total, iters=8, reps=10)
+out = {"probe_same_size": {k: round(v, 2) for k, v in probe.items()}}
 twins = [base.twin() for _ in range(67)]
 for chunk in (1 << 20, 2 << 20, 4 << 20):
-    for ring in (2, 8, 68):
-        for graph in (True, False):
+    for ring in (8, 16, 34, 68):
+        for graph in ((True, False) if chunk == 4 << 20 else (True,)):
             ws = [base] + twins[:ring - 1]
             for w in ws:
                 w.chunk_bytes = chunk
@@ -31,4 +30,5 @@ for chunk in (1 << 20, 2 << 20, 4 << 20):
             key = f"chunk{chunk >> 20}M_ring{ring}_{'graph' if graph else 'direct'}"
             out[key] = {"ms": round(best, 4), "bidir_gbs": round(bidir, 2), "frac": round(bidir / probe["bidir"], 3)}
             print(key, out[key], flush=True)
+out["probe_same_size_after"] = {k: round(v, 2) for k, v in N.link_probe(base.ctx, base.total, iters=8, reps=10).items()}
 print(json.dumps(out))

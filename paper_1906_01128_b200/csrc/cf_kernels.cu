@@ -29,10 +29,14 @@
 #include "cf_internal.h"
 
 #include <algorithm>
+#include <type_traits>
 
 // tuning knobs (design experiments: tools/build_variants.sh)
 #ifndef CF_SCALE_MINB
 #define CF_SCALE_MINB 6
+#endif
+#ifndef CF_GROUP_MINB
+#define CF_GROUP_MINB CF_SCALE_MINB
 #endif
 #ifndef CF_GROUP_U
 #define CF_GROUP_U 4
@@ -236,7 +240,12 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
                                                          const int32_t* __restrict__ level,
                                                          const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                          uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                         uint64_t* bad, uint64_t res_tag) {
+                                                         uint64_t* bad, uint64_t res_tag, const uint64_t* tab_src,
+                                                         uint64_t* tab_dst, uint64_t tab_words) {
+  if (tab_words) {   // the window's tables, pulled from mapped host memory (no other reader yet)
+    for (uint64_t i = threadIdx.x; i < tab_words; i += blockDim.x) tab_dst[i] = tab_src[i];
+    __syncthreads();
+  }
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
   __syncthreads();
   for (uint64_t i0 = 0; i0 < ntargets; i0 += blockDim.x) {   // every lane runs every round (warp-collective walk)
@@ -273,7 +282,7 @@ __device__ __forceinline__ Walk walk_uniform(const uint8_t* image, const cf_chai
   const unsigned lane = threadIdx.x & 31;
   const uint32_t q = sh.q;
   const uint32_t ord = u.ord0 + uint32_t(i);
-  const uint32_t parent = ord / q;
+  const uint32_t parent = q > 1 ? uint32_t(__umul64hi(uint64_t(ord), u.qmagic)) : ord;   // ord / q
   const uint32_t j = ord - parent * q;
   const int lead = max(0, int(lane) - int(j));
   uint64_t blk = 0;
@@ -312,10 +321,33 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
   Walk w;
   if (uni.on) {   // warp-uniform branch: every lane of the warp takes it
     w = walk_uniform(image, sh, uni, i, from);
-    od = 0;
-    if (act && w.node && uni.own_misaligned &&
-        (reinterpret_cast<uintptr_t>(w.node + (w.leaf ? LEAF_OFF_A : OFF_A)) & 7))
-      od = 0x80000000u;
+    if (!act) return;
+    if (!w.node) {
+      ea[i] = 0;
+      count[i] = 0;
+      raise_bad(bad, i | res_tag);
+      return;
+    }
+    // the record's A field: 8-byte aligned -> one 64-bit load (an attach CTA may be rewriting
+    // it); at 4 mod 8 -> this thread owns it (no other reader or writer): two u32 accesses
+    uint32_t* fa = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(w.node) + (w.leaf ? LEAF_OFF_A : OFF_A));
+    const bool mis = (reinterpret_cast<uintptr_t>(fa) & 7) != 0;
+    uint64_t v = mis ? (uint64_t(fa[0]) | (uint64_t(fa[1]) << 32)) : *reinterpret_cast<const uint64_t*>(fa);
+    if (mis && uni.own_misaligned) {   // owned field: attach it here
+      const uint64_t dlt = v - from;
+      if (dlt >= total) {
+        ea[i] = 0;
+        count[i] = 0;
+        raise_bad(bad, i);
+        return;
+      }
+      v = to + dlt;
+      fa[0] = uint32_t(v);
+      fa[1] = uint32_t(v >> 32);
+    }
+    ea[i] = xlate(v, from, image, sh.image_bytes);
+    count[i] = *reinterpret_cast<const uint32_t*>(w.node + OFF_NA);
+    return;
   } else {
     od = act ? ordinal[i] : 0;
     w = walk_chain_coop(image, sh, act ? (root ? root[i] : sh.root_off) : 0, act ? level[i] : 0, od, from, act);
@@ -759,12 +791,17 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
 }
 
 // One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
-// blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part.
-template <typename T, bool CHASE>
-__global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArgs a, T s) {
+// blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part, and the
+// rest relocate (a detach riding in the launch).  PATH specialises the kernel for launches with
+// only tiles or only groups (the common cases: C2 / C4), so each gets its own register budget
+// under the 6-CTA/SM launch bound instead of the union of both paths' (no spills).
+enum { PATH_ALL = 0, PATH_TILES = 1, PATH_GROUPS = 2 };
+template <typename T, bool CHASE, int PATH>
+__global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_GROUPS ? CF_GROUP_MINB : CF_SCALE_MINB)
+    k_scale(ScaleArgs a, T s) {
   constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
   const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
-  if (blockIdx.x < ntiles) {
+  if (PATH != PATH_GROUPS && blockIdx.x < ntiles) {
     // lane 0 of every warp maps the tile to its part (binary search over the launch's first-tile
     // table) and reads the part and its resolved address; the warp gets them by shuffle -- one
     // search and one metadata load per warp instead of per thread
@@ -806,12 +843,14 @@ __global__ void __launch_bounds__(SCALE_THREADS, CF_SCALE_MINB) k_scale(ScaleArg
                    a.reloc.tag);
     return;
   }
-  const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
+  if constexpr (PATH != PATH_TILES) {
+    const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
 #if CF_GROUP_WARP
-  scale_group_warp<T, CHASE>(a, g, s);
+    scale_group_warp<T, CHASE>(a, g, s);
 #else
-  scale_group<T, CHASE>(a, g, s);
+    scale_group<T, CHASE>(a, g, s);
 #endif
+  }
 }
 
 // ---------------------------------------------------------------- naive fix-up
@@ -1019,11 +1058,13 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                          cudaStream_t s, uint64_t res_tag) {
-  if (nsites == 0 && ntargets == 0) return CF_OK;
+                          cudaStream_t s, uint64_t res_tag, const void* tab_src, void* tab_dst, uint64_t tab_bytes) {
+  if (nsites == 0 && ntargets == 0 && tab_bytes == 0) return CF_OK;
+  if (tab_bytes & 7) return fail(CF_E_INVALID, "table block must be a multiple of 8 bytes");
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
   k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level, ordinal, ntargets,
-                                        ea, count, bad, res_tag);
+                                        ea, count, bad, res_tag, static_cast<const uint64_t*>(tab_src),
+                                        static_cast<uint64_t*>(tab_dst), tab_bytes / 8);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -1037,7 +1078,7 @@ int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, cons
   if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
   k_attach_resolve_wide<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level,
                                                          ordinal, ntargets, ea, count, bad, unsigned(ab), res_tag,
-                                                         uni ? *uni : UniTargets{0, 0, 0, 0});
+                                                         uni ? *uni : UniTargets{0, 0, 0, 0, 0});
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -1068,12 +1109,22 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
   // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware
   // CTA launcher keeps more independent loads in flight than a loop re-locating its part
   const unsigned grid = unsigned(units);
+  const bool tiles = work.tile_end > work.tile_begin, groups = work.group_end > work.group_begin;
+  const int path = (tiles && groups) ? PATH_ALL : (groups ? PATH_GROUPS : PATH_TILES);
+  auto go = [&](auto tag_t, auto tag_chase) {
+    using T = decltype(tag_t);
+    constexpr bool C = decltype(tag_chase)::value;
+    const T sc = T(scale);
+    if (path == PATH_TILES) k_scale<T, C, PATH_TILES><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
+    else if (path == PATH_GROUPS) k_scale<T, C, PATH_GROUPS><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
+    else k_scale<T, C, PATH_ALL><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
+  };
   if (elem == 4) {
-    if (mode == CF_MODE_CHASE) k_scale<float, true><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
-    else k_scale<float, false><<<grid, SCALE_THREADS, 0, s>>>(a, float(scale));
+    if (mode == CF_MODE_CHASE) go(float{}, std::true_type{});
+    else go(float{}, std::false_type{});
   } else {
-    if (mode == CF_MODE_CHASE) k_scale<double, true><<<grid, SCALE_THREADS, 0, s>>>(a, scale);
-    else k_scale<double, false><<<grid, SCALE_THREADS, 0, s>>>(a, scale);
+    if (mode == CF_MODE_CHASE) go(double{}, std::true_type{});
+    else go(double{}, std::false_type{});
   }
   CF_LAUNCHED(ctx);
   return CF_OK;

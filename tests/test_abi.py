@@ -124,12 +124,15 @@ def test_sass_chase_mode_keeps_per_access_chain_loads():
                          text=True, check=True, cwd=str(REPO)).stdout
     rows = {}
     for line in out.splitlines()[2:]:
-        t, mode, total, ld128, st128, chain = [x.strip() for x in line.strip("|").split("|")]
-        rows[(t, mode)] = (int(total), int(ld128), int(st128), int(chain))
+        t, mode, path, total, ld128, st128, chain = [x.strip() for x in line.strip("|").split("|")]
+        rows[(t, mode, path)] = (int(total), int(ld128), int(st128), int(chain))
+    paths = {p for _, _, p in rows}
+    assert paths == {"tiles", "groups", "tiles+groups"}, paths
     for t in ("float", "double"):
-        assert rows[(t, "resolved")][3] == 0
-        assert rows[(t, "chase")][3] > 0
-        assert rows[(t, "resolved")][1] > 0 and rows[(t, "resolved")][2] > 0
+        for p in paths:
+            assert rows[(t, "resolved", p)][3] == 0
+            assert rows[(t, "chase", p)][3] > 0
+            assert rows[(t, "resolved", p)][1] > 0 and rows[(t, "resolved", p)][2] > 0
 
 
 def test_numa_binding_is_scoped():

@@ -26,12 +26,14 @@ for name, c in funcs.items():
         continue
     t = "float" if "IfLb" in name else "double"
     mode = "chase" if "Lb1" in name else "resolved"
+    pm = re.search(r"Lb[01]ELi(\d)E", name)
+    path = {"0": "tiles+groups", "1": "tiles", "2": "groups"}.get(pm.group(1), "?") if pm else "all"
     total = sum(c.values())
     chain = sum(v for k, v in c.items() if k.startswith("LDG") and "CONSTANT" in k)
     vec_ld = sum(v for k, v in c.items() if k.startswith("LDG") and "128" in k)
     vec_st = sum(v for k, v in c.items() if k.startswith("STG") and "128" in k)
-    rows.append((t, mode, total, vec_ld, vec_st, chain))
-print("| type | mode | static SASS instructions | LDG.128 | STG.128 | chain loads (LDG.*.CONSTANT) |")
-print("|---|---|---|---|---|---|")
+    rows.append((t, mode, path, total, vec_ld, vec_st, chain))
+print("| type | mode | work path | static SASS instructions | LDG.128 | STG.128 | chain loads (LDG.*.CONSTANT) |")
+print("|---|---|---|---|---|---|---|")
 for r in rows:
     print("| " + " | ".join(str(x) for x in r) + " |")

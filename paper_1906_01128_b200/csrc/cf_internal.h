@@ -72,16 +72,12 @@ constexpr uint64_t FAULT_INDEX_MASK = (1ull << FAULT_SHIFT) - 1;
 int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites,
                     uint64_t nsites, uint64_t from, uint64_t to, uint64_t* bad, cudaStream_t s,
                     const uint32_t* idx = nullptr, uint64_t tag = 0);
-// One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).  With tab_bytes != 0
-// the CTA first copies the window's table block (8-byte multiple) from tab_src (mapped pinned
-// host memory) to tab_dst, the device mirror every table pointer of the launch points into.
+// One-CTA attach + resolve for small site/target counts (see SMALL_FUSED).
 constexpr uint64_t SMALL_FUSED = 4096;
-constexpr uint64_t TAB_ZC_MAX = 16384;
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                          cudaStream_t s, uint64_t res_tag = 0, const void* tab_src = nullptr, void* tab_dst = nullptr,
-                          uint64_t tab_bytes = 0);
+                          cudaStream_t s, uint64_t res_tag = 0);
 // A resolve range whose targets are consecutive ordinals ord0, ord0 + 1, ... at one level >= 1 of a
 // single dense tree, owning their A field exactly when it is misaligned (own_misaligned): the
 // resolver derives level / ordinal / ownership instead of reading the tables.

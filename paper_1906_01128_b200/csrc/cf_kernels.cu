@@ -240,12 +240,7 @@ __global__ void __launch_bounds__(1024) k_attach_resolve(uint8_t* __restrict__ i
                                                          const int32_t* __restrict__ level,
                                                          const uint32_t* __restrict__ ordinal, uint64_t ntargets,
                                                          uint64_t* __restrict__ ea, uint32_t* __restrict__ count,
-                                                         uint64_t* bad, uint64_t res_tag, const uint64_t* tab_src,
-                                                         uint64_t* tab_dst, uint64_t tab_words) {
-  if (tab_words) {   // the window's tables, pulled from mapped host memory (no other reader yet)
-    for (uint64_t i = threadIdx.x; i < tab_words; i += blockDim.x) tab_dst[i] = tab_src[i];
-    __syncthreads();
-  }
+                                                         uint64_t* bad, uint64_t res_tag) {
   for (uint64_t i = threadIdx.x; i < nsites; i += blockDim.x) relocate_one(image, total, sites, i, from, to, bad);
   __syncthreads();
   for (uint64_t i0 = 0; i0 < ntargets; i0 += blockDim.x) {   // every lane runs every round (warp-collective walk)
@@ -1058,13 +1053,11 @@ int launch_relocate(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t*
 int launch_attach_resolve(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root, const int32_t* level,
                           const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea, uint32_t* count, uint64_t* bad,
-                          cudaStream_t s, uint64_t res_tag, const void* tab_src, void* tab_dst, uint64_t tab_bytes) {
-  if (nsites == 0 && ntargets == 0 && tab_bytes == 0) return CF_OK;
-  if (tab_bytes & 7) return fail(CF_E_INVALID, "table block must be a multiple of 8 bytes");
+                          cudaStream_t s, uint64_t res_tag) {
+  if (nsites == 0 && ntargets == 0) return CF_OK;
   const unsigned threads = unsigned(std::min<uint64_t>(1024, std::max<uint64_t>(32, ((std::max(nsites, ntargets) + 31) / 32) * 32)));
   k_attach_resolve<<<1, threads, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level, ordinal, ntargets,
-                                        ea, count, bad, res_tag, static_cast<const uint64_t*>(tab_src),
-                                        static_cast<uint64_t*>(tab_dst), tab_bytes / 8);
+                                        ea, count, bad, res_tag);
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

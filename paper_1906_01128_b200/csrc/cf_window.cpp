@@ -62,10 +62,6 @@ struct cf_window {
   uint64_t off_zc_h2d = 0, off_zc_d2h = 0;
   // one pinned table block and its device mirror
   uint8_t* h_tab = nullptr;
-  // small table blocks (<= TAB_ZC_MAX, step 0 attached + resolved by the one-CTA kernel): that
-  // kernel pulls the block from the mapped pinned host copy itself (PCIe loads by the SMs)
-  // instead of a separate DMA ahead of chunk 0 -- one copy-engine operation less per window
-  bool tab_zc = false;
   uint8_t* d_tab = nullptr;
   uint64_t tab_bytes = 0;
   uint64_t off_sites = 0, off_det = 0, off_level = 0, off_ord = 0, off_root = 0, off_parts = 0, off_tb = 0,
@@ -638,15 +634,6 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     sg.tile_base = reinterpret_cast<const uint64_t*>(w->d_tab + w->off_tb);
     sg.groups = reinterpret_cast<const uint32_t*>(w->d_tab + w->off_grp);
   }
-  {
-    void* dp = nullptr;
-    const bool tab_mapped = cudaHostGetDevicePointer(&dp, w->h_tab, 0) == cudaSuccess && dp == w->h_tab;
-    cudaGetLastError();
-    const uint64_t ns0 = w->reloc_lo[1] - w->reloc_lo[0], nr0 = w->res_lo[1] - w->res_lo[0];
-    static const bool env_off = [] { const char* v = getenv("CF_TAB_ZC"); return v && v[0] == '0'; }();
-    w->tab_zc = tab_mapped && !env_off && w->tab_bytes <= TAB_ZC_MAX && (fl & CF_WIN_TABLES) && (fl & CF_WIN_ATTACH) &&
-                (fl & CF_WIN_RESOLVE) && !chase && ns0 && nr0 && ns0 <= SMALL_FUSED && nr0 <= SMALL_FUSED;
-  }
   // the device mirror starts valid so runs without CF_WIN_TABLES work
   ce = cudaMemcpyAsync(w->d_tab, w->h_tab, w->tab_bytes, cudaMemcpyHostToDevice, ctx->compute);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->compute);
@@ -1100,9 +1087,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     for (auto s : c->h2d) CF_CUDA(cudaStreamWaitEvent(s, w->ev_start, 0));
     CF_CUDA(cudaStreamWaitEvent(c->d2h, w->ev_start, 0));
   }
-  if ((fl & CF_WIN_TABLES) && w->tab_zc) {
-    h2d_bytes += w->tab_bytes;   // pulled over the link by the step-0 attach kernel (tab_zc)
-  } else if (fl & CF_WIN_TABLES) {
+  if (fl & CF_WIN_TABLES) {
     // the relocation / chain tables travel with the arena, first on the H2D copy stream
     // (an H2D copy on the compute stream serialises badly against the D2H engine)
     cudaStream_t s0 = c->h2d[0];
@@ -1138,11 +1123,9 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     const uint64_t ns = w->reloc_lo[k + 1] - w->reloc_lo[k], nr = w->res_lo[k + 1] - w->res_lo[k];
     const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
     if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
-      const bool pull = k == 0 && (fl & CF_WIN_TABLES) && w->tab_zc;
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
                                    drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
-                                   w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE,
-                                   pull ? w->h_tab : nullptr, pull ? w->d_tab : nullptr, pull ? w->tab_bytes : 0));
+                                   w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
     } else if (do_attach && do_resolve && w->wide_ok) {
       CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,

@@ -282,7 +282,7 @@ int cf_checksum_ranges(cf_ctx* ctx, const uint64_t* h_addr, const uint64_t* h_by
 /* Per-object transfers (naive_deep_copy / naive_copy_back, memory.py:358-361, 368-372; batched
  * selective copies): objects under 64 KiB whose both ends are SM-addressable (device, managed
  * or mapped pinned memory) are copied by one zero-copy kernel, one warp per object; the rest
- * by the copy engines (cudaMemcpyBatchAsync).  Synchronous. */
+ * by the copy engines (one cudaMemcpyAsync per object).  Synchronous. */
 int cf_copy_objects(cf_ctx* ctx, void* const* dsts, const void* const* srcs, const uint64_t* sizes, uint64_t count);
 /* Bulk copy by the SMs (16-byte aligned; either end may be mapped pinned host memory), async on
  * `stream` (NULL: the context's compute stream); ctas 0 = 4 per SM.  Host-link experiments. */

@@ -316,27 +316,10 @@ int cf_memcpy_batch(cf_ctx* c, void* const* dsts, const void* const* srcs, const
   if (count == 0) return CF_OK;
   CfDevice g(c);
   cudaStream_t s = stream ? (cudaStream_t)stream : c->compute;
-  // cudaMemcpyBatchAsync (CUDA >= 12.8) submits the per-object copies of naive_deep_copy
-  // (memory.py:358-361) as one driver call; it rejects the legacy stream, so s is non-blocking.
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof attr);
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0;
-  const uint64_t BATCH = 1u << 16;
-  for (uint64_t b = 0; b < count; b += BATCH) {
-    uint64_t m = count - b < BATCH ? count - b : BATCH;
-    size_t fail_idx = 0;
-    cudaError_t e = cudaMemcpyBatchAsync(const_cast<void**>(dsts + b), const_cast<void**>(srcs + b),
-                                         const_cast<size_t*>(reinterpret_cast<const size_t*>(sizes + b)),
-                                         m, &attr, &attr_idx, 1, &fail_idx, s);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      // fall back to individual async copies (same semantics, more driver calls)
-      for (uint64_t i = b; i < b + m; ++i)
-        CF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));
-    }
-  }
+  // one cudaMemcpyAsync per object (naive_deep_copy, memory.py:358-361), all on one non-blocking
+  // stream; the driver's batched submission call is not used (it is closed on the GPU pool)
+  for (uint64_t i = 0; i < count; ++i)
+    CF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));
   return CF_OK;
 }
 

@@ -398,7 +398,7 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
 typedef struct {
   uint64_t nsteps, nsegments, nsites, ntargets, nparts, ngroups, ntiles, table_bytes, zero_copy_node_segments;
   int32_t violations;
-  int32_t reserved;
+  int32_t leaf_owned;   /* 1: the leaf kernel owns the targets' A-field relocation (one-step uniform windows) */
   double plan_ms;
 } cf_plan_check;
 int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out);

@@ -96,7 +96,7 @@ class CfWindowDesc(C.Structure):
 class CfPlanCheck(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("nsteps", "nsegments", "nsites", "ntargets", "nparts", "ngroups", "ntiles",
                                          "table_bytes", "zero_copy_node_segments")] + \
-        [("violations", C.c_int32), ("reserved", C.c_int32), ("plan_ms", C.c_double)]
+        [("violations", C.c_int32), ("leaf_owned", C.c_int32), ("plan_ms", C.c_double)]
 
 
 class CfWindowStats(C.Structure):

@@ -85,6 +85,20 @@ struct UniTargets {
   uint32_t on, level, ord0, own_misaligned;
   uint64_t qmagic;   // floor((2^64 - 1) / q) + 1: n / q == __umul64hi(n, qmagic) for every u32 n (q >= 2)
 };
+// Leaf-owned relocation (one-step windows over a uniform range of dense leaf targets, RESOLVED
+// mode, small equal parts): the leaf kernel's group warps find each target's leaf record from its
+// parent's child block (parent table filled by k_attach_parents), attach the record's A field,
+// stream the array and detach the field again -- no per-target EA table, no per-leaf sites in the
+// attach / detach lists.  Part p of the step is target position p, elements [0, n_el); group g
+// holds parts [g gp, min((g + 1) gp, nt)).
+struct LeafOwn {
+  const uint64_t* parent;   // device: child block of parent ordinal p_first + p (0 = broken chain)
+  uint32_t on, level, o0, p_first, nparents, n_el, gp, nt;
+  uint64_t qmagic, from, to, total;
+};
+int launch_attach_parents(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const LeafOwn& own, uint64_t* parent,
+                          uint64_t* bad, cudaStream_t s);
 // Attach and resolve side by side in one launch (8-byte aligned pointer fields only).
 int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
@@ -107,7 +121,8 @@ struct RelocArgs {
 int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf_chain_shape& sh,
                  const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count, const cf_scale_work& work, double scale, uint64_t* bad,
-                 cudaStream_t s, const RelocArgs* fused_reloc = nullptr, uint64_t tag = 0);
+                 cudaStream_t s, const RelocArgs* fused_reloc = nullptr, uint64_t tag = 0, bool pdl = false,
+                 const LeafOwn* own = nullptr);
 int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* target_host,
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);

@@ -29,6 +29,7 @@
 #include "cf_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 // tuning knobs (design experiments: tools/build_variants.sh)
@@ -141,6 +142,12 @@ __device__ __forceinline__ uint64_t xlate(uint64_t v, uint64_t from, const uint8
   return (from && v - from < bytes) ? reinterpret_cast<uint64_t>(image) + (v - from) : v;
 }
 
+// A record of `size` bytes at address `next` lies wholly inside the image (a corrupted chain link
+// is reported, never followed past the image's end).
+__device__ __forceinline__ bool rec_inside(uint64_t next, const uint8_t* image, uint64_t bytes, uint64_t size) {
+  return bytes >= size && next - reinterpret_cast<uint64_t>(image) <= bytes - size;
+}
+
 template <bool CHASE>
 __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_shape& sh, uint64_t root_off,
                                            int level, uint64_t ordinal, uint64_t xlate_from = 0) {
@@ -164,7 +171,8 @@ __device__ __forceinline__ Walk walk_chain(const uint8_t* image, const cf_chain_
       qpow = qpow > 1 ? qpow / sh.q : 1;
     }
     const uint64_t next = blk + digit * child;
-    if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+    if (!rec_inside(next, image, sh.image_bytes, (dense && l == sh.depth) ? LEAF_NODE_SIZE : NODE_SIZE))
+      return {nullptr, false};
     p = reinterpret_cast<const uint8_t*>(next);
   }
   return {p, dense && level == sh.depth};
@@ -206,7 +214,8 @@ __device__ __forceinline__ Walk walk_chain_coop(const uint8_t* image, const cf_c
   if (!ok) return {nullptr, false};
   const uint64_t child = dense ? ((level < sh.depth) ? NODE_SIZE : LEAF_NODE_SIZE) : 0;
   const uint64_t next = blk + uint64_t(rem - parent * q) * child;
-  if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+  if (!rec_inside(next, image, sh.image_bytes, (dense && level == sh.depth) ? LEAF_NODE_SIZE : NODE_SIZE))
+    return {nullptr, false};
   return {reinterpret_cast<const uint8_t*>(next), dense && level == sh.depth};
 }
 
@@ -292,7 +301,7 @@ __device__ __forceinline__ Walk walk_uniform(const uint8_t* image, const cf_chai
   if (!ok) return {nullptr, false};
   const bool leaf = int(u.level) == int(sh.depth);
   const uint64_t next = blk + uint64_t(j) * (leaf ? LEAF_NODE_SIZE : NODE_SIZE);
-  if (next - reinterpret_cast<uint64_t>(image) >= sh.image_bytes) return {nullptr, false};
+  if (!rec_inside(next, image, sh.image_bytes, leaf ? LEAF_NODE_SIZE : NODE_SIZE)) return {nullptr, false};
   return {reinterpret_cast<const uint8_t*>(next), leaf};
 }
 
@@ -373,6 +382,141 @@ __global__ void __launch_bounds__(256) k_attach_resolve_wide(uint8_t* __restrict
   count[i] = ld_u32_any(w.node + OFF_NA);
 }
 
+// Uniform resolve range (C4: 1M consecutive leaf ordinals) with memory-level parallelism: each
+// warp takes a run of 32 x U consecutive targets.  Their parents are a handful of consecutive
+// ordinals one level up; lane j walks parent p_first + j (all in parallel, the upper hops are L2
+// hits), then every lane issues the U leaf-record loads of its targets back to back (independent,
+// coalesced: consecutive records), owned A fields are attached, and the EA / count entries are
+// stored.  The whole 1M-chain pass fits in about one wave with ~L + 1 dependent rounds per warp,
+// against ~5 waves of one chain per thread (k_attach_resolve_wide's uniform branch).  Results are
+// identical to walk_uniform's.  CTAs [0, att_blocks) relocate the other sites, as in the wide
+// kernel.  The launch lets the next kernel (the leaf kernel) start its prologue early
+// (programmatic dependent launch); that kernel waits for this grid's completion before reading.
+constexpr int UNI_U = 8;
+__global__ void __launch_bounds__(256) k_attach_resolve_uni(uint8_t* __restrict__ image, uint64_t total,
+                                                            const uint64_t* __restrict__ sites, uint64_t nsites,
+                                                            uint64_t from, uint64_t to, cf_chain_shape sh,
+                                                            uint64_t ntargets, uint64_t* __restrict__ ea,
+                                                            uint32_t* __restrict__ count, uint64_t* bad,
+                                                            unsigned att_blocks, uint64_t res_tag, UniTargets uni,
+                                                            unsigned per_warp_u) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (blockIdx.x < att_blocks) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < nsites) relocate_one(image, total, sites, i, from, to, bad);
+    return;
+  }
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned U = per_warp_u;   // 32 U targets per warp, chosen so the run's parents fit 32 lanes
+  const uint64_t wg = uint64_t(blockIdx.x - att_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t i0 = wg * 32 * U;
+  if (i0 >= ntargets) return;   // warp-uniform
+  const uint32_t q = sh.q;
+  const uint32_t o_first = uni.ord0 + uint32_t(i0);
+  const uint64_t rest = ntargets - i0;
+  const uint32_t n_here = uint32_t(rest < uint64_t(32) * U ? rest : uint64_t(32) * U);
+  auto divq = [&](uint32_t o) -> uint32_t { return q > 1 ? uint32_t(__umul64hi(uint64_t(o), uni.qmagic)) : o; };
+  const uint32_t p_first = divq(o_first), p_last = divq(o_first + n_here - 1);
+  // parents: lane j walks p_first + j
+  uint64_t blk = 0;
+  int ok = 1;
+  if (lane <= p_last - p_first) {
+    const Walk pw = walk_chain<false>(image, sh, sh.root_off, int(uni.level) - 1, p_first + lane, from);
+    if (pw.node == nullptr || pw.leaf) ok = 0;
+    else blk = xlate(ld_u64_any(pw.node + OFF_LNEXT), from, image, sh.image_bytes);
+  }
+  const bool leaf = int(uni.level) == int(sh.depth);
+  const uint64_t child = leaf ? LEAF_NODE_SIZE : NODE_SIZE;
+  const uint32_t off_a = leaf ? LEAF_OFF_A : OFF_A;
+  const uint64_t img = reinterpret_cast<uint64_t>(image);
+  uint32_t* fa[UNI_U];
+  uint64_t v[UNI_U];
+  uint32_t cnt[UNI_U];
+  unsigned good = 0;   // bit u: target u of this lane has a record inside the image
+#pragma unroll
+  for (int u = 0; u < UNI_U; ++u) {
+    fa[u] = nullptr;
+    v[u] = 0;
+    cnt[u] = 0;
+    if (unsigned(u) >= U) continue;   // warp-uniform
+    const uint32_t k = uint32_t(u) * 32 + lane;
+    const uint32_t ord = o_first + k;
+    const uint32_t par = divq(ord);
+    const unsigned src = min(par - p_first, 31u);
+    const uint64_t b = __shfl_sync(0xffffffffu, blk, src);
+    const int pok = __shfl_sync(0xffffffffu, ok, src);
+    if (k >= n_here) continue;
+    const uint64_t rec = b + uint64_t(ord - par * q) * child;
+    if (!pok || !rec_inside(rec, image, sh.image_bytes, child)) continue;
+    fa[u] = reinterpret_cast<uint32_t*>(rec + off_a);
+    good |= 1u << u;
+  }
+  // the U record loads of every lane, back to back (A: one 64-bit load when 8-byte aligned -- an
+  // attach CTA may be rewriting it -- else 2 x u32 of an owned field)
+#pragma unroll
+  for (int u = 0; u < UNI_U; ++u) {
+    if (!(good >> u & 1)) continue;
+    const bool mis = (reinterpret_cast<uintptr_t>(fa[u]) & 7) != 0;
+    v[u] = mis ? (uint64_t(fa[u][0]) | (uint64_t(fa[u][1]) << 32)) : *reinterpret_cast<const uint64_t*>(fa[u]);
+    cnt[u] = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(fa[u]) - off_a + OFF_NA);
+  }
+#pragma unroll
+  for (int u = 0; u < UNI_U; ++u) {
+    const uint64_t k = uint64_t(u) * 32 + lane;
+    if (unsigned(u) >= U || k >= n_here) continue;
+    const uint64_t i = i0 + k;
+    if (!(good >> u & 1)) {
+      ea[i] = 0;
+      count[i] = 0;
+      raise_bad(bad, i | res_tag);
+      continue;
+    }
+    uint64_t x = v[u];
+    if (uni.own_misaligned && (reinterpret_cast<uintptr_t>(fa[u]) & 7) != 0) {   // owned field: attach it here
+      const uint64_t dlt = x - from;
+      if (dlt >= total) {
+        ea[i] = 0;
+        count[i] = 0;
+        raise_bad(bad, i);
+        continue;
+      }
+      x = to + dlt;
+      fa[u][0] = uint32_t(x);
+      fa[u][1] = uint32_t(x >> 32);
+    }
+    ea[i] = xlate(x, from, image, sh.image_bytes);
+    count[i] = cnt[u];
+  }
+}
+
+// Leaf-owned windows: CTAs [0, att_blocks) attach the step's non-owned sites (node-level pointer
+// fields); the rest resolve each parent of the target range once -- walk to parent ordinal
+// p_first + p at level L - 1 and store its child block (translated: an attach CTA may not have
+// rewritten the field yet), 0 on a broken chain (fault index: the parent's first target).
+__global__ void __launch_bounds__(256) k_attach_parents(uint8_t* __restrict__ image, uint64_t total,
+                                                        const uint64_t* __restrict__ sites, uint64_t nsites,
+                                                        uint64_t from, uint64_t to, cf_chain_shape sh, LeafOwn own,
+                                                        uint64_t* __restrict__ parent, uint64_t* bad,
+                                                        unsigned att_blocks) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (blockIdx.x < att_blocks) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < nsites) relocate_one(image, total, sites, i, from, to, bad);
+    return;
+  }
+  const uint64_t p = uint64_t(blockIdx.x - att_blocks) * blockDim.x + threadIdx.x;
+  if (p >= own.nparents) return;
+  const uint32_t pord = own.p_first + uint32_t(p);
+  const Walk pw = walk_chain<false>(image, sh, sh.root_off, int(own.level) - 1, pord, from);
+  uint64_t blk = 0;
+  if (pw.node != nullptr && !pw.leaf) blk = xlate(ld_u64_any(pw.node + OFF_LNEXT), from, image, sh.image_bytes);
+  parent[p] = blk;
+  if (blk == 0) {
+    const uint64_t first = uint64_t(pord) * sh.q;
+    raise_bad(bad, (first > own.o0 ? first - own.o0 : 0) | FAULT_RESOLVE);
+  }
+}
+
 // ---------------------------------------------------------------- leaf kernel
 template <typename T> struct Vec;
 template <> struct Vec<float> {
@@ -428,7 +572,34 @@ struct ScaleArgs {
   uint64_t* bad;
   uint64_t tag;      // fault tag of the leaf kernel's own checks
   RelocArgs reloc;   // optional fused relocation (reloc.n == 0: none)
+  unsigned reloc_blocks;   // CTAs k * reloc_stride (k < reloc_blocks) run it, RELOC_U sites per thread
+  unsigned reloc_stride;
+  LeafOwn own;             // PATH_OWNED launches
 };
+
+// Fused relocation: RELOC_U sites per thread, each level of the idx -> site -> field chain issued
+// for all of them before the next (independent loads in flight), same checks and fault indices
+// as relocate_one.
+constexpr int RELOC_U = 4;
+__device__ __forceinline__ void relocate_multi(const RelocArgs& r, uint64_t base, uint64_t* bad) {
+  uint64_t st[RELOC_U], v[RELOC_U];
+#pragma unroll
+  for (int u = 0; u < RELOC_U; ++u) {
+    const uint64_t i = base + uint64_t(u) * SCALE_THREADS;
+    st[u] = i < r.n ? (r.idx ? r.sites[r.idx[i]] : r.sites[i]) : ~0ull;
+  }
+#pragma unroll
+  for (int u = 0; u < RELOC_U; ++u)
+    v[u] = (st[u] != ~0ull && st[u] + 8 <= r.total) ? ld_u64_any(r.image + st[u]) : 0;
+#pragma unroll
+  for (int u = 0; u < RELOC_U; ++u) {
+    const uint64_t i = base + uint64_t(u) * SCALE_THREADS;
+    if (i >= r.n) continue;
+    const uint64_t d = v[u] - r.from;   // wraps when v < from
+    if (st[u] + 8 > r.total || d >= r.total) { raise_bad(bad, i | r.tag); continue; }
+    st_u64_any(r.image + st[u], r.to + d);
+  }
+}
 
 // Array base + element count of target t: from the resolved table, or re-walked (CHASE).
 template <typename T, bool CHASE>
@@ -785,22 +956,155 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
   }
 }
 
-// One CTA per unit of work: blocks [0, ntiles) take one 16 KiB tile of a big part,
-// blocks [ntiles, ntiles + ngroups) take one group of small parts, one warp per part, and the
-// rest relocate (a detach riding in the launch).  PATH specialises the kernel for launches with
+// Leaf-owned group (LeafOwn): warp w owns parts g gp + w, + 8, ... (<= 4).  Lanes 0..3 find
+// their part's leaf record in its parent's child block (parent table: an L2 hit), read the
+// record's nA and A (one dependent DRAM round -- against groups -> parts -> EA table for the
+// table-driven group), attach A (device address written into the record, memory.py:316-323),
+// and check the span like target_array; the warp streams the parts' vectors as scale_group_warp
+// does, then the owners write the host value back (detach, memory.py:337-344).  Fault tags:
+// broken chain -> resolve, A outside the arena -> attach, span -> scale.
+template <typename T>
+__device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g, T s) {
+  using VT = Vec<T>;
+  using V = typename VT::V;
+  constexpr uint64_t VN = VT::N;
+  constexpr unsigned WARPS = SCALE_THREADS / 32;
+  constexpr unsigned PER = (GROUP_PARTS + WARPS - 1) / WARPS;
+  const LeafOwn& o = a.own;
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t q = a.sh.q;
+  const bool leaf = int(o.level) == int(a.sh.depth);
+  const uint64_t child = leaf ? LEAF_NODE_SIZE : NODE_SIZE;
+  const uint32_t off_a = leaf ? LEAF_OFF_A : OFF_A;
+  uint8_t* base = nullptr;   // attached array base (device), nullptr: nothing to stream
+  uint32_t* fa = nullptr;    // the record's A field, attached by this lane
+  uint64_t hv = 0, v0 = 0;
+  uint32_t nv = 0;
+  const uint32_t slot = warp + WARPS * lane;
+  const uint64_t pj = g * o.gp + slot;
+  if (lane < PER && slot < o.gp && pj < o.nt) {
+    const uint32_t ord = o.o0 + uint32_t(pj);
+    const uint32_t par = q > 1 ? uint32_t(__umul64hi(uint64_t(ord), o.qmagic)) : ord;
+    const uint64_t blk = o.parent[par - o.p_first];
+    const uint64_t rec = blk + uint64_t(ord - par * q) * child;
+    if (blk == 0 || !rec_inside(rec, a.image, a.sh.image_bytes, child)) {
+      raise_bad(a.bad, pj | FAULT_RESOLVE);
+    } else {
+      uint32_t* f = reinterpret_cast<uint32_t*>(rec + off_a);
+      const bool mis = (reinterpret_cast<uintptr_t>(f) & 7) != 0;
+      hv = mis ? (uint64_t(f[0]) | (uint64_t(f[1]) << 32)) : *reinterpret_cast<const uint64_t*>(f);
+      const uint64_t cnt = *reinterpret_cast<const uint32_t*>(rec + OFF_NA);
+      const uint64_t d = hv - o.from;
+      if (d >= o.total) {
+        raise_bad(a.bad, pj | FAULT_ATTACH);
+      } else {
+        const uint64_t dv = o.to + d;
+        if (mis) { f[0] = uint32_t(dv); f[1] = uint32_t(dv >> 32); }
+        else *reinterpret_cast<uint64_t*>(f) = dv;
+        fa = f;
+        uint8_t* arr = reinterpret_cast<uint8_t*>(dv);
+        if (uint64_t(o.n_el) > cnt || arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes ||
+            cnt * sizeof(T) > a.sh.image_bytes - uint64_t(arr - a.image)) {
+          raise_bad(a.bad, pj | FAULT_SCALE);
+        } else {
+          base = arr;
+          const uintptr_t first = reinterpret_cast<uintptr_t>(arr);
+          v0 = o.n_el;
+          if ((first % sizeof(T)) == 0) v0 = min(uint64_t(o.n_el), uint64_t(((16 - (first & 15)) & 15) / sizeof(T)));
+          nv = uint32_t((o.n_el - v0) / VN);
+        }
+      }
+    }
+  }
+  uint32_t pre[PER + 1];
+  pre[0] = 0;
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
+  uint8_t* bj[PER];
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j)
+    bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
+  const uint32_t total = pre[PER];
+  auto vptr = [&](uint32_t f) -> V* {
+    unsigned j = 0;
+#pragma unroll
+    for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
+    uint8_t* b = bj[0];
+    uint32_t off = pre[0];
+#pragma unroll
+    for (unsigned k = 1; k < PER; ++k)
+      if (j == k) { b = bj[k]; off = pre[k]; }
+    return reinterpret_cast<V*>(b) + (f - off);
+  };
+  constexpr int U = 4;
+  uint32_t f = lane;
+  for (; f + (U - 1) * 32 < total; f += U * 32) {
+    V r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = VT::ld(vptr(f + u * 32));
+#pragma unroll
+    for (int u = 0; u < U; ++u) VT::st(vptr(f + u * 32), VT::mul(r[u], s));
+  }
+  for (; f < total; f += 32) {
+    V* p = vptr(f);
+    VT::st(p, VT::mul(VT::ld(p), s));
+  }
+  // scalar heads / tails (packed layouts only)
+#pragma unroll
+  for (unsigned j = 0; j < PER; ++j) {
+    uint8_t* arr = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base), j));
+    const uint64_t vj0 = __shfl_sync(0xffffffffu, v0, j);
+    if (arr == nullptr) continue;
+    const uint64_t vj1 = vj0 + uint64_t(pre[j + 1] - pre[j]) * VN;
+    for (uint64_t i = lane; i < vj0; i += 32)
+      scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+    for (uint64_t i = vj1 + lane; i < o.n_el; i += 32)
+      scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
+  }
+  // detach: the host value back into the record
+  if (fa) {
+    if ((reinterpret_cast<uintptr_t>(fa) & 7) != 0) { fa[0] = uint32_t(hv); fa[1] = uint32_t(hv >> 32); }
+    else *reinterpret_cast<uint64_t*>(fa) = hv;
+  }
+}
+
+// One CTA per unit of work: after the fused relocation CTAs (a detach riding in the launch),
+// one 16 KiB tile of a big part per CTA, then one group of small parts per CTA (one warp per
+// part).  PATH specialises the kernel for launches with
 // only tiles or only groups (the common cases: C2 / C4), so each gets its own register budget
 // under the 6-CTA/SM launch bound instead of the union of both paths' (no spills).
-enum { PATH_ALL = 0, PATH_TILES = 1, PATH_GROUPS = 2 };
+enum { PATH_ALL = 0, PATH_TILES = 1, PATH_GROUPS = 2, PATH_OWNED = 3 };
 template <typename T, bool CHASE, int PATH>
-__global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_GROUPS ? CF_GROUP_MINB : CF_SCALE_MINB)
+__global__ void __launch_bounds__(SCALE_THREADS, (PATH == PATH_GROUPS || PATH == PATH_OWNED) ? CF_GROUP_MINB : CF_SCALE_MINB)
     k_scale(ScaleArgs a, T s) {
+  // launched as a programmatic dependent of the attach / resolve kernel: its CTAs may be resident
+  // before that grid has finished -- wait for its completion (and memory) before any read
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
+  // fused relocation CTAs (the detach riding in the launch) are spread evenly through the grid --
+  // CTA k * reloc_stride is relocation CTA k: in RESOLVED mode no leaf CTA reads a pointer field
+  // and every resolver that reads them has completed (stream order / griddepcontrol.wait), so the
+  // latency-bound relocation overlaps the streaming instead of forming a wave of its own (first)
+  // or trailing the drain (last)
+  unsigned b = blockIdx.x;
+  if (a.reloc_blocks) {
+    const unsigned k = b / a.reloc_stride;
+    if (b % a.reloc_stride == 0 && k < a.reloc_blocks) {
+      relocate_multi(a.reloc, uint64_t(k) * (SCALE_THREADS * RELOC_U) + threadIdx.x, a.bad);
+      return;
+    }
+    b -= min(k + 1, a.reloc_blocks);
+  }
+  if constexpr (PATH == PATH_OWNED) {
+    scale_group_owned<T>(a, b, s);
+    return;
+  }
   const uint64_t ntiles = a.w.tile_end - a.w.tile_begin;
-  if (PATH != PATH_GROUPS && blockIdx.x < ntiles) {
+  if (PATH != PATH_GROUPS && b < ntiles) {
     // lane 0 of every warp maps the tile to its part (binary search over the launch's first-tile
     // table) and reads the part and its resolved address; the warp gets them by shuffle -- one
     // search and one metadata load per warp instead of per thread
-    const uint64_t tile = a.w.tile_begin + blockIdx.x;
+    const uint64_t tile = a.w.tile_begin + b;
     const unsigned lane = threadIdx.x & 31;
     uint64_t t = 0, e0 = 0, e1 = 0, cnt = 0;
     uintptr_t arr_u = 0;
@@ -829,17 +1133,8 @@ __global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_GROUPS ? CF_GROUP_
     scale_range<T, CHASE, SCALE_UNROLL>(a, t, reinterpret_cast<uint8_t*>(arr_u), e0, e1, s, threadIdx.x, SCALE_THREADS);
     return;
   }
-  const uint64_t ngroups = a.w.group_end - a.w.group_begin;
-  if (blockIdx.x >= ntiles + ngroups) {
-    // fused relocation CTAs (detach riding in the leaf-kernel launch)
-    const uint64_t i = (blockIdx.x - ntiles - ngroups) * uint64_t(SCALE_THREADS) + threadIdx.x;
-    if (i < a.reloc.n)
-      relocate_one(a.reloc.image, a.reloc.total, a.reloc.sites, i, a.reloc.from, a.reloc.to, a.bad, a.reloc.idx,
-                   a.reloc.tag);
-    return;
-  }
   if constexpr (PATH != PATH_TILES) {
-    const uint64_t g = a.w.group_begin + (blockIdx.x - ntiles);
+    const uint64_t g = a.w.group_begin + (b - ntiles);
 #if CF_GROUP_WARP
     scale_group_warp<T, CHASE>(a, g, s);
 #else
@@ -1066,12 +1361,38 @@ int launch_attach_resolve_wide(cf_ctx* ctx, uint8_t* image, uint64_t total, cons
                                uint64_t from, uint64_t to, const cf_chain_shape& sh, const uint64_t* root,
                                const int32_t* level, const uint32_t* ordinal, uint64_t ntargets, uint64_t* ea,
                                uint32_t* count, uint64_t* bad, cudaStream_t s, uint64_t res_tag, const UniTargets* uni) {
-  const uint64_t ab = (nsites + 255) / 256, rb = (ntargets + 255) / 256;
+  const uint64_t ab = (nsites + 255) / 256;
+  if (uni && uni->on && sh.q >= 2 && ntargets) {
+    // memory-parallel uniform resolver: 32 U targets per warp, U as large as lets the run's
+    // parents (at most (32 U - 1) / q + 2 of them) fit one lane each
+    static const int u_env = getenv("CF_UNI_U") ? atoi(getenv("CF_UNI_U")) : UNI_U;   // design experiments
+    unsigned U = unsigned(std::max(1, std::min(UNI_U, u_env)));
+    while (U > 1 && (32 * U - 1) / sh.q + 2 > 32) U >>= 1;
+    const uint64_t per_cta = uint64_t(32) * U * 8;
+    const uint64_t rb = (ntargets + per_cta - 1) / per_cta;
+    if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
+    k_attach_resolve_uni<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, ntargets, ea, count,
+                                                          bad, unsigned(ab), res_tag, *uni, U);
+    CF_LAUNCHED(ctx);
+    return CF_OK;
+  }
+  const uint64_t rb = (ntargets + 255) / 256;
   if (ab + rb == 0) return CF_OK;
   if (ab + rb > 0x7FFFFFFFull) return fail(CF_E_INVALID, "attach/resolve grid too large");
   k_attach_resolve_wide<<<unsigned(ab + rb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, root, level,
                                                          ordinal, ntargets, ea, count, bad, unsigned(ab), res_tag,
                                                          uni ? *uni : UniTargets{0, 0, 0, 0, 0});
+  CF_LAUNCHED(ctx);
+  return CF_OK;
+}
+
+int launch_attach_parents(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
+                          uint64_t from, uint64_t to, const cf_chain_shape& sh, const LeafOwn& own, uint64_t* parent,
+                          uint64_t* bad, cudaStream_t s) {
+  const uint64_t ab = (nsites + 255) / 256, pb = (uint64_t(own.nparents) + 255) / 256;
+  if (ab + pb == 0) return CF_OK;
+  k_attach_parents<<<unsigned(ab + pb), 256, 0, s>>>(image, total, sites, nsites, from, to, sh, own, parent, bad,
+                                                     unsigned(ab));
   CF_LAUNCHED(ctx);
   return CF_OK;
 }
@@ -1089,28 +1410,52 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
                  const uint64_t* root, const int32_t* level, const uint32_t* ordinal, const uint64_t* ea,
                  const uint32_t* count,
                  const cf_scale_work& work, double scale, uint64_t* bad, cudaStream_t s,
-                 const RelocArgs* fused_reloc, uint64_t tag) {
+                 const RelocArgs* fused_reloc, uint64_t tag, bool pdl, const LeafOwn* own) {
   const uint64_t nreloc = fused_reloc ? fused_reloc->n : 0;
-  const uint64_t units = (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin) +
-                         (nreloc + SCALE_THREADS - 1) / SCALE_THREADS;
+  const uint64_t rblocks = (nreloc + SCALE_THREADS * RELOC_U - 1) / (SCALE_THREADS * RELOC_U);
+  const uint64_t owned_groups = own ? (uint64_t(own->nt) + own->gp - 1) / own->gp : 0;
+  const uint64_t units = own ? owned_groups + rblocks
+                             : (work.tile_end - work.tile_begin) + (work.group_end - work.group_begin) + rblocks;
   if (units == 0) return CF_OK;
   if (units > 0x7FFFFFFFull) return fail(CF_E_INVALID, "leaf kernel: %llu work units exceed one grid",
                                          (unsigned long long)units);
-  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, tag, RelocArgs{}};
+  static const bool reloc_first = getenv("CF_RELOC_FIRST") != nullptr;   // design experiments
+  const unsigned stride = (rblocks == 0 || reloc_first) ? 1u : unsigned(units / rblocks);
+  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, tag, RelocArgs{}, unsigned(rblocks), stride, LeafOwn{}};
   if (nreloc) a.reloc = *fused_reloc;
+  if (own) {
+    if (mode == CF_MODE_CHASE) return fail(CF_E_INVALID, "leaf-owned relocation needs RESOLVED mode");
+    a.own = *own;
+  }
   // one CTA per 16 KiB tile / small-part group: measured faster than a persistent grid-stride
   // grid on B200 (tools/scale_variants.cu: 6.7 vs 5.8 TB/s over the C2 shape) -- the hardware
   // CTA launcher keeps more independent loads in flight than a loop re-locating its part
   const unsigned grid = unsigned(units);
   const bool tiles = work.tile_end > work.tile_begin, groups = work.group_end > work.group_begin;
-  const int path = (tiles && groups) ? PATH_ALL : (groups ? PATH_GROUPS : PATH_TILES);
+  const int path = own ? PATH_OWNED : (tiles && groups) ? PATH_ALL : (groups ? PATH_GROUPS : PATH_TILES);
+  // pdl: the previous kernel on s is the attach / resolve launch -- let this grid launch as its
+  // programmatic dependent (k_scale waits for it with griddepcontrol.wait)
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(SCALE_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t le = cudaSuccess;
   auto go = [&](auto tag_t, auto tag_chase) {
     using T = decltype(tag_t);
     constexpr bool C = decltype(tag_chase)::value;
     const T sc = T(scale);
-    if (path == PATH_TILES) k_scale<T, C, PATH_TILES><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
-    else if (path == PATH_GROUPS) k_scale<T, C, PATH_GROUPS><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
-    else k_scale<T, C, PATH_ALL><<<grid, SCALE_THREADS, 0, s>>>(a, sc);
+    if constexpr (!C) {
+      if (path == PATH_OWNED) { le = cudaLaunchKernelEx(&cfg, k_scale<T, false, PATH_OWNED>, a, sc); return; }
+    }
+    if (path == PATH_TILES) le = cudaLaunchKernelEx(&cfg, k_scale<T, C, PATH_TILES>, a, sc);
+    else if (path == PATH_GROUPS) le = cudaLaunchKernelEx(&cfg, k_scale<T, C, PATH_GROUPS>, a, sc);
+    else le = cudaLaunchKernelEx(&cfg, k_scale<T, C, PATH_ALL>, a, sc);
   };
   if (elem == 4) {
     if (mode == CF_MODE_CHASE) go(float{}, std::true_type{});
@@ -1119,6 +1464,7 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
     if (mode == CF_MODE_CHASE) go(double{}, std::true_type{});
     else go(double{}, std::false_type{});
   }
+  if (le != cudaSuccess) return fail(CF_E_CUDA, "leaf kernel launch: %s", cudaGetErrorString(le));
   CF_LAUNCHED(ctx);
   return CF_OK;
 }

@@ -51,6 +51,13 @@ struct cf_window {
   bool owned_attach = false;
   std::vector<uint64_t> res_lo;        // resolve-target ranges per step
   std::vector<UniTargets> uni;         // per step: the resolve range is uniform (no table reads)
+  // leaf-owned relocation (LeafOwn; one-step windows): the leaf kernel attaches / detaches every
+  // target's A field itself; those sites trail step 0's attach list (after attach_n[0]) and its
+  // detach list (after det_keep0), so runs without all four device phases still use the full lists
+  bool leaf_own = false;
+  LeafOwn own{};
+  uint64_t det_keep0 = 0;
+  uint64_t* d_parent = nullptr;
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step
   std::vector<std::vector<uint32_t>> released;  // segments whose copy-back may start after step k
@@ -140,6 +147,7 @@ void destroy(cf_window* w) {
   if (w->d_tab) cudaFree(w->d_tab);
   if (w->d_ea) cudaFree(w->d_ea);
   if (w->d_count) cudaFree(w->d_count);
+  if (w->d_parent) cudaFree(w->d_parent);
   for (auto e : w->ev_h2d) cudaEventDestroy(e);
   for (auto e : w->ev_rel) cudaEventDestroy(e);
   for (auto e : w->ev_k0) cudaEventDestroy(e);
@@ -526,6 +534,38 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     w->seg[c] = sw.append(tri);
   }
   mark("o:work");
+  // ---- leaf-owned relocation: one step, RESOLVED, one dense tree, the targets a uniform range of
+  //      leaf records whose parts are whole, equal, small arrays in target order (C4)
+  static const bool no_leaf_own = getenv("CF_NO_LEAF_OWN") != nullptr;   // A/B switch (design experiments)
+  if (!no_leaf_own && nch == 1 && dense && !chase && w->wide_ok && t->tree_root.size() <= 1 && q >= 2 && nt > 0 &&
+      nt < (1ull << 31) && w->uni[0].on && int(w->uni[0].level) == int(t->spec.depth) && w->res_lo[1] == nt) {
+    const cf_scale_work& s0 = w->seg[0];
+    bool ok = s0.tile_end == s0.tile_begin && sw.nparts() == nt && sw.ngroups() > 0;
+    const uint64_t n_el = ok ? sw.parts[2] : 0, gp = ok ? uint64_t(sw.groups[1]) - sw.groups[0] : 0;
+    ok = ok && n_el > 0 && gp >= 1 && gp <= GROUP_PARTS && n_el < (1ull << 32) && sw.ngroups() == (nt + gp - 1) / gp;
+    for (uint64_t p2 = 0; p2 < nt && ok; ++p2) ok = sw.parts[3 * p2] == p2 && sw.parts[3 * p2 + 1] == 0 && sw.parts[3 * p2 + 2] == n_el;
+    for (uint64_t g = 0; g < sw.ngroups() && ok; ++g)
+      ok = sw.groups[2 * g] == g * gp && sw.groups[2 * g + 1] == std::min(nt, (g + 1) * gp);
+    if (ok) {
+      // every target's A field is owned: step 0's sites = the attach CTAs' share, then the owned tail
+      std::vector<uint64_t> fas(nt);
+      for (uint64_t i = 0; i < nt; ++i) fas[i] = t->arr_owner[desc->h_targets[i]] + LEAF_OFF_A;
+      std::sort(fas.begin(), fas.end());
+      std::vector<uint64_t> keep, own;
+      for (uint64_t r = 0; r < nsites; ++r) (std::binary_search(fas.begin(), fas.end(), reloc[r]) ? own : keep).push_back(reloc[r]);
+      ok = own.size() == nt;
+      if (ok) {
+        std::copy(keep.begin(), keep.end(), reloc.begin());
+        std::copy(own.begin(), own.end(), reloc.begin() + keep.size());
+        w->attach_n[0] = keep.size();
+        std::fill(owned_target.begin(), owned_target.end(), uint8_t(1));
+        w->leaf_own = true;
+        const uint32_t o0 = w->uni[0].ord0;
+        w->own = LeafOwn{nullptr, 1u, w->uni[0].level, o0, uint32_t(o0 / q), uint32_t((o0 + nt - 1) / q - o0 / q + 1),
+                         uint32_t(n_el), uint32_t(gp), uint32_t(nt), w->uni[0].qmagic, 0, 0, 0};
+      }
+    }
+  }
   // detach order: positions in the (step-ordered) relocation table, grouped by release step
   std::vector<uint32_t> det(nsites);
   {
@@ -534,6 +574,10 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     for (int64_t k = 0; k < int64_t(nsites); ++k) srel[k] = release[six.at(reloc[k])];
     bucket_order(srel, nch, sidx, w->det_lo);
     for (uint64_t k = 0; k < nsites; ++k) det[k] = uint32_t(sidx[k]);
+    if (w->leaf_own) {   // one step: the non-owned sites first, the owned tail last
+      std::stable_partition(det.begin(), det.end(), [&](uint32_t r) { return r < w->attach_n[0]; });
+      w->det_keep0 = w->attach_n[0];
+    }
   }
   mark("orders");
   w->released.assign(nch, {});
@@ -609,6 +653,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_count, std::max<uint64_t>(nt, 1) * 4);
+  if (ce == cudaSuccess && w->leaf_own) ce = cudaMalloc(&w->d_parent, uint64_t(w->own.nparents) * 8);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "window tables: %s", cudaGetErrorString(ce)); }
   if (nsites) memcpy(w->h_tab + w->off_sites, reloc.data(), nsites * 8);
   if (nsites) memcpy(w->h_tab + w->off_det, det.data(), nsites * 4);
@@ -861,6 +906,36 @@ struct Checker {
         if (D.release[sg] != c) bad("site %llu detached at step %llu, its segment is released at %llu",
                                     (unsigned long long)D.reloc[r], (unsigned long long)c, (unsigned long long)D.release[sg]);
       }
+    for (uint64_t r = 0; r < seen.size(); ++r)
+      if (!seen[r]) bad("site %llu never detached", (unsigned long long)D.reloc[r]);
+    // 6b. leaf-owned windows: the detach CTAs take exactly the attach CTAs' sites (the owned tail
+    //     goes home through the leaf kernel), and the work list has the shape the kernel derives
+    //     arithmetically (part p = target position p, [0, n_el); group g = parts [g gp, (g + 1) gp))
+    if (w->leaf_own) {
+      const LeafOwn& o = w->own;
+      if (nch != 1 || w->det_keep0 != w->attach_n[0]) bad("leaf-owned window: %llu steps, %llu detached of %llu attached",
+                                                         (unsigned long long)nch, (unsigned long long)w->det_keep0,
+                                                         (unsigned long long)w->attach_n[0]);
+      for (uint64_t j = 0; j < D.det.size(); ++j)
+        if ((D.det[j] < w->attach_n[0]) != (j < w->det_keep0)) { bad("leaf-owned detach list not split at %llu", (unsigned long long)j); break; }
+      if (o.nt != nt || D.sw.nparts() != nt) bad("leaf-owned window: %u targets, %llu parts", o.nt, (unsigned long long)D.sw.nparts());
+      for (uint64_t p = 0; p < D.sw.nparts() && p < nt; ++p) {
+        const uint64_t i = D.torder[p];
+        const int64_t a = d->h_targets[i];
+        if (P[3 * p] != p || P[3 * p + 1] != 0 || P[3 * p + 2] != o.n_el || t->arr_count[a] != o.n_el ||
+            t->arr_level[a] != int(o.level) || t->arr_ordinal[a] != uint64_t(o.o0) + p) {
+          bad("leaf-owned part %llu does not match its target", (unsigned long long)p);
+          break;
+        }
+      }
+      for (uint64_t g = 0; g < D.sw.ngroups(); ++g)
+        if (D.sw.groups[2 * g] != g * o.gp || D.sw.groups[2 * g + 1] != std::min<uint64_t>(nt, (g + 1) * o.gp)) {
+          bad("leaf-owned group %llu is not [g gp, (g + 1) gp)", (unsigned long long)g);
+          break;
+        }
+      if (uint64_t(o.p_first) != o.o0 / q || uint64_t(o.p_first) + o.nparents != (uint64_t(o.o0) + nt - 1) / q + 1)
+        bad("leaf-owned parent range [%u, +%u) does not cover the targets' parents", o.p_first, o.nparents);
+    }
     // 7. copy-back: every segment exactly once, at its release step
     std::vector<uint8_t> home(nseg, 0);
     for (uint64_t c = 0; c < nch; ++c)
@@ -903,6 +978,7 @@ int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out) {
   out->ntiles = w->dry->sw.next_tile;
   out->table_bytes = w->tab_bytes;
   out->zero_copy_node_segments = w->zc ? w->zc_n : 0;
+  out->leaf_owned = w->leaf_own ? 1 : 0;
   Checker ck{desc->tree, desc, w};
   ck.run();
   out->violations = ck.violations;
@@ -1122,7 +1198,20 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     }
     const uint64_t ns = w->reloc_lo[k + 1] - w->reloc_lo[k], nr = w->res_lo[k + 1] - w->res_lo[k];
     const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
-    if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
+    bool resolved_last = false;   // the last op on cs is the attach / resolve launch
+    constexpr uint32_t PHASES = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH;
+    const bool owned_step = w->leaf_own && k == 0 && (fl & PHASES) == PHASES && !chase;
+    LeafOwn own = w->own;
+    if (owned_step) {
+      // node-level sites attached || parents resolved; the leaf kernel owns the leaf A fields
+      own.parent = w->d_parent;
+      own.from = d.host_base;
+      own.to = dimg;
+      own.total = w->total;
+      CF_TRY(launch_attach_parents(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh, own,
+                                   w->d_parent, c->d_bad, cs));
+      resolved_last = true;
+    } else if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
                                    drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr, w->d_ea + w->res_lo[k],
                                    w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
@@ -1130,7 +1219,8 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
                                         w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE,
-                                        w->uni[k].on && !no_uni ? &w->uni[k] : nullptr));
+                                        w->uni[k].on && !no_uni && !w->leaf_own ? &w->uni[k] : nullptr));
+      resolved_last = true;
     } else {
       if (do_attach)
         CF_TRY(launch_relocate(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, c->d_bad, cs, nullptr,
@@ -1142,15 +1232,19 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     }
     // In RESOLVED mode the leaf kernel never reads pointer fields, and every resolve that reads
     // the fields detached at this step has already run: the detach rides in the same launch.
-    const bool fuse_detach = (fl & CF_WIN_DETACH) && (fl & CF_WIN_SCALE) && !chase && !timing;
+    const bool fuse_detach = ((fl & CF_WIN_DETACH) && (fl & CF_WIN_SCALE) && !chase && !timing) || owned_step;
     if (fl & CF_WIN_SCALE) {
       const cf_scale_work& sg = w->seg[k];
-      const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
+      const uint64_t nd = !fuse_detach ? 0 : owned_step ? w->det_keep0 : w->det_lo[k + 1] - w->det_lo[k];
       if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
         RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base, FAULT_DETACH};
+        // programmatic dependent launch behind the one-launch attach || resolve (its CTAs are
+        // resident and waiting when the resolver's last wave drains)
+        static const bool no_pdl = getenv("CF_NO_PDL") != nullptr;   // A/B switch (design experiments)
         CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
-                            nd ? &det : nullptr, FAULT_SCALE));
+                            nd ? &det : nullptr, FAULT_SCALE, resolved_last && !timing && !no_pdl,
+                            owned_step ? &own : nullptr));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }

@@ -130,3 +130,32 @@ def test_pointerchain_window_plans_with_interleaved_layouts():
         rc = N.lib().cf_selective_plan_check(n, N.ptr(host), N.ptr(dev), N.ptr(cnt), 4,
                                              rng.choice([1 << 16, 1 << 18, 1 << 20]), 1, C.byref(steps))
         assert rc == 0, (trial, N.last_error())
+
+
+def test_leaf_owned_one_step_plans():
+    """One-step windows over a uniform range of dense leaf targets hand the leaf A-field relocation
+    to the leaf kernel (LeafOwn): the checker verifies the split attach / detach lists and the
+    arithmetic work-list shape; multi-step, chase, packed and forest windows keep the tables."""
+    import sys
+    from conftest import REPO
+    sys.path.insert(0, str(REPO))
+    import bench
+    spec, policy, _ = bench.make_spec("C4")
+    out = check(spec, 16, policy, 0, flags=N.CF_WIN_RESIDENT)
+    assert out.nsteps == 1 and out.leaf_owned == 1
+    assert check(spec, 16, policy, 32 << 20).leaf_owned == 0                       # multi-step e2e window
+    assert check(cf.DenseSpec(100, 16, 2, elem=4), 16, "all_leaves", 0, mode=N.CF_MODE_CHASE).leaf_owned == 0
+    assert check(cf.DenseSpec(7, 9, 4, elem=4), 1, "all_leaves", 0).leaf_owned == 0   # packed: node fields at 4 mod 8
+    owned = 0
+    rng = random.Random(7)
+    for _ in range(40):
+        q = rng.randint(1, 40)
+        depth = rng.randint(1, 4)
+        while q ** depth > 200000:
+            depth -= 1
+        spec = cf.DenseSpec(q, rng.choice([1, 3, 16, 64, 300, 5000]), depth, elem=rng.choice([4, 8]),
+                            leaf_only=rng.random() < 0.5)
+        out = check(spec, rng.choice([8, 16]), rng.choice(["all_leaves", "ref"]), 0,
+                    flags=rng.choice([N.CF_WIN_RESIDENT, N.CF_WIN_FULL]))
+        owned += out.leaf_owned
+    assert owned > 5

@@ -11,6 +11,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--runs", type=int, default=4)
 ap.add_argument("--mode", default="resolved")
 ap.add_argument("--full", action="store_true")
+ap.add_argument("--graph", action="store_true", help="resident steps replayed from a CUDA graph (fused detach, PDL)")
 ap.add_argument("--dense", default="", help="q,n,depth,elem: a leaves-only dense spec instead of --config")
 ap.add_argument("--align", type=int, default=16)
 a = ap.parse_args()
@@ -27,6 +28,6 @@ if a.full:
 else:
     w.upload_raw()
     for i in range(a.runs):
-        st = w.run_resident(scale=2.0 if i % 2 == 0 else 0.5)
+        st = w.run_resident(scale=2.0 if i % 2 == 0 else 0.5, graph=a.graph)
 print(f"{a.config} total={w.total} ms_total={st.ms_total:.4f} ms_kernel={st.ms_kernel:.4f} launches={st.launches}")
 w.close()

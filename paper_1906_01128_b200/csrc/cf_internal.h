@@ -141,7 +141,10 @@ inline uint64_t tiles_for(uint64_t elems, int elem) {
 #define CF_GROUP_KB 32
 #endif
 constexpr uint64_t GROUP_BYTES = uint64_t(CF_GROUP_KB) << 10;
-constexpr uint32_t GROUP_PARTS = 32;
+#ifndef CF_GROUP_PARTS
+#define CF_GROUP_PARTS 32
+#endif
+constexpr uint32_t GROUP_PARTS = CF_GROUP_PARTS;
 
 // Host-side builder of the leaf-kernel work list (see cf_scale_work in the header).
 struct ScaleWork {

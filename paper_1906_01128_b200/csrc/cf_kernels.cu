@@ -45,6 +45,15 @@
 #ifndef CF_GROUP_WARP
 #define CF_GROUP_WARP 1
 #endif
+#ifndef CF_OWN_MINB
+#define CF_OWN_MINB 4
+#endif
+#ifndef CF_OWN_U
+#define CF_OWN_U 8
+#endif
+#ifndef CF_OWN_CONTIG
+#define CF_OWN_CONTIG 0
+#endif
 #ifndef CF_ROW_ALIGN
 #define CF_ROW_ALIGN 128
 #endif
@@ -980,7 +989,11 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
   uint32_t* fa = nullptr;    // the record's A field, attached by this lane
   uint64_t hv = 0, v0 = 0;
   uint32_t nv = 0;
+#if CF_OWN_CONTIG
+  const uint32_t slot = warp * PER + lane;   // warp w: parts [w PER, (w + 1) PER) of the group
+#else
   const uint32_t slot = warp + WARPS * lane;
+#endif
   const uint64_t pj = g * o.gp + slot;
   if (lane < PER && slot < o.gp && pj < o.nt) {
     const uint32_t ord = o.o0 + uint32_t(pj);
@@ -1036,7 +1049,7 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
       if (j == k) { b = bj[k]; off = pre[k]; }
     return reinterpret_cast<V*>(b) + (f - off);
   };
-  constexpr int U = 4;
+  constexpr int U = CF_OWN_U;
   uint32_t f = lane;
   for (; f + (U - 1) * 32 < total; f += U * 32) {
     V r[U];
@@ -1075,7 +1088,7 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
 // under the 6-CTA/SM launch bound instead of the union of both paths' (no spills).
 enum { PATH_ALL = 0, PATH_TILES = 1, PATH_GROUPS = 2, PATH_OWNED = 3 };
 template <typename T, bool CHASE, int PATH>
-__global__ void __launch_bounds__(SCALE_THREADS, (PATH == PATH_GROUPS || PATH == PATH_OWNED) ? CF_GROUP_MINB : CF_SCALE_MINB)
+__global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_OWNED ? CF_OWN_MINB : PATH == PATH_GROUPS ? CF_GROUP_MINB : CF_SCALE_MINB)
     k_scale(ScaleArgs a, T s) {
   // launched as a programmatic dependent of the attach / resolve kernel: its CTAs may be resident
   // before that grid has finished -- wait for its completion (and memory) before any read

@@ -45,6 +45,9 @@
 #ifndef CF_GROUP_WARP
 #define CF_GROUP_WARP 1
 #endif
+#ifndef CF_GROUP_WARP_U
+#define CF_GROUP_WARP_U 4
+#endif
 #ifndef CF_OWN_MINB
 #define CF_OWN_MINB 4
 #endif
@@ -933,7 +936,7 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
     if (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
     return reinterpret_cast<V*>(b) + (f - off);
   };
-  constexpr int U = 4;
+  constexpr int U = CF_GROUP_WARP_U;
   uint32_t f = lane;
   for (; f + (U - 1) * 32 < total; f += U * 32) {
     V* ptr[U];

@@ -128,6 +128,7 @@ SANITIZE = r'''
 import sys
 sys.path.insert(0, ".")
 import paper_1906_01128_b200 as cf
+from paper_1906_01128_b200 import _native as N
 specs = [cf.DenseSpec(3, 301, 2, elem=4), cf.DenseSpec(4, 5000, 3, elem=4, leaf_only=True),
          cf.LinearSpec(4, 777, "allinit_allused"), cf.DenseSpec(3, 17, 2),
          cf.ForestSpec(cf.LinearSpec(3, 1000, "LLinit_LLused", elem=4), 20, scatter_seed=5),
@@ -140,6 +141,16 @@ for spec in specs:
             w.upload_raw()
             w.run_resident(scale=0.5)
             w.close()
+# uniform leaf ranges: the memory-parallel resolver (multi-step windows, > 4096 targets) and the
+# leaf-owned group path (one-step resident windows), f32 and f64
+for spec in (cf.DenseSpec(16, 4, 4, elem=4, leaf_only=True), cf.DenseSpec(9, 3, 4, elem=8, leaf_only=True)):
+    for chunk in (0, 1 << 16):
+        w = cf.DeepCopyWindow(spec, seed=3, policy="all_leaves", align=16, chunk_bytes=chunk)
+        w.run(scale=2.0)
+        w.upload_raw()
+        w.run_resident(scale=0.5)
+        w.run_n(3, flags=N.CF_WIN_RESIDENT | N.CF_WIN_GRAPH)
+        w.close()
 for scheme in ("marshalling", "naive", "pointerchain", "uvm"):
     m, mach = cf.execute_case(cf.DenseSpec(2, 64, 3), scheme, cf.CostModel(), seed=1)
     mach.close()
@@ -156,6 +167,17 @@ for mode in ("resolved", "chase"):
         raise SystemExit("corrupted leaf pointer was not rejected")
     except cf.WildAccess:
         pass
+w.close()
+# the same corruption in a leaf-owned resident step (the leaf kernel attaches that field itself)
+w = cf.DeepCopyWindow(cf.DenseSpec(16, 4, 4, elem=4, leaf_only=True), seed=1, policy="all_leaves", align=16)
+f = int(w.table(N.CF_TAB_ARR_OWNER)[int(w.targets[-1])]) + 4
+w.host_src()[f:f + 8] = list((w.src + w.total - 8).to_bytes(8, "little"))
+w.upload_raw()
+try:
+    w.run_resident(scale=2.0)
+    raise SystemExit("corrupted leaf pointer was not rejected (leaf-owned)")
+except cf.WildAccess:
+    pass
 w.close()
 print("sanitized ok")
 '''

@@ -247,4 +247,20 @@ def resident(tree: OTree, idx: np.ndarray, dev: np.ndarray, host_base: int, dev_
 
 
 def default_threads() -> int:
-    return int(os.environ.get("CF_ORACLE_THREADS", "0")) or (os.cpu_count() or 1)
+    """Host threads for the CPU legs: CF_ORACLE_THREADS, else every CPU this process may run on
+    (its affinity mask, not the machine's count), as granted by OpenMP (measured team size)."""
+    want = int(os.environ.get("CF_ORACLE_THREADS", "0"))
+    if not want:
+        try:
+            want = len(os.sched_getaffinity(0))
+        except (AttributeError, OSError):
+            want = os.cpu_count() or 1
+    return threads_used(want)
+
+
+def threads_used(n: int) -> int:
+    """The team size OpenMP grants for n threads (orc_threads_used)."""
+    f = lib().orc_threads_used
+    f.restype = C.c_int
+    f.argtypes = [C.c_int]
+    return int(f(int(n)))

@@ -127,12 +127,14 @@ def test_sass_chase_mode_keeps_per_access_chain_loads():
         t, mode, path, total, ld128, st128, chain = [x.strip() for x in line.strip("|").split("|")]
         rows[(t, mode, path)] = (int(total), int(ld128), int(st128), int(chain))
     paths = {p for _, _, p in rows}
-    assert paths == {"tiles", "groups", "tiles+groups"}, paths
+    assert paths == {"tiles", "groups", "tiles+groups", "leaf-owned groups"}, paths
     for t in ("float", "double"):
         for p in paths:
             assert rows[(t, "resolved", p)][3] == 0
-            assert rows[(t, "chase", p)][3] > 0
+            if p != "leaf-owned groups":   # RESOLVED-only path (no chase instantiation)
+                assert rows[(t, "chase", p)][3] > 0
             assert rows[(t, "resolved", p)][1] > 0 and rows[(t, "resolved", p)][2] > 0
+        assert (t, "chase", "leaf-owned groups") not in rows
 
 
 def test_numa_binding_is_scoped():

@@ -27,7 +27,7 @@ for name, c in funcs.items():
     t = "float" if "IfLb" in name else "double"
     mode = "chase" if "Lb1" in name else "resolved"
     pm = re.search(r"Lb[01]ELi(\d)E", name)
-    path = {"0": "tiles+groups", "1": "tiles", "2": "groups"}.get(pm.group(1), "?") if pm else "all"
+    path = {"0": "tiles+groups", "1": "tiles", "2": "groups", "3": "leaf-owned groups"}.get(pm.group(1), "?") if pm else "all"
     total = sum(c.values())
     chain = sum(v for k, v in c.items() if k.startswith("LDG") and "CONSTANT" in k)
     vec_ld = sum(v for k, v in c.items() if k.startswith("LDG") and "128" in k)

@@ -51,12 +51,14 @@ struct cf_window {
   bool owned_attach = false;
   std::vector<uint64_t> res_lo;        // resolve-target ranges per step
   std::vector<UniTargets> uni;         // per step: the resolve range is uniform (no table reads)
-  // leaf-owned relocation (LeafOwn; one-step windows): the leaf kernel attaches / detaches every
-  // target's A field itself; those sites trail step 0's attach list (after attach_n[0]) and its
-  // detach list (after det_keep0), so runs without all four device phases still use the full lists
-  bool leaf_own = false;
-  LeafOwn own{};
-  uint64_t det_keep0 = 0;
+  // leaf-owned relocation (LeafOwn): per step, a consecutive range of leaf targets whose whole
+  // arrays are scaled at that step; the leaf kernel attaches / detaches their A fields itself, so
+  // they appear in no table (no site, no resolve entry, no part).  Planned only when the window
+  // runs all four device phases (flags are fixed at plan time).
+  bool own_any = false;
+  std::vector<LeafOwn> own_step;       // per step (on == 0: none)
+  uint64_t parent_base = 0;            // parent ordinal of d_parent[0]
+  uint64_t own_parents = 0;            // d_parent entries
   uint64_t* d_parent = nullptr;
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step
@@ -94,6 +96,7 @@ struct cf_window {
     std::vector<uint64_t> reloc, torder, ready, release, seg_step, part_step;
     std::vector<uint32_t> det;
     std::vector<uint8_t> owned;   // per target (desc order): resolver attaches its own A field
+    std::vector<uint64_t> lown;   // per target: step whose leaf kernel owns its relocation (nsteps: none)
     cf::ScaleWork sw;
   };
   Dry* dry = nullptr;
@@ -417,7 +420,94 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
       for (uint64_t sg = 0; sg < nseg; ++sg) release[sg] = std::max(release[sg], v[sg]);
   }
   const bool chase = desc->mode == CF_MODE_CHASE;
-  {   // chain fields are read until the target's resolve (chase: until its last piece)
+  // attach || resolve in one launch: safe when every field a resolver may read while the attach
+  // CTAs rewrite it is 8-byte aligned (one atomic 64-bit access).  Dense 12-byte leaf records put
+  // every other leaf's A field at 4 mod 8; a resolver is that field's only reader, so when the
+  // field is attached in the step that resolves its target, the resolver attaches it itself.
+  w->aligned8 = std::all_of(sites, sites + nsites, [](uint64_t o) { return (o & 7) == 0; });
+  {
+    bool misaligned_only_leaf_a = dense && !chase;
+    if (misaligned_only_leaf_a && !w->aligned8) {
+      std::vector<uint64_t> leafs;
+      for (const auto& tr : t->level_nodes)
+        if (tr.size() > size_t(t->spec.depth)) leafs.insert(leafs.end(), tr[size_t(t->spec.depth)].begin(), tr[size_t(t->spec.depth)].end());
+      std::sort(leafs.begin(), leafs.end());
+      for (uint64_t i = 0; i < nsites && misaligned_only_leaf_a; ++i)
+        if (sites[i] & 7) misaligned_only_leaf_a = std::binary_search(leafs.begin(), leafs.end(), sites[i] - LEAF_OFF_A);
+    }
+    w->wide_ok = w->aligned8 || misaligned_only_leaf_a;
+    w->owned_attach = w->wide_ok && !w->aligned8;
+  }
+  // ---- leaf-owned relocation (LeafOwn): a leaf target whose whole, group-sized array is scaled in
+  //      one step is owned by that step's leaf kernel when the step's such targets are one run of
+  //      consecutive ordinals with equal counts (dense single tree, RESOLVED, aligned node fields)
+  std::vector<uint64_t> lown(nt, nch);
+  w->own_step.assign(nch, LeafOwn{});
+  {
+    static const bool no_leaf_own = getenv("CF_NO_LEAF_OWN") != nullptr;   // A/B switch (design experiments)
+    constexpr uint32_t PHASES = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH;
+    if (!no_leaf_own && (fl & PHASES) == PHASES && !(fl & CF_WIN_UVM) && dense && !chase && w->wide_ok &&
+        t->tree_root.size() <= 1 && q >= 2 && t->spec.depth >= 1 && nt > 0 && nt < (1ull << 31)) {
+      std::vector<uint32_t> npc(nt, 0);
+      std::vector<uint64_t> pst(nt, 0);
+      std::vector<uint8_t> whole(nt, 0);
+      for (const Part& pp : parts) {
+        ++npc[pp.t];
+        pst[pp.t] = pp.step;
+        whole[pp.t] = pp.b == 0 && pp.e == t->arr_count[desc->h_targets[pp.t]];
+      }
+      std::vector<std::vector<std::pair<uint64_t, uint64_t>>> cand(nch);   // per step: (ordinal, target)
+      for (uint64_t i = 0; i < nt; ++i) {
+        const int64_t a = desc->h_targets[i];
+        const uint64_t n = t->arr_count[a];
+        if (t->arr_level[a] != int(t->spec.depth) || npc[i] != 1 || !whole[i] || n == 0 || n * e >= TILE_BYTES) continue;
+        cand[pst[i]].push_back({t->arr_ordinal[a], i});
+      }
+      for (uint64_t k = 0; k < nch; ++k) {
+        auto& c = cand[k];
+        if (c.empty()) continue;
+        std::sort(c.begin(), c.end());
+        const uint64_t n_el = t->arr_count[desc->h_targets[c[0].second]];
+        bool ok = c.back().first - c.front().first + 1 == c.size() && c.back().first < (1ull << 31);
+        for (size_t j = 0; j < c.size() && ok; ++j) ok = t->arr_count[desc->h_targets[c[j].second]] == n_el;
+        if (!ok) continue;
+        // the table path's grouping rule (ScaleWork::append): <= GROUP_PARTS parts, <= GROUP_BYTES
+        const uint64_t gp = std::max<uint64_t>(1, std::min<uint64_t>(GROUP_PARTS, GROUP_BYTES / (n_el * e)));
+        const uint32_t o0 = uint32_t(c.front().first), cn = uint32_t(c.size());
+        w->own_step[k] = LeafOwn{nullptr, 1u, uint32_t(t->spec.depth), o0, uint32_t(o0 / q),
+                                 uint32_t((uint64_t(o0) + cn - 1) / q - o0 / q + 1), uint32_t(n_el), uint32_t(gp), cn,
+                                 ~0ull / q + 1, 0, 0, 0};
+        for (auto& pr : c) lown[pr.second] = k;
+        w->own_any = true;
+      }
+    }
+  }
+  if (w->own_any) {
+    // owned targets leave every table: their parts, their resolve entries, their A-field sites
+    parts.erase(std::remove_if(parts.begin(), parts.end(), [&](const Part& pp) { return lown[pp.t] < nch; }), parts.end());
+    std::vector<uint64_t> ofa;
+    for (uint64_t i = 0; i < nt; ++i)
+      if (lown[i] < nch) ofa.push_back(t->arr_owner[desc->h_targets[i]] + LEAF_OFF_A);
+    std::sort(ofa.begin(), ofa.end());
+    std::vector<uint64_t> nrl, nlo(nch + 1, 0);
+    nrl.reserve(reloc.size() - ofa.size());
+    for (uint64_t k = 0; k < nch; ++k) {
+      nlo[k] = nrl.size();
+      for (uint64_t r = w->reloc_lo[k]; r < w->reloc_lo[k + 1]; ++r)
+        if (!std::binary_search(ofa.begin(), ofa.end(), reloc[r])) nrl.push_back(reloc[r]);
+    }
+    nlo[nch] = nrl.size();
+    reloc.swap(nrl);
+    w->reloc_lo.swap(nlo);
+    uint64_t p0 = ~0ull, p1 = 0;
+    for (const LeafOwn& o : w->own_step)
+      if (o.on) { p0 = std::min<uint64_t>(p0, o.p_first); p1 = std::max<uint64_t>(p1, uint64_t(o.p_first) + o.nparents); }
+    w->parent_base = p0;
+    w->own_parents = p1 - p0;
+  }
+  const uint64_t nrel = reloc.size();   // sites in the tables (all sites but the leaf-owned A fields)
+  {   // chain fields are read until the target's resolve (chase: until its last piece; leaf-owned:
+      // until its leaf kernel, which reads and writes the record)
     int nthr = 1;
 #ifdef _OPENMP
     nthr = nt > (1u << 14) ? omp_get_max_threads() : 1;
@@ -433,7 +523,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
 #pragma omp for schedule(static)
       for (int64_t ii = 0; ii < int64_t(nt); ++ii) {
         const uint64_t i = uint64_t(ii);
-        const uint64_t v = chase ? std::max(ready[i], max_step[i]) : ready[i];
+        const uint64_t v = chase ? std::max(ready[i], max_step[i]) : lown[i] < nch ? std::max(ready[i], lown[i]) : ready[i];
         for (uint64_t f = fld_lo[i]; f < fld_lo[i + 1]; ++f) R[fld_seg[f]] = std::max(R[fld_seg[f]], v);
       }
     }
@@ -443,36 +533,24 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
 
   mark("parts");
   // ---- order targets by ready step, parts by step, detach sites by release step
+  // (leaf-owned targets go to a bucket past the last step: they are never resolved from tables)
   std::vector<uint64_t> torder;
-  bucket_order(ready, nch, torder, w->res_lo);
+  {
+    std::vector<uint64_t> rkey(nt);
+    for (uint64_t i = 0; i < nt; ++i) rkey[i] = lown[i] < nch ? nch : ready[i];
+    bucket_order(rkey, nch + 1, torder, w->res_lo);
+  }
+  const uint64_t nt_tab = w->res_lo[nch];   // targets with table entries (resolved from tables)
   std::vector<uint64_t> tpos(nt);
   for (uint64_t k = 0; k < nt; ++k) tpos[torder[k]] = k;
-  // attach || resolve in one launch: safe when every field a resolver may read while the attach
-  // CTAs rewrite it is 8-byte aligned (one atomic 64-bit access).  Dense 12-byte leaf records put
-  // every other leaf's A field at 4 mod 8; a resolver is that field's only reader, so when the
-  // field is attached in the step that resolves its target, the resolver attaches it itself.
-  w->aligned8 = std::all_of(sites, sites + nsites, [](uint64_t o) { return (o & 7) == 0; });
   std::vector<uint8_t> owned_target(nt, 0);
-  {
-    bool misaligned_only_leaf_a = dense && !chase;
-    if (misaligned_only_leaf_a && !w->aligned8) {
-      std::vector<uint64_t> leafs;
-      for (const auto& tr : t->level_nodes)
-        if (tr.size() > size_t(t->spec.depth)) leafs.insert(leafs.end(), tr[size_t(t->spec.depth)].begin(), tr[size_t(t->spec.depth)].end());
-      std::sort(leafs.begin(), leafs.end());
-      for (uint64_t i = 0; i < nsites && misaligned_only_leaf_a; ++i)
-        if (sites[i] & 7) misaligned_only_leaf_a = std::binary_search(leafs.begin(), leafs.end(), sites[i] - LEAF_OFF_A);
-    }
-    w->wide_ok = w->aligned8 || misaligned_only_leaf_a;
-    w->owned_attach = w->wide_ok && !w->aligned8;
-  }
   w->attach_n.assign(nch, 0);
   for (uint64_t k = 0; k < nch; ++k) w->attach_n[k] = w->reloc_lo[k + 1] - w->reloc_lo[k];
   if (w->owned_attach) {
-    std::vector<uint8_t> owned_site(nsites, 0);
+    std::vector<uint8_t> owned_site(nrel, 0);
     for (uint64_t i = 0; i < nt; ++i) {
       const int64_t a = desc->h_targets[i];
-      if (t->arr_level[a] != int(t->spec.depth)) continue;             // leaf records only
+      if (t->arr_level[a] != int(t->spec.depth) || lown[i] < nch) continue;   // table-resolved leaf records only
       const uint64_t fa = t->arr_owner[a] + LEAF_OFF_A;
       if ((fa & 7) == 0 || step_of(fa) != ready[i]) continue;        // aligned, or attached earlier
       const uint64_t r = uint64_t(std::lower_bound(reloc.begin() + w->reloc_lo[ready[i]], reloc.begin() + w->reloc_lo[ready[i] + 1], fa) -
@@ -534,50 +612,14 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     w->seg[c] = sw.append(tri);
   }
   mark("o:work");
-  // ---- leaf-owned relocation: one step, RESOLVED, one dense tree, the targets a uniform range of
-  //      leaf records whose parts are whole, equal, small arrays in target order (C4)
-  static const bool no_leaf_own = getenv("CF_NO_LEAF_OWN") != nullptr;   // A/B switch (design experiments)
-  if (!no_leaf_own && nch == 1 && dense && !chase && w->wide_ok && t->tree_root.size() <= 1 && q >= 2 && nt > 0 &&
-      nt < (1ull << 31) && w->uni[0].on && int(w->uni[0].level) == int(t->spec.depth) && w->res_lo[1] == nt) {
-    const cf_scale_work& s0 = w->seg[0];
-    bool ok = s0.tile_end == s0.tile_begin && sw.nparts() == nt && sw.ngroups() > 0;
-    const uint64_t n_el = ok ? sw.parts[2] : 0, gp = ok ? uint64_t(sw.groups[1]) - sw.groups[0] : 0;
-    ok = ok && n_el > 0 && gp >= 1 && gp <= GROUP_PARTS && n_el < (1ull << 32) && sw.ngroups() == (nt + gp - 1) / gp;
-    for (uint64_t p2 = 0; p2 < nt && ok; ++p2) ok = sw.parts[3 * p2] == p2 && sw.parts[3 * p2 + 1] == 0 && sw.parts[3 * p2 + 2] == n_el;
-    for (uint64_t g = 0; g < sw.ngroups() && ok; ++g)
-      ok = sw.groups[2 * g] == g * gp && sw.groups[2 * g + 1] == std::min(nt, (g + 1) * gp);
-    if (ok) {
-      // every target's A field is owned: step 0's sites = the attach CTAs' share, then the owned tail
-      std::vector<uint64_t> fas(nt);
-      for (uint64_t i = 0; i < nt; ++i) fas[i] = t->arr_owner[desc->h_targets[i]] + LEAF_OFF_A;
-      std::sort(fas.begin(), fas.end());
-      std::vector<uint64_t> keep, own;
-      for (uint64_t r = 0; r < nsites; ++r) (std::binary_search(fas.begin(), fas.end(), reloc[r]) ? own : keep).push_back(reloc[r]);
-      ok = own.size() == nt;
-      if (ok) {
-        std::copy(keep.begin(), keep.end(), reloc.begin());
-        std::copy(own.begin(), own.end(), reloc.begin() + keep.size());
-        w->attach_n[0] = keep.size();
-        std::fill(owned_target.begin(), owned_target.end(), uint8_t(1));
-        w->leaf_own = true;
-        const uint32_t o0 = w->uni[0].ord0;
-        w->own = LeafOwn{nullptr, 1u, w->uni[0].level, o0, uint32_t(o0 / q), uint32_t((o0 + nt - 1) / q - o0 / q + 1),
-                         uint32_t(n_el), uint32_t(gp), uint32_t(nt), w->uni[0].qmagic, 0, 0, 0};
-      }
-    }
-  }
   // detach order: positions in the (step-ordered) relocation table, grouped by release step
-  std::vector<uint32_t> det(nsites);
+  std::vector<uint32_t> det(nrel);
   {
-    std::vector<uint64_t> srel(nsites), sidx;
-#pragma omp parallel for schedule(static) if (nsites > (1u << 15))
-    for (int64_t k = 0; k < int64_t(nsites); ++k) srel[k] = release[six.at(reloc[k])];
+    std::vector<uint64_t> srel(nrel), sidx;
+#pragma omp parallel for schedule(static) if (nrel > (1u << 15))
+    for (int64_t k = 0; k < int64_t(nrel); ++k) srel[k] = release[six.at(reloc[k])];
     bucket_order(srel, nch, sidx, w->det_lo);
-    for (uint64_t k = 0; k < nsites; ++k) det[k] = uint32_t(sidx[k]);
-    if (w->leaf_own) {   // one step: the non-owned sites first, the owned tail last
-      std::stable_partition(det.begin(), det.end(), [&](uint32_t r) { return r < w->attach_n[0]; });
-      w->det_keep0 = w->attach_n[0];
-    }
+    for (uint64_t k = 0; k < nrel; ++k) det[k] = uint32_t(sidx[k]);
   }
   mark("orders");
   w->released.assign(nch, {});
@@ -624,11 +666,11 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   auto al8 = [](uint64_t x) { return (x + 7) & ~7ull; };
   w->has_roots = t->tree_root.size() > 1;   // single trees use the shape's root
   w->off_sites = 0;
-  w->off_det = al8(w->off_sites + nsites * 8);
-  w->off_level = al8(w->off_det + nsites * 4);
-  w->off_ord = al8(w->off_level + nt * 4);
-  w->off_root = al8(w->off_ord + nt * 4);
-  w->off_parts = al8(w->off_root + (w->has_roots ? nt * 8 : 0));
+  w->off_det = al8(w->off_sites + nrel * 8);
+  w->off_level = al8(w->off_det + nrel * 4);
+  w->off_ord = al8(w->off_level + nt_tab * 4);
+  w->off_root = al8(w->off_ord + nt_tab * 4);
+  w->off_parts = al8(w->off_root + (w->has_roots ? nt_tab * 8 : 0));
   w->off_tb = al8(w->off_parts + sw.parts.size() * 4);
   w->off_grp = al8(w->off_tb + sw.tile_base.size() * 8);
   w->off_zc_h2d = al8(w->off_grp + sw.groups.size() * 4 + 8);
@@ -644,6 +686,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
     D.seg_step = std::move(seg_step);
     D.part_step = std::move(pstep);
     D.owned = std::move(owned_target);
+    D.lown = std::move(lown);
     D.sw = std::move(sw);
     mark("tables");
     *out = w;
@@ -653,14 +696,14 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tab, w->tab_bytes);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_ea, std::max<uint64_t>(nt, 1) * 8);
   if (ce == cudaSuccess) ce = cudaMalloc(&w->d_count, std::max<uint64_t>(nt, 1) * 4);
-  if (ce == cudaSuccess && w->leaf_own) ce = cudaMalloc(&w->d_parent, uint64_t(w->own.nparents) * 8);
+  if (ce == cudaSuccess && w->own_any) ce = cudaMalloc(&w->d_parent, w->own_parents * 8);
   if (ce != cudaSuccess) { cudaGetLastError(); destroy(w); return fail(CF_E_OOM, "window tables: %s", cudaGetErrorString(ce)); }
-  if (nsites) memcpy(w->h_tab + w->off_sites, reloc.data(), nsites * 8);
-  if (nsites) memcpy(w->h_tab + w->off_det, det.data(), nsites * 4);
+  if (nrel) memcpy(w->h_tab + w->off_sites, reloc.data(), nrel * 8);
+  if (nrel) memcpy(w->h_tab + w->off_det, det.data(), nrel * 4);
   int32_t* lv = reinterpret_cast<int32_t*>(w->h_tab + w->off_level);
   uint32_t* od = reinterpret_cast<uint32_t*>(w->h_tab + w->off_ord);
   uint64_t* rt = reinterpret_cast<uint64_t*>(w->h_tab + w->off_root);
-  for (uint64_t k = 0; k < nt; ++k) {
+  for (uint64_t k = 0; k < nt_tab; ++k) {
     const int64_t a = desc->h_targets[torder[k]];
     lv[k] = t->arr_level[a];
     od[k] = uint32_t(t->arr_ordinal[a]) | (owned_target[torder[k]] ? 0x80000000u : 0u);   // bit 31: attach own A field
@@ -745,9 +788,12 @@ struct Checker {
     if (x != total) bad("segments end at %llu, arena is %llu bytes", (unsigned long long)x, (unsigned long long)total);
     if (w->step_seg_lo.size() != nch + 1 || w->step_seg_lo.back() != nseg) bad("step table malformed");
     // 2. sites: each once, in the step that uploads both its ends
+    // (leaf-owned targets' A fields are relocated by their leaf kernel, not from the table)
     std::vector<uint64_t> rs(D.reloc);
+    for (uint64_t i = 0; i < nt; ++i)
+      if (D.lown[i] < nch) rs.push_back(t->arr_owner[d->h_targets[i]] + LEAF_OFF_A);
     std::sort(rs.begin(), rs.end());
-    if (rs != t->site_sorted) bad("relocation table is not a permutation of the sites");
+    if (rs != t->site_sorted) bad("relocation table + leaf-owned fields are not a permutation of the sites");
     for (uint64_t k = 0; k < nch; ++k)
       for (uint64_t i = w->reloc_lo[k]; i < w->reloc_lo[k + 1]; ++i) {
         const uint64_t s0 = D.reloc[i];
@@ -803,9 +849,13 @@ struct Checker {
                                (unsigned long long)D.ready[i], (unsigned long long)r);
     }
     for (uint64_t c = 0; c < nch; ++c)
-      for (uint64_t k = w->res_lo[c]; k < w->res_lo[c + 1]; ++k)
+      for (uint64_t k = w->res_lo[c]; k < w->res_lo[c + 1]; ++k) {
         if (D.ready[D.torder[k]] != c) bad("target resolved at step %llu is ready at %llu", (unsigned long long)c,
                                            (unsigned long long)D.ready[D.torder[k]]);
+        if (D.lown[D.torder[k]] < nch) bad("leaf-owned target %llu also resolved from the tables", (unsigned long long)D.torder[k]);
+      }
+    for (uint64_t k = w->res_lo[nch]; k < nt; ++k)
+      if (D.lown[D.torder[k]] >= nch) bad("target %llu is neither resolved nor leaf-owned", (unsigned long long)D.torder[k]);
     // 3b. one-launch attach || resolve: no misaligned field in the attach CTAs' list is read by a
     //     resolver of the same step; every owned field sits in its target's step's owned tail
     if (w->wide_ok) {
@@ -877,6 +927,49 @@ struct Checker {
         }
       }
     }
+    // 4b. leaf-owned ranges: step k's range [o0, o0 + nt) is exactly its owned targets (leaf level,
+    //     count n_el), each whole and after its bytes and its chain; group / parent shape as the
+    //     kernel derives them
+    {
+      std::vector<std::vector<uint64_t>> by_step(nch);
+      for (uint64_t i = 0; i < nt; ++i)
+        if (D.lown[i] < nch) by_step[D.lown[i]].push_back(i);
+      for (uint64_t k = 0; k < nch; ++k) {
+        const LeafOwn& o = w->own_step[k];
+        if (!o.on) { if (!by_step[k].empty()) bad("step %llu owns targets without a range", (unsigned long long)k); continue; }
+        if (by_step[k].size() != o.nt) bad("step %llu: %u owned range, %zu owned targets", (unsigned long long)k, o.nt, by_step[k].size());
+        const uint64_t gp_rule = std::max<uint64_t>(1, std::min<uint64_t>(GROUP_PARTS, GROUP_BYTES / (uint64_t(o.n_el) * e)));
+        if (o.gp != gp_rule || o.level != uint32_t(t->spec.depth) || o.level < 1 || uint64_t(o.p_first) != o.o0 / q ||
+            uint64_t(o.p_first) + o.nparents != (uint64_t(o.o0) + o.nt - 1) / q + 1)
+          bad("step %llu: leaf-owned range shape (gp %u, level %u, parents [%u, +%u))", (unsigned long long)k, o.gp, o.level,
+              o.p_first, o.nparents);
+        if (uint64_t(o.p_first) < w->parent_base || uint64_t(o.p_first) + o.nparents > w->parent_base + w->own_parents)
+          bad("step %llu: parents outside the parent table", (unsigned long long)k);
+        std::vector<uint8_t> hit(o.nt, 0);
+        for (uint64_t i : by_step[k]) {
+          const int64_t a = d->h_targets[i];
+          const uint64_t od = t->arr_ordinal[a];
+          if (t->arr_level[a] != int(t->spec.depth) || od < o.o0 || od - o.o0 >= o.nt || hit[od - o.o0]++ ||
+              t->arr_count[a] != o.n_el) {
+            bad("leaf-owned target %llu (ordinal %llu) outside step %llu's range", (unsigned long long)i, (unsigned long long)od,
+                (unsigned long long)k);
+            continue;
+          }
+          if (D.ready[i] > k) bad("leaf-owned target %llu scaled at step %llu before its chain (step %llu)", (unsigned long long)i,
+                                  (unsigned long long)k, (unsigned long long)D.ready[i]);
+          const uint64_t b0 = t->arr_off[a], b1 = b0 + uint64_t(o.n_el) * e;
+          for (size_t z = size_t(std::upper_bound(sorted_lo.begin(), sorted_lo.end(), b0) - sorted_lo.begin()) - 1;
+               z < sorted_lo.size() && sorted_lo[z] < b1; ++z) {
+            const uint32_t sg = sorted_seg[z];
+            if (D.seg_step[sg] > k) bad("leaf-owned target %llu scaled at step %llu before segment %u lands", (unsigned long long)i,
+                                        (unsigned long long)k, sg);
+            need_release[sg] = std::max(need_release[sg], k);
+          }
+          cover[i].push_back({0, o.n_el});
+          max_part[i] = std::max(max_part[i], k);
+        }
+      }
+    }
     for (uint64_t i = 0; i < nt; ++i) {
       const uint64_t n = t->arr_count[d->h_targets[i]];
       auto& cv = cover[i];
@@ -888,8 +981,9 @@ struct Checker {
       }
       if (y != n) bad("target %llu: parts cover [0, %llu) of %llu elements", (unsigned long long)i, (unsigned long long)y,
                       (unsigned long long)n);
+      // a leaf-owned target's record is read and written by its leaf kernel
       for (uint32_t sg : chain_segs[i])
-        need_release[sg] = std::max(need_release[sg], chase ? std::max(D.ready[i], max_part[i]) : D.ready[i]);
+        need_release[sg] = std::max(need_release[sg], (chase || D.lown[i] < nch) ? std::max(D.ready[i], max_part[i]) : D.ready[i]);
     }
     // 5. release: no segment goes home before its last reader / writer
     for (uint64_t sg = 0; sg < nseg; ++sg)
@@ -908,34 +1002,6 @@ struct Checker {
       }
     for (uint64_t r = 0; r < seen.size(); ++r)
       if (!seen[r]) bad("site %llu never detached", (unsigned long long)D.reloc[r]);
-    // 6b. leaf-owned windows: the detach CTAs take exactly the attach CTAs' sites (the owned tail
-    //     goes home through the leaf kernel), and the work list has the shape the kernel derives
-    //     arithmetically (part p = target position p, [0, n_el); group g = parts [g gp, (g + 1) gp))
-    if (w->leaf_own) {
-      const LeafOwn& o = w->own;
-      if (nch != 1 || w->det_keep0 != w->attach_n[0]) bad("leaf-owned window: %llu steps, %llu detached of %llu attached",
-                                                         (unsigned long long)nch, (unsigned long long)w->det_keep0,
-                                                         (unsigned long long)w->attach_n[0]);
-      for (uint64_t j = 0; j < D.det.size(); ++j)
-        if ((D.det[j] < w->attach_n[0]) != (j < w->det_keep0)) { bad("leaf-owned detach list not split at %llu", (unsigned long long)j); break; }
-      if (o.nt != nt || D.sw.nparts() != nt) bad("leaf-owned window: %u targets, %llu parts", o.nt, (unsigned long long)D.sw.nparts());
-      for (uint64_t p = 0; p < D.sw.nparts() && p < nt; ++p) {
-        const uint64_t i = D.torder[p];
-        const int64_t a = d->h_targets[i];
-        if (P[3 * p] != p || P[3 * p + 1] != 0 || P[3 * p + 2] != o.n_el || t->arr_count[a] != o.n_el ||
-            t->arr_level[a] != int(o.level) || t->arr_ordinal[a] != uint64_t(o.o0) + p) {
-          bad("leaf-owned part %llu does not match its target", (unsigned long long)p);
-          break;
-        }
-      }
-      for (uint64_t g = 0; g < D.sw.ngroups(); ++g)
-        if (D.sw.groups[2 * g] != g * o.gp || D.sw.groups[2 * g + 1] != std::min<uint64_t>(nt, (g + 1) * o.gp)) {
-          bad("leaf-owned group %llu is not [g gp, (g + 1) gp)", (unsigned long long)g);
-          break;
-        }
-      if (uint64_t(o.p_first) != o.o0 / q || uint64_t(o.p_first) + o.nparents != (uint64_t(o.o0) + nt - 1) / q + 1)
-        bad("leaf-owned parent range [%u, +%u) does not cover the targets' parents", o.p_first, o.nparents);
-    }
     // 7. copy-back: every segment exactly once, at its release step
     std::vector<uint8_t> home(nseg, 0);
     for (uint64_t c = 0; c < nch; ++c)
@@ -978,7 +1044,8 @@ int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out) {
   out->ntiles = w->dry->sw.next_tile;
   out->table_bytes = w->tab_bytes;
   out->zero_copy_node_segments = w->zc ? w->zc_n : 0;
-  out->leaf_owned = w->leaf_own ? 1 : 0;
+  out->leaf_owned = 0;
+  for (const LeafOwn& o : w->own_step) out->leaf_owned += o.on ? 1 : 0;   // steps with a leaf-owned range
   Checker ck{desc->tree, desc, w};
   ck.run();
   out->violations = ck.violations;
@@ -1199,17 +1266,22 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     const uint64_t ns = w->reloc_lo[k + 1] - w->reloc_lo[k], nr = w->res_lo[k + 1] - w->res_lo[k];
     const bool do_attach = (fl & CF_WIN_ATTACH) && ns, do_resolve = (fl & CF_WIN_RESOLVE) && !chase && nr;
     bool resolved_last = false;   // the last op on cs is the attach / resolve launch
-    constexpr uint32_t PHASES = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH;
-    const bool owned_step = w->leaf_own && k == 0 && (fl & PHASES) == PHASES && !chase;
-    LeafOwn own = w->own;
+    // leaf-owned step (planned only when the window runs all four device phases, RESOLVED)
+    const bool owned_step = w->own_any && w->own_step[k].on;
+    LeafOwn own{};
     if (owned_step) {
-      // node-level sites attached || parents resolved; the leaf kernel owns the leaf A fields
-      own.parent = w->d_parent;
+      own = w->own_step[k];
+      own.parent = w->d_parent + (own.p_first - w->parent_base);
       own.from = d.host_base;
       own.to = dimg;
       own.total = w->total;
-      CF_TRY(launch_attach_parents(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh, own,
-                                   w->d_parent, c->d_bad, cs));
+      // every site of the step attached (the resolver-owned tail too: its resolvers run after)
+      // || the owned range's parents resolved into the parent table
+      CF_TRY(launch_attach_parents(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh, own,
+                                   w->d_parent + (own.p_first - w->parent_base), c->d_bad, cs));
+      if (nr)   // the step's other targets, from the tables (their fields are attached by now)
+        CF_TRY(launch_resolve(c, img, w->sh, drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
+                              w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE));
       resolved_last = true;
     } else if (do_attach && do_resolve && ns <= SMALL_FUSED && nr <= SMALL_FUSED) {
       CF_TRY(launch_attach_resolve(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh,
@@ -1219,7 +1291,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       CF_TRY(launch_attach_resolve_wide(c, img, w->total, dsites + w->reloc_lo[k], w->attach_n[k], d.host_base, dimg, w->sh,
                                         drt ? drt + w->res_lo[k] : nullptr, dlv + w->res_lo[k], dod + w->res_lo[k], nr,
                                         w->d_ea + w->res_lo[k], w->d_count + w->res_lo[k], c->d_bad, cs, FAULT_RESOLVE,
-                                        w->uni[k].on && !no_uni && !w->leaf_own ? &w->uni[k] : nullptr));
+                                        w->uni[k].on && !no_uni ? &w->uni[k] : nullptr));
       resolved_last = true;
     } else {
       if (do_attach)
@@ -1235,16 +1307,26 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
     const bool fuse_detach = ((fl & CF_WIN_DETACH) && (fl & CF_WIN_SCALE) && !chase && !timing) || owned_step;
     if (fl & CF_WIN_SCALE) {
       const cf_scale_work& sg = w->seg[k];
-      const uint64_t nd = !fuse_detach ? 0 : owned_step ? w->det_keep0 : w->det_lo[k + 1] - w->det_lo[k];
-      if (sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin || nd) {
+      const bool table_parts = sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin;
+      const uint64_t nd = fuse_detach ? w->det_lo[k + 1] - w->det_lo[k] : 0;
+      // programmatic dependent launch behind the attach / resolve launch (its CTAs are resident
+      // and waiting when the resolver's last wave drains)
+      static const bool no_pdl = getenv("CF_NO_PDL") != nullptr;   // A/B switch (design experiments)
+      const bool pdl = resolved_last && !timing && !no_pdl;
+      RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base, FAULT_DETACH};
+      if (owned_step) {
+        // the owned range (with the step's detach riding along), then any table-driven parts
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
-        RelocArgs det{img, w->total, dsites, ddet + w->det_lo[k], nd, dimg, d.host_base, FAULT_DETACH};
-        // programmatic dependent launch behind the one-launch attach || resolve (its CTAs are
-        // resident and waiting when the resolver's last wave drains)
-        static const bool no_pdl = getenv("CF_NO_PDL") != nullptr;   // A/B switch (design experiments)
         CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
-                            nd ? &det : nullptr, FAULT_SCALE, resolved_last && !timing && !no_pdl,
-                            owned_step ? &own : nullptr));
+                            nd ? &det : nullptr, FAULT_SCALE, pdl, &own));
+        if (table_parts)
+          CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
+                              nullptr, FAULT_SCALE));
+        if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
+      } else if (table_parts || nd) {
+        if (timing) CF_CUDA(cudaEventRecord(w->ev_k0[k], cs));
+        CF_TRY(launch_scale(c, w->elem, d.mode, img, w->sh, drt, dlv, dod, w->d_ea, w->d_count, sg, d.scale, c->d_bad, cs,
+                            nd ? &det : nullptr, FAULT_SCALE, pdl));
         if (timing) CF_CUDA(cudaEventRecord(w->ev_k1[k], cs));
       }
     }
@@ -1297,7 +1379,9 @@ int finish(cf_window* w, cf_window_stats* st, uint64_t launches0, uint64_t h2d, 
     if (kernel_times) {
       for (uint64_t k = 0; k < nch; ++k) {
         const cf_scale_work& sg = w->seg[k];
-        if (!(w->d.flags & CF_WIN_SCALE) || (sg.tile_end == sg.tile_begin && sg.group_end == sg.group_begin)) continue;
+        const bool launched = sg.tile_end > sg.tile_begin || sg.group_end > sg.group_begin ||
+                              (w->own_any && w->own_step[k].on);
+        if (!(w->d.flags & CF_WIN_SCALE) || !launched) continue;
         float ms = 0;
         CF_CUDA(cudaEventElapsedTime(&ms, w->ev_k0[k], w->ev_k1[k]));
         ks += ms;

@@ -4,7 +4,8 @@ targets per warp, parents walked one per lane) and the leaf kernel launches as i
 dependent.  Every case is checked byte for byte against the oracle's expected arena
 (scenarios.py:270-284 resolve, harness.py:307-309 scale, memory.py:316-344 attach / detach) through
 the pipelined window (one step and many small steps, so ranges start at arbitrary ordinals and
-split parent runs), its graph replay, and the resident step.  The fan-outs q cover every run
+split parent runs -- the multi-step windows own each step's run of whole leaves, the leaves split at
+step boundaries go through the tables), its graph replay, and the resident step.  The fan-outs q cover every run
 width U the launcher picks (q = 2 forces U = 1 ... q >= 9 allows U = 8), leaf records at 4 mod 8
 (owned attach) and aligned, f32 and f64."""
 import numpy as np
@@ -40,6 +41,8 @@ CASES = [
     (33, 3, 17, 4, False),
     (100, 2, 256, 4, True),
     (100, 3, 4, 4, True),
+    (5000, 1, 2, 4, True),     # depth 1: the parent is the root
+    (4500, 1, 7, 8, False),
 ]
 
 

@@ -610,8 +610,14 @@ def summary_block(name: str, elem: int, device: int, chunk_mb: int, numa_node: i
         # (one window's copy-in before any copy-out, and the reverse at the end) stay a small share
         steps = max(steps, 100)
     try:
-        st_e2e, _ = m.timed(N.CF_WIN_FULL | m.gflag, warmup, steps, dist)
-        e2e_ms = st_e2e.ms_total / steps
+        # small graphs: three batches, the median one reported (a 0.1 ms window is sensitive to
+        # host-side hiccups of a single batch; all three are in the block)
+        batches = 3 if m.total < (64 << 20) else 1
+        runs = []
+        for _ in range(batches):
+            st, _w = m.timed(N.CF_WIN_FULL | m.gflag, warmup, steps, dist)
+            runs.append((st.ms_total / steps, st))
+        e2e_ms, st_e2e = sorted(runs, key=lambda r: r[0])[len(runs) // 2]
         m.w.upload_raw()
         st_res, _ = m.timed(N.CF_WIN_RESIDENT | m.gflag, warmup, steps, dist)
         res_ms = st_res.ms_total / steps
@@ -628,6 +634,8 @@ def summary_block(name: str, elem: int, device: int, chunk_mb: int, numa_node: i
                 "kernel_share_of_resident_step": round(k_ms / res_ms, 4),
                 "e2e_ms_per_step": round(e2e_ms, 4), "e2e_gbs": round(m.total / (e2e_ms * 1e-3) / 1e9, 3),
                 "steps": steps,
+                **({"e2e_batches_ms_per_step": [round(r[0], 4) for r in runs], "e2e_batch": "median of 3"}
+                   if batches > 1 else {}),
                 "link_probe_gbs": probe, "link_probe_bytes": LINK_PROBE_BYTES if probe is link_1g else m.total,
                 "frac_of_link_roofline": round(ideal / e2e_ms, 4),
                 "e2e_windows": m.e2e_layout}

@@ -710,23 +710,32 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
         t_nodes = nodes[used]
     else:
         sel = idx if policy != "ref" or forest else handle.target_indices("ref")
-        L = handle.arr_level[sel].astype(np.int64)
+        # the tree-shape columns of the walk (immutable per tree and target set) are gathered once;
+        # the pointer values are read from memory on every call
+        wcache = handle.__dict__.setdefault("_uvm_walk_cache", {})
+        key = (policy, len(sel), int(sel[0]) if len(sel) else -1, int(sel[-1]) if len(sel) else -1)
+        cols = wcache.get(key)
+        if cols is None or not np.array_equal(cols[0], sel):
+            cols = wcache[key] = (np.array(sel, copy=True), handle.arr_level[sel].astype(np.int64),
+                                  handle.arr_root[sel].astype(np.int64), handle.arr_ordinal[sel].astype(np.int64))
+        L, ords = cols[1], cols[3]
         fields, t_nodes = [], []
-        node = handle.arr_root[sel].astype(np.int64)
-        ords = handle.arr_ordinal[sel].astype(np.int64)
+        node = cols[2].copy()
         depth = 0 if linear else tree.depth
         q = 1 if linear else tree.q
+        one_level = L.size > 0 and int(L.min()) == int(L.max())   # e.g. every leaf: no masks
         for lv in range(1, int(L.max()) + 1 if L.size else 1):
-            act = L >= lv
+            act = slice(None) if one_level else L >= lv
             # many chains share their upper nodes: read each distinct Lnext field once
-            un, inv = np.unique(node[act], return_inverse=True)
+            un, inv = _unique_inverse(node[act])
             fields.append(un + OFF_LNEXT)
             blk = rd(un + OFF_LNEXT)[inv]
             if linear:
                 node[act] = blk
             else:
                 child = NODE_SIZE if lv < depth else LEAF_NODE_SIZE
-                digit = (ords[act] // q ** (L[act] - lv)) % q
+                pw = q ** (int(L[0]) - lv) if one_level else q ** (L[act] - lv)
+                digit = (ords[act] // pw) % q
                 node[act] = blk + child * digit
         leaf = (~np.asarray(linear)) & (L == depth) if not linear else np.zeros(L.shape, bool)
         fields.append(node + np.where(leaf, LEAF_OFF_A, OFF_A))
@@ -749,7 +758,31 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
     starts = handle.arr_off[arr].astype(np.int64)[keep] + base
     dirty = (starts // page, (starts + e * (cnt[keep] - 1)) // page)   # page ranges, inclusive
     f = np.concatenate([np.asarray(x, np.int64) for x in fields]) if fields else np.zeros(0, np.int64)
-    return np.unique((f + base) // page), dirty
+    return _distinct_pages((f + base) // page), dirty
+
+
+def _unique_inverse(x: np.ndarray):
+    """np.unique(x, return_inverse=True); O(n) when x is already non-decreasing (targets in
+    ordinal order over a DFS layout -- C4's 1M chains), a sort otherwise."""
+    if x.size > 1 and bool((x[1:] >= x[:-1]).all()):
+        first = np.empty(x.size, bool)
+        first[0] = True
+        np.not_equal(x[1:], x[:-1], out=first[1:])
+        return x[first], np.cumsum(first) - 1
+    return np.unique(x, return_inverse=True)
+
+
+def _distinct_pages(p: np.ndarray) -> np.ndarray:
+    """Sorted distinct page numbers (np.unique) by a bitmap over their span when that span is
+    small (a tree's pages), a sort otherwise."""
+    if p.size == 0:
+        return p
+    lo, hi = int(p.min()), int(p.max())
+    if hi - lo > 8 * p.size + (1 << 20):
+        return np.unique(p)
+    m = np.zeros(hi - lo + 1, bool)
+    m[p - lo] = True
+    return np.nonzero(m)[0].astype(np.int64) + lo
 
 
 def _merged_ranges(handle: TreeHandle, idx: np.ndarray, gap: int) -> list:
@@ -838,8 +871,9 @@ def _uvm_account_kernel(machine: Machine, handle: TreeHandle, prep: DevicePrep, 
     # the array pages written (dirty)
     machine.uvm_touch_pages(fields, "read", "device")
     if dlo.size:
-        machine.uvm_touch_ranges(dlo, dhi, "read", "device")
-        machine.uvm_touch_ranges(dlo, dhi, "write", "device")
+        mask = machine.uvm_range_mask(dlo, dhi)   # the same pages for the read and the write
+        machine.uvm_touch_mask(mask, "read", "device")
+        machine.uvm_touch_mask(mask, "write", "device")
 
 
 def _kernel_args(handle: TreeHandle, policy: str):

@@ -767,18 +767,28 @@ class Machine:
 
     def uvm_touch_ranges(self, lo_pages, hi_pages, access: str, actor: str) -> int:
         """Touch every page of the inclusive page ranges [lo, hi] (each page once)."""
+        return self.uvm_touch_mask(self.uvm_range_mask(lo_pages, hi_pages), access, actor)
+
+    def uvm_range_mask(self, lo_pages, hi_pages) -> np.ndarray:
+        """Boolean mask over the page table of the pages in the inclusive ranges [lo, hi];
+        WildAccess if any of them was never registered."""
         if self.uvm is None:
             raise SimMemoryError("uvm_touch outside UVM mode")
         u = self.uvm
         lo = np.asarray(lo_pages, np.int64)
         hi = np.asarray(hi_pages, np.int64)
-        a = np.searchsorted(u._pages, lo, side="left")
-        b = np.searchsorted(u._pages, hi, side="right")
+        n = u._pages.size
+        if n and int(u._pages[-1]) - int(u._pages[0]) + 1 == n:   # one contiguous registration
+            first = int(u._pages[0])
+            a = np.clip(lo - first, 0, n)
+            b = np.clip(hi - first + 1, 0, n)
+        else:
+            a = np.searchsorted(u._pages, lo, side="left")
+            b = np.searchsorted(u._pages, hi, side="right")
         if ((b - a) != (hi - lo + 1)).any():   # some page of a range was never registered
             raise WildAccess("unified access hits no registered page")
-        n = u._pages.size + 1   # coverage mask by a difference array
-        d = np.bincount(a, minlength=n) - np.bincount(b, minlength=n)
-        return self.uvm_touch_mask(np.cumsum(d[:-1]) > 0, access, actor)
+        d = np.bincount(a, minlength=n + 1) - np.bincount(b, minlength=n + 1)   # difference array
+        return np.cumsum(d[:-1]) > 0
 
     def uvm_touch_mask(self, mask: np.ndarray, access: str, actor: str) -> int:
         """Touch the registered pages selected by a boolean mask over the page table."""

@@ -52,7 +52,7 @@
 #define CF_OWN_MINB 4
 #endif
 #ifndef CF_OWN_U
-#define CF_OWN_U 8
+#define CF_OWN_U 4
 #endif
 #ifndef CF_OWN_CONTIG
 #define CF_OWN_CONTIG 0
@@ -877,8 +877,11 @@ __device__ __forceinline__ void scale_group(const ScaleArgs& a, uint64_t g, T s)
 
 // Small-part group, warp-local version: warp w owns parts p0+w, p0+w+8, ... (<= 4 with 32-part
 // groups).  Lanes 0..3 fetch those parts' metadata in parallel (one dependent-load round per
-// warp, no CTA barrier), the warp prefix-sums their vector counts in registers, and then streams
-// the flattened (part, vector) sequence with 4 independent 128-bit loads in flight per lane.
+// warp, no CTA barrier) into the warp's slots in shared memory, the warp prefix-sums their vector
+// counts in registers, and then streams the flattened (part, vector) sequence with 4 independent
+// 128-bit loads in flight per lane, reading each vector's part base from shared memory (an LDS:
+// keeping 4 bases and the head / tail bounds in registers across the streaming loop spilled them
+// to local memory under the 6-CTA/SM register budget).
 template <typename T, bool CHASE>
 __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g, T s) {
   using VT = Vec<T>;
@@ -886,68 +889,62 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
   constexpr uint64_t VN = VT::N;
   constexpr unsigned WARPS = SCALE_THREADS / 32;
   constexpr unsigned PER = (GROUP_PARTS + WARPS - 1) / WARPS;  // parts per warp
+  struct Slot { uint8_t* vbase; uint8_t* arr; uint64_t e0, e1, v0, t; };   // vbase = arr + v0 (vectors)
+  __shared__ Slot slots[WARPS][PER];
   const uint32_t p0 = a.w.groups[2 * g], p1 = a.w.groups[2 * g + 1];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Slot* my = slots[warp];
   // lane j < PER: metadata of part p0 + warp + WARPS * j
-  uint8_t* base = nullptr;
-  uint64_t v0 = 0, e0 = 0, e1 = 0, t = 0;
   uint32_t nv = 0;
   const uint64_t pj = uint64_t(p0) + warp + uint64_t(WARPS) * lane;
-  if (lane < PER && pj < p1) {
-    t = a.w.parts[3 * pj];
-    e0 = a.w.parts[3 * pj + 1];
-    e1 = a.w.parts[3 * pj + 2];
-    uint64_t cnt;
-    if (!target_array<T, CHASE>(a, t, base, cnt) || e1 > cnt) {
-      raise_bad(a.bad, t | a.tag);
-      base = nullptr;
-      v0 = e1;
-    } else {
-      const uintptr_t first = reinterpret_cast<uintptr_t>(base + e0 * sizeof(T));
-      v0 = e1;
-      if ((first % sizeof(T)) == 0) v0 = min(e1, e0 + ((16 - (first & 15)) & 15) / sizeof(T));
-      nv = uint32_t((e1 - v0) / VN);
+  if (lane < PER) {
+    uint8_t* base = nullptr;
+    uint64_t v0 = 0, e0 = 0, e1 = 0, t = 0;
+    if (pj < p1) {
+      t = a.w.parts[3 * pj];
+      e0 = a.w.parts[3 * pj + 1];
+      e1 = a.w.parts[3 * pj + 2];
+      uint64_t cnt;
+      if (!target_array<T, CHASE>(a, t, base, cnt) || e1 > cnt) {
+        raise_bad(a.bad, t | a.tag);
+        base = nullptr;
+        v0 = e1;
+      } else {
+        const uintptr_t first = reinterpret_cast<uintptr_t>(base + e0 * sizeof(T));
+        v0 = e1;
+        if ((first % sizeof(T)) == 0) v0 = min(e1, e0 + ((16 - (first & 15)) & 15) / sizeof(T));
+        nv = uint32_t((e1 - v0) / VN);
+      }
     }
+    my[lane] = Slot{base + v0 * sizeof(T), base, e0, e1, v0, t};
   }
   // exclusive prefix of nv over lanes 0..PER-1, broadcast to the warp
+  __syncwarp();   // the slots are visible to the whole warp
   uint32_t pre[PER + 1];
   pre[0] = 0;
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
-  uint8_t* bj[PER];
-  uint64_t tj[PER], oj[PER];
-#pragma unroll
-  for (unsigned j = 0; j < PER; ++j) {
-    bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
-    tj[j] = __shfl_sync(0xffffffffu, t, j);
-    oj[j] = __shfl_sync(0xffffffffu, v0 * sizeof(T), j);
-  }
   const uint32_t total = pre[PER];
   auto vptr = [&](uint32_t f) -> V* {
     unsigned j = 0;
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
-    uint8_t* b = bj[0];
     uint32_t off = pre[0];
-    uint64_t tt = tj[0], bo = oj[0];
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k)
-      if (j == k) { b = bj[k]; off = pre[k]; tt = tj[k]; bo = oj[k]; }
-    if (CHASE) b = chase_base<true>(a, tt, nullptr) + bo;  // address re-derived through the chain
+      if (j == k) off = pre[k];
+    uint8_t* b = CHASE ? chase_base<true>(a, my[j].t, nullptr) + my[j].v0 * sizeof(T)   // re-derived through the chain
+                       : my[j].vbase;
     return reinterpret_cast<V*>(b) + (f - off);
   };
   constexpr int U = CF_GROUP_WARP_U;
   uint32_t f = lane;
   for (; f + (U - 1) * 32 < total; f += U * 32) {
-    V* ptr[U];
     V r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      ptr[u] = vptr(f + u * 32);
-      r[u] = VT::ld(ptr[u]);
-    }
+    for (int u = 0; u < U; ++u) r[u] = VT::ld(vptr(f + u * 32));
 #pragma unroll
-    for (int u = 0; u < U; ++u) VT::st(ptr[u], VT::mul(r[u], s));
+    for (int u = 0; u < U; ++u) VT::st(vptr(f + u * 32), VT::mul(r[u], s));
   }
   for (; f < total; f += 32) {
     V* p = vptr(f);
@@ -956,14 +953,13 @@ __device__ __forceinline__ void scale_group_warp(const ScaleArgs& a, uint64_t g,
   // scalar heads / tails (packed layouts only)
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) {
-    const uint64_t ej0 = __shfl_sync(0xffffffffu, e0, j), ej1 = __shfl_sync(0xffffffffu, e1, j);
-    const uint64_t vj0 = __shfl_sync(0xffffffffu, v0, j);
-    uint8_t* arr = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base), j));
+    const Slot& sj = my[j];
+    uint8_t* arr = sj.arr;
     if (arr == nullptr) continue;
-    const uint64_t vj1 = vj0 + uint64_t(pre[j + 1] - pre[j]) * VN;
-    for (uint64_t i = ej0 + lane; i < vj0; i += 32)
+    const uint64_t vj1 = sj.v0 + uint64_t(pre[j + 1] - pre[j]) * VN;
+    for (uint64_t i = sj.e0 + lane; i < sj.v0; i += 32)
       scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
-    for (uint64_t i = vj1 + lane; i < ej1; i += 32)
+    for (uint64_t i = vj1 + lane; i < sj.e1; i += 32)
       scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
   }
 }
@@ -982,15 +978,14 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
   constexpr uint64_t VN = VT::N;
   constexpr unsigned WARPS = SCALE_THREADS / 32;
   constexpr unsigned PER = (GROUP_PARTS + WARPS - 1) / WARPS;
+  // per part: the vector base, the array (nullptr: nothing to stream), its A field (attached by
+  // this warp, nullptr: not attached) and host value -- in shared memory, not registers, across
+  // the streaming loop (see scale_group_warp)
+  struct Slot { uint8_t* vbase; uint8_t* arr; uint32_t* fa; uint64_t hv, v0; };
+  __shared__ Slot slots[WARPS][PER];
   const LeafOwn& o = a.own;
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t q = a.sh.q;
-  const bool leaf = int(o.level) == int(a.sh.depth);
-  const uint64_t child = leaf ? LEAF_NODE_SIZE : NODE_SIZE;
-  const uint32_t off_a = leaf ? LEAF_OFF_A : OFF_A;
-  uint8_t* base = nullptr;   // attached array base (device), nullptr: nothing to stream
-  uint32_t* fa = nullptr;    // the record's A field, attached by this lane
-  uint64_t hv = 0, v0 = 0;
+  Slot* my = slots[warp];
   uint32_t nv = 0;
 #if CF_OWN_CONTIG
   const uint32_t slot = warp * PER + lane;   // warp w: parts [w PER, (w + 1) PER) of the group
@@ -998,59 +993,65 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
   const uint32_t slot = warp + WARPS * lane;
 #endif
   const uint64_t pj = g * o.gp + slot;
-  if (lane < PER && slot < o.gp && pj < o.nt) {
-    const uint32_t ord = o.o0 + uint32_t(pj);
-    const uint32_t par = q > 1 ? uint32_t(__umul64hi(uint64_t(ord), o.qmagic)) : ord;
-    const uint64_t blk = o.parent[par - o.p_first];
-    const uint64_t rec = blk + uint64_t(ord - par * q) * child;
-    if (blk == 0 || !rec_inside(rec, a.image, a.sh.image_bytes, child)) {
-      raise_bad(a.bad, pj | FAULT_RESOLVE);
-    } else {
-      uint32_t* f = reinterpret_cast<uint32_t*>(rec + off_a);
-      const bool mis = (reinterpret_cast<uintptr_t>(f) & 7) != 0;
-      hv = mis ? (uint64_t(f[0]) | (uint64_t(f[1]) << 32)) : *reinterpret_cast<const uint64_t*>(f);
-      const uint64_t cnt = *reinterpret_cast<const uint32_t*>(rec + OFF_NA);
-      const uint64_t d = hv - o.from;
-      if (d >= o.total) {
-        raise_bad(a.bad, pj | FAULT_ATTACH);
+  if (lane < PER) {
+    uint8_t* base = nullptr;   // attached array base (device), nullptr: nothing to stream
+    uint32_t* fa = nullptr;    // the record's A field, attached by this lane
+    uint64_t hv = 0, v0 = 0;
+    if (slot < o.gp && pj < o.nt) {
+      const uint32_t q = a.sh.q;
+      const bool leaf = int(o.level) == int(a.sh.depth);
+      const uint64_t child = leaf ? LEAF_NODE_SIZE : NODE_SIZE;
+      const uint32_t off_a = leaf ? LEAF_OFF_A : OFF_A;
+      const uint32_t ord = o.o0 + uint32_t(pj);
+      const uint32_t par = q > 1 ? uint32_t(__umul64hi(uint64_t(ord), o.qmagic)) : ord;
+      const uint64_t blk = o.parent[par - o.p_first];
+      const uint64_t rec = blk + uint64_t(ord - par * q) * child;
+      if (blk == 0 || !rec_inside(rec, a.image, a.sh.image_bytes, child)) {
+        raise_bad(a.bad, pj | FAULT_RESOLVE);
       } else {
-        const uint64_t dv = o.to + d;
-        if (mis) { f[0] = uint32_t(dv); f[1] = uint32_t(dv >> 32); }
-        else *reinterpret_cast<uint64_t*>(f) = dv;
-        fa = f;
-        uint8_t* arr = reinterpret_cast<uint8_t*>(dv);
-        if (uint64_t(o.n_el) > cnt || arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes ||
-            cnt * sizeof(T) > a.sh.image_bytes - uint64_t(arr - a.image)) {
-          raise_bad(a.bad, pj | FAULT_SCALE);
+        uint32_t* f = reinterpret_cast<uint32_t*>(rec + off_a);
+        const bool mis = (reinterpret_cast<uintptr_t>(f) & 7) != 0;
+        hv = mis ? (uint64_t(f[0]) | (uint64_t(f[1]) << 32)) : *reinterpret_cast<const uint64_t*>(f);
+        const uint64_t cnt = *reinterpret_cast<const uint32_t*>(rec + OFF_NA);
+        const uint64_t d = hv - o.from;
+        if (d >= o.total) {
+          raise_bad(a.bad, pj | FAULT_ATTACH);
         } else {
-          base = arr;
-          const uintptr_t first = reinterpret_cast<uintptr_t>(arr);
-          v0 = o.n_el;
-          if ((first % sizeof(T)) == 0) v0 = min(uint64_t(o.n_el), uint64_t(((16 - (first & 15)) & 15) / sizeof(T)));
-          nv = uint32_t((o.n_el - v0) / VN);
+          const uint64_t dv = o.to + d;
+          if (mis) { f[0] = uint32_t(dv); f[1] = uint32_t(dv >> 32); }
+          else *reinterpret_cast<uint64_t*>(f) = dv;
+          fa = f;
+          uint8_t* arr = reinterpret_cast<uint8_t*>(dv);
+          if (uint64_t(o.n_el) > cnt || arr < a.image || uint64_t(arr - a.image) > a.sh.image_bytes ||
+              cnt * sizeof(T) > a.sh.image_bytes - uint64_t(arr - a.image)) {
+            raise_bad(a.bad, pj | FAULT_SCALE);
+          } else {
+            base = arr;
+            const uintptr_t first = reinterpret_cast<uintptr_t>(arr);
+            v0 = o.n_el;
+            if ((first % sizeof(T)) == 0) v0 = min(uint64_t(o.n_el), uint64_t(((16 - (first & 15)) & 15) / sizeof(T)));
+            nv = uint32_t((o.n_el - v0) / VN);
+          }
         }
       }
     }
+    my[lane] = Slot{base + v0 * sizeof(T), base, fa, hv, v0};
   }
+  __syncwarp();   // the slots are visible to the whole warp
   uint32_t pre[PER + 1];
   pre[0] = 0;
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) pre[j + 1] = pre[j] + __shfl_sync(0xffffffffu, nv, j);
-  uint8_t* bj[PER];
-#pragma unroll
-  for (unsigned j = 0; j < PER; ++j)
-    bj[j] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base + v0 * sizeof(T)), j));
   const uint32_t total = pre[PER];
   auto vptr = [&](uint32_t f) -> V* {
     unsigned j = 0;
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k) j += f >= pre[k];
-    uint8_t* b = bj[0];
     uint32_t off = pre[0];
 #pragma unroll
     for (unsigned k = 1; k < PER; ++k)
-      if (j == k) { b = bj[k]; off = pre[k]; }
-    return reinterpret_cast<V*>(b) + (f - off);
+      if (j == k) off = pre[k];
+    return reinterpret_cast<V*>(my[j].vbase) + (f - off);
   };
   constexpr int U = CF_OWN_U;
   uint32_t f = lane;
@@ -1068,17 +1069,19 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
   // scalar heads / tails (packed layouts only)
 #pragma unroll
   for (unsigned j = 0; j < PER; ++j) {
-    uint8_t* arr = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(base), j));
-    const uint64_t vj0 = __shfl_sync(0xffffffffu, v0, j);
+    uint8_t* arr = my[j].arr;
     if (arr == nullptr) continue;
-    const uint64_t vj1 = vj0 + uint64_t(pre[j + 1] - pre[j]) * VN;
+    const uint64_t vj0 = my[j].v0, vj1 = vj0 + uint64_t(pre[j + 1] - pre[j]) * VN;
     for (uint64_t i = lane; i < vj0; i += 32)
       scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
     for (uint64_t i = vj1 + lane; i < o.n_el; i += 32)
       scalar_st<T>(arr + i * sizeof(T), mul_rn<T>(scalar_ld<T>(arr + i * sizeof(T)), s));
   }
-  // detach: the host value back into the record
-  if (fa) {
+  // detach: the owners write the host value back into the record (after their warp's stores of
+  // the array -- other lanes' stores are to the array, never to the record)
+  if (lane < PER && my[lane].fa) {
+    uint32_t* fa = my[lane].fa;
+    const uint64_t hv = my[lane].hv;
     if ((reinterpret_cast<uintptr_t>(fa) & 7) != 0) { fa[0] = uint32_t(hv); fa[1] = uint32_t(hv >> 32); }
     else *reinterpret_cast<uint64_t*>(fa) = hv;
   }

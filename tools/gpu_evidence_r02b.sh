@@ -2,7 +2,7 @@
 # Round-2 evidence after the leaf-owned C4 path: GPU suite, bench lines (C2 default with
 # per_config, C3, C4, C5, reference arm), launch lists, full ncu captures.  Outputs in gpurun_out/r02b/.
 set -u
-OUT=gpurun_out/r02b; mkdir -p $OUT
+OUT=${OUT:-gpurun_out/r02b}; mkdir -p $OUT
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/gputests.log 2>&1; echo "gpu tests rc=$?"; tail -2 $OUT/gputests.log
 timeout 900 python bench.py > $OUT/bench_C2.json 2> $OUT/bench_C2.err; head -c 300 $OUT/bench_C2.json; echo
 for CFG in C3 C4; do

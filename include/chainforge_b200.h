@@ -393,8 +393,13 @@ int cf_window_plan(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out);
  * partition the arena; every site is attached once, in the step that uploads it; every target's
  * chain -- walked through the tree's site table -- has landed by its resolve step and ends at its
  * array's owner; the leaf-kernel parts tile each target's elements once, after their bytes land;
- * no segment is detached or copied back before its last reader or writer.  Returns
- * CF_E_STATE (first violation in cf_last_error) if any invariant fails. */
+ * no segment is detached or copied back before its last reader or writer.  Leaf-owned ranges
+ * (steps whose whole small leaf arrays form one run of consecutive ordinals: the leaf kernel
+ * attaches, streams and detaches them, and they appear in no table) are checked too: table sites
+ * plus owned A fields are every site exactly once, each owned target lies in its step's range
+ * with that range's count, after its bytes and chain, and its record stays on the device until
+ * its leaf kernel ran.  Returns CF_E_STATE (first violation in cf_last_error) if any invariant
+ * fails. */
 typedef struct {
   uint64_t nsteps, nsegments, nsites, ntargets, nparts, ngroups, ntiles, table_bytes, zero_copy_node_segments;
   int32_t violations;

@@ -1,5 +1,6 @@
 """Soak test: minutes of back-to-back windows in every mode on every config, verifying the result
-after each batch against payload_values x the net scale.  Catches rare races (the torn pointer
+after each batch against payload_values x the net scale (dense configs: the whole copy-back against
+the oracle's expected arena).  Catches rare races (the torn pointer
 read needed ~1000 windows).  python tools/soak.py SECONDS [configs...]"""
 import sys
 import time
@@ -31,6 +32,15 @@ for cfg in cfgs:
     t = w.twin()
     off, cnt, lvl = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT), w.table(N.CF_TAB_ARR_LEVEL)
     src = w.host_src().copy()
+    # the whole copy-back of the twin (scale 0.5 last) against the oracle's expected arena
+    from oracle import oracle as O
+    kind = {"DenseSpec": O.DENSE}.get(type(spec).__name__)
+    full = None
+    if kind is not None:
+        ot = O.build(O.OSpec(kind, spec.q, spec.n, spec.depth, elem=spec.elem, leaf_only=spec.leaf_only, align=align),
+                     1, ptr_base=w.src)
+        pol = {"all_leaves": O.TARGET_ALL_LEAVES, "all_arrays": O.TARGET_ALL_ARRAYS, "ref": O.TARGET_REF}[policy]
+        full = O.expected_after_window(ot, O.targets(ot, pol), 0.5)[:w.total]
     end = min(deadline, time.time() + per)
     it = 0
     while time.time() < end:
@@ -43,6 +53,8 @@ for cfg in cfgs:
         # checks: the image is back to the source, the twin's copy-back holds leaves x 0.5
         assert np.array_equal(w.image_bytes(), src), (cfg, it, "resident")
         got = t.host_dst()
+        if full is not None:
+            assert np.array_equal(got, full), (cfg, it, "whole copy-back")
         for i in (int(w.targets[0]), int(w.targets[len(w.targets) // 2]), int(w.targets[-1])):
             a, n = int(off[i]), int(cnt[i])
             dt = np.float32 if spec.elem == 4 else np.float64

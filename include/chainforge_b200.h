@@ -428,6 +428,12 @@ int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_eve
 int cf_window_run_n_flushed(cf_window* w, int nruns, double scale_even, double scale_odd, void* flush_buf,
                             uint64_t flush_bytes, cf_window_stats* stats);
 int cf_window_set_scale(cf_window* w, double scale);
+/* Diagnostics (tests): CF_WIN_DEBUG_KEEP_LEAF_ATTACHED makes the leaf kernel of leaf-owned steps
+ * skip the detach of the A fields it attached, so the image (and a copy-back) shows the device
+ * addresses it wrote -- evidence that leaf-owned relocation attaches.  Drops the window's cached
+ * graphs.  0 restores normal windows. */
+enum { CF_WIN_DEBUG_KEEP_LEAF_ATTACHED = 1 };
+int cf_window_debug(cf_window* w, uint32_t flags);
 int cf_window_free(cf_window* w);
 
 #ifdef __cplusplus

@@ -38,6 +38,7 @@ CF_WIN_FULL = (CF_WIN_H2D | CF_WIN_TABLES | CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_
                | CF_WIN_DETACH | CF_WIN_D2H)
 CF_WIN_RESIDENT = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH
 CF_WIN_UVM = 1 << 8
+CF_WIN_DEBUG_KEEP_LEAF_ATTACHED = 1
 NO_BAD = (1 << 64) - 1
 
 _TAB_DTYPES = {CF_TAB_NODE_LEVEL: np.int32, CF_TAB_NODE_SIZE: np.uint32, CF_TAB_ARR_LEVEL: np.int32}
@@ -56,7 +57,7 @@ EXPORTED = (
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_ring", "cf_window_run_n_flushed",
-    "cf_window_set_scale",
+    "cf_window_set_scale", "cf_window_debug",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
 )
@@ -181,6 +182,7 @@ def _declare(L):
         "cf_window_run_ring": (C.c_int, [C.POINTER(P), C.c_int, C.c_int, C.c_double, C.c_double,
                                          C.POINTER(CfWindowStats)]),
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
+        "cf_window_debug": (C.c_int, [P, C.c_uint32]),
         "cf_window_run_n_flushed": (C.c_int, [P, C.c_int, C.c_double, C.c_double, P, U64, C.POINTER(CfWindowStats)]),
         "cf_window_free": (C.c_int, [P]),
         "cf_uvm_prefetch": (C.c_int, [P, P, U64, C.c_int, P]),

@@ -95,6 +95,7 @@ struct LeafOwn {
   const uint64_t* parent;   // device: child block of parent ordinal p_first + p (0 = broken chain)
   uint32_t on, level, o0, p_first, nparents, n_el, gp, nt;
   uint64_t qmagic, from, to, total;
+  uint32_t keep_attached;   // diagnostics: skip the detach (CF_WIN_DEBUG_KEEP_LEAF_ATTACHED)
 };
 int launch_attach_parents(cf_ctx* ctx, uint8_t* image, uint64_t total, const uint64_t* sites, uint64_t nsites,
                           uint64_t from, uint64_t to, const cf_chain_shape& sh, const LeafOwn& own, uint64_t* parent,

@@ -1079,7 +1079,7 @@ __device__ __forceinline__ void scale_group_owned(const ScaleArgs& a, uint64_t g
   }
   // detach: the owners write the host value back into the record (after their warp's stores of
   // the array -- other lanes' stores are to the array, never to the record)
-  if (lane < PER && my[lane].fa) {
+  if (lane < PER && my[lane].fa && !o.keep_attached) {
     uint32_t* fa = my[lane].fa;
     const uint64_t hv = my[lane].hv;
     if ((reinterpret_cast<uintptr_t>(fa) & 7) != 0) { fa[0] = uint32_t(hv); fa[1] = uint32_t(hv >> 32); }

@@ -59,6 +59,7 @@ struct cf_window {
   std::vector<LeafOwn> own_step;       // per step (on == 0: none)
   uint64_t parent_base = 0;            // parent ordinal of d_parent[0]
   uint64_t own_parents = 0;            // d_parent entries
+  uint32_t debug = 0;                  // CF_WIN_DEBUG_* (cf_window_debug)
   uint64_t* d_parent = nullptr;
   std::vector<cf_scale_work> seg;      // leaf-kernel work per step (device pointers set at plan)
   std::vector<uint64_t> det_lo;        // detach-site ranges per step
@@ -1053,6 +1054,18 @@ int cf_window_plan_check(const cf_window_desc* desc, cf_plan_check* out) {
   return ck.violations ? CF_E_STATE : CF_OK;
 }
 
+int cf_window_debug(cf_window* w, uint32_t flags) {
+  if (!w) return fail(CF_E_INVALID, "null window");
+  CfDevice g(w->ctx);
+  if (!w->graphs.empty()) {   // captured with the old setting
+    CF_CUDA(cudaStreamSynchronize(w->stream));
+    for (auto& gr : w->graphs) CF_CUDA(cudaGraphExecDestroy(gr.exec));
+    w->graphs.clear();
+  }
+  w->debug = flags;
+  return CF_OK;
+}
+
 int cf_window_set_scale(cf_window* w, double scale) {
   if (!w) return fail(CF_E_INVALID, "null window");
   w->d.scale = scale;
@@ -1275,6 +1288,7 @@ int enqueue(cf_window* w, bool timing, uint64_t* h2d_out, uint64_t* d2h_out) {
       own.from = d.host_base;
       own.to = dimg;
       own.total = w->total;
+      own.keep_attached = (w->debug & CF_WIN_DEBUG_KEEP_LEAF_ATTACHED) ? 1u : 0u;
       // every site of the step attached (the resolver-owned tail too: its resolvers run after)
       // || the owned range's parents resolved into the parent table
       CF_TRY(launch_attach_parents(c, img, w->total, dsites + w->reloc_lo[k], ns, d.host_base, dimg, w->sh, own,

@@ -134,3 +134,37 @@ def test_leaf_owned_relocation_faults(cf, bad, exc):
         src[:] = keep
     finally:
         w.close()
+
+
+def test_leaf_owned_steps_attach_the_leaf_fields(cf, oracle):
+    """Leaf-owned relocation really attaches: with the detach suppressed (CF_WIN_DEBUG_KEEP_LEAF_ATTACHED)
+    every owned leaf record's A field holds the device address of its array (image + offset, the
+    value memory.py:316-323 writes), in the resident image and in a multi-step window's copy-back;
+    every other byte is the normal window's result (node pointers detached, leaves scaled)."""
+    from paper_1906_01128_b200 import _native as N
+    spec = cf.DenseSpec(16, 4, 4, elem=4, leaf_only=True)
+    w = cf.DeepCopyWindow(spec, seed=2, policy="all_leaves", align=16, chunk_bytes=1 << 16)
+    try:
+        ot = oracle.build(oracle.spec_from_json({"kind": "dense", "q": 16, "n": 4, "depth": 4}, elem=4, align=16,
+                                                leaf_only=True), 2, ptr_base=w.src)
+        want = oracle.expected_after_window(ot, oracle.targets(ot, oracle.TARGET_ALL_LEAVES), 2.0)[:w.total]
+        owner, off = w.table(N.CF_TAB_ARR_OWNER), w.table(N.CF_TAB_ARR_OFF)
+        fields = np.array([int(owner[t]) + 4 for t in w.targets.tolist()], np.int64)
+        attached = want.copy()
+        for f, t in zip(fields.tolist(), w.targets.tolist()):
+            attached[f:f + 8] = np.frombuffer(int(w.image + int(off[t])).to_bytes(8, "little"), np.uint8)
+        res = w._window(N.CF_WIN_RESIDENT, 0, "resolved")
+        full = w._window(N.CF_WIN_FULL, w.chunk_bytes, "resolved")
+        for h in (res, full):
+            N.check(N.lib().cf_window_debug(h, N.CF_WIN_DEBUG_KEEP_LEAF_ATTACHED))
+        w.upload_raw()
+        assert w.run_resident(scale=2.0).bad == NO_BAD
+        assert np.array_equal(w.image_bytes(), attached), "resident image"
+        assert w.run(scale=2.0).bad == NO_BAD
+        assert np.array_equal(w.host_dst(), attached), "multi-step window copy-back"
+        for h in (res, full):
+            N.check(N.lib().cf_window_debug(h, 0))
+        assert w.run(scale=2.0).bad == NO_BAD
+        assert np.array_equal(w.host_dst(), want)
+    finally:
+        w.close()

@@ -98,7 +98,8 @@ def workload_config(name: str, world: int, leaf_elems: int = 0, elem: int = 4) -
             "l2": ("inputs >= 1 GiB per GPU exceed the 126 MB L2 (no flush needed)" if per_gpu >= L2_FLUSH_BELOW else
                    "working set below 512 MiB: the GPU arm's e2e steps rotate over device images and copy-back "
                    f"buffers totalling >= {RING_BYTES >> 20} MiB (inputs larger than the 126 MB L2); its resident "
-                   "steps are each preceded by an L2 flush (512 MiB device memset) outside the timed intervals"),
+                   "steps are each preceded by an L2 flush (a read pass over a 512 MiB device buffer: clean lines, nothing "
+                   "written back inside a step) outside the timed intervals"),
             "parallelism": f"dp{world} ({scaling}-scaled subtree shards, one per GPU, no data-path collective)"}
 
 
@@ -463,8 +464,10 @@ def verify_gather(w, shard, spec, dist: Dist, device: int, ndev: int, src_factor
 
 
 class L2Flush:
-    """Evicts the L2 between timed steps (a 512 MiB device memset on the window's stream, outside
-    the timed intervals) and times each step on the device (CUDA events inside the window)."""
+    """Evicts the L2 between timed steps (a read pass over a 512 MiB device buffer on the window's
+    stream, outside the timed intervals: the L2 is left holding clean lines, so nothing of the
+    flush is written back inside a timed step) and times each step on the device (CUDA events
+    inside the window)."""
 
     def __init__(self, w):
         import ctypes as C
@@ -473,9 +476,10 @@ class L2Flush:
         self.N, self.w = N, w
         self.buf = C.c_void_p()
         N.check(N.lib().cf_dev_alloc(w.ctx.handle, L2_FLUSH_BELOW, C.byref(self.buf)))
+        N.check(N.lib().cf_memset(w.ctx.handle, self.buf, 0x5A, L2_FLUSH_BELOW))   # defined contents
 
     def flush(self) -> None:
-        self.N.check(self.N.lib().cf_memset(self.w.ctx.handle, self.buf, 0x5A, L2_FLUSH_BELOW))
+        self.N.check(self.N.lib().cf_l2_evict(self.w.ctx.handle, self.buf, L2_FLUSH_BELOW))
 
     def steps(self, flags: int, n: int):
         return self.w.run_n_flushed(n, self.buf.value, L2_FLUSH_BELOW, flags=flags)

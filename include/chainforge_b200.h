@@ -158,6 +158,9 @@ int cf_dev_free(cf_ctx* ctx, void* p);
 int cf_memcpy(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int cf_memcpy_async(cf_ctx* ctx, void* dst, const void* src, uint64_t bytes, void* stream);
 int cf_memset(cf_ctx* ctx, void* dst, int value, uint64_t bytes);
+/* Benchmark plumbing: evict the L2 by a read pass over `bytes` of device memory at buf (clean
+ * lines, unlike a memset).  Synchronous on the context's compute stream. */
+int cf_l2_evict(cf_ctx* ctx, const void* buf, uint64_t bytes);
 /* Host-link roofline probe (no reference counterpart): plain cudaMemcpyAsync of
  * `bytes` between fresh pinned host buffers and HBM -- H2D alone, D2H alone, and H2D || D2H on
  * two streams -- each sample `iters` back-to-back copies, best of `reps` samples after one
@@ -422,9 +425,10 @@ int cf_window_run_pair(cf_window* w0, cf_window* w1, int nruns, double scale_eve
  * L2, so no step finds its data cached by an earlier one while the steps still overlap. */
 int cf_window_run_ring(cf_window* const* ws, int nw, int nruns, double scale_even, double scale_odd,
                        cf_window_stats* stats);
-/* As cf_window_run_n for working sets that fit the L2: before every window, a memset of
- * flush_bytes at flush_buf (device) evicts the L2; stats->ms_total is the sum of the windows' own
- * intervals (CUDA events after each flush and after each window), flushes excluded. */
+/* As cf_window_run_n for working sets that fit the L2: before every window, a read pass over
+ * flush_bytes at flush_buf (device) evicts the L2 (clean lines: nothing of the flush is written
+ * back inside the timed window); stats->ms_total is the sum of the windows' own intervals (CUDA
+ * events after each flush and after each window), flushes excluded. */
 int cf_window_run_n_flushed(cf_window* w, int nruns, double scale_even, double scale_odd, void* flush_buf,
                             uint64_t flush_bytes, cf_window_stats* stats);
 int cf_window_set_scale(cf_window* w, double scale);

@@ -128,6 +128,8 @@ int launch_naive_fixup(cf_ctx* ctx, const uint64_t* field_host, const uint64_t* 
                        uint64_t nsites, const uint64_t* map_host, const uint64_t* map_size,
                        const uint64_t* map_dev, uint64_t nmap, uint64_t* bad, cudaStream_t s);
 int launch_fill_u64(cf_ctx* ctx, uint64_t* p, uint64_t value, uint64_t n, cudaStream_t s);
+// L2 eviction by a read pass over a device buffer (clean lines: nothing to write back later).
+int launch_evict_read(cf_ctx* ctx, const void* buf, uint64_t bytes, cudaStream_t s);
 // (lo, hi) byte segments copied src+lo -> dst+lo by the SMs (mapped host memory allowed).
 int launch_seg_copy(cf_ctx* ctx, const uint64_t* segs, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t s);
 

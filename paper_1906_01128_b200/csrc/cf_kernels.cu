@@ -1334,6 +1334,19 @@ __global__ void __launch_bounds__(256) k_checksum(const uint64_t* __restrict__ a
   }
 }
 
+// L2 eviction by a read pass (benchmark plumbing): every line of the buffer is loaded, so the L2
+// ends up holding clean lines of it -- unlike a memset, whose dirty lines would be written back
+// inside the next timed window.  The (never true) store keeps the loads alive.
+__global__ void __launch_bounds__(256) k_evict_read(const uint4* __restrict__ p, uint64_t n16, uint32_t* sink) {
+  uint32_t acc = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = __ldcg(p + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u && sink) *sink = acc;
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t v, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -1554,6 +1567,14 @@ int debug_info(uint64_t* out, int reset) {
     static const uint64_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     CF_CUDA(cudaMemcpyToSymbol(g_dbg, z, sizeof z));
   }
+  return CF_OK;
+}
+
+int launch_evict_read(cf_ctx* ctx, const void* buf, uint64_t bytes, cudaStream_t s) {
+  if (bytes < 16) return CF_OK;
+  k_evict_read<<<unsigned(std::max(1, ctx->sm_count) * 8), 256, 0, s>>>(static_cast<const uint4*>(buf), bytes / 16,
+                                                                           nullptr);
+  CF_LAUNCHED(ctx);
   return CF_OK;
 }
 

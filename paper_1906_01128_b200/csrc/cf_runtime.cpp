@@ -302,6 +302,14 @@ int cf_memcpy_async(cf_ctx* c, void* dst, const void* src, uint64_t bytes, void*
   return CF_OK;
 }
 
+int cf_l2_evict(cf_ctx* c, const void* buf, uint64_t bytes) {
+  if (!c || (bytes && !buf)) return fail(CF_E_INVALID, "bad arguments");
+  CfDevice g(c);
+  CF_TRY(launch_evict_read(c, buf, bytes, c->compute));
+  CF_CUDA(cudaStreamSynchronize(c->compute));
+  return CF_OK;
+}
+
 int cf_memset(cf_ctx* c, void* dst, int value, uint64_t bytes) {
   if (!c) return fail(CF_E_INVALID, "null ctx");
   CfDevice g(c);

@@ -1158,8 +1158,9 @@ int cf_window_run_n_flushed(cf_window* w, int nruns, double scale_even, double s
   uint64_t h2d = 0, d2h = 0;
   CF_TRY(batch_begin(w->ctx, &w, 1, w->ev_first));
   for (int r = 0; r < nruns; ++r) {
-    // evict the working set from L2 (outside the timed interval), then time this window alone
-    if (flush_bytes) CF_CUDA(cudaMemsetAsync(flush_buf, 0x5A, flush_bytes, w->stream));
+    // evict the working set from L2 (outside the timed interval) with a read pass -- clean lines,
+    // so no write-back of the flush lands inside the window -- then time this window alone
+    if (flush_bytes) CF_TRY(launch_evict_read(w->ctx, flush_buf, flush_bytes, w->stream));
     CF_CUDA(cudaEventRecord(ev[2 * r], w->stream));
     w->d.scale = (r & 1) ? scale_odd : scale_even;
     uint64_t a = 0, b = 0;

@@ -43,6 +43,8 @@ CASES = [
     (100, 3, 4, 4, True),
     (5000, 1, 2, 4, True),     # depth 1: the parent is the root
     (4500, 1, 7, 8, False),
+    (65, 2, 2048, 4, True),    # 8 KiB leaves: 4 per group
+    (70, 2, 3801, 4, True),    # 15.2 KB leaves (just under a tile): 2 per group, scalar tails
 ]
 
 

@@ -626,6 +626,7 @@ def summary_block(name: str, elem: int, device: int, chunk_mb: int, numa_node: i
         st_res, _ = m.timed(N.CF_WIN_RESIDENT | m.gflag, warmup, steps, dist)
         res_ms = st_res.ms_total / steps
         k_ms, _ = m.kernel_ms(max(5, steps // 2))
+        table = table_resolve_block(m, name, warmup, steps, dist, res_ms)
         h2d, d2h = st_e2e.h2d_bytes // steps, st_e2e.d2h_bytes // steps
         probe = link_1g if m.total >= (64 << 20) else plain_link(m.w.ctx, m.total, iters=8)
         ideal = (h2d + d2h) / (probe["bidir"] * 1e9) * 1e3
@@ -642,9 +643,26 @@ def summary_block(name: str, elem: int, device: int, chunk_mb: int, numa_node: i
                    if batches > 1 else {}),
                 "link_probe_gbs": probe, "link_probe_bytes": LINK_PROBE_BYTES if probe is link_1g else m.total,
                 "frac_of_link_roofline": round(ideal / e2e_ms, 4),
-                "e2e_windows": m.e2e_layout}
+                "e2e_windows": m.e2e_layout,
+                **({"table_resolve": table} if table else {})}
     finally:
         m.close()
+
+
+def table_resolve_block(m, name: str, warmup: int, steps: int, dist, res_ms: float) -> dict:
+    """C4 (many small leaves): the same resident step planned without leaf ownership
+    (CF_WIN_TABLE_RESOLVE: every leaf resolved into the EA table, every site listed) -- the
+    table-driven design the leaf-owned step replaces, timed in the same run."""
+    if name != "C4":
+        return {}
+    N = m.N
+    m.w.upload_raw()
+    st, _ = m.timed(N.CF_WIN_RESIDENT | N.CF_WIN_TABLE_RESOLVE | m.gflag, warmup, steps, dist)
+    t_ms = dist.max(st.ms_total) / steps
+    m.w.upload_raw()
+    return {"resident_ms_per_step": round(t_ms, 4), "leaf_owned_resident_ms_per_step": round(res_ms, 4),
+            "what": "resident step planned with CF_WIN_TABLE_RESOLVE (EA table + full site list) vs the "
+                    "leaf-owned step of this line"}
 
 
 def run_ours(args, dist: Dist) -> None:
@@ -691,6 +709,8 @@ def run_ours(args, dist: Dist) -> None:
     res_wall_ms = dist.max(wall_res) * 1e3 / args.steps
     # ---- leaf-kernel duration (events around the k_scale launch, resident, after warm-up)
     kernel_ms, _ = m.kernel_ms(max(5, args.steps // 2))
+    # ---- C4: the table-driven resident step (no leaf ownership) beside it
+    table = table_resolve_block(m, args.config, args.warmup, args.steps, dist, res_ms) if not args.leaf_elems else {}
     # ---- chase-per-access comparison (same resident image)
     chase = {}
     if not args.skip_chase:
@@ -762,7 +782,8 @@ def run_ours(args, dist: Dist) -> None:
                      "ncu_dram_pct_of_peak": ncu_record(args.config).get("dram_pct_of_ncu_peak"),
                      "algorithmic_bytes_per_launch": m.kernel_traffic, "kernel_ms": round(kernel_ms, 4),
                      "share_of_resident_step": round(kernel_ms / res_ms, 4)},
-        "modes": {"resolved": {"kernel_ms": round(kernel_ms, 4), "hbm_gbs": round(achieved, 1)}, "chase": chase},
+        "modes": {"resolved": {"kernel_ms": round(kernel_ms, 4), "hbm_gbs": round(achieved, 1)}, "chase": chase,
+                  **({"table_resolve": table} if table else {})},
         "gpu_launches": int(st_res.launches),
         "numa": {"gpu_node": numa_node, "host_arenas": "allocated on the GPU's node" if numa_node >= 0 else "OS placement"},
         "gather": gather,

@@ -352,10 +352,13 @@ enum {
   CF_WIN_DETACH = 1u << 5,   /* inverse relocation before copy-back */
   CF_WIN_D2H = 1u << 6,      /* copy the image back to host_dst */
   CF_WIN_GRAPH = 1u << 7,    /* capture the enqueue sequence into a CUDA graph once, replay */
-  CF_WIN_UVM = 1u << 8       /* managed-memory tree (image == host_src == host_dst): the H2D / D2H
+  CF_WIN_UVM = 1u << 8,      /* managed-memory tree (image == host_src == host_dst): the H2D / D2H
                                 steps become chunked cudaMemPrefetchAsync to the GPU / back to the
                                 CPU on the copy streams, pipelined with resolve and leaf kernel
                                 (the UVM scheme with prefetch hints, memory.py:239-261) */
+  CF_WIN_TABLE_RESOLVE = 1u << 9  /* plan-time: no leaf-owned steps -- every target is resolved
+                                     into the EA table and every site is listed (the table-driven
+                                     design the leaf-owned path is measured against) */
 };
 
 typedef struct {

@@ -38,6 +38,7 @@ CF_WIN_FULL = (CF_WIN_H2D | CF_WIN_TABLES | CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_
                | CF_WIN_DETACH | CF_WIN_D2H)
 CF_WIN_RESIDENT = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH
 CF_WIN_UVM = 1 << 8
+CF_WIN_TABLE_RESOLVE = 1 << 9
 CF_WIN_DEBUG_KEEP_LEAF_ATTACHED = 1
 NO_BAD = (1 << 64) - 1
 

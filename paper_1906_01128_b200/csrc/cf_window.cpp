@@ -447,7 +447,7 @@ int plan_impl(cf_ctx* ctx, const cf_window_desc* desc, cf_window** out, bool dry
   {
     static const bool no_leaf_own = getenv("CF_NO_LEAF_OWN") != nullptr;   // A/B switch (design experiments)
     constexpr uint32_t PHASES = CF_WIN_ATTACH | CF_WIN_RESOLVE | CF_WIN_SCALE | CF_WIN_DETACH;
-    if (!no_leaf_own && (fl & PHASES) == PHASES && !(fl & CF_WIN_UVM) && dense && !chase && w->wide_ok &&
+    if (!no_leaf_own && !(fl & CF_WIN_TABLE_RESOLVE) && (fl & PHASES) == PHASES && !(fl & CF_WIN_UVM) && dense && !chase && w->wide_ok &&
         t->tree_root.size() <= 1 && q >= 2 && t->spec.depth >= 1 && nt > 0 && nt < (1ull << 31)) {
       std::vector<uint32_t> npc(nt, 0);
       std::vector<uint64_t> pst(nt, 0);

@@ -75,6 +75,10 @@ def test_uniform_ranges_match_oracle(cf, oracle, q, depth, n, elem, leaf_only):
                     w.upload_raw()
                     assert w.run_resident(scale=2.0, graph=True).bad == NO_BAD
                     assert np.array_equal(w.image_bytes(), want), (q, depth, n, "resident graph", rep)
+                # the same step planned without leaf ownership (EA table + full site list)
+                w.upload_raw()
+                assert w.run_n(1, flags=_flags().CF_WIN_RESIDENT | _flags().CF_WIN_TABLE_RESOLVE).bad == NO_BAD
+                assert np.array_equal(w.image_bytes(), want), (q, depth, n, "table resolve")
         finally:
             w.close()
 

@@ -145,6 +145,7 @@ def test_leaf_owned_plans():
     spec, policy, _ = bench.make_spec("C4")
     out = check(spec, 16, policy, 0, flags=N.CF_WIN_RESIDENT)
     assert out.nsteps == 1 and out.leaf_owned == 1
+    assert check(spec, 16, policy, 0, flags=N.CF_WIN_RESIDENT | N.CF_WIN_TABLE_RESOLVE).leaf_owned == 0
     # the multi-step e2e window: every step owns its run of whole 1 KiB leaves; only the node-level
     # sites, the few leaves split at step boundaries and the group lists stay in the tables
     out = check(spec, 16, policy, 32 << 20)

@@ -5,10 +5,19 @@
 //                  Machine.demarshal site loop, memory.py:337-344)
 //   k_resolve     pointerchain: walk each target chain once, emit its effective address
 //                 (targeted_arrays, scenarios.py:270-284, on the device)
+//   k_attach_resolve / _wide / _uni
+//                 attach and resolve in one launch: one CTA (small windows), side by side
+//                 (aligned fields), memory-parallel over uniform ordinal ranges (32 U targets
+//                 per warp, parents walked one per lane)
+//   k_attach_parents
+//                 leaf-owned steps: attach the step's sites || resolve the owned range's parents
+//                 into the parent table (the leaf kernel does the rest of each chain)
 //   k_scale       leaf kernel x *= s (_scale_block, harness.py:307-309) in two modes:
 //                   RESOLVED  reads the effective-address table (pointerchain)
 //                   CHASE     re-walks the chain per 16-byte access with non-hoistable loads
 //                             (Listing 2 per-iteration chain)
+//                 and, for leaf-owned steps (RESOLVED), a path whose warps find each leaf record
+//                 from the parent table, attach its A field, stream the array and detach it
 //   k_naive_fixup per-object deep-copy fix-ups through a sorted interval map
 //                 (naive_deep_copy + AddressMap.translate, memory.py:349-365, 409-419)
 //   k_seg_copy / k_copy_list
@@ -16,6 +25,7 @@
 //                 layouts, and per-object copies of small objects (naive / pointerchain schemes)
 //   k_checksum    per-leaf checksums for the multi-GPU result gather
 //   k_sm_copy     SM-driven bulk copy (host-link experiments only)
+//   k_evict_read  L2 eviction by a read pass (benchmark plumbing for L2-sized working sets)
 //
 // All of these are HBM/latency-bound integer or streaming work: no tensor cores.  The leaf
 // kernel is the HBM-roofline kernel: 16-byte vector loads/stores with streaming cache hints,

@@ -680,7 +680,15 @@ static_assert(TILE_BYTES / 16 + CF_SHIFT_ALIGN / 16 + 1 <= uint64_t(SHIFT_ROWS) 
               "one pass must cover a tile");
 
 template <bool CHASE>
-__device__ __forceinline__ void scale_f64_shifted(const ScaleArgs& a, uint64_t t, uint8_t* arr, uint64_t e0,
+#ifndef CF_F64_SHIFT_NOINLINE
+#define CF_F64_SHIFT_NOINLINE 0
+#endif
+#if CF_F64_SHIFT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void scale_f64_shifted(const ScaleArgs& a, uint64_t t, uint8_t* arr, uint64_t e0,
                                                   uint64_t e1, double s) {
   constexpr int U = SHIFT_ROWS;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -183,6 +183,15 @@ int cf_tree_build(const cf_tree* tree, void* host, uint64_t ptr_base, uint64_t s
  * array indices into out (capacity cap) and their number into *n. */
 int cf_tree_targets(const cf_tree* tree, int policy, int64_t* out, uint64_t cap, uint64_t* n);
 int cf_tree_chain_shape(const cf_tree* tree, cf_chain_shape* out);
+/* UVM scheme, host side (harness.py:261-304 walk through memory.py:378-394 uvm_touch): the sorted
+ * distinct pages of every pointer field the reference's kernel walk reads -- each target's Lnext
+ * chain from root_off[i] (arena offsets; dense digits of ordinal[i] in base q), then the terminal
+ * node's A field and, when count[i] > 0, its nA field -- reading the pointer values from the
+ * arena at `arena`.  A chain leaving the arena contributes the page of its first outside field
+ * and stops (the caller's page table then raises WildAccess).  out may be NULL to size the result. */
+int cf_uvm_walk_pages(const void* arena, uint64_t total, int kind, uint32_t q, int32_t depth, const uint64_t* root_off,
+                      const int32_t* level, const uint64_t* ordinal, const uint64_t* count, uint64_t n, uint64_t page,
+                      uint64_t* out, uint64_t cap, uint64_t* npages);
 int cf_tree_free(cf_tree* tree);
 
 /* ---------------- device kernels (sm_100a) ---------------- */

@@ -58,7 +58,7 @@ EXPORTED = (
     "cf_copy_objects", "cf_naive_fixup_host", "cf_debug_info", "cf_device_numa_node", "cf_bind_numa_node",
     "cf_sm_copy", "cf_host_write_words", "cf_window_plan_check", "cf_selective_plan_check",
     "cf_window_plan", "cf_window_run", "cf_window_run_n", "cf_window_run_pair", "cf_window_run_ring", "cf_window_run_n_flushed",
-    "cf_window_set_scale", "cf_window_debug", "cf_l2_evict",
+    "cf_window_set_scale", "cf_window_debug", "cf_l2_evict", "cf_uvm_walk_pages",
     "cf_window_free",
     "cf_uvm_prefetch", "cf_uvm_advise",
 )
@@ -185,6 +185,8 @@ def _declare(L):
         "cf_window_set_scale": (C.c_int, [P, C.c_double]),
         "cf_window_debug": (C.c_int, [P, C.c_uint32]),
         "cf_l2_evict": (C.c_int, [P, P, U64]),
+        "cf_uvm_walk_pages": (C.c_int, [P, U64, C.c_int, C.c_uint32, C.c_int32, P, P, P, P, U64, U64, P, U64,
+                                        C.POINTER(U64)]),
         "cf_window_run_n_flushed": (C.c_int, [P, C.c_int, C.c_double, C.c_double, P, U64, C.POINTER(CfWindowStats)]),
         "cf_window_free": (C.c_int, [P]),
         "cf_uvm_prefetch": (C.c_int, [P, P, U64, C.c_int, P]),

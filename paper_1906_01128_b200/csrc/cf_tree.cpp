@@ -390,6 +390,79 @@ int cf_tree_chain_shape(const cf_tree* t, cf_chain_shape* out) {
   return CF_OK;
 }
 
+int cf_uvm_walk_pages(const void* arena, uint64_t total, int kind, uint32_t q, int32_t depth, const uint64_t* root_off,
+                      const int32_t* level, const uint64_t* ordinal, const uint64_t* count, uint64_t n, uint64_t page,
+                      uint64_t* out, uint64_t cap, uint64_t* npages) {
+  if (!npages || (n && (!arena || !root_off || !level || !ordinal || !count)) || page == 0)
+    return fail(CF_E_INVALID, "bad arguments");
+  const uint8_t* a = static_cast<const uint8_t*>(arena);
+  const uint64_t base = reinterpret_cast<uint64_t>(arena);
+  const bool dense = kind == CF_DENSE;
+  const uint64_t p0 = base / page, np = (base + total + page - 1) / page - p0;
+  std::vector<uint8_t> hit(np, 0);          // pages inside the arena (benign same-value races)
+  std::vector<std::vector<uint64_t>> wild;   // per thread: pages of fields outside the arena
+  int nthr = 1;
+#ifdef _OPENMP
+  nthr = n > (1u << 14) ? omp_get_max_threads() : 1;
+#endif
+  wild.resize(size_t(nthr));
+#pragma omp parallel num_threads(nthr)
+  {
+    int me = 0;
+#ifdef _OPENMP
+    me = omp_get_thread_num();
+#endif
+    auto mark = [&](uint64_t off) {   // the page of the 8-byte field at arena offset off
+      const uint64_t pg = (base + off) / page;
+      if (pg >= p0 && pg - p0 < np) hit[pg - p0] = 1;
+      else wild[size_t(me)].push_back(pg);
+    };
+#pragma omp for schedule(static)
+    for (int64_t ii = 0; ii < int64_t(n); ++ii) {
+      const uint64_t i = uint64_t(ii);
+      const int L = level[i];
+      uint64_t node = root_off[i];
+      uint64_t pw = 1;
+      if (dense)
+        for (int l = 1; l < L; ++l) pw *= q;
+      bool ok = true;
+      for (int l = 1; l <= L && ok; ++l) {
+        const uint64_t f = node + OFF_LNEXT;
+        mark(f);
+        if (f + 8 > total) { ok = false; break; }   // a wild chain: its next field is outside
+        uint64_t v;
+        memcpy(&v, a + f, 8);
+        const uint64_t blk = v - base;   // wraps for values below the arena
+        if (dense) {
+          const uint64_t digit = (ordinal[i] / pw) % q;
+          pw = pw >= q ? pw / q : 1;
+          node = blk + digit * ((l == depth) ? LEAF_NODE_SIZE : NODE_SIZE);
+        } else {
+          node = blk;
+        }
+      }
+      if (!ok) continue;
+      const bool leaf = dense && L == depth;
+      mark(node + (leaf ? LEAF_OFF_A : OFF_A));
+      if (count[i]) mark(node + OFF_NA);
+    }
+  }
+  uint64_t k = 0;
+  std::vector<uint64_t> extra;
+  for (auto& v : wild) extra.insert(extra.end(), v.begin(), v.end());
+  std::sort(extra.begin(), extra.end());
+  extra.erase(std::unique(extra.begin(), extra.end()), extra.end());
+  // sorted output: wild pages below the arena, the arena's pages, wild pages above
+  auto emit = [&](uint64_t pg) { if (out && k < cap) out[k] = pg; ++k; };
+  size_t x = 0;
+  for (; x < extra.size() && extra[x] < p0; ++x) emit(extra[x]);
+  for (uint64_t j = 0; j < np; ++j)
+    if (hit[j]) emit(p0 + j);
+  for (; x < extra.size(); ++x) emit(extra[x]);
+  *npages = k;
+  return (out && k > cap) ? fail(CF_E_INVALID, "page buffer too small (%llu needed)", (unsigned long long)k) : CF_OK;
+}
+
 int cf_tree_free(cf_tree* t) {
   delete t;
   return CF_OK;

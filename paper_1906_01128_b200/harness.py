@@ -683,19 +683,15 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
     """Pages the reference's UVM walk touches and dirties (harness.py:261-304, memory.py:378-394):
     the sorted distinct pages of the chain fields it reads, and the inclusive page ranges of the
     arrays it scales (read, then written).  Used for the logical page-fault counters; the data
-    itself migrates under the CUDA driver.  Chains are walked level by level for all targets at
-    once; array pages stay ranges (a 1 GiB tree is 262,144 pages)."""
+    itself migrates under the CUDA driver.  The chains are walked through the arena's pointer
+    values by the native library (cf_uvm_walk_pages); array pages stay ranges (a 1 GiB tree is
+    262,144 pages)."""
     spec = handle.spec
     base, e = handle.base, spec.elem
     forest = isinstance(spec, ForestSpec)
     tree = spec.tree if forest else spec
     linear = isinstance(tree, LinearSpec)
-    view = N.host_view(base, handle.total_bytes)
     arr = None
-
-    def rd(offs: np.ndarray) -> np.ndarray:   # 8-byte pointer fields -> arena offsets
-        ix = offs.astype(np.int64)[:, None] + np.arange(8, dtype=np.int64)[None, :]
-        return view[ix].copy().view("<u8").ravel().astype(np.int64) - base
 
     if policy == "ref" and not forest and not linear:
         # always take the last child: the last node of every level in pre-order
@@ -710,37 +706,33 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
         t_nodes = nodes[used]
     else:
         sel = idx if policy != "ref" or forest else handle.target_indices("ref")
-        # the tree-shape columns of the walk (immutable per tree and target set) are gathered once;
-        # the pointer values are read from memory on every call
+        # the tree-shape columns of the walk and the arrays' page ranges (immutable per tree and
+        # target set) are gathered once; the pointer values are read from memory on every call,
+        # by the native walk (cf_uvm_walk_pages: one chain per target, distinct pages by bitmap)
         wcache = handle.__dict__.setdefault("_uvm_walk_cache", {})
-        key = (policy, len(sel), int(sel[0]) if len(sel) else -1, int(sel[-1]) if len(sel) else -1)
+        key = (policy, len(sel), int(sel[0]) if len(sel) else -1, int(sel[-1]) if len(sel) else -1, page)
         cols = wcache.get(key)
         if cols is None or not np.array_equal(cols[0], sel):
-            cols = wcache[key] = (np.array(sel, copy=True), handle.arr_level[sel].astype(np.int64),
-                                  handle.arr_root[sel].astype(np.int64), handle.arr_ordinal[sel].astype(np.int64))
-        L, ords = cols[1], cols[3]
-        fields, t_nodes = [], []
-        node = cols[2].copy()
-        depth = 0 if linear else tree.depth
-        q = 1 if linear else tree.q
-        one_level = L.size > 0 and int(L.min()) == int(L.max())   # e.g. every leaf: no masks
-        for lv in range(1, int(L.max()) + 1 if L.size else 1):
-            act = slice(None) if one_level else L >= lv
-            # many chains share their upper nodes: read each distinct Lnext field once
-            un, inv = _unique_inverse(node[act])
-            fields.append(un + OFF_LNEXT)
-            blk = rd(un + OFF_LNEXT)[inv]
-            if linear:
-                node[act] = blk
-            else:
-                child = NODE_SIZE if lv < depth else LEAF_NODE_SIZE
-                pw = q ** (int(L[0]) - lv) if one_level else q ** (L[act] - lv)
-                digit = (ords[act] // pw) % q
-                node[act] = blk + child * digit
-        leaf = (~np.asarray(linear)) & (L == depth) if not linear else np.zeros(L.shape, bool)
-        fields.append(node + np.where(leaf, LEAF_OFF_A, OFF_A))
-        t_nodes = node
-        arr, has = np.asarray(sel, np.int64), np.ones(len(sel), bool)   # each walk ends at its array's owner
+            cnt = handle.arr_count[sel].astype(np.uint64)
+            keep = cnt > 0
+            starts = handle.arr_off[sel].astype(np.int64)[keep] + base
+            dirty = (starts // page, (starts + e * (cnt[keep].astype(np.int64) - 1)) // page)
+            cols = wcache[key] = (np.array(sel, copy=True),
+                                  np.ascontiguousarray(handle.arr_level[sel], np.int32),
+                                  np.ascontiguousarray(handle.arr_root[sel], np.uint64),
+                                  np.ascontiguousarray(handle.arr_ordinal[sel], np.uint64),
+                                  np.ascontiguousarray(cnt), dirty)
+        _, lv, roots, ords, cnt, dirty = cols
+        n = len(sel)
+        kind, q, depth = (N.CF_LINEAR, 1, 0) if linear else (N.CF_DENSE, int(tree.q), int(tree.depth))
+        lib = N.lib()
+        need = C.c_uint64()
+        args = (C.c_void_p(base), handle.total_bytes, kind, q, depth, N.ptr(roots), N.ptr(lv), N.ptr(ords),
+                N.ptr(cnt), n, page)
+        N.check(lib.cf_uvm_walk_pages(*args, None, 0, C.byref(need)), "uvm walk")
+        pages = np.empty(max(int(need.value), 1), np.uint64)
+        N.check(lib.cf_uvm_walk_pages(*args, N.ptr(pages), len(pages), C.byref(need)), "uvm walk")
+        return pages[:int(need.value)].astype(np.int64), dirty
     if arr is None:
         # terminal nodes with an array (the fixed reference paths above): find it by owner
         t_nodes = np.asarray(t_nodes, np.int64)
@@ -759,17 +751,6 @@ def _uvm_device_pages(handle: TreeHandle, policy: str, idx: np.ndarray, page: in
     dirty = (starts // page, (starts + e * (cnt[keep] - 1)) // page)   # page ranges, inclusive
     f = np.concatenate([np.asarray(x, np.int64) for x in fields]) if fields else np.zeros(0, np.int64)
     return _distinct_pages((f + base) // page), dirty
-
-
-def _unique_inverse(x: np.ndarray):
-    """np.unique(x, return_inverse=True); O(n) when x is already non-decreasing (targets in
-    ordinal order over a DFS layout -- C4's 1M chains), a sort otherwise."""
-    if x.size > 1 and bool((x[1:] >= x[:-1]).all()):
-        first = np.empty(x.size, bool)
-        first[0] = True
-        np.not_equal(x[1:], x[:-1], out=first[1:])
-        return x[first], np.cumsum(first) - 1
-    return np.unique(x, return_inverse=True)
 
 
 def _distinct_pages(p: np.ndarray) -> np.ndarray:

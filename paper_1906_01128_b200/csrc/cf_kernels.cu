@@ -58,6 +58,12 @@
 #ifndef CF_GROUP_WARP_U
 #define CF_GROUP_WARP_U 4
 #endif
+#ifndef CF_RELOC_FASTMAP
+#define CF_RELOC_FASTMAP 1
+#endif
+#ifndef CF_PDL_WAIT_ALWAYS
+#define CF_PDL_WAIT_ALWAYS 0
+#endif
 #ifndef CF_OWN_MINB
 #define CF_OWN_MINB 4
 #endif
@@ -596,6 +602,9 @@ struct ScaleArgs {
   RelocArgs reloc;   // optional fused relocation (reloc.n == 0: none)
   unsigned reloc_blocks;   // CTAs k * reloc_stride (k < reloc_blocks) run it, RELOC_U sites per thread
   unsigned reloc_stride;
+  unsigned reloc_last;     // (reloc_blocks - 1) * reloc_stride: the last relocation CTA
+  unsigned reloc_magic;    // ceil(2^32 / reloc_stride): umulhi(b, magic) is b / stride or one more
+  unsigned pdl;            // launched as a programmatic dependent: wait for the primary grid
   LeafOwn own;             // PATH_OWNED launches
 };
 
@@ -1116,7 +1125,11 @@ __global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_OWNED ? CF_OWN_MIN
     k_scale(ScaleArgs a, T s) {
   // launched as a programmatic dependent of the attach / resolve kernel: its CTAs may be resident
   // before that grid has finished -- wait for its completion (and memory) before any read
+#if CF_PDL_WAIT_ALWAYS
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#else
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   constexpr uint64_t TILE = TILE_BYTES / sizeof(T);
   // fused relocation CTAs (the detach riding in the launch) are spread evenly through the grid --
   // CTA k * reloc_stride is relocation CTA k: in RESOLVED mode no leaf CTA reads a pointer field
@@ -1125,12 +1138,28 @@ __global__ void __launch_bounds__(SCALE_THREADS, PATH == PATH_OWNED ? CF_OWN_MIN
   // or trailing the drain (last)
   unsigned b = blockIdx.x;
   if (a.reloc_blocks) {
+#if CF_RELOC_FASTMAP
+    // CTAs past the last relocation slot (all but a few for C2's single detach CTA) skip the
+    // division; the rest divide by a multiply-high (CTA start latency matters on the tile path)
+    if (b > a.reloc_last) {
+      b -= a.reloc_blocks;
+    } else {
+      unsigned k = unsigned(__umulhi(b, a.reloc_magic));   // b / reloc_stride or one more
+      if (k * a.reloc_stride > b) --k;
+      if (b == k * a.reloc_stride && k < a.reloc_blocks) {
+        relocate_multi(a.reloc, uint64_t(k) * (SCALE_THREADS * RELOC_U) + threadIdx.x, a.bad);
+        return;
+      }
+      b -= min(k + 1, a.reloc_blocks);
+    }
+#else
     const unsigned k = b / a.reloc_stride;
     if (b % a.reloc_stride == 0 && k < a.reloc_blocks) {
       relocate_multi(a.reloc, uint64_t(k) * (SCALE_THREADS * RELOC_U) + threadIdx.x, a.bad);
       return;
     }
     b -= min(k + 1, a.reloc_blocks);
+#endif
   }
   if constexpr (PATH == PATH_OWNED) {
     scale_group_owned<T>(a, b, s);
@@ -1471,7 +1500,10 @@ int launch_scale(cf_ctx* ctx, int elem, int mode, const uint8_t* image, const cf
                                          (unsigned long long)units);
   static const bool reloc_first = getenv("CF_RELOC_FIRST") != nullptr;   // design experiments
   const unsigned stride = (rblocks == 0 || reloc_first) ? 1u : unsigned(units / rblocks);
-  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, tag, RelocArgs{}, unsigned(rblocks), stride, LeafOwn{}};
+  const unsigned rlast = rblocks ? unsigned(rblocks - 1) * stride : 0u;
+  const unsigned rmagic = stride > 1 ? unsigned((0x100000000ull + stride - 1) / stride) : 0u;
+  ScaleArgs a{image, sh, root, level, ordinal, ea, count, work, bad, tag, RelocArgs{}, unsigned(rblocks), stride,
+              rlast, rmagic, pdl ? 1u : 0u, LeafOwn{}};
   if (nreloc) a.reloc = *fused_reloc;
   if (own) {
     if (mode == CF_MODE_CHASE) return fail(CF_E_INVALID, "leaf-owned relocation needs RESOLVED mode");

@@ -159,6 +159,24 @@ class Dist:
             self.pg.destroy_process_group()
 
 
+def share_host_threads(dist: "Dist") -> None:
+    """torchrun pins OMP_NUM_THREADS=1 per rank; the native planner / builder (OpenMP, outside the
+    timed regions) then fills a rank's arena on one core.  Give each rank its share of this
+    process's CPUs instead (the oracle legs set their own thread counts)."""
+    if dist.world <= 1:
+        return
+    import ctypes
+    try:
+        cpus = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        cpus = os.cpu_count() or 1
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", dist.world))
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(max(1, cpus // max(1, local)))
+    except OSError:
+        pass
+
+
 def free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -895,6 +913,7 @@ def main(argv=None):
     if world is not None and int(world) != args.gpus:
         ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     dist = Dist()
+    share_host_threads(dist)
     try:
         if args.impl == "reference":
             run_reference(args, dist)

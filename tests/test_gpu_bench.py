@@ -50,3 +50,15 @@ def test_bench_line_contract_small(gpu):
     assert rec["e2e"]["host_link_gbs"]["bidir"] > 0 and rec["e2e"]["frac_of_link_roofline"] > 0
     ref = rec.get("cpu_baseline_reference_python", {})
     assert ref.get("kind") == "reference_python"
+
+
+def test_bench_gpus_4_strong_c5_subtree_shards(gpu):
+    """The strong-scaling launch the driver's scaling run uses for C5: four ranks (sharing this
+    box's GPU), one dense tree cut by subtree, every leaf checksum gathered and checked."""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--config", "C5", "--steps", "3", "--warmup", "3",
+                        "--leaf-elems", "262144", "--skip-schemes", "--skip-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900, cwd=str(REPO))
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
+    rec = _line(r.stdout)
+    assert rec["n_gpus"] == 4 and rec["scaling"] == "strong"
+    assert rec["gather"]["leaves"] == 64 and rec["gather"]["complete"] and rec["gather"]["checksums_match"]

@@ -223,6 +223,13 @@ for spec, align in ((cf.DenseSpec(3, 4099, 2), 1), (cf.DenseSpec(4, 3000, 2, ele
     off, cnt = w.table(N.CF_TAB_ARR_OFF), w.table(N.CF_TAB_ARR_COUNT)
     leaf_checksums(w.ctx, w.image, off[w.targets], cnt[w.targets], spec.elem)
     w.close()
+# leaf-owned steps (per-warp shared-memory slots, no CTA barrier): resident and multi-step
+w = cf.DeepCopyWindow(cf.DenseSpec(16, 8, 3, elem=4, leaf_only=True), seed=1, policy="all_leaves", align=16,
+                      chunk_bytes=16384)
+w.run(scale=2.0)
+w.upload_raw()
+w.run_resident(scale=2.0)
+w.close()
 print("race ok")
 '''
 

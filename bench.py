@@ -823,6 +823,9 @@ def run_ours(args, dist: Dist) -> None:
             if name != args.config:
                 line["per_config"][name] = summary_block(name, 4, device, args.chunk_mb, numa_node,
                                                          min(args.steps, 10), args.warmup, dist, peaks, link_plain)
+        # the reference's own dtype on the relocation-bound shape too (1M leaves of 256 float64)
+        line["per_config"]["C4_f64"] = summary_block("C4", 8, device, args.chunk_mb, numa_node, min(args.steps, 10),
+                                                     args.warmup, dist, peaks, link_plain)
     if dist.rank == 0 and not args.skip_schemes and args.config != "C5":
         line["schemes"] = compare_schemes(spec, policy, 3, device)
     if dist.rank == 0 and not args.skip_cpu_baseline:
